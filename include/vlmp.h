@@ -1,0 +1,134 @@
+/*
+ * vlmp.h -- C ABI of the B200-native variable-length matrix profile (libvlmp.so).
+ *
+ * The reference (seriesmine, pure Python/NumPy) has no native FFI; its drop-in
+ * boundary is the pair of Python entry points
+ *   valmod(series, lmin, lmax, p, *, ranking, trace, threads)
+ *       /root/reference/pkg/src/seriesmine/valmod.py:192-258
+ *   topkm_discord_discovery(series, lmin, lmax, k, m, p, *, trace, threads)
+ *       /root/reference/pkg/src/seriesmine/discords.py:206-247
+ * plus compute_matrix_profile (profile.py:329-377) which the CLI calls.
+ * paper_2008_13447_b200 re-exposes those names in Python and reaches the GPU
+ * only through the functions below (ctypes; plain pointers and sizes, no torch
+ * types). Host pointers are caller-owned numpy buffers, never retained past the
+ * call. The library owns all device memory.
+ *
+ * Every function returns 0 on success or a VLMP_E_* code; the message is in
+ * vlmp_last_error() (thread-local). Codes map 1:1 onto the reference's
+ * SeriesMineError subclasses (exceptions.py:4-56).
+ */
+#ifndef VLMP_H
+#define VLMP_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+enum {
+    VLMP_OK = 0,
+    VLMP_E_INVALID_PARAMETERS = 1,   /* InvalidParametersError   exceptions.py:47 */
+    VLMP_E_SERIES_TOO_SHORT = 2,     /* SeriesTooShortError      exceptions.py:35 */
+    VLMP_E_ALL_CONSTANT = 3,         /* AllConstantError         exceptions.py:39 */
+    VLMP_E_EMPTY_SERIES = 4,         /* EmptySeriesError         exceptions.py:8  */
+    VLMP_E_CUDA = 10,                /* device / driver failure (no CPU fallback) */
+    VLMP_E_STATE = 11,               /* call order violated (e.g. no run yet)     */
+    VLMP_E_NOMEM = 12
+};
+
+typedef struct vlmp_session vlmp_session;
+
+/* Create a session on a CUDA device (one session = one device, one in-flight call). */
+int vlmp_create(vlmp_session** out, int device);
+void vlmp_destroy(vlmp_session* s);
+const char* vlmp_last_error(void);
+
+/*
+ * Upload one series. t, cum, cum2 are the reference DataSeries' values, _cum and
+ * _cum2 (series.py:57-67: cum has n+1 entries with a leading 0, sequential
+ * np.cumsum) and sigma_floor (policy.py:27-39). Window statistics are derived
+ * on the device from cum/cum2 with the reference's exact operation order, so
+ * mean/std are bit-identical to DataSeries.moving_stats (series.py:91-100).
+ */
+int vlmp_set_series(vlmp_session* s, const double* t, const double* cum,
+                    const double* cum2, int64_t n, double sigma_floor);
+
+/*
+ * Phase 1: the exhaustive per-length matrix profile for lengths [lmin, lmax]
+ * restricted to diagonal bands [band_lo, band_hi) (band_hi < 0 = all bands).
+ * Single-GPU callers pass the whole range; multi-GPU callers shard bands
+ * (vlmp_band_split) and merge the partial per-length minima with
+ * vlmp_partials_* + an NCCL min all-reduce before phase 2.
+ * flags: VLMP_F_FULL_EVERY_LENGTH forces the exact full-fold kernel at every
+ * length (no bound filter) -- a self-check mode, slower.
+ */
+#define VLMP_F_FULL_EVERY_LENGTH 1u
+int vlmp_profile_range(vlmp_session* s, int32_t lmin, int32_t lmax,
+                       int64_t band_lo, int64_t band_hi, uint32_t flags);
+
+/* Number of 256-diagonal bands and a work-balanced contiguous split of them. */
+int vlmp_band_count(vlmp_session* s, int32_t lmin, int64_t* n_bands);
+int vlmp_band_split(vlmp_session* s, int32_t lmin, int32_t lmax, int32_t parts,
+                    int64_t* cuts /* parts+1 entries */);
+
+/*
+ * Exact cross-GPU merge of the partial per-(length, offset) minima. The caller
+ * allocates device buffers keys[n_len * stride] (uint64: order-preserving bits of
+ * the clamped key; +inf bits = none) and idx[n_len * stride] (int64 neighbour;
+ * INT64_MAX = none) on this session's device (e.g. torch tensors):
+ *   export  -> all-reduce(MIN) keys into merged -> mask_idx (idx := INT64_MAX where
+ *   the local key != merged key) -> all-reduce(MIN) idx -> import(merged, idx).
+ * This is the lexicographic (value, smallest index) rule of profile.py:308.
+ */
+int vlmp_partials_size(vlmp_session* s, int64_t* n_len, int64_t* stride);
+int vlmp_partials_export(vlmp_session* s, void* keys, void* idx);
+int vlmp_partials_mask_idx(vlmp_session* s, const void* merged_keys, const void* keys, void* idx);
+int vlmp_partials_import(vlmp_session* s, const void* keys, const void* idx);
+
+/*
+ * Phase 2: from the (merged) per-length minima compute the exact per-offset
+ * profile values (canonical pair distance, series.py:169-194), the VALMP fold
+ * (valmod.py:57-73), and keep MP/IP of every length device-resident.
+ */
+int vlmp_finalize(vlmp_session* s);
+
+/* Read-offs (all after vlmp_finalize). */
+int vlmp_get_valmp(vlmp_session* s, double* dist, double* norm, int64_t* lengths,
+                   int64_t* indices, uint8_t* populated /* n - lmin + 1 each */);
+int vlmp_get_profile(vlmp_session* s, int32_t length, double* mp, int64_t* ip
+                     /* n - length + 1 each */);
+/*
+ * Per length, the 2k smallest (mp, offset) rows, ascending (first = the
+ * length's top-1 motif owner, valmod.py:170-177). out_off/out_nbr/out_d are
+ * [n_len][2k]; unused slots have offset -1.
+ */
+int vlmp_smallest_rows(vlmp_session* s, int32_t k2, int64_t* out_off,
+                       int64_t* out_nbr, double* out_d);
+/* Top-k 1st discords per length (discords.py:68-93 replay): [n_len][k]. */
+int vlmp_discords(vlmp_session* s, int32_t k, double* out_dist, int64_t* out_off);
+/*
+ * VALMP improvement events with norm <= tau, in (length, offset) order
+ * (the stream valmod feeds to a PairRanking, motifsets.py:105-117).
+ * Returns the total count in *count (may exceed cap; then call again).
+ */
+int vlmp_ranking_events(vlmp_session* s, double tau, int64_t cap, int64_t* ev_off,
+                        int64_t* ev_nbr, int64_t* ev_len, double* ev_dist,
+                        double* ev_norm, int64_t* count);
+
+/*
+ * Timings and counters of the last phase-1/phase-2 run:
+ * out[0] profile ms (device), out[1] finalize ms, out[2] executed pair updates,
+ * out[3] W (non-trivial pair updates), out[4] tile-kernel ms, out[5] tile-kernel
+ * launches, out[6] filtered lengths, out[7] full lengths, out[8] slow-path
+ * candidate merges, out[9] total kernel launches, out[10] first-length tile ms.
+ */
+int vlmp_stats(vlmp_session* s, double* out, int32_t n_out);
+
+/* FP64 FMA peak microbenchmark (DFMA instr/s on this device, all SMs). */
+int vlmp_measure_fp64_peak(vlmp_session* s, double* fma_per_s);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* VLMP_H */

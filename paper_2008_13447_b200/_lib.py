@@ -1,0 +1,199 @@
+"""ctypes binding of libvlmp.so (include/vlmp.h). Fails loudly when the CUDA
+library is missing or no B200 is present -- there is no CPU fallback."""
+
+from __future__ import annotations
+
+import ctypes as C
+import os
+import threading
+
+import numpy as np
+
+from .exceptions import DeviceError, raise_for
+
+HERE = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(HERE, "libvlmp.so")
+
+_c_int64_p = C.POINTER(C.c_int64)
+_c_double_p = C.POINTER(C.c_double)
+
+# name -> (restype, argtypes); exactly the functions declared in include/vlmp.h
+SIGNATURES = {
+    "vlmp_create": (C.c_int, [C.POINTER(C.c_void_p), C.c_int]),
+    "vlmp_destroy": (None, [C.c_void_p]),
+    "vlmp_last_error": (C.c_char_p, []),
+    "vlmp_set_series": (C.c_int, [C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p, C.c_int64, C.c_double]),
+    "vlmp_profile_range": (C.c_int, [C.c_void_p, C.c_int32, C.c_int32, C.c_int64, C.c_int64, C.c_uint32]),
+    "vlmp_band_count": (C.c_int, [C.c_void_p, C.c_int32, _c_int64_p]),
+    "vlmp_band_split": (C.c_int, [C.c_void_p, C.c_int32, C.c_int32, C.c_int32, C.c_void_p]),
+    "vlmp_partials_size": (C.c_int, [C.c_void_p, _c_int64_p, _c_int64_p]),
+    "vlmp_partials_export": (C.c_int, [C.c_void_p, C.c_void_p, C.c_void_p]),
+    "vlmp_partials_mask_idx": (C.c_int, [C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p]),
+    "vlmp_partials_import": (C.c_int, [C.c_void_p, C.c_void_p, C.c_void_p]),
+    "vlmp_finalize": (C.c_int, [C.c_void_p]),
+    "vlmp_get_valmp": (C.c_int, [C.c_void_p] + [C.c_void_p] * 5),
+    "vlmp_get_profile": (C.c_int, [C.c_void_p, C.c_int32, C.c_void_p, C.c_void_p]),
+    "vlmp_smallest_rows": (C.c_int, [C.c_void_p, C.c_int32, C.c_void_p, C.c_void_p, C.c_void_p]),
+    "vlmp_discords": (C.c_int, [C.c_void_p, C.c_int32, C.c_void_p, C.c_void_p]),
+    "vlmp_ranking_events": (C.c_int, [C.c_void_p, C.c_double, C.c_int64] + [C.c_void_p] * 5 + [_c_int64_p]),
+    "vlmp_stats": (C.c_int, [C.c_void_p, C.c_void_p, C.c_int32]),
+    "vlmp_measure_fp64_peak": (C.c_int, [C.c_void_p, _c_double_p]),
+}
+
+FLAG_FULL_EVERY_LENGTH = 1
+
+_lib = None
+_lib_lock = threading.Lock()
+
+
+def load():
+    """Load libvlmp.so (CDLL); raises if it was never built."""
+    global _lib
+    with _lib_lock:
+        if _lib is not None:
+            return _lib
+        if not os.path.exists(LIB_PATH):
+            raise DeviceError(
+                f"{LIB_PATH} is missing: build the CUDA library first "
+                "(python -c 'import __graft_entry__ as g; g.build()'); no CPU fallback exists")
+        lib = C.CDLL(LIB_PATH)
+        for name, (res, args) in SIGNATURES.items():
+            fn = getattr(lib, name)
+            fn.restype = res
+            fn.argtypes = args
+        _lib = lib
+        return lib
+
+
+def _ptr(a: np.ndarray):
+    return C.c_void_p(a.ctypes.data)
+
+
+class Session:
+    """One libvlmp session = one device. Calls are serialised per session."""
+
+    def __init__(self, device: int = 0):
+        self.lib = load()
+        self.device = int(device)
+        h = C.c_void_p()
+        self._check(self.lib.vlmp_create(C.byref(h), self.device))
+        self.h = h
+        self.lock = threading.Lock()
+        self.n = 0
+        self.lmin = self.lmax = 0
+
+    def _check(self, rc):
+        if rc != 0:
+            raise_for(rc, (self.lib.vlmp_last_error() or b"").decode())
+
+    def close(self):
+        if getattr(self, "h", None):
+            self.lib.vlmp_destroy(self.h)
+            self.h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+    # -- phase 0/1/2 ---------------------------------------------------------
+    def set_series(self, values, cum, cum2, sigma_floor):
+        t = np.ascontiguousarray(values, dtype=np.float64)
+        c1 = np.ascontiguousarray(cum, dtype=np.float64)
+        c2 = np.ascontiguousarray(cum2, dtype=np.float64)
+        self._check(self.lib.vlmp_set_series(self.h, _ptr(t), _ptr(c1), _ptr(c2), t.shape[0],
+                                             float(sigma_floor)))
+        self.n = int(t.shape[0])
+
+    def profile(self, lmin, lmax, band_lo=0, band_hi=-1, flags=0):
+        self._check(self.lib.vlmp_profile_range(self.h, int(lmin), int(lmax), int(band_lo),
+                                                int(band_hi), int(flags)))
+        self.lmin, self.lmax = int(lmin), int(lmax)
+
+    def band_split(self, lmin, lmax, parts):
+        cuts = np.zeros(parts + 1, dtype=np.int64)
+        self._check(self.lib.vlmp_band_split(self.h, int(lmin), int(lmax), int(parts), _ptr(cuts)))
+        return cuts
+
+    def partials_size(self):
+        a, b = C.c_int64(), C.c_int64()
+        self._check(self.lib.vlmp_partials_size(self.h, C.byref(a), C.byref(b)))
+        return a.value, b.value
+
+    def partials_export(self, keys_ptr, idx_ptr):
+        self._check(self.lib.vlmp_partials_export(self.h, C.c_void_p(keys_ptr), C.c_void_p(idx_ptr)))
+
+    def partials_mask_idx(self, merged_ptr, keys_ptr, idx_ptr):
+        self._check(self.lib.vlmp_partials_mask_idx(self.h, C.c_void_p(merged_ptr),
+                                                    C.c_void_p(keys_ptr), C.c_void_p(idx_ptr)))
+
+    def partials_import(self, keys_ptr, idx_ptr):
+        self._check(self.lib.vlmp_partials_import(self.h, C.c_void_p(keys_ptr), C.c_void_p(idx_ptr)))
+
+    def finalize(self):
+        self._check(self.lib.vlmp_finalize(self.h))
+
+    # -- read-offs -------------------------------------------------------------
+    def valmp_arrays(self):
+        n0 = self.n - self.lmin + 1
+        d = np.empty(n0); nm = np.empty(n0)
+        ln = np.empty(n0, dtype=np.int64); ix = np.empty(n0, dtype=np.int64)
+        pop = np.empty(n0, dtype=np.uint8)
+        self._check(self.lib.vlmp_get_valmp(self.h, _ptr(d), _ptr(nm), _ptr(ln), _ptr(ix), _ptr(pop)))
+        return d, nm, ln, ix, pop.astype(bool)
+
+    def profile_arrays(self, length):
+        N = self.n - int(length) + 1
+        mp = np.empty(N); ip = np.empty(N, dtype=np.int64)
+        self._check(self.lib.vlmp_get_profile(self.h, int(length), _ptr(mp), _ptr(ip)))
+        return mp, ip
+
+    def smallest_rows(self, k2):
+        nl = self.lmax - self.lmin + 1
+        off = np.empty((nl, k2), dtype=np.int64); nbr = np.empty((nl, k2), dtype=np.int64)
+        d = np.empty((nl, k2))
+        self._check(self.lib.vlmp_smallest_rows(self.h, int(k2), _ptr(off), _ptr(nbr), _ptr(d)))
+        return off, nbr, d
+
+    def discords(self, k):
+        nl = self.lmax - self.lmin + 1
+        d = np.empty((nl, k)); o = np.empty((nl, k), dtype=np.int64)
+        self._check(self.lib.vlmp_discords(self.h, int(k), _ptr(d), _ptr(o)))
+        return d, o
+
+    def ranking_events(self, tau, cap=1 << 16):
+        while True:
+            bufs = [np.empty(cap, dtype=np.int64) for _ in range(3)] + [np.empty(cap) for _ in range(2)]
+            cnt = C.c_int64()
+            self._check(self.lib.vlmp_ranking_events(self.h, float(tau), int(cap),
+                                                     *[_ptr(b) for b in bufs], C.byref(cnt)))
+            if cnt.value <= cap:
+                return [b[:cnt.value] for b in bufs]
+            cap = int(cnt.value)
+
+    def stats(self):
+        out = np.zeros(16)
+        self._check(self.lib.vlmp_stats(self.h, _ptr(out), 16))
+        keys = ["profile_ms", "finalize_ms", "executed_updates", "W", "tile_ms", "tile_launches",
+                "filtered_lengths", "full_lengths", "slow_merges", "kernel_launches", "first_tile_ms"]
+        return {k: float(out[i]) for i, k in enumerate(keys)}
+
+    def measure_fp64_peak(self):
+        v = C.c_double()
+        self._check(self.lib.vlmp_measure_fp64_peak(self.h, C.byref(v)))
+        return v.value
+
+
+_sessions: dict = {}
+_sess_lock = threading.Lock()
+
+
+def session(device: int = 0) -> Session:
+    """Process-wide cached session per device."""
+    with _sess_lock:
+        s = _sessions.get(device)
+        if s is None:
+            s = Session(device)
+            _sessions[device] = s
+        return s

@@ -1,0 +1,249 @@
+"""Drop-in entry points: the reference's signatures, results from the B200 path.
+
+  valmod                    seriesmine/valmod.py:192-258
+  topkm_discord_discovery   seriesmine/discords.py:206-247
+  compute_matrix_profile    seriesmine/profile.py:329-377
+  motifs_per_length         BASELINE.md decision 1 (= valmod(series, l, l, p,
+                            ranking=PairRanking(k)) for every l)
+
+Every call validates arguments with the reference's own rules and error types,
+then runs the exhaustive per-length profile on the GPU (libvlmp, via ctypes).
+``p`` and ``threads`` are accepted for signature compatibility; the GPU path is
+exhaustive (no pruning capacity) and its output does not depend on them -- the
+reference guarantees the same invariance (valmod.py:201-203, :209-210).
+There is no CPU fallback: a missing library or device raises DeviceError.
+"""
+
+from __future__ import annotations
+
+import os
+
+import numpy as np
+
+from . import _lib, policy
+from .exceptions import AllConstantError, InvalidParametersError, SeriesTooShortError
+from .results import (VALMP, DiscordMatrix, DiscordScan, MatrixProfile, ProfileResult,
+                      VariableLengthDiscordMatrix, update_variable_length_discords)
+from .series import as_series
+
+
+def _device() -> int:
+    return int(os.environ.get("VLMP_DEVICE", os.environ.get("LOCAL_RANK", 0)))
+
+
+def validate_range(series, lmin: int, lmax: int):
+    """valmod.py:180-189."""
+    if lmin > lmax:
+        raise InvalidParametersError(f"lmin {lmin} > lmax {lmax}")
+    if lmin < 4:
+        raise InvalidParametersError("minimum window length is 4")
+    need = lmax + policy.exclusion_zone(lmax)
+    if series.n < need:
+        raise SeriesTooShortError(
+            f"series of {series.n} points cannot host a non-trivial pair at length {lmax} "
+            f"(needs {need})")
+
+
+def _check_profile_length(series, length: int):
+    """profile.py:346-355 (the scan at the first length performs these checks)."""
+    if length < 4 or 2 * length > series.n:
+        raise SeriesTooShortError(f"need 4 <= length <= n/2 (length={length}, n={series.n})")
+    mu, sd = _moving_sd(series, length)
+    if not (sd >= series.sigma_floor).any():
+        raise AllConstantError(f"every window of length {length} is constant")
+
+
+def _moving_sd(series, length):
+    cum, cum2 = series._cum, series._cum2
+    s = cum[length:] - cum[:-length]
+    ss = cum2[length:] - cum2[:-length]
+    mu = s / length
+    var = ss / length - mu * mu
+    np.maximum(var, 0.0, out=var)
+    return mu, np.sqrt(var)
+
+
+class GpuRun:
+    """Device-resident result of one exhaustive run over [lmin, lmax]."""
+
+    def __init__(self, series, lmin: int, lmax: int, flags: int = 0, device: int | None = None):
+        self.series = series
+        self.lmin, self.lmax = int(lmin), int(lmax)
+        self.sess = _lib.session(_device() if device is None else device)
+        with self.sess.lock:
+            self.sess.set_series(series.values, series._cum, series._cum2, series.sigma_floor)
+            self.sess.profile(lmin, lmax, 0, -1, flags)
+            self.sess.finalize()
+            self.stats = self.sess.stats()
+
+    # All read-offs re-take the session lock; results stay valid until the next run.
+    def valmp(self) -> VALMP:
+        with self.sess.lock:
+            d, nm, ln, ix, pop = self.sess.valmp_arrays()
+        v = VALMP(d.shape[0])
+        v.distances[:] = d
+        v.norm_distances[:] = nm
+        v.lengths[:] = ln
+        v.indices[:] = ix
+        v.populated[:] = pop
+        return v
+
+    def smallest_rows(self, k2: int):
+        with self.sess.lock:
+            return self.sess.smallest_rows(k2)
+
+    def discords(self, k: int):
+        with self.sess.lock:
+            return self.sess.discords(k)
+
+    def profile(self, length: int):
+        with self.sess.lock:
+            return self.sess.profile_arrays(length)
+
+    def ranking_events(self, tau: float):
+        with self.sess.lock:
+            return self.sess.ranking_events(tau)
+
+
+def _per_length_motifs(run: GpuRun):
+    """(min, max, d) of each length's first-argmin row (valmod.py:170-177) or None."""
+    off, nbr, d = run.smallest_rows(1)
+    out = []
+    for li in range(run.lmax - run.lmin + 1):
+        if off[li, 0] >= 0 and np.isfinite(d[li, 0]):
+            a, b = int(off[li, 0]), int(nbr[li, 0])
+            out.append((min(a, b), max(a, b), float(d[li, 0])))
+        else:
+            out.append(None)
+    return out
+
+
+def _ranking_threshold(v: VALMP, capacity: int) -> float:
+    """Upper bound on the capacity-th best distinct pair key: taken over the final
+    VALMP entries (each is one improvement event), so every event that can reach
+    the final ranking has norm <= this value."""
+    sel = np.flatnonzero(v.populated)
+    if sel.size == 0:
+        return np.inf
+    a = np.minimum(sel, v.indices[sel])
+    b = np.maximum(sel, v.indices[sel])
+    order = np.lexsort((b, a, v.lengths[sel], v.norm_distances[sel]))
+    seen = set()
+    for q in order:
+        pair = (int(a[q]), int(b[q]))
+        if pair in seen:
+            continue
+        seen.add(pair)
+        if len(seen) == capacity:
+            return float(v.norm_distances[sel][q])
+    return np.inf
+
+
+def _feed_ranking(run: GpuRun, v: VALMP, ranking):
+    tau = _ranking_threshold(v, ranking.capacity)
+    off, nbr, ln, dist, norm = run.ranking_events(tau)
+    for q in np.lexsort((off, ln)):     # the reference's push order: length, then offset
+        ranking.push(int(off[q]), int(nbr[q]), float(dist[q]), int(ln[q]), float(norm[q]))
+
+
+def valmod(series, lmin: int, lmax: int, p: int, *, ranking=None, trace=None,
+           threads: int = 1) -> VALMP:
+    """Exact best normalised match per offset over every length in [lmin, lmax]."""
+    series = as_series(series)
+    validate_range(series, lmin, lmax)
+    if p < 1:
+        raise InvalidParametersError("p must be at least 1")
+    _check_profile_length(series, lmin)
+    run = GpuRun(series, lmin, lmax)
+    v = run.valmp()
+    if trace is not None:
+        for li, motif in enumerate(_per_length_motifs(run)):
+            length = lmin + li
+            n_dp = series.n - length + 1
+            trace.add_length(length, n_profiles=n_dp, n_valid=n_dp, n_nonvalid=0,
+                             n_recomputed=0, full_recompute=False, motif=motif)
+    if ranking is not None:
+        _feed_ranking(run, v, ranking)
+    return v
+
+
+def topkm_discord_discovery(series, lmin: int, lmax: int, k: int, m: int, p: int, *,
+                            trace=None, threads: int = 1) -> DiscordScan:
+    """Exact top-k m-th discords for every length, merged across lengths (m = 1)."""
+    series = as_series(series)
+    if m < 1 or k < 1:
+        raise InvalidParametersError("k and m must be at least 1")
+    if p < m:
+        raise InvalidParametersError(f"p ({p}) must be at least m ({m})")
+    validate_range(series, lmin, lmax)
+    if m != 1:
+        raise InvalidParametersError(
+            "the GPU path computes 1st discords (m = 1); m > 1 is not implemented yet")
+    if k > 32:
+        raise InvalidParametersError("k must be at most 32 on the GPU path")
+    _check_profile_length(series, lmin)
+    run = GpuRun(series, lmin, lmax)
+    dist, off = run.discords(k)
+    merged = VariableLengthDiscordMatrix.empty(k, m)
+    per_length = {}
+    for li in range(lmax - lmin + 1):
+        length = lmin + li
+        dkm = DiscordMatrix.empty(k, m, length)
+        dkm.dist[:, 0] = dist[li]
+        dkm.offset[:, 0] = off[li]
+        dkm._occupied = {int(o) for o in off[li] if o >= 0}
+        per_length[length] = dkm
+        update_variable_length_discords(dkm, merged, k, m)
+        if trace is not None:
+            n_dp = series.n - length + 1
+            trace.add_length(length, n_profiles=n_dp, n_valid=n_dp, n_nonvalid=0,
+                             n_recomputed=0, full_recompute=False)
+    return DiscordScan(merged, per_length)
+
+
+def compute_matrix_profile(series, length: int, p: int, m_track: int = 0,
+                           threads: int = 1) -> ProfileResult:
+    """Exact matrix profile at one length (partials are not materialised)."""
+    series = as_series(series)
+    if length < 4 or 2 * length > series.n:
+        raise SeriesTooShortError(f"need 4 <= length <= n/2 (length={length}, n={series.n})")
+    if p < 1:
+        raise InvalidParametersError("p must be at least 1")
+    if m_track > 1:
+        raise InvalidParametersError("m_track > 1 is not implemented on the GPU path")
+    _check_profile_length(series, length)
+    run = GpuRun(series, length, length)
+    mp, ip = run.profile(length)
+    best_m = best_nbr = None
+    if m_track == 1:
+        best_m = mp[:, None].copy()
+        best_nbr = ip[:, None].copy()
+    return ProfileResult(MatrixProfile(mp, ip, length), None, best_m, best_nbr)
+
+
+def motifs_per_length(series, lmin: int, lmax: int, k: int):
+    """Per length, the k best distinct canonical pairs [(a, b, d), ...] keyed
+    (d*sqrt(1/l), l, a, b) -- BASELINE.md decision 1."""
+    series = as_series(series)
+    validate_range(series, lmin, lmax)
+    _check_profile_length(series, lmin)
+    if k < 1 or 2 * k > 64:
+        raise InvalidParametersError("k must be in [1, 32]")
+    run = GpuRun(series, lmin, lmax)
+    return _topk_from_rows(run, k)
+
+
+def _topk_from_rows(run: GpuRun, k: int):
+    off, nbr, d = run.smallest_rows(2 * k)
+    out = {}
+    for li in range(run.lmax - run.lmin + 1):
+        best = {}
+        for q in range(off.shape[1]):
+            if off[li, q] < 0 or not np.isfinite(d[li, q]):
+                break
+            a, b = sorted((int(off[li, q]), int(nbr[li, q])))
+            if (a, b) not in best or d[li, q] < best[(a, b)]:
+                best[(a, b)] = float(d[li, q])
+        items = sorted(((dv, a, b) for (a, b), dv in best.items()))
+        out[run.lmin + li] = [(a, b, dv) for dv, a, b in items[:k]]
+    return out

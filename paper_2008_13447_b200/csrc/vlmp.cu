@@ -1,0 +1,1175 @@
+// vlmp.cu -- B200 (sm_100a) variable-length z-normalised matrix profile.
+//
+// Hot path of arxiv 2008.13447 (MAD/VALMOD), rebuilt for the GPU: the exact
+// matrix profile of one series at every window length in [lmin, lmax], from
+// which VALMP, per-length motifs and discords are read off. Replaces the
+// reference's per-length STOMP scan (profile.py:288-377) and its drivers
+// (valmod.py:192-289, discords.py:144-247). See DESIGN.md for the derivations.
+//
+// Layout and kernels (all FP64, CUDA cores; no tensor cores -- not a contraction):
+//   k_params      per length: window mean/std from the host's prefix sums with the
+//                 reference's exact op order (series.py:91-100), and the SCAMP-style
+//                 recurrence factors df, dg, inv = 1/(sigma*sqrt(m)) (NaN = invalid),
+//                 stored D-interleaved ("permuted") so a warp's per-lane column
+//                 streams are coalesced.
+//   k_bound       per length > first: an upper bound U[o] on offset o's exact key
+//                 r' = 1 - corr, from the previous length's neighbours (+margin).
+//   k_tile<FULL>  one warp = one tile: 256 consecutive diagonals x S rows. Each lane
+//                 owns D=8 diagonals, walks rows with the covariance recurrence
+//                 cov(i,j) = cov(i-1,j-1) + df_i dg_j + df_j dg_i   (2 DFMA)
+//                 r' = 1 - cov * inv_i * inv_j                     (DMUL + DFMA)
+//                 FULL=false: a cell only needs 2 FSETP against U's high word
+//                 (ALU pipe); the rare passing cells merge (key,index) exactly with
+//                 a 128-bit CAS. FULL=true (first length): exact folds with packed
+//                 8-bit diagonal indices, warp-reduced rows, lane-travelling columns.
+//                 Seeds (cov at the tile's first row) are extended to the next
+//                 length with the Welford co-moment update.
+//   k_finalize    exact canonical pair distance of each winner (series.py:169-194).
+//   k_valmp, k_smallest, k_discords, k_events: read-offs (valmod.py:57-73,170-177;
+//                 discords.py:68-93; motifsets.py:105-117).
+
+#include <cuda_runtime.h>
+#include <stdint.h>
+#include <stdio.h>
+#include <string.h>
+#include <math.h>
+
+#include <algorithm>
+#include <mutex>
+#include <string>
+#include <vector>
+
+#include "../../include/vlmp.h"
+
+namespace {
+
+constexpr int D = 8;              // diagonals per lane
+constexpr int BAND = 32 * D;      // diagonals per warp tile
+constexpr int WARPS_PER_CTA = 4;
+constexpr unsigned FULLMASK = 0xffffffffu;
+constexpr unsigned long long KEY_NONE = 0x7FF0000000000000ull;   // bits of +inf
+constexpr long long IDX_NONE = 0x7FFFFFFFFFFFFFFFll;
+
+thread_local std::string g_err;
+
+int fail(int code, const std::string& msg) { g_err = msg; return code; }
+
+#define CU(call)                                                                   \
+    do {                                                                           \
+        cudaError_t e_ = (call);                                                   \
+        if (e_ != cudaSuccess)                                                     \
+            return fail(VLMP_E_CUDA, std::string(#call) + ": " + cudaGetErrorString(e_)); \
+    } while (0)
+
+__host__ __device__ inline long long pidx(long long x, long long P) { return (x & (D - 1)) * P + (x >> 3); }
+
+// ---------------------------------------------------------------------------------
+// exact window statistics (series.py:91-100): no contraction, numpy op order
+__device__ inline void win_stats(const double* __restrict__ cum, const double* __restrict__ cum2,
+                                 long long o, int m, double& mu, double& sd) {
+    double s = __dsub_rn(cum[o + m], cum[o]);
+    double ss = __dsub_rn(cum2[o + m], cum2[o]);
+    double L = (double)m;
+    double u = __ddiv_rn(s, L);
+    double var = __dsub_rn(__ddiv_rn(ss, L), __dmul_rn(u, u));
+    if (!(var >= 0.0)) var = 0.0;
+    mu = u;
+    sd = __dsqrt_rn(var);
+}
+
+// series.py:81-89 (stats: sigma = sqrt(var) if var > 0 else 0) -- used by pair_distance
+__device__ inline void win_stats_pd(const double* __restrict__ cum, const double* __restrict__ cum2,
+                                    long long o, int m, double& mu, double& sd) {
+    double s = __dsub_rn(cum[o + m], cum[o]);
+    double ss = __dsub_rn(cum2[o + m], cum2[o]);
+    double L = (double)m;
+    double u = __ddiv_rn(s, L);
+    double var = __dsub_rn(__ddiv_rn(ss, L), __dmul_rn(u, u));
+    mu = u;
+    sd = var > 0.0 ? __dsqrt_rn(var) : 0.0;
+}
+
+// canonical pair distance (series.py:169-194): dot in (min,max) order, sequential sum
+__device__ double pair_distance(const double* __restrict__ t, const double* __restrict__ cum,
+                                const double* __restrict__ cum2, long long i, long long j, int m,
+                                double floor_) {
+    long long a = i <= j ? i : j, b = i <= j ? j : i;
+    double mua, sda, mub, sdb;
+    win_stats_pd(cum, cum2, a, m, mua, sda);
+    win_stats_pd(cum, cum2, b, m, mub, sdb);
+    if (sda < floor_ || sdb < floor_) return INFINITY;
+    double qt = 0.0;
+    for (int k = 0; k < m; ++k) qt = __dadd_rn(qt, __dmul_rn(t[a + k], t[b + k]));
+    double L = (double)m;
+    double num = __dsub_rn(qt, __dmul_rn(__dmul_rn(L, mua), mub));
+    double den = __dmul_rn(__dmul_rn(L, sda), sdb);
+    double rad = __dmul_rn(__dmul_rn(2.0, L), __dsub_rn(1.0, __ddiv_rn(num, den)));
+    return rad > 0.0 ? __dsqrt_rn(rad) : 0.0;
+}
+
+// ---------------------------------------------------------------------------------
+struct ParamArgs {
+    const double* tn; const double* cum; const double* cum2;
+    double* df; double* dg; double* inv; double* mu;
+    long long n, N, A, P; int m; double floor_;
+};
+
+// per-length recurrence factors, permuted layout
+__global__ void k_params(ParamArgs a) {
+    long long o = blockIdx.x * (long long)blockDim.x + threadIdx.x;
+    if (o >= a.A) return;
+    const int m = a.m;
+    double mu_o = 0.0, sd_o = 0.0, mu_p = 0.0, sd_p = 0.0;
+    if (o < a.N) win_stats(a.cum, a.cum2, o, m, mu_o, sd_o);
+    if (o >= 1 && o - 1 < a.N) win_stats(a.cum, a.cum2, o - 1, m, mu_p, sd_p);
+    double inv = __longlong_as_double(0x7FF8000000000000ll);   // NaN: invalid window
+    if (o < a.N && sd_o >= a.floor_) inv = 1.0 / (sd_o * sqrt((double)m));
+    double df = 0.0, dg = 0.0;
+    if (o >= 1) {
+        double tl = a.tn[o + m - 1], tp = a.tn[o - 1];
+        df = (tl - tp) * 0.5;
+        dg = (tl - mu_o) + (tp - mu_p);
+    }
+    long long q = pidx(o, a.P);
+    a.df[q] = df; a.dg[q] = dg; a.inv[q] = inv; a.mu[q] = mu_o;
+}
+
+// ---------------------------------------------------------------------------------
+// bound U[o] >= the kernel's key of o's best cell, from the previous length's winners
+struct BoundArgs {
+    const double* tn; const double* mu; const double* inv;   // permuted (this length)
+    const long long* prev_idx;                              // natural, previous length winners
+    float* Uf;                                              // permuted
+    long long N, Nprev, A, P; int m, e; double margin;
+};
+
+__device__ inline double cell_key(const double* __restrict__ tn, long long o, long long c, int m,
+                                  double mo, double mc, double io, double ic) {
+    double cov = 0.0;
+    for (int k = 0; k < m; ++k) cov = fma(tn[o + k] - mo, tn[c + k] - mc, cov);
+    return fma(-(cov * io), ic, 1.0);
+}
+
+__global__ void k_bound(BoundArgs a) {
+    long long o = blockIdx.x * (long long)blockDim.x + threadIdx.x;
+    if (o >= a.A) return;
+    float out = -INFINITY;
+    if (o < a.N) {
+        long long qo = pidx(o, a.P);
+        double io = a.inv[qo];
+        if (io == io) {   // valid row
+            double mo = a.mu[qo];
+            long long cand[4];
+            int nc = 0;
+            long long c1 = (o < a.Nprev) ? a.prev_idx[o] : -1;
+            if (c1 >= 0 && c1 < IDX_NONE) { cand[nc++] = c1; cand[nc++] = c1 > o ? c1 + 1 : c1 - 1; }
+            if (o >= 1 && o - 1 < a.Nprev) { long long c = a.prev_idx[o - 1]; if (c >= 0 && c < IDX_NONE) cand[nc++] = c + 1; }
+            if (o + 1 < a.Nprev) { long long c = a.prev_idx[o + 1]; if (c >= 0 && c < IDX_NONE) cand[nc++] = c - 1; }
+            double best = INFINITY;
+            for (int q = 0; q < nc; ++q) {
+                long long c = cand[q];
+                bool dup = false;
+                for (int r = 0; r < q; ++r) dup |= (cand[r] == c);
+                if (dup || c < 0 || c >= a.N) continue;
+                long long dd = c > o ? c - o : o - c;
+                if (dd < a.e) continue;
+                long long qc = pidx(c, a.P);
+                double ic = a.inv[qc];
+                if (!(ic == ic)) continue;
+                double r = cell_key(a.tn, o, c, a.m, mo, a.mu[qc], io, ic);
+                best = fmin(best, r);
+            }
+            if (best < INFINITY) {
+                double U = fmax(best, 0.0) + a.margin;
+                out = __int_as_float(__double2hiint(U));   // x <= U  =>  hi(x) <= hi(U)
+            } else {
+                out = INFINITY;   // no bound: every cell of this offset is a candidate
+            }
+        }
+    }
+    a.Uf[pidx(o, a.P)] = out;
+}
+
+// ---------------------------------------------------------------------------------
+struct TileArgs {
+    const double* df; const double* dg; const double* inv; const float* Uf; const double* mu;
+    const double* tn;
+    const int2* tiles;
+    double* seeds;
+    ulonglong2* acc;               // this length's accumulators, natural offsets
+    unsigned long long* counters;  // [0] slow-path merges
+    long long P, N, dlo;
+    int n_tiles, S, m, e, update_seeds;
+};
+
+__device__ inline bool key_less(unsigned long long k1, long long i1, unsigned long long k2, long long i2) {
+    return k1 < k2 || (k1 == k2 && i1 < i2);
+}
+
+// exact lexicographic (key, idx) min into a 16-byte accumulator (128-bit CAS)
+__device__ void acc_merge(ulonglong2* slot, unsigned long long key, long long idx) {
+    unsigned __int128* p = reinterpret_cast<unsigned __int128*>(slot);
+    const volatile unsigned long long* vp = reinterpret_cast<volatile unsigned long long*>(slot);
+    unsigned __int128 cur = ((unsigned __int128)vp[1] << 64) | vp[0];
+    const unsigned __int128 want = ((unsigned __int128)(unsigned long long)idx << 64) | key;
+    while (key_less(key, idx, (unsigned long long)cur, (long long)(cur >> 64))) {
+        unsigned __int128 prev = atomicCAS(p, cur, want);
+        if (prev == cur) return;
+        cur = prev;
+    }
+}
+
+__device__ inline unsigned long long clamp_key(double r) {
+    return r < 0.0 ? 0ull : (unsigned long long)__double_as_longlong(r);
+}
+
+__device__ inline double pack_low8(double v, unsigned idx8) {
+    int lo = __double2loint(v), hi = __double2hiint(v);
+    lo = (lo & (int)0xFFFFFF00) | (int)idx8;
+    return __hiloint2double(hi, lo);
+}
+
+template <bool FULL, bool MASKED>
+__global__ void __launch_bounds__(WARPS_PER_CTA * 32)
+k_tile(TileArgs a) {
+    const int lane = threadIdx.x & 31;
+    const int wid = blockIdx.x * WARPS_PER_CTA + (threadIdx.x >> 5);
+    if (wid >= a.n_tiles) return;
+    const int2 tl = a.tiles[wid];
+    const long long d0 = a.dlo + (long long)tl.x * BAND;
+    const long long i0 = (long long)tl.y * a.S;
+    const long long rows_valid = a.N - d0 - i0;
+    if (rows_valid <= 0) return;
+    const long long P = a.P;
+    const int dbase = lane * D;
+    const long long cbase = i0 + d0 + dbase;   // column of slot 0 at row i0
+
+    bool sval[D];
+#pragma unroll
+    for (int s = 0; s < D; ++s) sval[s] = !MASKED || (d0 + dbase + s >= a.e);
+
+    double cov[D];
+    double* seedp = a.seeds + (long long)wid * BAND + dbase;
+#pragma unroll
+    for (int s = 0; s < D; ++s) cov[s] = seedp[s];
+
+    // Welford co-moment update of the seeds to length m+1:
+    // C_{m+1} = C_m + m/(m+1) * (x_m - mean_m(x)) * (y_m - mean_m(y))
+    if (a.update_seeds) {
+        const double w = (double)a.m / (double)(a.m + 1);
+        const double xi = (a.tn[i0 + a.m] - a.mu[pidx(i0, P)]) * w;
+#pragma unroll
+        for (int s = 0; s < D; ++s) {
+            long long c = cbase + s;
+            seedp[s] = fma(xi, a.tn[c + a.m] - a.mu[pidx(c, P)], cov[s]);
+        }
+    }
+
+    double cdf[D], cdg[D], cinv[D];
+    float cU[D];
+#pragma unroll
+    for (int s = 0; s < D; ++s) {
+        long long q = pidx(cbase + s, P);
+        cdf[s] = a.df[q]; cdg[s] = a.dg[q]; cinv[s] = a.inv[q];
+        cU[s] = FULL ? 0.f : a.Uf[q];
+    }
+    double colacc[D];
+    if (FULL) {
+#pragma unroll
+        for (int s = 0; s < D; ++s) colacc[s] = INFINITY;
+    }
+    double rowres = INFINITY, colres = INFINITY;   // FULL: per-group parallel merges
+    long long rowres_i = 0, colres_j = 0;
+    unsigned long long nmerge = 0;
+
+    const int S = a.S;
+    const int nrows = (int)(rows_valid < S ? rows_valid : S);
+    const int ngroups = (nrows - 1 + D - 1) / D;
+
+    // one row step: k = phys offset of logical slot 0; first = peeled first row
+    auto row_step = [&](long long i, int k, bool first) {
+        const long long qi = pidx(i, P);
+        const double rinv = a.inv[qi];
+        const float rU = FULL ? 0.f : a.Uf[qi];
+        if (!first) {
+            const int pn = (k + D - 1) & (D - 1);
+            const long long q = pidx(i + d0 + dbase + D - 1, P);
+            cdf[pn] = a.df[q]; cdg[pn] = a.dg[q]; cinv[pn] = a.inv[q];
+            if (!FULL) cU[pn] = a.Uf[q];
+            const double rdf = a.df[qi], rdg = a.dg[qi];
+#pragma unroll
+            for (int s = 0; s < D; ++s) {
+                const int p = (s + k) & (D - 1);
+                cov[s] = fma(rdf, cdg[p], cov[s]);
+                cov[s] = fma(cdf[p], rdg, cov[s]);
+            }
+        }
+        double r[D];
+#pragma unroll
+        for (int s = 0; s < D; ++s) {
+            const int p = (s + k) & (D - 1);
+            r[s] = fma(-(cov[s] * rinv), cinv[p], 1.0);
+        }
+        if (!FULL) {
+            bool pass = false;
+#pragma unroll
+            for (int s = 0; s < D; ++s) {
+                const int p = (s + k) & (D - 1);
+                const float h = __int_as_float(__double2hiint(r[s]));
+                pass |= sval[s] && ((h <= rU) | (h <= cU[p]));
+            }
+            if (__any_sync(FULLMASK, pass)) {
+#pragma unroll
+                for (int s = 0; s < D; ++s) {
+                    const int p = (s + k) & (D - 1);
+                    const float h = __int_as_float(__double2hiint(r[s]));
+                    const bool pr = sval[s] && (h <= rU), pc = sval[s] && (h <= cU[p]);
+                    if (pr | pc) {
+                        const unsigned long long key = clamp_key(r[s]);
+                        const long long j = i + d0 + dbase + s;
+                        if (pr) acc_merge(a.acc + i, key, j);
+                        if (pc) acc_merge(a.acc + j, key, i);
+                        nmerge += (unsigned)pr + (unsigned)pc;
+                    }
+                }
+            }
+        } else {
+            // rows: lane-local packed min, then warp all-reduce (packed diag index => no exact ties)
+            double rm = INFINITY;
+#pragma unroll
+            for (int s = 0; s < D; ++s) {
+                double v = r[s] < 0.0 ? 0.0 : r[s];     // clamp (NaN stays NaN)
+                if (!sval[s]) v = __longlong_as_double(0x7FF8000000000000ll);
+                const double pr = pack_low8(v, (unsigned)(dbase + s));
+                const double pc = pack_low8(v, (unsigned)(255 - (dbase + s)));
+                rm = pr < rm ? pr : rm;
+                const int p = (s + k) & (D - 1);
+                colacc[p] = pc < colacc[p] ? pc : colacc[p];
+            }
+#pragma unroll
+            for (int off = 16; off >= 1; off >>= 1) {
+                const double o = __shfl_xor_sync(FULLMASK, rm, off);
+                rm = o < rm ? o : rm;
+            }
+            // the exiting column (logical slot 0, phys k) travels to lane-1's slot D-1
+            const double x = colacc[k];
+            double y = __shfl_down_sync(FULLMASK, x, 1);
+            if (lane == 31) y = INFINITY;
+            colacc[k] = y;
+            const double x0 = __shfl_sync(FULLMASK, x, 0);   // lane 0's exiting column
+            // stash: lane ((i - i0 - 1) mod 32) keeps this row's result and the exiting column's;
+            // the warp merges 32 stashed results in parallel every 4 groups (flush_full)
+            const int slot = first ? 0 : (int)((i - i0 - 1) & 31);
+            if (lane == slot) { rowres = rm; rowres_i = i; colres = x0; colres_j = i + d0; }
+        }
+    };
+
+    auto flush_full = [&]() {
+        if (rowres < INFINITY) {
+            const unsigned long long b = (unsigned long long)__double_as_longlong(rowres);
+            acc_merge(a.acc + rowres_i, b & ~0xFFull, rowres_i + d0 + (long long)(b & 0xFFull));
+        }
+        if (colres < INFINITY) {
+            const unsigned long long b = (unsigned long long)__double_as_longlong(colres);
+            const long long diag = 255 - (long long)(b & 0xFFull);
+            acc_merge(a.acc + colres_j, b & ~0xFFull, colres_j - d0 - diag);
+        }
+        rowres = INFINITY; colres = INFINITY;
+    };
+
+    // peeled first row (cov = seed)
+    row_step(i0, 0, true);
+    if (FULL) flush_full();
+    long long i = i0 + 1;
+    for (int g = 0; g < ngroups; ++g) {
+#pragma unroll
+        for (int kk = 0; kk < D; ++kk) {
+            row_step(i, (kk + 1) & (D - 1), false);
+            ++i;
+        }
+        if (FULL && (g & 3) == 3) flush_full();
+    }
+    if (FULL) {
+        flush_full();
+        // remaining column accumulators: after the last row (phys offset kl), phys p holds the
+        // column of logical slot ((p - kl - 1) mod D) at row i (= last + 1)
+        const int kl = (ngroups * D) & (D - 1);   // phys offset of the last processed row
+#pragma unroll
+        for (int p = 0; p < D; ++p) {
+            const double v = colacc[p];
+            if (v < INFINITY) {
+                const int s = (p - kl - 1 + 2 * D) & (D - 1);
+                const long long j = i + d0 + dbase + s;
+                const unsigned long long b = (unsigned long long)__double_as_longlong(v);
+                const long long diag = 255 - (long long)(b & 0xFFull);
+                acc_merge(a.acc + j, b & ~0xFFull, j - d0 - diag);
+            }
+        }
+    }
+    if (!FULL && nmerge) atomicAdd(a.counters, nmerge);
+}
+
+// initial seeds: centred direct sums at the first length
+struct SeedArgs {
+    const double* tn; const double* mu; const int2* tiles; double* seeds;
+    long long P, dlo; int n_tiles, S, m;
+};
+
+__global__ void k_seed_init(SeedArgs a) {
+    const int lane = threadIdx.x & 31;
+    const int wid = blockIdx.x * WARPS_PER_CTA + (threadIdx.x >> 5);
+    if (wid >= a.n_tiles) return;
+    const int2 tl = a.tiles[wid];
+    const long long d0 = a.dlo + (long long)tl.x * BAND;
+    const long long i0 = (long long)tl.y * a.S;
+    const double mi = a.mu[pidx(i0, a.P)];
+    double acc[D], mc[D];
+    const long long cb = i0 + d0 + lane * D;
+#pragma unroll
+    for (int s = 0; s < D; ++s) { acc[s] = 0.0; mc[s] = a.mu[pidx(cb + s, a.P)]; }
+    for (int k = 0; k < a.m; ++k) {
+        const double x = a.tn[i0 + k] - mi;
+#pragma unroll
+        for (int s = 0; s < D; ++s) acc[s] = fma(x, a.tn[cb + s + k] - mc[s], acc[s]);
+    }
+    double* sp = a.seeds + (long long)wid * BAND + lane * D;
+#pragma unroll
+    for (int s = 0; s < D; ++s) sp[s] = acc[s];
+}
+
+__global__ void k_fill_acc(ulonglong2* acc, long long n) {
+    long long o = blockIdx.x * (long long)blockDim.x + threadIdx.x;
+    if (o < n) acc[o] = make_ulonglong2(KEY_NONE, (unsigned long long)IDX_NONE);
+}
+
+// previous-length winner indices (for the bound) straight from the accumulators
+__global__ void k_acc_idx(const ulonglong2* acc, long long* idx, long long n) {
+    long long o = blockIdx.x * (long long)blockDim.x + threadIdx.x;
+    if (o < n) { ulonglong2 v = acc[o]; idx[o] = v.x == KEY_NONE ? -1 : (long long)v.y; }
+}
+
+// ---------------------------------------------------------------------------------
+struct FinArgs {
+    const double* tn; const double* cum; const double* cum2;
+    const ulonglong2* acc;      // [n_len][A]
+    double* mp; int* ip;        // [n_len][A]
+    long long n, A; int lmin, n_len; double floor_;
+};
+
+__global__ void k_finalize(FinArgs a) {
+    const long long o = blockIdx.x * (long long)blockDim.x + threadIdx.x;
+    const int li = blockIdx.y;
+    const int m = a.lmin + li;
+    const long long N = a.n - m + 1;
+    if (o >= N) return;
+    const ulonglong2 v = a.acc[(long long)li * a.A + o];
+    double d = INFINITY; int j = -1;
+    if (v.x != KEY_NONE) {
+        j = (int)v.y;
+        d = pair_distance(a.tn, a.cum, a.cum2, o, j, m, a.floor_);
+    }
+    a.mp[(long long)li * a.A + o] = d;
+    a.ip[(long long)li * a.A + o] = j;
+}
+
+struct ValmpArgs {
+    const double* mp; const int* ip;
+    double* dist; double* norm; long long* len; long long* idx; unsigned char* pop;
+    long long n, A; int lmin, n_len;
+};
+
+// valmod.py:57-73: lnorm = mp * sqrt(1/length); strict improvement, ascending lengths
+__global__ void k_valmp(ValmpArgs a) {
+    const long long o = blockIdx.x * (long long)blockDim.x + threadIdx.x;
+    const long long n0 = a.n - a.lmin + 1;
+    if (o >= n0) return;
+    double bd = INFINITY, bn = INFINITY; long long bl = 0, bi = -1; bool pop = false;
+    for (int li = 0; li < a.n_len; ++li) {
+        const int m = a.lmin + li;
+        if (o > a.n - m) break;
+        const double mpv = a.mp[(long long)li * a.A + o];
+        const double ln = __dmul_rn(mpv, __dsqrt_rn(__ddiv_rn(1.0, (double)m)));
+        if (ln < INFINITY && (!pop || bn > ln)) {
+            bd = mpv; bn = ln; bl = m; bi = a.ip[(long long)li * a.A + o]; pop = true;
+        }
+    }
+    a.dist[o] = bd; a.norm[o] = bn; a.len[o] = bl; a.idx[o] = bi; a.pop[o] = pop ? 1 : 0;
+}
+
+// per length: the K smallest (mp, offset) rows (K <= 64), block-wide selection
+struct SmallArgs {
+    const double* mp; const int* ip; long long* off; long long* nbr; double* d;
+    long long n, A; int lmin, K;
+};
+
+__device__ inline bool row_less(double d1, long long o1, double d2, long long o2) {
+    return d1 < d2 || (d1 == d2 && o1 < o2);
+}
+
+__global__ void k_smallest(SmallArgs a) {
+    constexpr int T = 256, KMAX = 64;
+    const int li = blockIdx.x;
+    const int m = a.lmin + li;
+    const long long N = a.n - m + 1;
+    const double* mp = a.mp + (long long)li * a.A;
+    // each thread: local sorted list of K
+    double ld[KMAX]; long long lo[KMAX];
+    const int K = a.K;
+    for (int q = 0; q < K; ++q) { ld[q] = INFINITY; lo[q] = -1; }
+    for (long long o = threadIdx.x; o < N; o += T) {
+        const double v = mp[o];
+        if (!(v < INFINITY)) continue;
+        if (!row_less(v, o, ld[K - 1], lo[K - 1] < 0 ? (1ll << 62) : lo[K - 1])) continue;
+        int q = K - 1;
+        while (q > 0 && row_less(v, o, ld[q - 1], lo[q - 1] < 0 ? (1ll << 62) : lo[q - 1])) {
+            ld[q] = ld[q - 1]; lo[q] = lo[q - 1]; --q;
+        }
+        ld[q] = v; lo[q] = o;
+    }
+    __shared__ double sd[T];
+    __shared__ long long so[T];
+    // merge: repeated K rounds of block argmin over heads (K small)
+    __shared__ int head[T];
+    head[threadIdx.x] = 0;
+    __syncthreads();
+    for (int q = 0; q < K; ++q) {
+        const int h = head[threadIdx.x];
+        double v = h < K ? ld[h] : INFINITY;
+        long long ov = h < K ? lo[h] : -1;
+        if (ov < 0) v = INFINITY;
+        sd[threadIdx.x] = v; so[threadIdx.x] = ov < 0 ? (1ll << 62) : ov;
+        __syncthreads();
+        for (int w = T / 2; w >= 1; w >>= 1) {
+            if (threadIdx.x < w) {
+                if (row_less(sd[threadIdx.x + w], so[threadIdx.x + w], sd[threadIdx.x], so[threadIdx.x])) {
+                    sd[threadIdx.x] = sd[threadIdx.x + w]; so[threadIdx.x] = so[threadIdx.x + w];
+                }
+            }
+            __syncthreads();
+        }
+        const double bv = sd[0]; const long long bo = so[0];
+        __syncthreads();
+        if (bv < INFINITY && ov == bo) head[threadIdx.x] = h + 1;
+        if (threadIdx.x == 0) {
+            const long long dst = (long long)li * K + q;
+            if (bv < INFINITY) { a.off[dst] = bo; a.nbr[dst] = a.ip[(long long)li * a.A + bo]; a.d[dst] = bv; }
+            else { a.off[dst] = -1; a.nbr[dst] = -1; a.d[dst] = INFINITY; }
+        }
+        __syncthreads();
+    }
+}
+
+// per length: top-k 1st discords, ascending-offset greedy replay (discords.py:68-93,
+// :48-50, oracle.py:137-145) with the exact prefilter d > dist[k-1]; one warp per length
+struct DiscArgs {
+    const double* mp; double* out_d; long long* out_o;
+    long long n, A; int lmin, n_len, k;
+};
+
+__global__ void k_discords(DiscArgs a) {
+    const int lane = threadIdx.x & 31;
+    const int li = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
+    if (li >= a.n_len) return;
+    const int m = a.lmin + li;
+    const long long N = a.n - m + 1;
+    const long long e = (m + 1) / 2;
+    const double* mp = a.mp + (long long)li * a.A;
+    constexpr int KMAX = 32;
+    double cd[KMAX]; long long co[KMAX];
+    const int k = a.k;
+    for (int r = 0; r < k; ++r) { cd[r] = -INFINITY; co[r] = -1; }
+    for (long long base = 0; base < N; base += 32) {
+        const long long o = base + lane;
+        const double d = o < N ? mp[o] : INFINITY;
+        const double thr = cd[k - 1];
+        bool cand = (d < INFINITY) && (d > thr);
+        unsigned bal = __ballot_sync(FULLMASK, cand);
+        while (bal) {
+            const int src = __ffs(bal) - 1;
+            bal &= bal - 1;
+            const double dv = __shfl_sync(FULLMASK, d, src);
+            const long long ov = base + src;
+            bool triv = false;
+            for (int r = 0; r < k; ++r) triv |= (co[r] >= 0 && llabs(ov - co[r]) < e);
+            if (triv) continue;
+            for (int r = 0; r < k; ++r) {
+                if (dv > cd[r]) {
+                    for (int q = k - 1; q > r; --q) { cd[q] = cd[q - 1]; co[q] = co[q - 1]; }
+                    cd[r] = dv; co[r] = ov;
+                    break;
+                }
+            }
+        }
+    }
+    if (lane == 0) {
+        for (int r = 0; r < k; ++r) { a.out_d[(long long)li * k + r] = cd[r]; a.out_o[(long long)li * k + r] = co[r]; }
+    }
+}
+
+// VALMP improvement events with norm <= tau (motifsets.py:105-117 stream)
+struct EvArgs {
+    const double* mp; const int* ip; double tau;
+    long long* ev_off; long long* ev_nbr; long long* ev_len; double* ev_d; double* ev_n;
+    unsigned long long* count; long long cap;
+    long long n, A; int lmin, n_len;
+};
+
+__global__ void k_events(EvArgs a) {
+    const long long o = blockIdx.x * (long long)blockDim.x + threadIdx.x;
+    const long long n0 = a.n - a.lmin + 1;
+    if (o >= n0) return;
+    double bn = INFINITY; bool pop = false;
+    for (int li = 0; li < a.n_len; ++li) {
+        const int m = a.lmin + li;
+        if (o > a.n - m) break;
+        const double mpv = a.mp[(long long)li * a.A + o];
+        const double ln = __dmul_rn(mpv, __dsqrt_rn(__ddiv_rn(1.0, (double)m)));
+        if (ln < INFINITY && (!pop || bn > ln)) {
+            bn = ln; pop = true;
+            if (ln <= a.tau) {
+                const unsigned long long q = atomicAdd(a.count, 1ull);
+                if ((long long)q < a.cap) {
+                    a.ev_off[q] = o; a.ev_nbr[q] = a.ip[(long long)li * a.A + o]; a.ev_len[q] = m;
+                    a.ev_d[q] = mpv; a.ev_n[q] = ln;
+                }
+            }
+        }
+    }
+}
+
+// partial export / mask / import for the multi-GPU exact merge
+__global__ void k_export(const ulonglong2* acc, unsigned long long* keys, long long* idx, long long total) {
+    long long q = blockIdx.x * (long long)blockDim.x + threadIdx.x;
+    if (q < total) { ulonglong2 v = acc[q]; keys[q] = v.x; idx[q] = (long long)v.y; }
+}
+__global__ void k_mask_idx(const unsigned long long* merged, const unsigned long long* keys, long long* idx, long long total) {
+    long long q = blockIdx.x * (long long)blockDim.x + threadIdx.x;
+    if (q < total && keys[q] != merged[q]) idx[q] = IDX_NONE;
+}
+__global__ void k_import(ulonglong2* acc, const unsigned long long* keys, const long long* idx, long long total) {
+    long long q = blockIdx.x * (long long)blockDim.x + threadIdx.x;
+    if (q < total) acc[q] = make_ulonglong2(keys[q], (unsigned long long)idx[q]);
+}
+
+// FP64 FMA peak: 8 independent chains per thread
+__global__ void k_dfma_peak(double* out, int iters, double x) {
+    double a0 = x, a1 = x + 1, a2 = x + 2, a3 = x + 3, a4 = x + 4, a5 = x + 5, a6 = x + 6, a7 = x + 7;
+    const double b = 0.999999, c = 1e-9;
+    for (int it = 0; it < iters; ++it) {
+#pragma unroll
+        for (int u = 0; u < 16; ++u) {
+            a0 = fma(a0, b, c); a1 = fma(a1, b, c); a2 = fma(a2, b, c); a3 = fma(a3, b, c);
+            a4 = fma(a4, b, c); a5 = fma(a5, b, c); a6 = fma(a6, b, c); a7 = fma(a7, b, c);
+        }
+    }
+    double s = a0 + a1 + a2 + a3 + a4 + a5 + a6 + a7;
+    if (s == 12345.678) out[0] = s;
+}
+
+}  // namespace
+
+// =================================================================================
+struct vlmp_session {
+    int device = 0;
+    cudaStream_t stream = nullptr;
+    cudaEvent_t ev[8] = {};
+    std::mutex lock;
+    // series
+    long long n = 0, A = 0, P = 0;
+    double floor_ = 0.0;
+    double* d_tn = nullptr; double* d_cum = nullptr; double* d_cum2 = nullptr;
+    // per-length scratch
+    double* d_df = nullptr; double* d_dg = nullptr; double* d_inv = nullptr; double* d_mu = nullptr;
+    float* d_Uf = nullptr;
+    long long* d_previdx = nullptr;
+    // tiles / seeds
+    int2* d_tiles = nullptr; size_t tiles_cap = 0;
+    double* d_seeds = nullptr; size_t seeds_cap = 0;
+    // accumulators [n_len][A]
+    ulonglong2* d_acc = nullptr; size_t acc_cap = 0;
+    double* d_mp = nullptr; int* d_ip = nullptr; size_t mp_cap = 0;
+    unsigned long long* d_counters = nullptr;
+    // valmp
+    double* d_vdist = nullptr; double* d_vnorm = nullptr; long long* d_vlen = nullptr;
+    long long* d_vidx = nullptr; unsigned char* d_vpop = nullptr; size_t v_cap = 0;
+    // run state
+    int lmin = 0, lmax = 0, n_len = 0; bool have_profile = false, have_final = false;
+    double stats[16] = {};
+    std::vector<cudaEvent_t> lev;   // 2 per length: tile-kernel start/stop
+};
+
+namespace {
+
+template <class T>
+int ensure(T*& p, size_t& cap, size_t count) {
+    if (count <= cap && p) return 0;
+    if (p) cudaFree(p);
+    p = nullptr; cap = 0;
+    cudaError_t e = cudaMalloc((void**)&p, std::max<size_t>(count, 1) * sizeof(T));
+    if (e != cudaSuccess) return fail(VLMP_E_NOMEM, std::string("cudaMalloc: ") + cudaGetErrorString(e));
+    cap = count;
+    return 0;
+}
+
+template <class T>
+int ensure1(T*& p, size_t count) { size_t cap = 0; if (p) { cudaFree(p); p = nullptr; } return ensure(p, cap, count); }
+
+inline unsigned blocks(long long n, int t) { return (unsigned)((n + t - 1) / t); }
+
+int seg_rows(long long n) {
+    // S = 1 + G*D rows per tile; larger for longer series to bound the seed store
+    long long G = 128;
+    while ((1 + G * D) * 256 < n && G < 2048) G *= 2;
+    return (int)(1 + G * D);
+}
+
+long long dlo_for(int lmin) { return (lmin + 1) / 2; }
+
+long long n_bands_for(long long n, int lmin) {
+    long long N = n - lmin + 1;
+    long long dl = dlo_for(lmin);
+    return N - dl > 0 ? (N - dl + BAND - 1) / BAND : 0;
+}
+
+// work of band b summed over lengths: sum_l sum_{d in band, d >= e_l} (N_l - d)_+
+double band_work(long long n, int lmin, int lmax, long long b) {
+    double w = 0;
+    long long d_lo = dlo_for(lmin) + b * BAND, d_hi = d_lo + BAND;
+    for (int m = lmin; m <= lmax; ++m) {
+        long long N = n - m + 1, e = (m + 1) / 2;
+        long long lo = std::max(d_lo, e), hi = std::min(d_hi, N);
+        if (hi <= lo) continue;
+        // sum_{d=lo}^{hi-1} (N - d)
+        w += (double)(hi - lo) * (double)N - ((double)(lo + hi - 1) * (double)(hi - lo)) / 2.0;
+    }
+    return w;
+}
+
+}  // namespace
+
+extern "C" {
+
+const char* vlmp_last_error(void) { return g_err.c_str(); }
+
+int vlmp_create(vlmp_session** out, int device) {
+    if (!out) return fail(VLMP_E_INVALID_PARAMETERS, "null out");
+    int ndev = 0;
+    cudaError_t e = cudaGetDeviceCount(&ndev);
+    if (e != cudaSuccess || ndev == 0)
+        return fail(VLMP_E_CUDA, std::string("no CUDA device: ") + cudaGetErrorString(e));
+    if (device < 0 || device >= ndev) return fail(VLMP_E_INVALID_PARAMETERS, "bad device id");
+    CU(cudaSetDevice(device));
+    cudaDeviceProp prop;
+    CU(cudaGetDeviceProperties(&prop, device));
+    if (prop.major != 10) return fail(VLMP_E_CUDA, "libvlmp is built for sm_100a (B200) only");
+    vlmp_session* s = new vlmp_session();
+    s->device = device;
+    CU(cudaStreamCreateWithFlags(&s->stream, cudaStreamNonBlocking));
+    for (auto& ev : s->ev) CU(cudaEventCreate(&ev));
+    CU(cudaMalloc((void**)&s->d_counters, 8 * sizeof(unsigned long long)));
+    *out = s;
+    return 0;
+}
+
+void vlmp_destroy(vlmp_session* s) {
+    if (!s) return;
+    cudaSetDevice(s->device);
+    cudaStreamSynchronize(s->stream);
+    void* ptrs[] = {s->d_tn, s->d_cum, s->d_cum2, s->d_df, s->d_dg, s->d_inv, s->d_mu, s->d_Uf,
+                    s->d_previdx, s->d_tiles, s->d_seeds, s->d_acc, s->d_mp, s->d_ip, s->d_counters, s->d_vdist, s->d_vnorm, s->d_vlen, s->d_vidx, s->d_vpop};
+    for (void* p : ptrs) if (p) cudaFree(p);
+    for (auto& ev : s->ev) if (ev) cudaEventDestroy(ev);
+    for (auto& ev : s->lev) cudaEventDestroy(ev);
+    if (s->stream) cudaStreamDestroy(s->stream);
+    delete s;
+}
+
+int vlmp_set_series(vlmp_session* s, const double* t, const double* cum, const double* cum2,
+                    int64_t n, double sigma_floor) {
+    if (!s || !t || !cum || !cum2) return fail(VLMP_E_INVALID_PARAMETERS, "null argument");
+    if (n <= 0) return fail(VLMP_E_EMPTY_SERIES, "series holds no points");
+    std::lock_guard<std::mutex> g(s->lock);
+    CU(cudaSetDevice(s->device));
+    long long A = ((n + 1024 + 255) / 256) * 256 + 256;
+    s->n = n; s->A = A; s->P = A / D; s->floor_ = sigma_floor;
+    int rc;
+    if ((rc = ensure1(s->d_tn, 2 * A + 4096))) return rc;
+    if ((rc = ensure1(s->d_cum, n + 1))) return rc;
+    if ((rc = ensure1(s->d_cum2, n + 1))) return rc;
+    if ((rc = ensure1(s->d_df, A))) return rc;
+    if ((rc = ensure1(s->d_dg, A))) return rc;
+    if ((rc = ensure1(s->d_inv, A))) return rc;
+    if ((rc = ensure1(s->d_mu, A))) return rc;
+    if ((rc = ensure1(s->d_Uf, A))) return rc;
+    if ((rc = ensure1(s->d_previdx, A))) return rc;
+    CU(cudaMemsetAsync(s->d_tn, 0, (2 * A + 4096) * sizeof(double), s->stream));
+    CU(cudaMemcpyAsync(s->d_tn, t, n * sizeof(double), cudaMemcpyHostToDevice, s->stream));
+    CU(cudaMemcpyAsync(s->d_cum, cum, (n + 1) * sizeof(double), cudaMemcpyHostToDevice, s->stream));
+    CU(cudaMemcpyAsync(s->d_cum2, cum2, (n + 1) * sizeof(double), cudaMemcpyHostToDevice, s->stream));
+    CU(cudaStreamSynchronize(s->stream));
+    s->have_profile = s->have_final = false;
+    return 0;
+}
+
+int vlmp_band_count(vlmp_session* s, int32_t lmin, int64_t* n_bands) {
+    if (!s || !n_bands) return fail(VLMP_E_INVALID_PARAMETERS, "null argument");
+    *n_bands = n_bands_for(s->n, lmin);
+    return 0;
+}
+
+int vlmp_band_split(vlmp_session* s, int32_t lmin, int32_t lmax, int32_t parts, int64_t* cuts) {
+    if (!s || !cuts || parts < 1) return fail(VLMP_E_INVALID_PARAMETERS, "bad band split arguments");
+    long long nb = n_bands_for(s->n, lmin);
+    std::vector<double> w(nb);
+    double tot = 0;
+    for (long long b = 0; b < nb; ++b) { w[b] = band_work(s->n, lmin, lmax, b); tot += w[b]; }
+    cuts[0] = 0;
+    double acc = 0; long long b = 0;
+    for (int p = 1; p < parts; ++p) {
+        double target = tot * p / parts;
+        while (b < nb && acc + w[b] <= target) acc += w[b++];
+        cuts[p] = b;
+    }
+    cuts[parts] = nb;
+    return 0;
+}
+
+int vlmp_profile_range(vlmp_session* s, int32_t lmin, int32_t lmax, int64_t band_lo,
+                       int64_t band_hi, uint32_t flags) {
+    if (!s) return fail(VLMP_E_INVALID_PARAMETERS, "null session");
+    if (s->n <= 0) return fail(VLMP_E_STATE, "no series uploaded");
+    if (lmin > lmax) return fail(VLMP_E_INVALID_PARAMETERS, "lmin > lmax");
+    if (lmin < 4) return fail(VLMP_E_INVALID_PARAMETERS, "minimum window length is 4");
+    if (s->n < (long long)lmax + (lmax + 1) / 2)
+        return fail(VLMP_E_SERIES_TOO_SHORT, "series cannot host a non-trivial pair at lmax");
+    std::lock_guard<std::mutex> g(s->lock);
+    CU(cudaSetDevice(s->device));
+    cudaStream_t st = s->stream;
+    const long long n = s->n, A = s->A, P = s->P;
+    const int n_len = lmax - lmin + 1;
+    const long long nb = n_bands_for(n, lmin);
+    if (band_hi < 0 || band_hi > nb) band_hi = nb;
+    if (band_lo < 0) band_lo = 0;
+    const int S = seg_rows(n);
+    const long long N0 = n - lmin + 1, dl = dlo_for(lmin);
+    // tile list (band-major) for this shard, using N at lmin (superset of later lengths)
+    std::vector<int2> tiles;
+    std::vector<long long> band_first;   // first tile index of each band in the shard
+    for (long long b = band_lo; b < band_hi; ++b) {
+        band_first.push_back((long long)tiles.size());
+        long long d0 = dl + b * BAND;
+        long long rows = N0 - d0;
+        for (long long sg = 0; sg * S < rows; ++sg) tiles.push_back(make_int2((int)b, (int)sg));
+    }
+    band_first.push_back((long long)tiles.size());
+    const long long T = (long long)tiles.size();
+    int rc;
+    if ((rc = ensure(s->d_tiles, s->tiles_cap, (size_t)std::max<long long>(T, 1)))) return rc;
+    if ((rc = ensure(s->d_seeds, s->seeds_cap, (size_t)std::max<long long>(T, 1) * BAND))) return rc;
+    if ((rc = ensure(s->d_acc, s->acc_cap, (size_t)n_len * A))) return rc;
+    if (T) CU(cudaMemcpyAsync(s->d_tiles, tiles.data(), T * sizeof(int2), cudaMemcpyHostToDevice, st));
+    k_fill_acc<<<blocks((long long)n_len * A, 256), 256, 0, st>>>(s->d_acc, (long long)n_len * A);
+    CU(cudaMemsetAsync(s->d_counters, 0, 8 * sizeof(unsigned long long), st));
+    CU(cudaEventRecord(s->ev[0], st));
+
+    double executed = 0, launches = 0, n_filtered = 0, n_full = 0, tile_ms = 0, klaunch = 2;
+    const double margin = 1.0 / (1 << 26);
+    for (int li = 0; li < n_len; ++li) {
+        const int m = lmin + li;
+        const long long N = n - m + 1;
+        const int e = (m + 1) / 2;
+        ParamArgs pa{s->d_tn, s->d_cum, s->d_cum2, s->d_df, s->d_dg, s->d_inv, s->d_mu, n, N, A, P, m, s->floor_};
+        k_params<<<blocks(A, 256), 256, 0, st>>>(pa);
+        ++klaunch;
+        const bool full = (li == 0) || (flags & VLMP_F_FULL_EVERY_LENGTH);
+        if (li == 0 && T) {
+            SeedArgs sa{s->d_tn, s->d_mu, s->d_tiles, s->d_seeds, P, dl, (int)T, S, m};
+            k_seed_init<<<blocks(T * 32, WARPS_PER_CTA * 32), WARPS_PER_CTA * 32, 0, st>>>(sa);
+            ++klaunch;
+        }
+        if (!full) {
+            k_acc_idx<<<blocks(N + 1, 256), 256, 0, st>>>(s->d_acc + (long long)(li - 1) * A, s->d_previdx, N + 1);
+            BoundArgs ba{s->d_tn, s->d_mu, s->d_inv, s->d_previdx, s->d_Uf, N, N + 1, A, P, m, e, margin};
+            k_bound<<<blocks(A, 128), 128, 0, st>>>(ba);
+            klaunch += 2;
+        }
+        // tiles: skip bands entirely inside the exclusion zone; masked = bands straddling it
+        long long b_skip = band_lo, b_mask = band_lo;
+        while (b_skip < band_hi && dl + b_skip * BAND + BAND - 1 < e) ++b_skip;
+        b_mask = b_skip;
+        while (b_mask < band_hi && dl + b_mask * BAND < e) ++b_mask;
+        const long long t_skip = band_first[b_skip - band_lo];
+        const long long t_mask = band_first[b_mask - band_lo];
+        TileArgs ta{s->d_df, s->d_dg, s->d_inv, s->d_Uf, s->d_mu, s->d_tn, s->d_tiles, s->d_seeds,
+                    s->d_acc + (long long)li * A, s->d_counters, P, N, dl, 0, S, m, e, li + 1 < n_len};
+        while (s->lev.size() < (size_t)2 * (li + 1)) {
+            cudaEvent_t ev; CU(cudaEventCreate(&ev)); s->lev.push_back(ev);
+        }
+        CU(cudaEventRecord(s->lev[2 * li], st));
+        auto launch = [&](long long t0, long long t1, bool masked) {
+            if (t1 <= t0) return;
+            TileArgs tb = ta;
+            tb.tiles = s->d_tiles + t0;
+            tb.seeds = s->d_seeds + t0 * BAND;
+            tb.n_tiles = (int)(t1 - t0);
+            unsigned g = blocks(t1 - t0, WARPS_PER_CTA);
+            if (full) {
+                if (masked) k_tile<true, true><<<g, WARPS_PER_CTA * 32, 0, st>>>(tb);
+                else k_tile<true, false><<<g, WARPS_PER_CTA * 32, 0, st>>>(tb);
+            } else {
+                if (masked) k_tile<false, true><<<g, WARPS_PER_CTA * 32, 0, st>>>(tb);
+                else k_tile<false, false><<<g, WARPS_PER_CTA * 32, 0, st>>>(tb);
+            }
+            launches += 1; klaunch += 1;
+        };
+        launch(t_skip, t_mask, true);
+        launch(t_mask, T, false);
+        CU(cudaEventRecord(s->lev[2 * li + 1], st));
+        CU(cudaGetLastError());
+        // executed cell updates (upper triangle cells swept by the launched tiles)
+        for (long long b = b_skip; b < band_hi; ++b) {
+            long long d0 = dl + b * BAND;
+            long long rows = N - d0;
+            if (rows <= 0) continue;
+            executed += (double)rows * BAND;
+        }
+        if (full) n_full += 1; else n_filtered += 1;
+    }
+    CU(cudaEventRecord(s->ev[1], st));
+    CU(cudaEventSynchronize(s->ev[1]));
+    double first_ms = 0;
+    for (int li = 0; li < n_len; ++li) {
+        float lm = 0; CU(cudaEventElapsedTime(&lm, s->lev[2 * li], s->lev[2 * li + 1]));
+        tile_ms += lm;
+        if (li == 0) first_ms = lm;
+    }
+    float ms = 0; CU(cudaEventElapsedTime(&ms, s->ev[0], s->ev[1]));
+    unsigned long long cnt[8];
+    CU(cudaMemcpy(cnt, s->d_counters, sizeof(cnt), cudaMemcpyDeviceToHost));
+    double W = 0;
+    for (int m = lmin; m <= lmax; ++m) {
+        long long k = (n - m + 1) - (m + 1) / 2;
+        if (k > 0) W += (double)k * (double)(k + 1) / 2.0;
+    }
+    s->lmin = lmin; s->lmax = lmax; s->n_len = n_len;
+    s->have_profile = true; s->have_final = false;
+    memset(s->stats, 0, sizeof(s->stats));
+    s->stats[0] = ms; s->stats[2] = executed; s->stats[3] = W; s->stats[4] = tile_ms;
+    s->stats[5] = launches; s->stats[6] = n_filtered; s->stats[7] = n_full; s->stats[8] = (double)cnt[0];
+    s->stats[9] = klaunch; s->stats[10] = first_ms;
+    return 0;
+}
+
+int vlmp_partials_size(vlmp_session* s, int64_t* n_len, int64_t* stride) {
+    if (!s || !s->have_profile) return fail(VLMP_E_STATE, "no profile run");
+    *n_len = s->n_len; *stride = s->A;
+    return 0;
+}
+
+int vlmp_partials_export(vlmp_session* s, void* keys, void* idx) {
+    if (!s || !s->have_profile) return fail(VLMP_E_STATE, "no profile run");
+    std::lock_guard<std::mutex> g(s->lock);
+    CU(cudaSetDevice(s->device));
+    const long long total = (long long)s->n_len * s->A;
+    k_export<<<blocks(total, 256), 256, 0, s->stream>>>(s->d_acc, (unsigned long long*)keys, (long long*)idx, total);
+    CU(cudaGetLastError());
+    CU(cudaStreamSynchronize(s->stream));
+    return 0;
+}
+
+int vlmp_partials_mask_idx(vlmp_session* s, const void* merged_keys, const void* keys, void* idx) {
+    if (!s || !s->have_profile) return fail(VLMP_E_STATE, "no profile run");
+    std::lock_guard<std::mutex> g(s->lock);
+    CU(cudaSetDevice(s->device));
+    const long long total = (long long)s->n_len * s->A;
+    k_mask_idx<<<blocks(total, 256), 256, 0, s->stream>>>((const unsigned long long*)merged_keys,
+                                                            (const unsigned long long*)keys, (long long*)idx, total);
+    CU(cudaGetLastError());
+    CU(cudaStreamSynchronize(s->stream));
+    return 0;
+}
+
+int vlmp_partials_import(vlmp_session* s, const void* keys, const void* idx) {
+    if (!s || !s->have_profile) return fail(VLMP_E_STATE, "no profile run");
+    std::lock_guard<std::mutex> g(s->lock);
+    CU(cudaSetDevice(s->device));
+    const long long total = (long long)s->n_len * s->A;
+    k_import<<<blocks(total, 256), 256, 0, s->stream>>>(s->d_acc, (const unsigned long long*)keys, (const long long*)idx, total);
+    CU(cudaGetLastError());
+    CU(cudaStreamSynchronize(s->stream));
+    return 0;
+}
+
+int vlmp_finalize(vlmp_session* s) {
+    if (!s || !s->have_profile) return fail(VLMP_E_STATE, "no profile run");
+    std::lock_guard<std::mutex> g(s->lock);
+    CU(cudaSetDevice(s->device));
+    cudaStream_t st = s->stream;
+    const long long A = s->A, n = s->n;
+    int rc;
+    if ((size_t)s->n_len * A > s->mp_cap || !s->d_mp || !s->d_ip) {
+        if ((rc = ensure1(s->d_mp, (size_t)s->n_len * A))) return rc;
+        if ((rc = ensure1(s->d_ip, (size_t)s->n_len * A))) return rc;
+        s->mp_cap = (size_t)s->n_len * A;
+    }
+    const long long n0 = n - s->lmin + 1;
+    size_t vc = s->v_cap;
+    if (vc < (size_t)n0 || !s->d_vdist) {
+        if ((rc = ensure1(s->d_vdist, n0))) return rc;
+        if ((rc = ensure1(s->d_vnorm, n0))) return rc;
+        if ((rc = ensure1(s->d_vlen, n0))) return rc;
+        if ((rc = ensure1(s->d_vidx, n0))) return rc;
+        if ((rc = ensure1(s->d_vpop, n0))) return rc;
+        s->v_cap = n0;
+    }
+    CU(cudaEventRecord(s->ev[4], st));
+    FinArgs fa{s->d_tn, s->d_cum, s->d_cum2, s->d_acc, s->d_mp, s->d_ip, n, A, s->lmin, s->n_len, s->floor_};
+    dim3 grid(blocks(n0, 128), s->n_len);
+    k_finalize<<<grid, 128, 0, st>>>(fa);
+    ValmpArgs va{s->d_mp, s->d_ip, s->d_vdist, s->d_vnorm, s->d_vlen, s->d_vidx, s->d_vpop, n, A, s->lmin, s->n_len};
+    k_valmp<<<blocks(n0, 256), 256, 0, st>>>(va);
+    CU(cudaEventRecord(s->ev[5], st));
+    CU(cudaGetLastError());
+    CU(cudaEventSynchronize(s->ev[5]));
+    float ms = 0; CU(cudaEventElapsedTime(&ms, s->ev[4], s->ev[5]));
+    s->stats[1] = ms;
+    s->stats[9] += 2;
+    s->have_final = true;
+    return 0;
+}
+
+int vlmp_get_valmp(vlmp_session* s, double* dist, double* norm, int64_t* lengths, int64_t* indices,
+                   uint8_t* populated) {
+    if (!s || !s->have_final) return fail(VLMP_E_STATE, "not finalized");
+    std::lock_guard<std::mutex> g(s->lock);
+    CU(cudaSetDevice(s->device));
+    const long long n0 = s->n - s->lmin + 1;
+    CU(cudaMemcpyAsync(dist, s->d_vdist, n0 * 8, cudaMemcpyDeviceToHost, s->stream));
+    CU(cudaMemcpyAsync(norm, s->d_vnorm, n0 * 8, cudaMemcpyDeviceToHost, s->stream));
+    CU(cudaMemcpyAsync(lengths, s->d_vlen, n0 * 8, cudaMemcpyDeviceToHost, s->stream));
+    CU(cudaMemcpyAsync(indices, s->d_vidx, n0 * 8, cudaMemcpyDeviceToHost, s->stream));
+    CU(cudaMemcpyAsync(populated, s->d_vpop, n0, cudaMemcpyDeviceToHost, s->stream));
+    CU(cudaStreamSynchronize(s->stream));
+    return 0;
+}
+
+int vlmp_get_profile(vlmp_session* s, int32_t length, double* mp, int64_t* ip) {
+    if (!s || !s->have_final) return fail(VLMP_E_STATE, "not finalized");
+    if (length < s->lmin || length > s->lmax) return fail(VLMP_E_INVALID_PARAMETERS, "length outside the run");
+    std::lock_guard<std::mutex> g(s->lock);
+    CU(cudaSetDevice(s->device));
+    const long long N = s->n - length + 1;
+    const long long off = (long long)(length - s->lmin) * s->A;
+    std::vector<int> tmp(N);
+    CU(cudaMemcpyAsync(mp, s->d_mp + off, N * 8, cudaMemcpyDeviceToHost, s->stream));
+    CU(cudaMemcpyAsync(tmp.data(), s->d_ip + off, N * 4, cudaMemcpyDeviceToHost, s->stream));
+    CU(cudaStreamSynchronize(s->stream));
+    for (long long o = 0; o < N; ++o) ip[o] = tmp[o];
+    return 0;
+}
+
+int vlmp_smallest_rows(vlmp_session* s, int32_t k2, int64_t* out_off, int64_t* out_nbr, double* out_d) {
+    if (!s || !s->have_final) return fail(VLMP_E_STATE, "not finalized");
+    if (k2 < 1 || k2 > 64) return fail(VLMP_E_INVALID_PARAMETERS, "k2 must be in [1, 64]");
+    std::lock_guard<std::mutex> g(s->lock);
+    CU(cudaSetDevice(s->device));
+    const long long cnt = (long long)s->n_len * k2;
+    long long* d_off = nullptr; long long* d_nbr = nullptr; double* d_d = nullptr;
+    CU(cudaMallocAsync((void**)&d_off, cnt * 8, s->stream));
+    CU(cudaMallocAsync((void**)&d_nbr, cnt * 8, s->stream));
+    CU(cudaMallocAsync((void**)&d_d, cnt * 8, s->stream));
+    SmallArgs sa{s->d_mp, s->d_ip, d_off, d_nbr, d_d, s->n, s->A, s->lmin, k2};
+    k_smallest<<<s->n_len, 256, 0, s->stream>>>(sa);
+    CU(cudaGetLastError());
+    CU(cudaMemcpyAsync(out_off, d_off, cnt * 8, cudaMemcpyDeviceToHost, s->stream));
+    CU(cudaMemcpyAsync(out_nbr, d_nbr, cnt * 8, cudaMemcpyDeviceToHost, s->stream));
+    CU(cudaMemcpyAsync(out_d, d_d, cnt * 8, cudaMemcpyDeviceToHost, s->stream));
+    CU(cudaFreeAsync(d_off, s->stream)); CU(cudaFreeAsync(d_nbr, s->stream)); CU(cudaFreeAsync(d_d, s->stream));
+    CU(cudaStreamSynchronize(s->stream));
+    s->stats[9] += 1;
+    return 0;
+}
+
+int vlmp_discords(vlmp_session* s, int32_t k, double* out_dist, int64_t* out_off) {
+    if (!s || !s->have_final) return fail(VLMP_E_STATE, "not finalized");
+    if (k < 1 || k > 32) return fail(VLMP_E_INVALID_PARAMETERS, "k must be in [1, 32]");
+    std::lock_guard<std::mutex> g(s->lock);
+    CU(cudaSetDevice(s->device));
+    const long long cnt = (long long)s->n_len * k;
+    double* d_d = nullptr; long long* d_o = nullptr;
+    CU(cudaMallocAsync((void**)&d_d, cnt * 8, s->stream));
+    CU(cudaMallocAsync((void**)&d_o, cnt * 8, s->stream));
+    DiscArgs da{s->d_mp, d_d, d_o, s->n, s->A, s->lmin, s->n_len, k};
+    k_discords<<<blocks((long long)s->n_len * 32, 128), 128, 0, s->stream>>>(da);
+    CU(cudaGetLastError());
+    CU(cudaMemcpyAsync(out_dist, d_d, cnt * 8, cudaMemcpyDeviceToHost, s->stream));
+    CU(cudaMemcpyAsync(out_off, d_o, cnt * 8, cudaMemcpyDeviceToHost, s->stream));
+    CU(cudaFreeAsync(d_d, s->stream)); CU(cudaFreeAsync(d_o, s->stream));
+    CU(cudaStreamSynchronize(s->stream));
+    s->stats[9] += 1;
+    return 0;
+}
+
+int vlmp_ranking_events(vlmp_session* s, double tau, int64_t cap, int64_t* ev_off, int64_t* ev_nbr,
+                        int64_t* ev_len, double* ev_dist, double* ev_norm, int64_t* count) {
+    if (!s || !s->have_final) return fail(VLMP_E_STATE, "not finalized");
+    std::lock_guard<std::mutex> g(s->lock);
+    CU(cudaSetDevice(s->device));
+    cudaStream_t st = s->stream;
+    long long c = std::max<long long>(cap, 1);
+    long long *d_o, *d_nb, *d_l; double *d_d, *d_n; unsigned long long* d_c;
+    CU(cudaMallocAsync((void**)&d_o, c * 8, st)); CU(cudaMallocAsync((void**)&d_nb, c * 8, st));
+    CU(cudaMallocAsync((void**)&d_l, c * 8, st)); CU(cudaMallocAsync((void**)&d_d, c * 8, st));
+    CU(cudaMallocAsync((void**)&d_n, c * 8, st)); CU(cudaMallocAsync((void**)&d_c, 8, st));
+    CU(cudaMemsetAsync(d_c, 0, 8, st));
+    const long long n0 = s->n - s->lmin + 1;
+    EvArgs ea{s->d_mp, s->d_ip, tau, d_o, d_nb, d_l, d_d, d_n, d_c, cap, s->n, s->A, s->lmin, s->n_len};
+    k_events<<<blocks(n0, 256), 256, 0, st>>>(ea);
+    CU(cudaGetLastError());
+    unsigned long long hc = 0;
+    CU(cudaMemcpyAsync(&hc, d_c, 8, cudaMemcpyDeviceToHost, st));
+    CU(cudaStreamSynchronize(st));
+    long long take = std::min<long long>((long long)hc, cap);
+    if (take > 0) {
+        CU(cudaMemcpyAsync(ev_off, d_o, take * 8, cudaMemcpyDeviceToHost, st));
+        CU(cudaMemcpyAsync(ev_nbr, d_nb, take * 8, cudaMemcpyDeviceToHost, st));
+        CU(cudaMemcpyAsync(ev_len, d_l, take * 8, cudaMemcpyDeviceToHost, st));
+        CU(cudaMemcpyAsync(ev_dist, d_d, take * 8, cudaMemcpyDeviceToHost, st));
+        CU(cudaMemcpyAsync(ev_norm, d_n, take * 8, cudaMemcpyDeviceToHost, st));
+    }
+    CU(cudaFreeAsync(d_o, st)); CU(cudaFreeAsync(d_nb, st)); CU(cudaFreeAsync(d_l, st));
+    CU(cudaFreeAsync(d_d, st)); CU(cudaFreeAsync(d_n, st)); CU(cudaFreeAsync(d_c, st));
+    CU(cudaStreamSynchronize(st));
+    *count = (int64_t)hc;
+    return 0;
+}
+
+int vlmp_stats(vlmp_session* s, double* out, int32_t n_out) {
+    if (!s || !out) return fail(VLMP_E_INVALID_PARAMETERS, "null argument");
+    for (int q = 0; q < n_out && q < 16; ++q) out[q] = s->stats[q];
+    return 0;
+}
+
+int vlmp_measure_fp64_peak(vlmp_session* s, double* fma_per_s) {
+    if (!s || !fma_per_s) return fail(VLMP_E_INVALID_PARAMETERS, "null argument");
+    std::lock_guard<std::mutex> g(s->lock);
+    CU(cudaSetDevice(s->device));
+    int sms = 0;
+    CU(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, s->device));
+    double* d_out = nullptr;
+    CU(cudaMalloc((void**)&d_out, 8));
+    const int threads = 512, per_sm = 4, iters = 2048;
+    const unsigned grid = sms * per_sm;
+    k_dfma_peak<<<grid, threads, 0, s->stream>>>(d_out, 16, 1.0);   // warm-up
+    CU(cudaEventRecord(s->ev[6], s->stream));
+    k_dfma_peak<<<grid, threads, 0, s->stream>>>(d_out, iters, 1.0);
+    CU(cudaEventRecord(s->ev[7], s->stream));
+    CU(cudaEventSynchronize(s->ev[7]));
+    float ms = 0; CU(cudaEventElapsedTime(&ms, s->ev[6], s->ev[7]));
+    CU(cudaFree(d_out));
+    const double fmas = (double)grid * threads * iters * 16.0 * 8.0;
+    *fma_per_s = fmas / (ms * 1e-3);
+    return 0;
+}
+
+}  // extern "C"
