@@ -1,0 +1,291 @@
+"""Benchmark: pair-length distance updates/s of the variable-length matrix profile.
+
+Contract (driver): ``python bench.py --gpus N --steps K --warmup W [--impl reference]``
+prints ONE JSON line on rank 0. N>1 runs under torchrun, one process per GPU.
+
+Workload: BASELINE.json configs[1] (config 2): n = 65,536 fp64 random walk (seed 1)
+with a planted pair (length 300 at 5234/10194), lengths 256..384, top-3 motifs and
+top-3 discords per length. A step = one exhaustive pass of the hot path over that
+series: per-length profiles (tile kernels) + exact per-offset values + VALMP +
+per-length top-k rows + per-length discord replay.
+Metric: W / step time, W = sum_l (N_l - e_l)(N_l - e_l + 1)/2 non-trivial window
+pairs; the kernels evaluate every one of them (no pruning).
+"""
+
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import subprocess
+import sys
+import threading
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+METRIC = "pair-length distance updates/s (1/2/4/8 B200) and % FMA roofline vs CPU ref"
+UNIT = "updates/s"
+
+
+def _args():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=5)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--config", type=int, default=2)
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    return ap.parse_args()
+
+
+def _dist_env():
+    rank = int(os.environ.get("RANK", 0))
+    world = int(os.environ.get("WORLD_SIZE", 1))
+    local = int(os.environ.get("LOCAL_RANK", 0))
+    return rank, world, local
+
+
+class ClockSampler:
+    """nvidia-smi clocks + throttle reasons sampled during the timed region."""
+
+    Q = ("clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.hw_slowdown,"
+         "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+         "clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, device):
+        self.device = device
+        self.samples = []
+        self._stop = threading.Event()
+        self._t = None
+
+    def _run(self):
+        while not self._stop.is_set():
+            try:
+                out = subprocess.run(["nvidia-smi", "-i", str(self.device), f"--query-gpu={self.Q}",
+                                      "--format=csv,noheader,nounits"], capture_output=True,
+                                     text=True, timeout=5).stdout.strip()
+                if out:
+                    self.samples.append([x.strip() for x in out.split(",")])
+            except Exception:
+                pass
+            self._stop.wait(0.2)
+
+    def __enter__(self):
+        self._t = threading.Thread(target=self._run, daemon=True)
+        self._t.start()
+        return self
+
+    def __exit__(self, *exc):
+        self._stop.set()
+        self._t.join(timeout=10)
+
+    def summary(self):
+        if not self.samples:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unsampled"]}
+        sm = [float(s[0]) for s in self.samples if s[0].replace(".", "").isdigit()]
+        mx = [float(s[1]) for s in self.samples if s[1].replace(".", "").isdigit()]
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = sorted({names[k] for s in self.samples for k in range(4)
+                          if len(s) > 3 + k and s[3 + k].lower() == "active"})
+        return {"sm_mhz": float(np.median(sm)) if sm else None,
+                "sm_max_mhz": max(mx) if mx else None, "reasons": reasons,
+                "samples": len(self.samples)}
+
+
+def _workload(cfg):
+    from paper_2008_13447_b200 import gen
+    c = gen.CONFIGS[cfg]
+    return c, gen.series_for(cfg), gen.pair_updates(c.n, c.lmin, c.lmax)
+
+
+def _peaks():
+    path = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    try:
+        return json.load(open(path))
+    except Exception:
+        return {}
+
+
+def cpu_sample(series, c, target_s=12.0, threads=None):
+    """The oracle (C restatement of the reference's exhaustive scan) on a bounded
+    sample of the same workload: whole per-length profiles at evenly spaced lengths
+    until ~target_s of work. Returns (updates/s, cores, description)."""
+    from oracle import oracle
+    threads = threads or os.cpu_count()
+    lengths = list(np.linspace(c.lmin, c.lmax, 9).astype(int))
+    done, t_used, upd = [], 0.0, 0
+    for L in lengths:
+        t0 = time.perf_counter()
+        oracle.profile(series, int(L), nthreads=threads)
+        t_used += time.perf_counter() - t0
+        N = series.n - L + 1
+        k = N - (L + 1) // 2
+        upd += k * (k + 1) // 2
+        done.append(int(L))
+        if t_used >= target_s:
+            break
+    return upd / t_used, threads, (f"full exact profiles (all rows) at lengths {done} of "
+                                   f"{c.lmin}..{c.lmax}, oracle/vlmp_oracle.c, {threads} threads, "
+                                   f"{t_used:.1f} s")
+
+
+def run_reference(args):
+    rank, world, local = _dist_env()
+    if rank != 0:
+        return
+    from paper_2008_13447_b200 import ingest
+    c, t, W = _workload(args.config)
+    s = ingest(t)
+    for _ in range(args.warmup):
+        cpu_sample(s, c, target_s=1.0)
+    vals = []
+    t0 = time.perf_counter()
+    for _ in range(args.steps):
+        v, cores, desc = cpu_sample(s, c, target_s=10.0)
+        vals.append(v)
+    wall = time.perf_counter() - t0
+    value = float(np.mean(vals))
+    line = {
+        "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
+        "warmup": args.warmup, "ms_per_step": wall * 1e3 / args.steps, "higher_is_better": True,
+        "scaling": "strong", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+        "impl": "reference",
+        "config": {"workload": f"config {args.config}: {c.note}", "n": c.n, "lmin": c.lmin,
+                   "lmax": c.lmax, "k_motif": c.k_motif, "k_discord": c.k_discord},
+        "cpu_baseline": {"value": value, "unit": UNIT, "cores": cores, "kind": "port",
+                         "sample": desc},
+        "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line), flush=True)
+
+
+def run_ours(args):
+    rank, world, local = _dist_env()
+    import torch
+    from paper_2008_13447_b200 import _lib, api, distributed, ingest
+    c, t, W = _workload(args.config)
+    s = ingest(t)
+    torch.cuda.set_device(local)
+    group = None
+    if world > 1:
+        import torch.distributed as dist
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    sess = _lib.session(local)
+    k2 = max(2 * c.k_motif, 2)
+    kd = max(c.k_discord, 1)
+
+    def step():
+        if world > 1:
+            distributed.profile_sharded(sess, s, c.lmin, c.lmax, rank, world, group)
+        else:
+            with sess.lock:
+                sess.profile(c.lmin, c.lmax, 0, -1, 0)
+                sess.finalize()
+        with sess.lock:
+            rows = sess.smallest_rows(k2)
+            disc = sess.discords(kd)
+        return rows, disc
+
+    with sess.lock:
+        sess.set_series(s.values, s._cum, s._cum2, s.sigma_floor)   # inputs resident in HBM
+    for _ in range(max(args.warmup, 3)):
+        step()
+    if world > 1:
+        torch.distributed.barrier()
+    torch.cuda.synchronize()
+    tile_ms, launches = 0.0, 0
+    with ClockSampler(local) as clk:
+        sess.event_record(0)
+        for _ in range(args.steps):
+            step()
+            st = sess.stats()
+            tile_ms += st["tile_ms"]
+            launches += int(st["kernel_launches"]) + 2
+        sess.event_record(1)
+        ms = sess.event_elapsed_ms()
+    torch.cuda.synchronize()
+    if world > 1:
+        import torch.distributed as dist
+        tt = torch.tensor([ms, tile_ms], device="cuda")
+        dist.all_reduce(tt, op=dist.ReduceOp.MAX)
+        ms, tile_ms = float(tt[0]), float(tt[1])
+        dist.barrier()
+    step_ms = ms / args.steps
+    value = W / (step_ms * 1e-3)
+
+    # e2e through the public API: host arrays in, host results out, every step
+    e2e_line = None
+    if rank == 0 and world == 1:
+        from paper_2008_13447_b200 import mine
+        for _ in range(2):
+            mine(s, c.lmin, c.lmax, k_motif=c.k_motif, k_discord=c.k_discord)
+        t0 = time.perf_counter()
+        reps = max(2, min(args.steps, 5))
+        for _ in range(reps):
+            res = mine(s, c.lmin, c.lmax, k_motif=c.k_motif, k_discord=c.k_discord)
+        e2e_s = (time.perf_counter() - t0) / reps
+        n0 = s.n - c.lmin + 1
+        nl = c.lmax - c.lmin + 1
+        e2e_line = {"value": W / e2e_s, "unit": UNIT,
+                    "h2d_bytes_per_step": int(8 * (s.n + 2 * (s.n + 1))),
+                    "d2h_bytes_per_step": int(n0 * (8 * 4 + 1) + nl * (2 * c.k_motif * 24 + kd * 16)),
+                    "ms_per_step": e2e_s * 1e3}
+
+    if rank != 0:
+        if world > 1:
+            torch.distributed.destroy_process_group()
+        return
+    # roofline of the dominant kernel (k_tile): 4 FP64 FMA-pipe instructions per update
+    peak_dfma = sess.measure_fp64_peak()
+    avg_tile_s = tile_ms * 1e-3 / args.steps
+    achieved = W * 4 * 2 / avg_tile_s / 1e12          # TFLOP/s (2 flops per FMA-pipe instr)
+    peak = peak_dfma * 2 / 1e12
+    prof_traffic = None
+    tr_path = os.path.join(ROOT, "profiles", "tile_traffic.json")
+    if os.path.exists(tr_path):
+        try:
+            prof_traffic = json.load(open(tr_path)).get("bytes_per_step")
+        except Exception:
+            prof_traffic = None
+    cpu = None
+    if world == 1 and not args.no_cpu_baseline:
+        v, cores, desc = cpu_sample(s, c, target_s=12.0)
+        cpu = {"value": v, "unit": UNIT, "cores": cores, "kind": "port", "sample": desc}
+    line = {
+        "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
+        "warmup": max(args.warmup, 3), "ms_per_step": step_ms, "higher_is_better": True,
+        "scaling": "strong", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+        "config": {"workload": f"config {args.config}: {c.note}", "n": c.n, "lmin": c.lmin,
+                   "lmax": c.lmax, "k_motif": c.k_motif, "k_discord": c.k_discord,
+                   "W_updates": W, "parallelism": f"diagonal bands x{world}",
+                   "l2": "working set (series + per-length params, 2.6 MB) is L2-resident by design; "
+                         "no flush: the kernel is FP64-bound, not memory-bound"},
+        "roofline": {"bound": "fp64_fma", "achieved": achieved, "peak": peak, "unit": "TFLOP/s",
+                     "frac": achieved / peak, "traffic": prof_traffic,
+                     "peak_source": "measured DFMA microbenchmark (vlmp_measure_fp64_peak); "
+                                    "MEASURED_PEAKS.json has no FP64 figure",
+                     "kernel": "k_tile", "avg_tile_ms_per_step": avg_tile_s * 1e3},
+        "cpu_baseline": cpu,
+        "e2e": e2e_line,
+        "gpu_launches": launches,
+        "clocks": clk.summary(),
+    }
+    print(json.dumps(line), flush=True)
+    if world > 1:
+        torch.distributed.destroy_process_group()
+
+
+def main():
+    args = _args()
+    if args.impl == "reference":
+        run_reference(args)
+    else:
+        run_ours(args)
+
+
+if __name__ == "__main__":
+    main()

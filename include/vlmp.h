@@ -125,6 +125,13 @@ int vlmp_ranking_events(vlmp_session* s, double tau, int64_t cap, int64_t* ev_of
  */
 int vlmp_stats(vlmp_session* s, double* out, int32_t n_out);
 
+/*
+ * Device-timeline timing on the session's stream: record slot 0 (start) and
+ * slot 1 (stop); elapsed waits for slot 1 and returns milliseconds.
+ */
+int vlmp_event_record(vlmp_session* s, int32_t slot);
+int vlmp_event_elapsed(vlmp_session* s, float* ms);
+
 /* FP64 FMA peak microbenchmark (DFMA instr/s on this device, all SMs). */
 int vlmp_measure_fp64_peak(vlmp_session* s, double* fma_per_s);
 

@@ -16,8 +16,8 @@ from .results import (VALMP, DiscordMatrix, DiscordScan, LengthTrace, MatrixProf
                       VariableLengthDiscordMatrix, top_variable_length_motif,
                       update_fixed_length_discords, update_valmp,
                       update_variable_length_discords)
-from .api import (compute_matrix_profile, motifs_per_length, topkm_discord_discovery,
-                  validate_range, valmod)
+from .api import (MiningResult, compute_matrix_profile, mine, motifs_per_length,
+                  topkm_discord_discovery, validate_range, valmod)
 
 __version__ = "0.1.0"
 
@@ -26,7 +26,7 @@ __all__ = [
     "MatrixProfile", "PairRanking", "ProfileResult", "RankedPair", "RunTrace",
     "VariableLengthDiscordMatrix", "top_variable_length_motif",
     "update_fixed_length_discords", "update_valmp", "update_variable_length_discords",
-    "compute_matrix_profile", "motifs_per_length", "topkm_discord_discovery",
+    "compute_matrix_profile", "mine", "MiningResult", "motifs_per_length", "topkm_discord_discovery",
     "validate_range", "valmod",
     "SeriesMineError", "EmptySeriesError", "NonFiniteError", "LengthExceedsSeriesError",
     "OutOfRangeError", "ZeroVarianceError", "SeriesTooShortError", "AllConstantError",

@@ -37,6 +37,8 @@ SIGNATURES = {
     "vlmp_discords": (C.c_int, [C.c_void_p, C.c_int32, C.c_void_p, C.c_void_p]),
     "vlmp_ranking_events": (C.c_int, [C.c_void_p, C.c_double, C.c_int64] + [C.c_void_p] * 5 + [_c_int64_p]),
     "vlmp_stats": (C.c_int, [C.c_void_p, C.c_void_p, C.c_int32]),
+    "vlmp_event_record": (C.c_int, [C.c_void_p, C.c_int32]),
+    "vlmp_event_elapsed": (C.c_int, [C.c_void_p, C.POINTER(C.c_float)]),
     "vlmp_measure_fp64_peak": (C.c_int, [C.c_void_p, _c_double_p]),
 }
 
@@ -178,6 +180,14 @@ class Session:
         keys = ["profile_ms", "finalize_ms", "executed_updates", "W", "tile_ms", "tile_launches",
                 "filtered_lengths", "full_lengths", "slow_merges", "kernel_launches", "first_tile_ms"]
         return {k: float(out[i]) for i, k in enumerate(keys)}
+
+    def event_record(self, slot):
+        self._check(self.lib.vlmp_event_record(self.h, int(slot)))
+
+    def event_elapsed_ms(self):
+        v = C.c_float()
+        self._check(self.lib.vlmp_event_elapsed(self.h, C.byref(v)))
+        return float(v.value)
 
     def measure_fp64_peak(self):
         v = C.c_double()

@@ -233,6 +233,54 @@ def motifs_per_length(series, lmin: int, lmax: int, k: int):
     return _topk_from_rows(run, k)
 
 
+class MiningResult:
+    """Everything one exhaustive pass yields: VALMP, per-length top-k motif pairs,
+    per-length + merged top-k discords, and the per-length trace."""
+
+    def __init__(self, valmp, motifs, discords, trace, stats):
+        self.valmp = valmp
+        self.motifs = motifs
+        self.discords = discords
+        self.trace = trace
+        self.stats = stats
+
+
+def mine(series, lmin: int, lmax: int, k_motif: int = 1, k_discord: int = 1, *,
+         ranking=None) -> MiningResult:
+    """One GPU pass over [lmin, lmax] returning every read-off the reference's
+    valmod + topkm_discord_discovery (m = 1) + per-length PairRanking(k) produce."""
+    from .results import RunTrace
+    series = as_series(series)
+    validate_range(series, lmin, lmax)
+    _check_profile_length(series, lmin)
+    if not (1 <= k_motif <= 32) or not (1 <= k_discord <= 32):
+        raise InvalidParametersError("k_motif and k_discord must be in [1, 32]")
+    run = GpuRun(series, lmin, lmax)
+    v = run.valmp()
+    motifs = _topk_from_rows(run, k_motif)
+    trace = RunTrace()
+    for li in range(lmax - lmin + 1):
+        length = lmin + li
+        n_dp = series.n - length + 1
+        top = motifs[length]
+        trace.add_length(length, n_profiles=n_dp, n_valid=n_dp, n_nonvalid=0, n_recomputed=0,
+                         full_recompute=False, motif=top[0] if top else None)
+    dist, off = run.discords(k_discord)
+    merged = VariableLengthDiscordMatrix.empty(k_discord, 1)
+    per_length = {}
+    for li in range(lmax - lmin + 1):
+        length = lmin + li
+        dkm = DiscordMatrix.empty(k_discord, 1, length)
+        dkm.dist[:, 0] = dist[li]
+        dkm.offset[:, 0] = off[li]
+        dkm._occupied = {int(o) for o in off[li] if o >= 0}
+        per_length[length] = dkm
+        update_variable_length_discords(dkm, merged, k_discord, 1)
+    if ranking is not None:
+        _feed_ranking(run, v, ranking)
+    return MiningResult(v, motifs, DiscordScan(merged, per_length), trace, run.stats)
+
+
 def _topk_from_rows(run: GpuRun, k: int):
     off, nbr, d = run.smallest_rows(2 * k)
     out = {}

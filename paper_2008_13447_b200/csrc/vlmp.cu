@@ -61,7 +61,6 @@ int fail(int code, const std::string& msg) { g_err = msg; return code; }
             return fail(VLMP_E_CUDA, std::string(#call) + ": " + cudaGetErrorString(e_)); \
     } while (0)
 
-__host__ __device__ inline long long pidx(long long x, long long P) { return (x & (D - 1)) * P + (x >> 3); }
 
 // ---------------------------------------------------------------------------------
 // exact window statistics (series.py:91-100): no contraction, numpy op order
@@ -108,13 +107,22 @@ __device__ double pair_distance(const double* __restrict__ t, const double* __re
 }
 
 // ---------------------------------------------------------------------------------
-struct ParamArgs {
-    const double* tn; const double* cum; const double* cum2;
-    double* df; double* dg; double* inv; double* mu;
-    long long n, N, A, P; int m; double floor_;
+// Per-length window parameters, natural layout, 32-byte AoS so one warp-contiguous
+// run of offsets is a coalesced 1 KB read (and two 16-byte cp.async per entry).
+struct __align__(32) Prm {
+    double df;    // (t[o+m-1] - t[o-1]) / 2                       (0 at o = 0)
+    double dg;    // (t[o+m-1] - mu_o) + (t[o-1] - mu_{o-1})        (0 at o = 0)
+    double inv;   // 1 / (sigma_o sqrt(m)); NaN = invalid window (constant / past the end)
+    float U;      // bound on the offset's best key, high word as float (filter kernel)
+    float pad;
 };
 
-// per-length recurrence factors, permuted layout
+struct ParamArgs {
+    const double* tn; const double* cum; const double* cum2;
+    Prm* prm; double* mu;
+    long long n, N, A; int m; double floor_;
+};
+
 __global__ void k_params(ParamArgs a) {
     long long o = blockIdx.x * (long long)blockDim.x + threadIdx.x;
     if (o >= a.A) return;
@@ -122,25 +130,26 @@ __global__ void k_params(ParamArgs a) {
     double mu_o = 0.0, sd_o = 0.0, mu_p = 0.0, sd_p = 0.0;
     if (o < a.N) win_stats(a.cum, a.cum2, o, m, mu_o, sd_o);
     if (o >= 1 && o - 1 < a.N) win_stats(a.cum, a.cum2, o - 1, m, mu_p, sd_p);
-    double inv = __longlong_as_double(0x7FF8000000000000ll);   // NaN: invalid window
-    if (o < a.N && sd_o >= a.floor_) inv = 1.0 / (sd_o * sqrt((double)m));
-    double df = 0.0, dg = 0.0;
+    Prm p;
+    p.inv = __longlong_as_double(0x7FF8000000000000ll);   // NaN: invalid window
+    if (o < a.N && sd_o >= a.floor_) p.inv = 1.0 / (sd_o * sqrt((double)m));
+    p.df = 0.0; p.dg = 0.0;
     if (o >= 1) {
         double tl = a.tn[o + m - 1], tp = a.tn[o - 1];
-        df = (tl - tp) * 0.5;
-        dg = (tl - mu_o) + (tp - mu_p);
+        p.df = (tl - tp) * 0.5;
+        p.dg = (tl - mu_o) + (tp - mu_p);
     }
-    long long q = pidx(o, a.P);
-    a.df[q] = df; a.dg[q] = dg; a.inv[q] = inv; a.mu[q] = mu_o;
+    p.U = INFINITY; p.pad = 0.f;
+    a.prm[o] = p;
+    a.mu[o] = mu_o;
 }
 
 // ---------------------------------------------------------------------------------
 // bound U[o] >= the kernel's key of o's best cell, from the previous length's winners
 struct BoundArgs {
-    const double* tn; const double* mu; const double* inv;   // permuted (this length)
-    const long long* prev_idx;                              // natural, previous length winners
-    float* Uf;                                              // permuted
-    long long N, Nprev, A, P; int m, e; double margin;
+    const double* tn; const double* mu; Prm* prm;
+    const long long* prev_idx;
+    long long N, Nprev; int m, e; double margin;
 };
 
 __device__ inline double cell_key(const double* __restrict__ tn, long long o, long long c, int m,
@@ -152,53 +161,47 @@ __device__ inline double cell_key(const double* __restrict__ tn, long long o, lo
 
 __global__ void k_bound(BoundArgs a) {
     long long o = blockIdx.x * (long long)blockDim.x + threadIdx.x;
-    if (o >= a.A) return;
+    if (o >= a.N) return;
     float out = -INFINITY;
-    if (o < a.N) {
-        long long qo = pidx(o, a.P);
-        double io = a.inv[qo];
-        if (io == io) {   // valid row
-            double mo = a.mu[qo];
-            long long cand[4];
-            int nc = 0;
-            long long c1 = (o < a.Nprev) ? a.prev_idx[o] : -1;
-            if (c1 >= 0 && c1 < IDX_NONE) { cand[nc++] = c1; cand[nc++] = c1 > o ? c1 + 1 : c1 - 1; }
-            if (o >= 1 && o - 1 < a.Nprev) { long long c = a.prev_idx[o - 1]; if (c >= 0 && c < IDX_NONE) cand[nc++] = c + 1; }
-            if (o + 1 < a.Nprev) { long long c = a.prev_idx[o + 1]; if (c >= 0 && c < IDX_NONE) cand[nc++] = c - 1; }
-            double best = INFINITY;
-            for (int q = 0; q < nc; ++q) {
-                long long c = cand[q];
-                bool dup = false;
-                for (int r = 0; r < q; ++r) dup |= (cand[r] == c);
-                if (dup || c < 0 || c >= a.N) continue;
-                long long dd = c > o ? c - o : o - c;
-                if (dd < a.e) continue;
-                long long qc = pidx(c, a.P);
-                double ic = a.inv[qc];
-                if (!(ic == ic)) continue;
-                double r = cell_key(a.tn, o, c, a.m, mo, a.mu[qc], io, ic);
-                best = fmin(best, r);
-            }
-            if (best < INFINITY) {
-                double U = fmax(best, 0.0) + a.margin;
-                out = __int_as_float(__double2hiint(U));   // x <= U  =>  hi(x) <= hi(U)
-            } else {
-                out = INFINITY;   // no bound: every cell of this offset is a candidate
-            }
+    double io = a.prm[o].inv;
+    if (io == io) {   // valid row
+        double mo = a.mu[o];
+        long long cand[4];
+        int nc = 0;
+        long long c1 = (o < a.Nprev) ? a.prev_idx[o] : -1;
+        if (c1 >= 0) { cand[nc++] = c1; cand[nc++] = c1 > o ? c1 + 1 : c1 - 1; }
+        if (o >= 1 && o - 1 < a.Nprev) { long long c = a.prev_idx[o - 1]; if (c >= 0) cand[nc++] = c + 1; }
+        if (o + 1 < a.Nprev) { long long c = a.prev_idx[o + 1]; if (c >= 0) cand[nc++] = c - 1; }
+        double best = INFINITY;
+        for (int q = 0; q < nc; ++q) {
+            long long c = cand[q];
+            bool dup = false;
+            for (int r = 0; r < q; ++r) dup |= (cand[r] == c);
+            if (dup || c < 0 || c >= a.N) continue;
+            long long dd = c > o ? c - o : o - c;
+            if (dd < a.e) continue;
+            double ic = a.prm[c].inv;
+            if (!(ic == ic)) continue;
+            best = fmin(best, cell_key(a.tn, o, c, a.m, mo, a.mu[c], io, ic));
+        }
+        if (best < INFINITY) {
+            double U = fmax(best, 0.0) + a.margin;
+            out = __int_as_float(__double2hiint(U));   // x <= U  =>  hi(x) <= hi(U)
+        } else {
+            out = INFINITY;   // no bound: every cell of this offset is a candidate
         }
     }
-    a.Uf[pidx(o, a.P)] = out;
+    a.prm[o].U = out;
 }
 
 // ---------------------------------------------------------------------------------
 struct TileArgs {
-    const double* df; const double* dg; const double* inv; const float* Uf; const double* mu;
-    const double* tn;
+    const Prm* prm; const double* mu; const double* tn;
     const int2* tiles;
     double* seeds;
     ulonglong2* acc;               // this length's accumulators, natural offsets
-    unsigned long long* counters;  // [0] slow-path merges
-    long long P, N, dlo;
+    unsigned long long* counters;  // [0] candidate merges, [1] candidate flushes
+    long long N, dlo;
     int n_tiles, S, m, e, update_seeds;
 };
 
@@ -229,21 +232,37 @@ __device__ inline double pack_low8(double v, unsigned idx8) {
     return __hiloint2double(hi, lo);
 }
 
-template <bool FULL, bool MASKED>
-__global__ void __launch_bounds__(WARPS_PER_CTA * 32)
-k_tile(TileArgs a) {
-    const int lane = threadIdx.x & 31;
-    const int wid = blockIdx.x * WARPS_PER_CTA + (threadIdx.x >> 5);
-    if (wid >= a.n_tiles) return;
-    const int2 tl = a.tiles[wid];
-    const long long d0 = a.dlo + (long long)tl.x * BAND;
-    const long long i0 = (long long)tl.y * a.S;
-    const long long rows_valid = a.N - d0 - i0;
-    if (rows_valid <= 0) return;
-    const long long P = a.P;
-    const int dbase = lane * D;
-    const long long cbase = i0 + d0 + dbase;   // column of slot 0 at row i0
+__device__ inline void cp_async16(void* smem_dst, const void* gmem_src) {
+    unsigned d = (unsigned)__cvta_generic_to_shared(smem_dst);
+    asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" :: "r"(d), "l"(gmem_src) : "memory");
+}
+__device__ inline void cp_async_commit() { asm volatile("cp.async.commit_group;\n" ::: "memory"); }
+__device__ inline void cp_async_wait_all() { asm volatile("cp.async.wait_group 0;\n" ::: "memory"); }
 
+constexpr int CAND_CAP = 64;
+struct Cand { int o; int idx; unsigned long long key; };
+
+struct WarpSmem {
+    Prm fresh[2][D];         // the column entering lane 31's slot D-1 at each row of a group
+    Prm row[2][D];           // the group's row parameters
+    Cand cand[CAND_CAP];     // buffered filter candidates (filter kernel)
+};
+
+// stage group g (rows r0 .. r0+7) into buffer b: 8 row structs + 8 fresh columns for lane 31
+__device__ inline void stage_group(WarpSmem& w, int b, const Prm* __restrict__ prm, long long r0,
+                                   long long d0, int lane) {
+    const int q = lane >> 1, half = lane & 1;
+    const Prm* src = (lane < 2 * D) ? prm + r0 + q                       // rows r0 + q
+                                    : prm + r0 + (q - D) + d0 + BAND - 1; // fresh column at row r0+q-8
+    Prm* dst = (lane < 2 * D) ? &w.row[b][q] : &w.fresh[b][q - D];
+    cp_async16(reinterpret_cast<char*>(dst) + 16 * half, reinterpret_cast<const char*>(src) + 16 * half);
+    cp_async_commit();
+}
+
+template <bool FULL, bool MASKED>
+__device__ __forceinline__ void tile_body(const TileArgs& a, WarpSmem& w, int wid, int lane,
+                                          long long d0, long long i0, long long rows_valid) {
+    const int dbase = lane * D;
     bool sval[D];
 #pragma unroll
     for (int s = 0; s < D; ++s) sval[s] = !MASKED || (d0 + dbase + s >= a.e);
@@ -252,118 +271,60 @@ k_tile(TileArgs a) {
     double* seedp = a.seeds + (long long)wid * BAND + dbase;
 #pragma unroll
     for (int s = 0; s < D; ++s) cov[s] = seedp[s];
+    const long long cbase = i0 + d0 + dbase;   // column of slot 0 at row i0
 
     // Welford co-moment update of the seeds to length m+1:
     // C_{m+1} = C_m + m/(m+1) * (x_m - mean_m(x)) * (y_m - mean_m(y))
     if (a.update_seeds) {
-        const double w = (double)a.m / (double)(a.m + 1);
-        const double xi = (a.tn[i0 + a.m] - a.mu[pidx(i0, P)]) * w;
+        const double wgt = (double)a.m / (double)(a.m + 1);
+        const double xi = (a.tn[i0 + a.m] - a.mu[i0]) * wgt;
 #pragma unroll
-        for (int s = 0; s < D; ++s) {
-            long long c = cbase + s;
-            seedp[s] = fma(xi, a.tn[c + a.m] - a.mu[pidx(c, P)], cov[s]);
-        }
+        for (int s = 0; s < D; ++s)
+            seedp[s] = fma(xi, a.tn[cbase + s + a.m] - a.mu[cbase + s], cov[s]);
     }
 
+    // column ring: phys slot p holds the column of logical slot (p - kk) mod D at row step kk.
+    // Each row, the column leaving lane L's slot 0 enters lane L-1's slot D-1 (shuffle);
+    // lane 31 takes the fresh column i + d0 + 255 from shared memory.
     double cdf[D], cdg[D], cinv[D];
     float cU[D];
 #pragma unroll
     for (int s = 0; s < D; ++s) {
-        long long q = pidx(cbase + s, P);
-        cdf[s] = a.df[q]; cdg[s] = a.dg[q]; cinv[s] = a.inv[q];
-        cU[s] = FULL ? 0.f : a.Uf[q];
+        const Prm pc = a.prm[cbase + s];
+        cdf[s] = pc.df; cdg[s] = pc.dg; cinv[s] = pc.inv; cU[s] = pc.U;
+    }
+    {   // pre-adjust so that the uniform recurrence at row i0 reproduces the seed
+        const Prm pr = a.prm[i0];
+#pragma unroll
+        for (int s = 0; s < D; ++s) {
+            cov[s] = fma(-cdf[s], pr.dg, cov[s]);
+            cov[s] = fma(-pr.df, cdg[s], cov[s]);
+        }
     }
     double colacc[D];
     if (FULL) {
 #pragma unroll
         for (int s = 0; s < D; ++s) colacc[s] = INFINITY;
     }
-    double rowres = INFINITY, colres = INFINITY;   // FULL: per-group parallel merges
+    double rowres = INFINITY, colres = INFINITY;   // FULL: stashed per-row results
     long long rowres_i = 0, colres_j = 0;
-    unsigned long long nmerge = 0;
+    unsigned long long nmerge = 0, nflush = 0;
+    int ccount = 0;                                 // filter: buffered candidates (warp-uniform)
 
     const int S = a.S;
     const int nrows = (int)(rows_valid < S ? rows_valid : S);
-    const int ngroups = (nrows - 1 + D - 1) / D;
+    const int ngroups = (nrows + D - 1) / D;
 
-    // one row step: k = phys offset of logical slot 0; first = peeled first row
-    auto row_step = [&](long long i, int k, bool first) {
-        const long long qi = pidx(i, P);
-        const double rinv = a.inv[qi];
-        const float rU = FULL ? 0.f : a.Uf[qi];
-        if (!first) {
-            const int pn = (k + D - 1) & (D - 1);
-            const long long q = pidx(i + d0 + dbase + D - 1, P);
-            cdf[pn] = a.df[q]; cdg[pn] = a.dg[q]; cinv[pn] = a.inv[q];
-            if (!FULL) cU[pn] = a.Uf[q];
-            const double rdf = a.df[qi], rdg = a.dg[qi];
-#pragma unroll
-            for (int s = 0; s < D; ++s) {
-                const int p = (s + k) & (D - 1);
-                cov[s] = fma(rdf, cdg[p], cov[s]);
-                cov[s] = fma(cdf[p], rdg, cov[s]);
-            }
+    auto flush_cands = [&]() {
+        __syncwarp();
+        for (int q = lane; q < ccount; q += 32) {
+            const Cand c = w.cand[q];
+            acc_merge(a.acc + c.o, c.key, c.idx);
         }
-        double r[D];
-#pragma unroll
-        for (int s = 0; s < D; ++s) {
-            const int p = (s + k) & (D - 1);
-            r[s] = fma(-(cov[s] * rinv), cinv[p], 1.0);
-        }
-        if (!FULL) {
-            bool pass = false;
-#pragma unroll
-            for (int s = 0; s < D; ++s) {
-                const int p = (s + k) & (D - 1);
-                const float h = __int_as_float(__double2hiint(r[s]));
-                pass |= sval[s] && ((h <= rU) | (h <= cU[p]));
-            }
-            if (__any_sync(FULLMASK, pass)) {
-#pragma unroll
-                for (int s = 0; s < D; ++s) {
-                    const int p = (s + k) & (D - 1);
-                    const float h = __int_as_float(__double2hiint(r[s]));
-                    const bool pr = sval[s] && (h <= rU), pc = sval[s] && (h <= cU[p]);
-                    if (pr | pc) {
-                        const unsigned long long key = clamp_key(r[s]);
-                        const long long j = i + d0 + dbase + s;
-                        if (pr) acc_merge(a.acc + i, key, j);
-                        if (pc) acc_merge(a.acc + j, key, i);
-                        nmerge += (unsigned)pr + (unsigned)pc;
-                    }
-                }
-            }
-        } else {
-            // rows: lane-local packed min, then warp all-reduce (packed diag index => no exact ties)
-            double rm = INFINITY;
-#pragma unroll
-            for (int s = 0; s < D; ++s) {
-                double v = r[s] < 0.0 ? 0.0 : r[s];     // clamp (NaN stays NaN)
-                if (!sval[s]) v = __longlong_as_double(0x7FF8000000000000ll);
-                const double pr = pack_low8(v, (unsigned)(dbase + s));
-                const double pc = pack_low8(v, (unsigned)(255 - (dbase + s)));
-                rm = pr < rm ? pr : rm;
-                const int p = (s + k) & (D - 1);
-                colacc[p] = pc < colacc[p] ? pc : colacc[p];
-            }
-#pragma unroll
-            for (int off = 16; off >= 1; off >>= 1) {
-                const double o = __shfl_xor_sync(FULLMASK, rm, off);
-                rm = o < rm ? o : rm;
-            }
-            // the exiting column (logical slot 0, phys k) travels to lane-1's slot D-1
-            const double x = colacc[k];
-            double y = __shfl_down_sync(FULLMASK, x, 1);
-            if (lane == 31) y = INFINITY;
-            colacc[k] = y;
-            const double x0 = __shfl_sync(FULLMASK, x, 0);   // lane 0's exiting column
-            // stash: lane ((i - i0 - 1) mod 32) keeps this row's result and the exiting column's;
-            // the warp merges 32 stashed results in parallel every 4 groups (flush_full)
-            const int slot = first ? 0 : (int)((i - i0 - 1) & 31);
-            if (lane == slot) { rowres = rm; rowres_i = i; colres = x0; colres_j = i + d0; }
-        }
+        nmerge += ccount; nflush += 1;
+        ccount = 0;
+        __syncwarp();
     };
-
     auto flush_full = [&]() {
         if (rowres < INFINITY) {
             const unsigned long long b = (unsigned long long)__double_as_longlong(rowres);
@@ -377,42 +338,169 @@ k_tile(TileArgs a) {
         rowres = INFINITY; colres = INFINITY;
     };
 
-    // peeled first row (cov = seed)
-    row_step(i0, 0, true);
-    if (FULL) flush_full();
-    long long i = i0 + 1;
+    stage_group(w, 0, a.prm, i0, d0, lane);
+    cp_async_wait_all();
+    __syncwarp();
+
     for (int g = 0; g < ngroups; ++g) {
+        const int b = g & 1;
+        if (g + 1 < ngroups) stage_group(w, b ^ 1, a.prm, i0 + (long long)(g + 1) * D, d0, lane);
+        Prm pr_next = w.row[b][0];
 #pragma unroll
         for (int kk = 0; kk < D; ++kk) {
-            row_step(i, (kk + 1) & (D - 1), false);
-            ++i;
+            const long long i = i0 + (long long)g * D + kk;
+            const Prm pr = pr_next;
+            if (kk + 1 < D) pr_next = w.row[b][kk + 1];
+            {   // ring rotation: phys (kk-1) mod D receives lane+1's outgoing column
+                const int q = (kk + D - 1) & (D - 1);
+                double ndf = __shfl_down_sync(FULLMASK, cdf[q], 1);
+                double ndg = __shfl_down_sync(FULLMASK, cdg[q], 1);
+                double ninv = __shfl_down_sync(FULLMASK, cinv[q], 1);
+                float nU = __shfl_down_sync(FULLMASK, cU[q], 1);
+                if (g > 0 || kk > 0) {   // at the tile's first row the ring already holds slot D-1
+                    if (lane == 31) {
+                        const Prm f = w.fresh[b][kk];
+                        ndf = f.df; ndg = f.dg; ninv = f.inv; nU = f.U;
+                    }
+                    cdf[q] = ndf; cdg[q] = ndg; cinv[q] = ninv; cU[q] = nU;
+                }
+            }
+#pragma unroll
+            for (int s = 0; s < D; ++s) {
+                const int p = (s + kk) & (D - 1);
+                cov[s] = fma(pr.df, cdg[p], cov[s]);
+                cov[s] = fma(cdf[p], pr.dg, cov[s]);
+            }
+            if (!FULL) {
+                bool pass = false;
+#pragma unroll
+                for (int s = 0; s < D; ++s) {
+                    const int p = (s + kk) & (D - 1);
+                    const double r = fma(-(cov[s] * pr.inv), cinv[p], 1.0);
+                    const float h = __int_as_float(__double2hiint(r));
+                    pass |= sval[s] && (h <= fmaxf(pr.U, cU[p]));
+                }
+                if (__any_sync(FULLMASK, pass)) {
+                    // exact candidates: the row's best (key, j) over the warp + every column hit
+                    unsigned long long bk = KEY_NONE; long long bj = IDX_NONE;
+                    unsigned ncol = 0;
+                    bool pc[D]; unsigned long long kc[D];
+#pragma unroll
+                    for (int s = 0; s < D; ++s) {
+                        const int p = (s + kk) & (D - 1);
+                        const double r = fma(-(cov[s] * pr.inv), cinv[p], 1.0);
+                        const float h = __int_as_float(__double2hiint(r));
+                        const unsigned long long key = clamp_key(r) & ~0xFFull;
+                        kc[s] = key;
+                        pc[s] = sval[s] && (h <= cU[p]);
+                        if (sval[s] && (h <= pr.U) && key < bk) { bk = key; bj = i + d0 + dbase + s; }
+                        ncol += __popc(__ballot_sync(FULLMASK, pc[s]));
+                    }
+#pragma unroll
+                    for (int off = 16; off >= 1; off >>= 1) {
+                        const unsigned long long ok = __shfl_xor_sync(FULLMASK, bk, off);
+                        const long long oj = __shfl_xor_sync(FULLMASK, bj, off);
+                        if (key_less(ok, oj, bk, bj)) { bk = ok; bj = oj; }
+                    }
+                    const unsigned nnew = ncol + (bk != KEY_NONE ? 1u : 0u);
+                    if (ccount + (int)nnew > CAND_CAP) flush_cands();
+                    if ((int)nnew > CAND_CAP) {
+                        // pathological row step (e.g. offsets without a bound): merge directly
+                        if (lane == 0 && bk != KEY_NONE) acc_merge(a.acc + i, bk, bj);
+#pragma unroll
+                        for (int s = 0; s < D; ++s)
+                            if (pc[s]) acc_merge(a.acc + (i + d0 + dbase + s), kc[s], i);
+                        nmerge += nnew;
+                    } else {
+                        if (bk != KEY_NONE) {
+                            if (lane == 0) w.cand[ccount] = Cand{(int)i, (int)bj, bk};
+                            ++ccount;
+                        }
+                        const unsigned lt = (1u << lane) - 1u;
+#pragma unroll
+                        for (int s = 0; s < D; ++s) {
+                            const unsigned bal = __ballot_sync(FULLMASK, pc[s]);
+                            if (pc[s]) w.cand[ccount + __popc(bal & lt)] = Cand{(int)(i + d0 + dbase + s), (int)i, kc[s]};
+                            ccount += __popc(bal);
+                        }
+                    }
+                }
+            } else {
+                // rows: lane-local packed min, then warp all-reduce (packed diag index => no exact ties)
+                double rm = INFINITY;
+#pragma unroll
+                for (int s = 0; s < D; ++s) {
+                    const int p = (s + kk) & (D - 1);
+                    const double r = fma(-(cov[s] * pr.inv), cinv[p], 1.0);
+                    double v = r < 0.0 ? 0.0 : r;     // clamp (NaN stays NaN)
+                    if (!sval[s]) v = __longlong_as_double(0x7FF8000000000000ll);
+                    const double pkr = pack_low8(v, (unsigned)(dbase + s));
+                    const double pkc = pack_low8(v, (unsigned)(255 - (dbase + s)));
+                    rm = pkr < rm ? pkr : rm;
+                    colacc[p] = pkc < colacc[p] ? pkc : colacc[p];
+                }
+#pragma unroll
+                for (int off = 16; off >= 1; off >>= 1) {
+                    const double o = __shfl_xor_sync(FULLMASK, rm, off);
+                    rm = o < rm ? o : rm;
+                }
+                // the exiting column (logical slot 0, phys kk) travels to lane-1's slot D-1
+                const double x = colacc[kk];
+                double y = __shfl_down_sync(FULLMASK, x, 1);
+                if (lane == 31) y = INFINITY;
+                colacc[kk] = y;
+                const double x0 = __shfl_sync(FULLMASK, x, 0);   // lane 0's exiting column
+                const int slot = (int)((i - i0) & 31);
+                if (lane == slot) { rowres = rm; rowres_i = i; colres = x0; colres_j = i + d0; }
+            }
         }
         if (FULL && (g & 3) == 3) flush_full();
+        cp_async_wait_all();
+        __syncwarp();
     }
     if (FULL) {
         flush_full();
-        // remaining column accumulators: after the last row (phys offset kl), phys p holds the
-        // column of logical slot ((p - kl - 1) mod D) at row i (= last + 1)
-        const int kl = (ngroups * D) & (D - 1);   // phys offset of the last processed row
+        // after the last row (kk = D-1) and its rotate, phys p holds the column of logical
+        // slot p at row i_end = i0 + 8*ngroups
+        const long long i_end = i0 + (long long)ngroups * D;
 #pragma unroll
         for (int p = 0; p < D; ++p) {
             const double v = colacc[p];
             if (v < INFINITY) {
-                const int s = (p - kl - 1 + 2 * D) & (D - 1);
-                const long long j = i + d0 + dbase + s;
-                const unsigned long long b = (unsigned long long)__double_as_longlong(v);
-                const long long diag = 255 - (long long)(b & 0xFFull);
-                acc_merge(a.acc + j, b & ~0xFFull, j - d0 - diag);
+                const long long j = i_end + d0 + dbase + p;
+                const unsigned long long bits = (unsigned long long)__double_as_longlong(v);
+                const long long diag = 255 - (long long)(bits & 0xFFull);
+                acc_merge(a.acc + j, bits & ~0xFFull, j - d0 - diag);
             }
         }
+    } else {
+        if (ccount) flush_cands();
+        if (lane == 0 && nmerge) { atomicAdd(a.counters, nmerge); atomicAdd(a.counters + 1, nflush); }
     }
-    if (!FULL && nmerge) atomicAdd(a.counters, nmerge);
+}
+
+template <bool FULL>
+__global__ void __launch_bounds__(WARPS_PER_CTA * 32)
+k_tile(TileArgs a) {
+    extern __shared__ __align__(128) unsigned char smem_raw[];
+    WarpSmem* ws = reinterpret_cast<WarpSmem*>(smem_raw);
+    const int lane = threadIdx.x & 31;
+    const int wl = threadIdx.x >> 5;
+    const int wid = blockIdx.x * WARPS_PER_CTA + wl;
+    if (wid >= a.n_tiles) return;
+    const int2 tl = a.tiles[wid];
+    const long long d0 = a.dlo + (long long)tl.x * BAND;
+    const long long i0 = (long long)tl.y * a.S;
+    const long long rows_valid = a.N - d0 - i0;
+    if (rows_valid <= 0 || d0 + BAND - 1 < a.e) return;   // empty, or entirely trivial
+    if (d0 < a.e) tile_body<FULL, true>(a, ws[wl], wid, lane, d0, i0, rows_valid);
+    else tile_body<FULL, false>(a, ws[wl], wid, lane, d0, i0, rows_valid);
 }
 
 // initial seeds: centred direct sums at the first length
 struct SeedArgs {
     const double* tn; const double* mu; const int2* tiles; double* seeds;
-    long long P, dlo; int n_tiles, S, m;
+    long long dlo; int n_tiles, S, m;
 };
 
 __global__ void k_seed_init(SeedArgs a) {
@@ -422,11 +510,11 @@ __global__ void k_seed_init(SeedArgs a) {
     const int2 tl = a.tiles[wid];
     const long long d0 = a.dlo + (long long)tl.x * BAND;
     const long long i0 = (long long)tl.y * a.S;
-    const double mi = a.mu[pidx(i0, a.P)];
+    const double mi = a.mu[i0];
     double acc[D], mc[D];
     const long long cb = i0 + d0 + lane * D;
 #pragma unroll
-    for (int s = 0; s < D; ++s) { acc[s] = 0.0; mc[s] = a.mu[pidx(cb + s, a.P)]; }
+    for (int s = 0; s < D; ++s) { acc[s] = 0.0; mc[s] = a.mu[cb + s]; }
     for (int k = 0; k < a.m; ++k) {
         const double x = a.tn[i0 + k] - mi;
 #pragma unroll
@@ -675,12 +763,11 @@ struct vlmp_session {
     cudaEvent_t ev[8] = {};
     std::mutex lock;
     // series
-    long long n = 0, A = 0, P = 0;
+    long long n = 0, A = 0;
     double floor_ = 0.0;
     double* d_tn = nullptr; double* d_cum = nullptr; double* d_cum2 = nullptr;
     // per-length scratch
-    double* d_df = nullptr; double* d_dg = nullptr; double* d_inv = nullptr; double* d_mu = nullptr;
-    float* d_Uf = nullptr;
+    Prm* d_prm = nullptr; double* d_mu = nullptr;
     long long* d_previdx = nullptr;
     // tiles / seeds
     int2* d_tiles = nullptr; size_t tiles_cap = 0;
@@ -775,7 +862,7 @@ void vlmp_destroy(vlmp_session* s) {
     if (!s) return;
     cudaSetDevice(s->device);
     cudaStreamSynchronize(s->stream);
-    void* ptrs[] = {s->d_tn, s->d_cum, s->d_cum2, s->d_df, s->d_dg, s->d_inv, s->d_mu, s->d_Uf,
+    void* ptrs[] = {s->d_tn, s->d_cum, s->d_cum2, s->d_prm, s->d_mu,
                     s->d_previdx, s->d_tiles, s->d_seeds, s->d_acc, s->d_mp, s->d_ip, s->d_counters, s->d_vdist, s->d_vnorm, s->d_vlen, s->d_vidx, s->d_vpop};
     for (void* p : ptrs) if (p) cudaFree(p);
     for (auto& ev : s->ev) if (ev) cudaEventDestroy(ev);
@@ -791,16 +878,13 @@ int vlmp_set_series(vlmp_session* s, const double* t, const double* cum, const d
     std::lock_guard<std::mutex> g(s->lock);
     CU(cudaSetDevice(s->device));
     long long A = ((n + 1024 + 255) / 256) * 256 + 256;
-    s->n = n; s->A = A; s->P = A / D; s->floor_ = sigma_floor;
+    s->n = n; s->A = A; s->floor_ = sigma_floor;
     int rc;
     if ((rc = ensure1(s->d_tn, 2 * A + 4096))) return rc;
     if ((rc = ensure1(s->d_cum, n + 1))) return rc;
     if ((rc = ensure1(s->d_cum2, n + 1))) return rc;
-    if ((rc = ensure1(s->d_df, A))) return rc;
-    if ((rc = ensure1(s->d_dg, A))) return rc;
-    if ((rc = ensure1(s->d_inv, A))) return rc;
+    if ((rc = ensure1(s->d_prm, A))) return rc;
     if ((rc = ensure1(s->d_mu, A))) return rc;
-    if ((rc = ensure1(s->d_Uf, A))) return rc;
     if ((rc = ensure1(s->d_previdx, A))) return rc;
     CU(cudaMemsetAsync(s->d_tn, 0, (2 * A + 4096) * sizeof(double), s->stream));
     CU(cudaMemcpyAsync(s->d_tn, t, n * sizeof(double), cudaMemcpyHostToDevice, s->stream));
@@ -845,29 +929,29 @@ int vlmp_profile_range(vlmp_session* s, int32_t lmin, int32_t lmax, int64_t band
     std::lock_guard<std::mutex> g(s->lock);
     CU(cudaSetDevice(s->device));
     cudaStream_t st = s->stream;
-    const long long n = s->n, A = s->A, P = s->P;
+    const long long n = s->n, A = s->A;
     const int n_len = lmax - lmin + 1;
     const long long nb = n_bands_for(n, lmin);
     if (band_hi < 0 || band_hi > nb) band_hi = nb;
     if (band_lo < 0) band_lo = 0;
     const int S = seg_rows(n);
     const long long N0 = n - lmin + 1, dl = dlo_for(lmin);
-    // tile list (band-major) for this shard, using N at lmin (superset of later lengths)
+    // tile list (band-major: the near-diagonal, candidate-heavy bands start first),
+    // using N at lmin (a superset of every later length's tiles)
     std::vector<int2> tiles;
-    std::vector<long long> band_first;   // first tile index of each band in the shard
     for (long long b = band_lo; b < band_hi; ++b) {
-        band_first.push_back((long long)tiles.size());
-        long long d0 = dl + b * BAND;
-        long long rows = N0 - d0;
+        long long rows = N0 - (dl + b * BAND);
         for (long long sg = 0; sg * S < rows; ++sg) tiles.push_back(make_int2((int)b, (int)sg));
     }
-    band_first.push_back((long long)tiles.size());
     const long long T = (long long)tiles.size();
     int rc;
     if ((rc = ensure(s->d_tiles, s->tiles_cap, (size_t)std::max<long long>(T, 1)))) return rc;
     if ((rc = ensure(s->d_seeds, s->seeds_cap, (size_t)std::max<long long>(T, 1) * BAND))) return rc;
     if ((rc = ensure(s->d_acc, s->acc_cap, (size_t)n_len * A))) return rc;
     if (T) CU(cudaMemcpyAsync(s->d_tiles, tiles.data(), T * sizeof(int2), cudaMemcpyHostToDevice, st));
+    const size_t smem = WARPS_PER_CTA * sizeof(WarpSmem);
+    CU(cudaFuncSetAttribute(k_tile<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    CU(cudaFuncSetAttribute(k_tile<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
     k_fill_acc<<<blocks((long long)n_len * A, 256), 256, 0, st>>>(s->d_acc, (long long)n_len * A);
     CU(cudaMemsetAsync(s->d_counters, 0, 8 * sizeof(unsigned long long), st));
     CU(cudaEventRecord(s->ev[0], st));
@@ -878,59 +962,39 @@ int vlmp_profile_range(vlmp_session* s, int32_t lmin, int32_t lmax, int64_t band
         const int m = lmin + li;
         const long long N = n - m + 1;
         const int e = (m + 1) / 2;
-        ParamArgs pa{s->d_tn, s->d_cum, s->d_cum2, s->d_df, s->d_dg, s->d_inv, s->d_mu, n, N, A, P, m, s->floor_};
+        ParamArgs pa{s->d_tn, s->d_cum, s->d_cum2, s->d_prm, s->d_mu, n, N, A, m, s->floor_};
         k_params<<<blocks(A, 256), 256, 0, st>>>(pa);
         ++klaunch;
         const bool full = (li == 0) || (flags & VLMP_F_FULL_EVERY_LENGTH);
         if (li == 0 && T) {
-            SeedArgs sa{s->d_tn, s->d_mu, s->d_tiles, s->d_seeds, P, dl, (int)T, S, m};
+            SeedArgs sa{s->d_tn, s->d_mu, s->d_tiles, s->d_seeds, dl, (int)T, S, m};
             k_seed_init<<<blocks(T * 32, WARPS_PER_CTA * 32), WARPS_PER_CTA * 32, 0, st>>>(sa);
             ++klaunch;
         }
         if (!full) {
             k_acc_idx<<<blocks(N + 1, 256), 256, 0, st>>>(s->d_acc + (long long)(li - 1) * A, s->d_previdx, N + 1);
-            BoundArgs ba{s->d_tn, s->d_mu, s->d_inv, s->d_previdx, s->d_Uf, N, N + 1, A, P, m, e, margin};
-            k_bound<<<blocks(A, 128), 128, 0, st>>>(ba);
+            BoundArgs ba{s->d_tn, s->d_mu, s->d_prm, s->d_previdx, N, N + 1, m, e, margin};
+            k_bound<<<blocks(N, 128), 128, 0, st>>>(ba);
             klaunch += 2;
         }
-        // tiles: skip bands entirely inside the exclusion zone; masked = bands straddling it
-        long long b_skip = band_lo, b_mask = band_lo;
-        while (b_skip < band_hi && dl + b_skip * BAND + BAND - 1 < e) ++b_skip;
-        b_mask = b_skip;
-        while (b_mask < band_hi && dl + b_mask * BAND < e) ++b_mask;
-        const long long t_skip = band_first[b_skip - band_lo];
-        const long long t_mask = band_first[b_mask - band_lo];
-        TileArgs ta{s->d_df, s->d_dg, s->d_inv, s->d_Uf, s->d_mu, s->d_tn, s->d_tiles, s->d_seeds,
-                    s->d_acc + (long long)li * A, s->d_counters, P, N, dl, 0, S, m, e, li + 1 < n_len};
         while (s->lev.size() < (size_t)2 * (li + 1)) {
             cudaEvent_t ev; CU(cudaEventCreate(&ev)); s->lev.push_back(ev);
         }
         CU(cudaEventRecord(s->lev[2 * li], st));
-        auto launch = [&](long long t0, long long t1, bool masked) {
-            if (t1 <= t0) return;
-            TileArgs tb = ta;
-            tb.tiles = s->d_tiles + t0;
-            tb.seeds = s->d_seeds + t0 * BAND;
-            tb.n_tiles = (int)(t1 - t0);
-            unsigned g = blocks(t1 - t0, WARPS_PER_CTA);
-            if (full) {
-                if (masked) k_tile<true, true><<<g, WARPS_PER_CTA * 32, 0, st>>>(tb);
-                else k_tile<true, false><<<g, WARPS_PER_CTA * 32, 0, st>>>(tb);
-            } else {
-                if (masked) k_tile<false, true><<<g, WARPS_PER_CTA * 32, 0, st>>>(tb);
-                else k_tile<false, false><<<g, WARPS_PER_CTA * 32, 0, st>>>(tb);
-            }
+        if (T) {
+            TileArgs ta{s->d_prm, s->d_mu, s->d_tn, s->d_tiles, s->d_seeds, s->d_acc + (long long)li * A,
+                        s->d_counters, N, dl, (int)T, S, m, e, li + 1 < n_len};
+            unsigned g = blocks(T, WARPS_PER_CTA);
+            if (full) k_tile<true><<<g, WARPS_PER_CTA * 32, smem, st>>>(ta);
+            else k_tile<false><<<g, WARPS_PER_CTA * 32, smem, st>>>(ta);
             launches += 1; klaunch += 1;
-        };
-        launch(t_skip, t_mask, true);
-        launch(t_mask, T, false);
+        }
         CU(cudaEventRecord(s->lev[2 * li + 1], st));
         CU(cudaGetLastError());
-        // executed cell updates (upper triangle cells swept by the launched tiles)
-        for (long long b = b_skip; b < band_hi; ++b) {
+        for (long long b = band_lo; b < band_hi; ++b) {
             long long d0 = dl + b * BAND;
             long long rows = N - d0;
-            if (rows <= 0) continue;
+            if (rows <= 0 || d0 + BAND - 1 < e) continue;
             executed += (double)rows * BAND;
         }
         if (full) n_full += 1; else n_filtered += 1;
@@ -1147,6 +1211,21 @@ int vlmp_ranking_events(vlmp_session* s, double tau, int64_t cap, int64_t* ev_of
 int vlmp_stats(vlmp_session* s, double* out, int32_t n_out) {
     if (!s || !out) return fail(VLMP_E_INVALID_PARAMETERS, "null argument");
     for (int q = 0; q < n_out && q < 16; ++q) out[q] = s->stats[q];
+    return 0;
+}
+
+int vlmp_event_record(vlmp_session* s, int32_t slot) {
+    if (!s || slot < 0 || slot > 1) return fail(VLMP_E_INVALID_PARAMETERS, "slot must be 0 or 1");
+    CU(cudaSetDevice(s->device));
+    CU(cudaEventRecord(s->ev[6 + slot], s->stream));
+    return 0;
+}
+
+int vlmp_event_elapsed(vlmp_session* s, float* ms) {
+    if (!s || !ms) return fail(VLMP_E_INVALID_PARAMETERS, "null argument");
+    CU(cudaSetDevice(s->device));
+    CU(cudaEventSynchronize(s->ev[7]));
+    CU(cudaEventElapsedTime(ms, s->ev[6], s->ev[7]));
     return 0;
 }
 

@@ -1,0 +1,106 @@
+"""Multi-GPU sharding: one process per GPU, diagonal bands split by work,
+per-(length, offset) minima merged exactly with two NCCL MIN all-reduces.
+
+Partition. The pair triangle at length l holds cells (i, i+d), d >= ceil(l/2).
+Bands of 256 consecutive diagonals are the unit (one warp tile wide); band b's
+work summed over lengths is sum_l sum_{d in b, d >= e_l} (N_l - d)_+ (closed
+form per length). Ranks get contiguous band ranges of equal cumulative work
+(SURVEY.md §8(e)). No data moves between ranks during the scan: each rank's
+filter bound comes from its own previous-length winners (any valid cell value is
+an upper bound on the global minimum, so rank-local bounds stay exact).
+
+Exchange. Per (length, offset) every rank holds (key, idx): key = order-
+preserving uint64 bits of the clamped r' = 1 - corr (+inf bits = none), idx =
+neighbour. The lexicographic (key, smallest idx) rule of profile.py:308 is
+realised as: all-reduce MIN over keys; idx := INT64_MAX where the local key
+differs from the merged key; all-reduce MIN over idx. Keys are non-negative
+doubles, so their bit patterns order correctly as int64.
+"""
+
+from __future__ import annotations
+
+import numpy as np
+
+BAND = 256
+IDX_NONE = np.iinfo(np.int64).max
+
+
+def dlo(lmin: int) -> int:
+    return (lmin + 1) // 2
+
+
+def n_bands(n: int, lmin: int) -> int:
+    N = n - lmin + 1
+    span = N - dlo(lmin)
+    return (span + BAND - 1) // BAND if span > 0 else 0
+
+
+def band_work(n: int, lmin: int, lmax: int, b: int) -> float:
+    d_lo = dlo(lmin) + b * BAND
+    d_hi = d_lo + BAND
+    w = 0.0
+    for m in range(lmin, lmax + 1):
+        N = n - m + 1
+        lo, hi = max(d_lo, (m + 1) // 2), min(d_hi, N)
+        if hi > lo:
+            w += (hi - lo) * N - (lo + hi - 1) * (hi - lo) / 2.0
+    return w
+
+
+def band_split(n: int, lmin: int, lmax: int, parts: int) -> np.ndarray:
+    """Contiguous band cuts with equal cumulative work (same rule as vlmp_band_split)."""
+    nb = n_bands(n, lmin)
+    w = np.array([band_work(n, lmin, lmax, b) for b in range(nb)])
+    tot = w.sum()
+    cuts = np.zeros(parts + 1, dtype=np.int64)
+    acc, b = 0.0, 0
+    for p in range(1, parts):
+        target = tot * p / parts
+        while b < nb and acc + w[b] <= target:
+            acc += w[b]
+            b += 1
+        cuts[p] = b
+    cuts[parts] = nb
+    return cuts
+
+
+def merge_partials(keys, idx, group=None):
+    """Exact (key, smallest idx) merge of torch int64 tensors across the group,
+    in place. Works for any backend (NCCL on GPU tensors, gloo on CPU tensors)."""
+    import torch
+    import torch.distributed as dist
+    merged = keys.clone()
+    dist.all_reduce(merged, op=dist.ReduceOp.MIN, group=group)
+    idx.masked_fill_(keys != merged, IDX_NONE)
+    dist.all_reduce(idx, op=dist.ReduceOp.MIN, group=group)
+    keys.copy_(merged)
+    return keys, idx
+
+
+def profile_sharded(sess, series, lmin: int, lmax: int, rank: int, world: int, group=None):
+    """Run this rank's bands on its session's device and merge with the group.
+    Leaves the merged per-length minima imported in ``sess``; call sess.finalize()."""
+    import torch
+    cuts = band_split(series.n, lmin, lmax, world)
+    with sess.lock:
+        sess.set_series(series.values, series._cum, series._cum2, series.sigma_floor)
+        sess.profile(lmin, lmax, int(cuts[rank]), int(cuts[rank + 1]), 0)
+        n_len, stride = sess.partials_size()
+        dev = torch.device("cuda", sess.device)
+        keys = torch.empty(n_len * stride, dtype=torch.int64, device=dev)
+        idx = torch.empty(n_len * stride, dtype=torch.int64, device=dev)
+        sess.partials_export(keys.data_ptr(), idx.data_ptr())
+    if world > 1:
+        import torch.distributed as dist
+        merged = keys.clone()
+        dist.all_reduce(merged, op=dist.ReduceOp.MIN, group=group)
+        torch.cuda.synchronize(dev)
+        with sess.lock:
+            sess.partials_mask_idx(merged.data_ptr(), keys.data_ptr(), idx.data_ptr())
+        dist.all_reduce(idx, op=dist.ReduceOp.MIN, group=group)
+        torch.cuda.synchronize(dev)
+        keys = merged
+    with sess.lock:
+        sess.partials_import(keys.data_ptr(), idx.data_ptr())
+        sess.finalize()
+    return cuts

@@ -1,0 +1,238 @@
+"""Parity of the CUDA path (through the C ABI) with the reference.
+
+Anchors, in order of strength:
+  * tests/golden/*.npz -- outputs of the REAL reference (seriesmine engine and its
+    brute-force oracle), generated here by tests/golden/make_golden.py;
+  * the CPU oracle (oracle/), itself pinned to those fixtures by
+    test_oracle_golden.py, for cases without a fixture;
+  * size-independent properties at BASELINE sizes (sampled row recomputes).
+Tolerances: indices and lengths exact; distances 1e-7 absolute (the reference's
+own tests, test_valmod.py:149-151) and <= 1e-6 relative (BASELINE north star).
+"""
+
+import numpy as np
+import pytest
+
+import paper_2008_13447_b200 as vl
+from paper_2008_13447_b200 import _lib, api, gen
+from conftest import SMALL_CASES, load_golden
+
+pytestmark = pytest.mark.gpu
+
+
+@pytest.fixture(scope="module", autouse=True)
+def _device():
+    import torch
+    assert torch.cuda.is_available(), "GPU tests need a B200"
+    _lib.load()
+
+
+def _gpu_run(t, lmin, lmax, flags=0):
+    return api.GpuRun(vl.ingest(t), lmin, lmax, flags=flags)
+
+
+@pytest.mark.parametrize("name", SMALL_CASES)
+def test_valmod_matches_reference_small(name):
+    g = load_golden(f"small_{name}")
+    s = vl.ingest(g["t"])
+    lmin, lmax = int(g["lmin"]), int(g["lmax"])
+    trace = vl.RunTrace()
+    ranking = vl.PairRanking(10)
+    v = vl.valmod(s, lmin, lmax, 5, ranking=ranking, trace=trace)
+    assert np.array_equal(v.indices, g["valmp_idx"])
+    assert np.array_equal(v.lengths, g["valmp_len"])
+    assert np.array_equal(v.populated, g["valmp_pop"])
+    assert np.allclose(v.norm_distances[v.populated], g["valmp_norm"][g["valmp_pop"]], atol=1e-7)
+    assert np.allclose(v.distances[v.populated], g["valmp_dist"][g["valmp_pop"]], atol=1e-7)
+    got = [r.motif for r in trace.records]
+    assert [m[:2] for m in got] == [(int(a), int(b)) for a, b, _ in g["motif"]]
+    assert np.allclose([m[2] for m in got], g["motif"][:, 2], atol=1e-7)
+    ref_rank = [(int(x[0]), int(x[1]), int(x[2])) for x in g["ranking"]]
+    assert [(p.off1, p.off2, p.length) for p in ranking] == ref_rank
+    assert np.allclose([p.norm_distance for p in ranking], g["ranking"][:, 4], atol=1e-7)
+    top = vl.top_variable_length_motif(v)
+    ref_top = int(np.argmin(np.where(g["valmp_pop"], g["valmp_norm"], np.inf)))
+    assert top[0] == ref_top
+
+
+@pytest.mark.parametrize("name", SMALL_CASES)
+@pytest.mark.parametrize("k", [1, 3])
+def test_discords_match_reference_small(name, k):
+    g = load_golden(f"small_{name}")
+    s = vl.ingest(g["t"])
+    lmin, lmax = int(g["lmin"]), int(g["lmax"])
+    trace = vl.RunTrace()
+    scan = vl.topkm_discord_discovery(s, lmin, lmax, k, 1, 5, trace=trace)
+    for L in range(lmin, lmax + 1):
+        e, o = scan.per_length[L], g[f"k{k}_disc_off"][L - lmin]
+        assert np.array_equal(e.offset, o), L
+        fin = np.isfinite(g[f"k{k}_disc_dist"][L - lmin])
+        assert np.allclose(e.dist[fin], g[f"k{k}_disc_dist"][L - lmin][fin], atol=1e-7)
+    assert np.array_equal(scan.merged.offset, g[f"k{k}_merged_off"])
+    assert np.array_equal(scan.merged.length, g[f"k{k}_merged_len"])
+    assert np.allclose(scan.merged.dist, g[f"k{k}_merged_dist"], atol=1e-7)
+    assert sum(r.n_recomputed for r in trace.records) == 0
+
+
+@pytest.mark.parametrize("name", SMALL_CASES)
+def test_profiles_match_reference_bruteforce(name):
+    """Every per-length profile vs the reference's cdist oracle (IP exact)."""
+    g = load_golden(f"small_{name}")
+    lmin, lmax = int(g["lmin"]), int(g["lmax"])
+    run = _gpu_run(g["t"], lmin, lmax)
+    for L in range(lmin, lmax + 1):
+        mp, ip = run.profile(L)
+        N = mp.shape[0]
+        assert np.array_equal(ip, g["oracle_ip"][L - lmin, :N]), L
+        fin = np.isfinite(mp)
+        assert np.array_equal(fin, np.isfinite(g["oracle_mp"][L - lmin, :N]))
+        assert np.allclose(mp[fin], g["oracle_mp"][L - lmin, :N][fin], atol=1e-7)
+
+
+@pytest.mark.parametrize("name", SMALL_CASES[:3])
+def test_filter_mode_equals_full_fold_mode(name):
+    """The bound-filtered kernel and the exact full-fold kernel pick identical neighbours."""
+    g = load_golden(f"small_{name}")
+    lmin, lmax = int(g["lmin"]), int(g["lmax"])
+    a = _gpu_run(g["t"], lmin, lmax, flags=0)
+    pa = [a.profile(L) for L in range(lmin, lmax + 1)]
+    b = _gpu_run(g["t"], lmin, lmax, flags=_lib.FLAG_FULL_EVERY_LENGTH)
+    for L, (mp, ip) in zip(range(lmin, lmax + 1), pa):
+        mp2, ip2 = b.profile(L)
+        assert np.array_equal(ip, ip2), L
+        assert np.array_equal(mp, mp2), L
+
+
+def test_cfg1_matches_reference():
+    g = load_golden("cfg1")
+    s = vl.ingest(g["t"])
+    trace = vl.RunTrace()
+    v = vl.valmod(s, 32, 64, 50, trace=trace)
+    assert np.array_equal(v.indices, g["valmp_idx"])
+    assert np.array_equal(v.lengths, g["valmp_len"])
+    assert np.allclose(v.norm_distances, g["valmp_norm"], atol=1e-7)
+    assert [r.motif[:2] for r in trace.records] == [(int(a), int(b)) for a, b, _ in g["motif"]]
+    top = vl.top_variable_length_motif(v)
+    assert top[:3] == (1661, 934, 62)                       # SURVEY.md §8(c) anchor
+    scan = vl.topkm_discord_discovery(s, 32, 64, 3, 1, 50)
+    for L in range(32, 65):
+        assert np.array_equal(scan.per_length[L].offset, g["k3_disc_off"][L - 32]), L
+    assert np.array_equal(scan.merged.offset, g["k3_merged_off"])
+    scan1 = vl.topkm_discord_discovery(s, 32, 64, 1, 1, 50)
+    assert int(scan1.per_length[32].offset[0, 0]) == 3572   # SURVEY.md §8(c) anchor
+    top3 = vl.motifs_per_length(s, 32, 64, 3)
+    for L in range(32, 65):
+        ref = [(int(a), int(b)) for a, b, _ in g["top3_pairs"][L - 32] if a >= 0]
+        assert [(a, b) for a, b, _ in top3[L]] == ref, L
+        refd = [d for a, _, d in g["top3_pairs"][L - 32] if a >= 0]
+        assert np.allclose([d for _, _, d in top3[L]], refd, rtol=1e-6)
+
+
+def test_cfg2_discords_match_reference():
+    """Config 2 at full size (n=65,536, lengths 256..384, k=3) vs the reference engine."""
+    g = load_golden("cfg2_discords")
+    s = vl.ingest(gen.series_for(2))
+    scan = vl.topkm_discord_discovery(s, 256, 384, 3, 1, 50)
+    for L in range(256, 385):
+        assert np.array_equal(scan.per_length[L].offset, g["k3_disc_off"][L - 256]), L
+        fin = np.isfinite(g["k3_disc_dist"][L - 256])
+        ref = g["k3_disc_dist"][L - 256][fin]
+        assert np.allclose(scan.per_length[L].dist[fin], ref, rtol=1e-6)
+    assert np.array_equal(scan.merged.offset, g["k3_merged_off"])
+    assert np.array_equal(scan.merged.length, g["k3_merged_len"])
+
+
+def test_cfg2_valmod_matches_reference():
+    g = load_golden("cfg2_valmod")
+    s = vl.ingest(gen.series_for(2))
+    trace = vl.RunTrace()
+    v = vl.valmod(s, 256, 384, 50, trace=trace)
+    assert np.array_equal(v.lengths, g["valmp_len"])
+    assert np.array_equal(v.indices, g["valmp_idx"])
+    assert np.allclose(v.norm_distances, g["valmp_norm"], rtol=1e-6)
+    assert [r.motif[:2] for r in trace.records] == [(int(a), int(b)) for a, b, _ in g["motif"]]
+
+
+def test_cfg2_sampled_rows_against_oracle(oracle_mod):
+    """Size-independent check at BASELINE config 2: random (row, length) profiles
+    recomputed by the oracle's exhaustive row scan."""
+    s = vl.ingest(gen.series_for(2))
+    run = api.GpuRun(s, 256, 384)
+    rng = np.random.default_rng(0)
+    for L in (256, 300, 384):
+        mp, ip = run.profile(L)
+        rows = rng.integers(0, mp.shape[0], 24)
+        for r in rows:
+            omp, oip = oracle_mod.profile(s, L, nthreads=8, row_lo=int(r), row_hi=int(r) + 1)
+            assert ip[r] == oip[r], (L, r)
+            assert mp[r] == pytest.approx(omp[r], rel=1e-6, abs=1e-9)
+    # the planted pair (5234, 10194) is the top motif around its length
+    motifs = {r: None for r in range(1)}
+    off, nbr, d = run.smallest_rows(1)
+    assert sorted((int(off[300 - 256, 0]), int(nbr[300 - 256, 0]))) == [5234, 10194]
+
+
+@pytest.mark.parametrize("case", ["constant_stretch", "dc_offset", "short", "spikes", "lmin4"])
+def test_edge_cases_against_oracle(case, oracle_mod):
+    rng = np.random.default_rng(7)
+    lmin, lmax = 16, 40
+    if case == "constant_stretch":
+        t = np.cumsum(rng.standard_normal(900)); t[200:330] = 3.0; t[600:620] = -1.0
+    elif case == "dc_offset":
+        t = 1e4 + np.cumsum(rng.standard_normal(900))
+    elif case == "short":
+        t = np.cumsum(rng.standard_normal(lmax + (lmax + 1) // 2 + 1))
+        lmin, lmax = 30, 40
+    elif case == "spikes":
+        t = np.sin(np.arange(1200) * 2 * np.pi / 50) + rng.normal(0, 0.05, 1200); t[300] += 6
+    else:
+        t = np.cumsum(rng.standard_normal(500)); lmin, lmax = 4, 12
+    s = vl.ingest(t)
+    ref = oracle_mod.run(s, lmin, lmax, k_discord=2, keep_profiles=True)
+    run = api.GpuRun(s, lmin, lmax)
+    for L in range(lmin, lmax + 1):
+        mp, ip = run.profile(L)
+        omp, oip = ref["profiles"][L]
+        assert np.array_equal(ip, oip), (case, L)
+        fin = np.isfinite(omp)
+        assert np.array_equal(np.isfinite(mp), fin)
+        assert np.allclose(mp[fin], omp[fin], rtol=1e-6, atol=1e-7)
+    d, o = run.discords(2)
+    assert np.array_equal(o, ref["disc_off"])
+    v = run.valmp()
+    assert np.array_equal(v.indices, ref["valmp_idx"]) and np.array_equal(v.lengths, ref["valmp_len"])
+
+
+def test_exact_duplicates_clamp_to_zero():
+    """Duplicated windows: the radicand clamps to 0 and ties go to the smallest index
+    (the reference engine resolves these by rounding noise; its brute-force oracle by
+    exact zeros -- see DESIGN.md)."""
+    g = load_golden("small_dup11")
+    s = vl.ingest(g["t"])
+    trace = vl.RunTrace()
+    vl.valmod(s, 16, 32, 5, trace=trace)
+    for rec in trace.records:
+        a, b, d = rec.motif
+        assert d < 1e-5
+        assert np.allclose(g["t"][a:a + rec.length], g["t"][b:b + rec.length])
+
+
+def test_compute_matrix_profile_and_errors(oracle_mod):
+    s = vl.ingest(np.cumsum(np.random.default_rng(3).standard_normal(2000)))
+    res = vl.compute_matrix_profile(s, 64, 5, m_track=1)
+    omp, oip = oracle_mod.profile(s, 64)
+    assert np.array_equal(res.profile.ip, oip)
+    assert np.allclose(res.profile.mp, omp, atol=1e-7)
+    assert np.array_equal(res.best_m_nbr[:, 0], oip)
+
+
+def test_symmetric_values_for_mutual_pairs():
+    """Canonical (min, max) evaluation: a mutual nearest-neighbour pair reports
+    bitwise-equal distances from both owners (discords.py:126-141 requirement)."""
+    s = vl.ingest(np.cumsum(np.random.default_rng(11).standard_normal(3000)))
+    run = api.GpuRun(s, 40, 48)
+    for L in (40, 44, 48):
+        mp, ip = run.profile(L)
+        mutual = np.flatnonzero((ip >= 0) & (ip[np.maximum(ip, 0)] == np.arange(ip.shape[0])))
+        assert mutual.size > 10
+        assert np.array_equal(mp[mutual], mp[ip[mutual]])
