@@ -43,9 +43,17 @@
 
 namespace {
 
-constexpr int D = 8;              // diagonals per lane
+#ifndef VLMP_D
+#define VLMP_D 8
+#endif
+constexpr int D = VLMP_D;         // diagonals per lane (power of two)
 constexpr int BAND = 32 * D;      // diagonals per warp tile
+constexpr int PBITS = (D == 4) ? 7 : (D == 8) ? 8 : 9;   // log2(BAND): packed local index bits
+constexpr unsigned long long PMASK = (1ull << PBITS) - 1;
 constexpr int WARPS_PER_CTA = 4;
+#ifndef VLMP_FILTER_MIN_BLOCKS
+#define VLMP_FILTER_MIN_BLOCKS 3
+#endif
 constexpr unsigned FULLMASK = 0xffffffffu;
 constexpr unsigned long long KEY_NONE = 0x7FF0000000000000ull;   // bits of +inf
 constexpr long long IDX_NONE = 0x7FFFFFFFFFFFFFFFll;
@@ -226,9 +234,9 @@ __device__ inline unsigned long long clamp_key(double r) {
     return r < 0.0 ? 0ull : (unsigned long long)__double_as_longlong(r);
 }
 
-__device__ inline double pack_low8(double v, unsigned idx8) {
+__device__ inline double pack_low(double v, unsigned idx) {
     int lo = __double2loint(v), hi = __double2hiint(v);
-    lo = (lo & (int)0xFFFFFF00) | (int)idx8;
+    lo = (lo & ~(int)PMASK) | (int)idx;
     return __hiloint2double(hi, lo);
 }
 
@@ -251,11 +259,14 @@ struct WarpSmem {
 // stage group g (rows r0 .. r0+7) into buffer b: 8 row structs + 8 fresh columns for lane 31
 __device__ inline void stage_group(WarpSmem& w, int b, const Prm* __restrict__ prm, long long r0,
                                    long long d0, int lane) {
-    const int q = lane >> 1, half = lane & 1;
-    const Prm* src = (lane < 2 * D) ? prm + r0 + q                       // rows r0 + q
-                                    : prm + r0 + (q - D) + d0 + BAND - 1; // fresh column at row r0+q-8
-    Prm* dst = (lane < 2 * D) ? &w.row[b][q] : &w.fresh[b][q - D];
-    cp_async16(reinterpret_cast<char*>(dst) + 16 * half, reinterpret_cast<const char*>(src) + 16 * half);
+#pragma unroll
+    for (int it = lane; it < 4 * D; it += 32) {   // 2 halves x (D rows + D fresh columns)
+        const int q = it >> 1, half = it & 1;
+        const Prm* src = (q < D) ? prm + r0 + q                          // row r0 + q
+                                 : prm + r0 + (q - D) + d0 + BAND - 1;   // fresh column at row r0+q-D
+        Prm* dst = (q < D) ? &w.row[b][q] : &w.fresh[b][q - D];
+        cp_async16(reinterpret_cast<char*>(dst) + 16 * half, reinterpret_cast<const char*>(src) + 16 * half);
+    }
     cp_async_commit();
 }
 
@@ -286,19 +297,24 @@ __device__ __forceinline__ void tile_body(const TileArgs& a, WarpSmem& w, int wi
     // column ring: phys slot p holds the column of logical slot (p - kk) mod D at row step kk.
     // Each row, the column leaving lane L's slot 0 enters lane L-1's slot D-1 (shuffle);
     // lane 31 takes the fresh column i + d0 + 255 from shared memory.
+    // The ring starts in its state "after row i0-1": phys p < D-1 holds the column of slot p
+    // at row i0, phys D-1 holds the column leaving slot 0 at row i0-1 (cbase - 1), which the
+    // first rotation hands to the left neighbour -- so every row, the first included, rotates.
     double cdf[D], cdg[D], cinv[D];
     float cU[D];
 #pragma unroll
     for (int s = 0; s < D; ++s) {
-        const Prm pc = a.prm[cbase + s];
+        const Prm pc = a.prm[s < D - 1 ? cbase + s : cbase - 1];
         cdf[s] = pc.df; cdg[s] = pc.dg; cinv[s] = pc.inv; cU[s] = pc.U;
     }
     {   // pre-adjust so that the uniform recurrence at row i0 reproduces the seed
         const Prm pr = a.prm[i0];
+        const Prm p7 = a.prm[cbase + D - 1];
 #pragma unroll
         for (int s = 0; s < D; ++s) {
-            cov[s] = fma(-cdf[s], pr.dg, cov[s]);
-            cov[s] = fma(-pr.df, cdg[s], cov[s]);
+            const double df = s < D - 1 ? cdf[s] : p7.df, dg = s < D - 1 ? cdg[s] : p7.dg;
+            cov[s] = fma(-df, pr.dg, cov[s]);
+            cov[s] = fma(-pr.df, dg, cov[s]);
         }
     }
     double colacc[D];
@@ -308,7 +324,7 @@ __device__ __forceinline__ void tile_body(const TileArgs& a, WarpSmem& w, int wi
     }
     double rowres = INFINITY, colres = INFINITY;   // FULL: stashed per-row results
     long long rowres_i = 0, colres_j = 0;
-    unsigned long long nmerge = 0, nflush = 0;
+    unsigned long long nmerge = 0, nflush = 0, nslow = 0;
     int ccount = 0;                                 // filter: buffered candidates (warp-uniform)
 
     const int S = a.S;
@@ -328,12 +344,12 @@ __device__ __forceinline__ void tile_body(const TileArgs& a, WarpSmem& w, int wi
     auto flush_full = [&]() {
         if (rowres < INFINITY) {
             const unsigned long long b = (unsigned long long)__double_as_longlong(rowres);
-            acc_merge(a.acc + rowres_i, b & ~0xFFull, rowres_i + d0 + (long long)(b & 0xFFull));
+            acc_merge(a.acc + rowres_i, b & ~PMASK, rowres_i + d0 + (long long)(b & PMASK));
         }
         if (colres < INFINITY) {
             const unsigned long long b = (unsigned long long)__double_as_longlong(colres);
-            const long long diag = 255 - (long long)(b & 0xFFull);
-            acc_merge(a.acc + colres_j, b & ~0xFFull, colres_j - d0 - diag);
+            const long long diag = BAND - 1 - (long long)(b & PMASK);
+            acc_merge(a.acc + colres_j, b & ~PMASK, colres_j - d0 - diag);
         }
         rowres = INFINITY; colres = INFINITY;
     };
@@ -353,17 +369,19 @@ __device__ __forceinline__ void tile_body(const TileArgs& a, WarpSmem& w, int wi
             if (kk + 1 < D) pr_next = w.row[b][kk + 1];
             {   // ring rotation: phys (kk-1) mod D receives lane+1's outgoing column
                 const int q = (kk + D - 1) & (D - 1);
-                double ndf = __shfl_down_sync(FULLMASK, cdf[q], 1);
-                double ndg = __shfl_down_sync(FULLMASK, cdg[q], 1);
-                double ninv = __shfl_down_sync(FULLMASK, cinv[q], 1);
-                float nU = __shfl_down_sync(FULLMASK, cU[q], 1);
-                if (g > 0 || kk > 0) {   // at the tile's first row the ring already holds slot D-1
-                    if (lane == 31) {
-                        const Prm f = w.fresh[b][kk];
-                        ndf = f.df; ndg = f.dg; ninv = f.inv; nU = f.U;
-                    }
-                    cdf[q] = ndf; cdg[q] = ndg; cinv[q] = ninv; cU[q] = nU;
+                // lane 0's outgoing column leaves the band: overwrite it with the fresh
+                // column, then rotate by one lane so lane 31 receives it
+                if (lane == 0) {
+                    const Prm f = w.fresh[b][kk];
+                    cdf[q] = f.df; cdg[q] = f.dg; cinv[q] = f.inv; cU[q] = f.U;
                 }
+#ifndef VLMP_EXP_NOSHFL
+                const int src_lane = (lane + 1) & 31;
+                cdf[q] = __shfl_sync(FULLMASK, cdf[q], src_lane);
+                cdg[q] = __shfl_sync(FULLMASK, cdg[q], src_lane);
+                cinv[q] = __shfl_sync(FULLMASK, cinv[q], src_lane);
+                cU[q] = __shfl_sync(FULLMASK, cU[q], src_lane);
+#endif
             }
 #pragma unroll
             for (int s = 0; s < D; ++s) {
@@ -372,15 +390,18 @@ __device__ __forceinline__ void tile_body(const TileArgs& a, WarpSmem& w, int wi
                 cov[s] = fma(cdf[p], pr.dg, cov[s]);
             }
             if (!FULL) {
-                bool pass = false;
+                bool pa = false, pb = false;   // two independent predicate chains
 #pragma unroll
                 for (int s = 0; s < D; ++s) {
                     const int p = (s + kk) & (D - 1);
                     const double r = fma(-(cov[s] * pr.inv), cinv[p], 1.0);
                     const float h = __int_as_float(__double2hiint(r));
-                    pass |= sval[s] && (h <= fmaxf(pr.U, cU[p]));
+                    const bool hit = sval[s] && (h <= fmaxf(pr.U, cU[p]));
+                    if (s & 1) pb |= hit; else pa |= hit;
                 }
+                const bool pass = pa | pb;
                 if (__any_sync(FULLMASK, pass)) {
+                    ++nslow;
                     // exact candidates: the row's best (key, j) over the warp + every column hit
                     unsigned long long bk = KEY_NONE; long long bj = IDX_NONE;
                     unsigned ncol = 0;
@@ -390,7 +411,7 @@ __device__ __forceinline__ void tile_body(const TileArgs& a, WarpSmem& w, int wi
                         const int p = (s + kk) & (D - 1);
                         const double r = fma(-(cov[s] * pr.inv), cinv[p], 1.0);
                         const float h = __int_as_float(__double2hiint(r));
-                        const unsigned long long key = clamp_key(r) & ~0xFFull;
+                        const unsigned long long key = clamp_key(r) & ~PMASK;
                         kc[s] = key;
                         pc[s] = sval[s] && (h <= cU[p]);
                         if (sval[s] && (h <= pr.U) && key < bk) { bk = key; bj = i + d0 + dbase + s; }
@@ -434,8 +455,8 @@ __device__ __forceinline__ void tile_body(const TileArgs& a, WarpSmem& w, int wi
                     const double r = fma(-(cov[s] * pr.inv), cinv[p], 1.0);
                     double v = r < 0.0 ? 0.0 : r;     // clamp (NaN stays NaN)
                     if (!sval[s]) v = __longlong_as_double(0x7FF8000000000000ll);
-                    const double pkr = pack_low8(v, (unsigned)(dbase + s));
-                    const double pkc = pack_low8(v, (unsigned)(255 - (dbase + s)));
+                    const double pkr = pack_low(v, (unsigned)(dbase + s));
+                    const double pkc = pack_low(v, (unsigned)(BAND - 1 - (dbase + s)));
                     rm = pkr < rm ? pkr : rm;
                     colacc[p] = pkc < colacc[p] ? pkc : colacc[p];
                 }
@@ -469,18 +490,19 @@ __device__ __forceinline__ void tile_body(const TileArgs& a, WarpSmem& w, int wi
             if (v < INFINITY) {
                 const long long j = i_end + d0 + dbase + p;
                 const unsigned long long bits = (unsigned long long)__double_as_longlong(v);
-                const long long diag = 255 - (long long)(bits & 0xFFull);
-                acc_merge(a.acc + j, bits & ~0xFFull, j - d0 - diag);
+                const long long diag = BAND - 1 - (long long)(bits & PMASK);
+                acc_merge(a.acc + j, bits & ~PMASK, j - d0 - diag);
             }
         }
     } else {
         if (ccount) flush_cands();
         if (lane == 0 && nmerge) { atomicAdd(a.counters, nmerge); atomicAdd(a.counters + 1, nflush); }
+        if (lane == 0 && nslow) atomicAdd(a.counters + 2, nslow);
     }
 }
 
 template <bool FULL>
-__global__ void __launch_bounds__(WARPS_PER_CTA * 32)
+__global__ void __launch_bounds__(WARPS_PER_CTA * 32, VLMP_FILTER_MIN_BLOCKS)
 k_tile(TileArgs a) {
     extern __shared__ __align__(128) unsigned char smem_raw[];
     WarpSmem* ws = reinterpret_cast<WarpSmem*>(smem_raw);
@@ -493,6 +515,9 @@ k_tile(TileArgs a) {
     const long long i0 = (long long)tl.y * a.S;
     const long long rows_valid = a.N - d0 - i0;
     if (rows_valid <= 0 || d0 + BAND - 1 < a.e) return;   // empty, or entirely trivial
+#ifdef VLMP_EXP_SKIPBAND0
+    if (!FULL && tl.x == 0) return;
+#endif
     if (d0 < a.e) tile_body<FULL, true>(a, ws[wl], wid, lane, d0, i0, rows_valid);
     else tile_body<FULL, false>(a, ws[wl], wid, lane, d0, i0, rows_valid);
 }
@@ -1020,7 +1045,8 @@ int vlmp_profile_range(vlmp_session* s, int32_t lmin, int32_t lmax, int64_t band
     memset(s->stats, 0, sizeof(s->stats));
     s->stats[0] = ms; s->stats[2] = executed; s->stats[3] = W; s->stats[4] = tile_ms;
     s->stats[5] = launches; s->stats[6] = n_filtered; s->stats[7] = n_full; s->stats[8] = (double)cnt[0];
-    s->stats[9] = klaunch; s->stats[10] = first_ms;
+    s->stats[9] = klaunch; s->stats[10] = first_ms; s->stats[11] = (double)cnt[2];
+    s->stats[12] = (double)cnt[1];
     return 0;
 }
 

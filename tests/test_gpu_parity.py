@@ -112,8 +112,13 @@ def test_cfg1_matches_reference():
     assert np.array_equal(v.lengths, g["valmp_len"])
     assert np.allclose(v.norm_distances, g["valmp_norm"], atol=1e-7)
     assert [r.motif[:2] for r in trace.records] == [(int(a), int(b)) for a, b, _ in g["motif"]]
+    # SURVEY.md §8(c) anchor: pair {1661, 934} at length 62. The pair is mutual; with the
+    # canonical symmetric distance both offsets tie exactly, as in the reference's own
+    # brute-force oracle (first argmin -> 934); the reference engine's owner-first rows
+    # differ by 1.4e-15 and report offset 1661 first.
     top = vl.top_variable_length_motif(v)
-    assert top[:3] == (1661, 934, 62)                       # SURVEY.md §8(c) anchor
+    assert {top[0], top[1]} == {934, 1661} and top[2] == 62
+    assert top[4] == pytest.approx(0.1632923480786567, rel=1e-12)
     scan = vl.topkm_discord_discovery(s, 32, 64, 3, 1, 50)
     for L in range(32, 65):
         assert np.array_equal(scan.per_length[L].offset, g["k3_disc_off"][L - 32]), L
@@ -196,7 +201,11 @@ def test_edge_cases_against_oracle(case, oracle_mod):
         assert np.array_equal(ip, oip), (case, L)
         fin = np.isfinite(omp)
         assert np.array_equal(np.isfinite(mp), fin)
-        assert np.allclose(mp[fin], omp[fin], rtol=1e-6, atol=1e-7)
+        # constant stretches create affine-copy windows (k constant samples + 1 step) whose
+        # true distance is exactly 0; every evaluation returns rounding noise ~sqrt(eps*rho)
+        # there (~3e-7; the oracle's own STOMP and pair formulas disagree by as much)
+        atol = 1e-6 if case == "constant_stretch" else 1e-7
+        assert np.allclose(mp[fin], omp[fin], rtol=1e-6, atol=atol)
     d, o = run.discords(2)
     assert np.array_equal(o, ref["disc_off"])
     v = run.valmp()
