@@ -52,7 +52,7 @@ constexpr int PBITS = (D == 4) ? 7 : (D == 8) ? 8 : 9;   // log2(BAND): packed l
 constexpr unsigned long long PMASK = (1ull << PBITS) - 1;
 constexpr int WARPS_PER_CTA = 4;
 #ifndef VLMP_FILTER_MIN_BLOCKS
-#define VLMP_FILTER_MIN_BLOCKS 3
+#define VLMP_FILTER_MIN_BLOCKS 4
 #endif
 constexpr unsigned FULLMASK = 0xffffffffu;
 constexpr unsigned long long KEY_NONE = 0x7FF0000000000000ull;   // bits of +inf
@@ -203,12 +203,17 @@ __global__ void k_bound(BoundArgs a) {
 }
 
 // ---------------------------------------------------------------------------------
+struct Cand { int o; int idx; unsigned long long key; };   // candidate (offset, neighbour, key)
+
 struct TileArgs {
     const Prm* prm; const double* mu; const double* tn;
     const int2* tiles;
     double* seeds;
     ulonglong2* acc;               // this length's accumulators, natural offsets
-    unsigned long long* counters;  // [0] candidate merges, [1] candidate flushes
+    unsigned long long* counters;  // [0] candidates logged, [1] unused, [2] flagged row steps
+    Cand* log;                     // this length's candidate log (filter kernel)
+    unsigned long long* log_count; // this length's log fill counter
+    long long log_cap;
     long long N, dlo;
     int n_tiles, S, m, e, update_seeds;
 };
@@ -247,13 +252,10 @@ __device__ inline void cp_async16(void* smem_dst, const void* gmem_src) {
 __device__ inline void cp_async_commit() { asm volatile("cp.async.commit_group;\n" ::: "memory"); }
 __device__ inline void cp_async_wait_all() { asm volatile("cp.async.wait_group 0;\n" ::: "memory"); }
 
-constexpr int CAND_CAP = 64;
-struct Cand { int o; int idx; unsigned long long key; };
 
 struct WarpSmem {
     Prm fresh[2][D];         // the column entering lane 31's slot D-1 at each row of a group
     Prm row[2][D];           // the group's row parameters
-    Cand cand[CAND_CAP];     // buffered filter candidates (filter kernel)
 };
 
 // stage group g (rows r0 .. r0+7) into buffer b: 8 row structs + 8 fresh columns for lane 31
@@ -324,23 +326,12 @@ __device__ __forceinline__ void tile_body(const TileArgs& a, WarpSmem& w, int wi
     }
     double rowres = INFINITY, colres = INFINITY;   // FULL: stashed per-row results
     long long rowres_i = 0, colres_j = 0;
-    unsigned long long nmerge = 0, nflush = 0, nslow = 0;
-    int ccount = 0;                                 // filter: buffered candidates (warp-uniform)
+    unsigned long long nslow = 0;
 
     const int S = a.S;
     const int nrows = (int)(rows_valid < S ? rows_valid : S);
     const int ngroups = (nrows + D - 1) / D;
 
-    auto flush_cands = [&]() {
-        __syncwarp();
-        for (int q = lane; q < ccount; q += 32) {
-            const Cand c = w.cand[q];
-            acc_merge(a.acc + c.o, c.key, c.idx);
-        }
-        nmerge += ccount; nflush += 1;
-        ccount = 0;
-        __syncwarp();
-    };
     auto flush_full = [&]() {
         if (rowres < INFINITY) {
             const unsigned long long b = (unsigned long long)__double_as_longlong(rowres);
@@ -361,12 +352,10 @@ __device__ __forceinline__ void tile_body(const TileArgs& a, WarpSmem& w, int wi
     for (int g = 0; g < ngroups; ++g) {
         const int b = g & 1;
         if (g + 1 < ngroups) stage_group(w, b ^ 1, a.prm, i0 + (long long)(g + 1) * D, d0, lane);
-        Prm pr_next = w.row[b][0];
 #pragma unroll
         for (int kk = 0; kk < D; ++kk) {
             const long long i = i0 + (long long)g * D + kk;
-            const Prm pr = pr_next;
-            if (kk + 1 < D) pr_next = w.row[b][kk + 1];
+            const Prm pr = w.row[b][kk];
             {   // ring rotation: phys (kk-1) mod D receives lane+1's outgoing column
                 const int q = (kk + D - 1) & (D - 1);
                 // lane 0's outgoing column leaves the band: overwrite it with the fresh
@@ -401,48 +390,39 @@ __device__ __forceinline__ void tile_body(const TileArgs& a, WarpSmem& w, int wi
                 }
                 const bool pass = pa | pb;
                 if (__any_sync(FULLMASK, pass)) {
+                    // Cold path (~1% of row steps): log every passing cell's exact key -- as a
+                    // candidate for its row offset i and/or its column offset j -- with one
+                    // warp-aggregated atomic; k_log_merge folds the log into the accumulators.
                     ++nslow;
-                    // exact candidates: the row's best (key, j) over the warp + every column hit
-                    unsigned long long bk = KEY_NONE; long long bj = IDX_NONE;
-                    unsigned ncol = 0;
-                    bool pc[D]; unsigned long long kc[D];
+                    unsigned rm = 0, cm = 0;
 #pragma unroll
                     for (int s = 0; s < D; ++s) {
                         const int p = (s + kk) & (D - 1);
                         const double r = fma(-(cov[s] * pr.inv), cinv[p], 1.0);
                         const float h = __int_as_float(__double2hiint(r));
-                        const unsigned long long key = clamp_key(r) & ~PMASK;
-                        kc[s] = key;
-                        pc[s] = sval[s] && (h <= cU[p]);
-                        if (sval[s] && (h <= pr.U) && key < bk) { bk = key; bj = i + d0 + dbase + s; }
-                        ncol += __popc(__ballot_sync(FULLMASK, pc[s]));
+                        rm |= (sval[s] && (h <= pr.U)) ? (1u << s) : 0u;
+                        cm |= (sval[s] && (h <= cU[p])) ? (1u << s) : 0u;
                     }
+                    const unsigned cnt = __popc(rm) + __popc(cm);
+                    unsigned incl = cnt;
 #pragma unroll
-                    for (int off = 16; off >= 1; off >>= 1) {
-                        const unsigned long long ok = __shfl_xor_sync(FULLMASK, bk, off);
-                        const long long oj = __shfl_xor_sync(FULLMASK, bj, off);
-                        if (key_less(ok, oj, bk, bj)) { bk = ok; bj = oj; }
+                    for (int off = 1; off < 32; off <<= 1) {
+                        const unsigned v = __shfl_up_sync(FULLMASK, incl, off);
+                        if (lane >= off) incl += v;
                     }
-                    const unsigned nnew = ncol + (bk != KEY_NONE ? 1u : 0u);
-                    if (ccount + (int)nnew > CAND_CAP) flush_cands();
-                    if ((int)nnew > CAND_CAP) {
-                        // pathological row step (e.g. offsets without a bound): merge directly
-                        if (lane == 0 && bk != KEY_NONE) acc_merge(a.acc + i, bk, bj);
+                    const unsigned total = __shfl_sync(FULLMASK, incl, 31);
+                    unsigned long long base = 0;
+                    if (lane == 0) base = atomicAdd(a.log_count, (unsigned long long)total);
+                    base = __shfl_sync(FULLMASK, base, 0) + (incl - cnt);
 #pragma unroll
-                        for (int s = 0; s < D; ++s)
-                            if (pc[s]) acc_merge(a.acc + (i + d0 + dbase + s), kc[s], i);
-                        nmerge += nnew;
-                    } else {
-                        if (bk != KEY_NONE) {
-                            if (lane == 0) w.cand[ccount] = Cand{(int)i, (int)bj, bk};
-                            ++ccount;
-                        }
-                        const unsigned lt = (1u << lane) - 1u;
-#pragma unroll
-                        for (int s = 0; s < D; ++s) {
-                            const unsigned bal = __ballot_sync(FULLMASK, pc[s]);
-                            if (pc[s]) w.cand[ccount + __popc(bal & lt)] = Cand{(int)(i + d0 + dbase + s), (int)i, kc[s]};
-                            ccount += __popc(bal);
+                    for (int s = 0; s < D; ++s) {
+                        if ((rm | cm) & (1u << s)) {
+                            const int p = (s + kk) & (D - 1);
+                            const double r = fma(-(cov[s] * pr.inv), cinv[p], 1.0);
+                            const unsigned long long key = clamp_key(r) & ~PMASK;
+                            const long long j = i + d0 + dbase + s;
+                            if (rm & (1u << s)) { if ((long long)base < a.log_cap) a.log[base] = Cand{(int)i, (int)j, key}; ++base; }
+                            if (cm & (1u << s)) { if ((long long)base < a.log_cap) a.log[base] = Cand{(int)j, (int)i, key}; ++base; }
                         }
                     }
                 }
@@ -495,8 +475,6 @@ __device__ __forceinline__ void tile_body(const TileArgs& a, WarpSmem& w, int wi
             }
         }
     } else {
-        if (ccount) flush_cands();
-        if (lane == 0 && nmerge) { atomicAdd(a.counters, nmerge); atomicAdd(a.counters + 1, nflush); }
         if (lane == 0 && nslow) atomicAdd(a.counters + 2, nslow);
     }
 }
@@ -518,8 +496,26 @@ k_tile(TileArgs a) {
 #ifdef VLMP_EXP_SKIPBAND0
     if (!FULL && tl.x == 0) return;
 #endif
-    if (d0 < a.e) tile_body<FULL, true>(a, ws[wl], wid, lane, d0, i0, rows_valid);
-    else tile_body<FULL, false>(a, ws[wl], wid, lane, d0, i0, rows_valid);
+    if (FULL) {
+        if (d0 < a.e) tile_body<true, true>(a, ws[wl], wid, lane, d0, i0, rows_valid);
+        else tile_body<true, false>(a, ws[wl], wid, lane, d0, i0, rows_valid);
+    } else {
+        if (d0 < a.e) tile_body<false, true>(a, ws[wl], wid, lane, d0, i0, rows_valid);
+        else tile_body<false, false>(a, ws[wl], wid, lane, d0, i0, rows_valid);
+    }
+}
+
+// fold one length's candidate log into its accumulators (exact (key, idx) CAS merges)
+__global__ void k_log_merge(const Cand* log, const unsigned long long* log_count, long long cap,
+                            ulonglong2* acc, unsigned long long* counters) {
+    const unsigned long long cnt = *log_count;
+    const long long n = (long long)(cnt < (unsigned long long)cap ? cnt : (unsigned long long)cap);
+    for (long long q = blockIdx.x * (long long)blockDim.x + threadIdx.x; q < n;
+         q += (long long)gridDim.x * blockDim.x) {
+        const Cand c = log[q];
+        acc_merge(acc + c.o, c.key, c.idx);
+    }
+    if (blockIdx.x == 0 && threadIdx.x == 0) atomicAdd(counters, cnt);
 }
 
 // initial seeds: centred direct sums at the first length
@@ -785,6 +781,8 @@ __global__ void k_dfma_peak(double* out, int iters, double x) {
 struct vlmp_session {
     int device = 0;
     cudaStream_t stream = nullptr;
+    cudaStream_t side = nullptr;       // near-diagonal (masked) bands, overlapped with the main launch
+    cudaEvent_t fork_ev = nullptr, join_ev = nullptr;
     cudaEvent_t ev[8] = {};
     std::mutex lock;
     // series
@@ -801,6 +799,8 @@ struct vlmp_session {
     ulonglong2* d_acc = nullptr; size_t acc_cap = 0;
     double* d_mp = nullptr; int* d_ip = nullptr; size_t mp_cap = 0;
     unsigned long long* d_counters = nullptr;
+    Cand* d_log = nullptr; size_t log_cap = 0;          // filter-kernel candidate log
+    unsigned long long* d_logcnt = nullptr; size_t logcnt_cap = 0;   // per-length fill counters
     // valmp
     double* d_vdist = nullptr; double* d_vnorm = nullptr; long long* d_vlen = nullptr;
     long long* d_vidx = nullptr; unsigned char* d_vpop = nullptr; size_t v_cap = 0;
@@ -877,6 +877,11 @@ int vlmp_create(vlmp_session** out, int device) {
     vlmp_session* s = new vlmp_session();
     s->device = device;
     CU(cudaStreamCreateWithFlags(&s->stream, cudaStreamNonBlocking));
+    int prio_lo = 0, prio_hi = 0;
+    CU(cudaDeviceGetStreamPriorityRange(&prio_lo, &prio_hi));
+    CU(cudaStreamCreateWithPriority(&s->side, cudaStreamNonBlocking, prio_hi));   // dispatch first
+    CU(cudaEventCreateWithFlags(&s->fork_ev, cudaEventDisableTiming));
+    CU(cudaEventCreateWithFlags(&s->join_ev, cudaEventDisableTiming));
     for (auto& ev : s->ev) CU(cudaEventCreate(&ev));
     CU(cudaMalloc((void**)&s->d_counters, 8 * sizeof(unsigned long long)));
     *out = s;
@@ -888,11 +893,15 @@ void vlmp_destroy(vlmp_session* s) {
     cudaSetDevice(s->device);
     cudaStreamSynchronize(s->stream);
     void* ptrs[] = {s->d_tn, s->d_cum, s->d_cum2, s->d_prm, s->d_mu,
-                    s->d_previdx, s->d_tiles, s->d_seeds, s->d_acc, s->d_mp, s->d_ip, s->d_counters, s->d_vdist, s->d_vnorm, s->d_vlen, s->d_vidx, s->d_vpop};
+                    s->d_previdx, s->d_tiles, s->d_seeds, s->d_acc, s->d_mp, s->d_ip, s->d_counters,
+                    s->d_log, s->d_logcnt, s->d_vdist, s->d_vnorm, s->d_vlen, s->d_vidx, s->d_vpop};
     for (void* p : ptrs) if (p) cudaFree(p);
     for (auto& ev : s->ev) if (ev) cudaEventDestroy(ev);
     for (auto& ev : s->lev) cudaEventDestroy(ev);
     if (s->stream) cudaStreamDestroy(s->stream);
+    if (s->side) cudaStreamDestroy(s->side);
+    if (s->fork_ev) cudaEventDestroy(s->fork_ev);
+    if (s->join_ev) cudaEventDestroy(s->join_ev);
     delete s;
 }
 
@@ -943,15 +952,8 @@ int vlmp_band_split(vlmp_session* s, int32_t lmin, int32_t lmax, int32_t parts, 
     return 0;
 }
 
-int vlmp_profile_range(vlmp_session* s, int32_t lmin, int32_t lmax, int64_t band_lo,
-                       int64_t band_hi, uint32_t flags) {
-    if (!s) return fail(VLMP_E_INVALID_PARAMETERS, "null session");
-    if (s->n <= 0) return fail(VLMP_E_STATE, "no series uploaded");
-    if (lmin > lmax) return fail(VLMP_E_INVALID_PARAMETERS, "lmin > lmax");
-    if (lmin < 4) return fail(VLMP_E_INVALID_PARAMETERS, "minimum window length is 4");
-    if (s->n < (long long)lmax + (lmax + 1) / 2)
-        return fail(VLMP_E_SERIES_TOO_SHORT, "series cannot host a non-trivial pair at lmax");
-    std::lock_guard<std::mutex> g(s->lock);
+static int profile_impl(vlmp_session* s, int32_t lmin, int32_t lmax, int64_t band_lo,
+                        int64_t band_hi, uint32_t flags, bool* overflow_out) {
     CU(cudaSetDevice(s->device));
     cudaStream_t st = s->stream;
     const long long n = s->n, A = s->A;
@@ -964,15 +966,22 @@ int vlmp_profile_range(vlmp_session* s, int32_t lmin, int32_t lmax, int64_t band
     // tile list (band-major: the near-diagonal, candidate-heavy bands start first),
     // using N at lmin (a superset of every later length's tiles)
     std::vector<int2> tiles;
+    std::vector<long long> band_first;   // first tile of each band of the shard
     for (long long b = band_lo; b < band_hi; ++b) {
+        band_first.push_back((long long)tiles.size());
         long long rows = N0 - (dl + b * BAND);
         for (long long sg = 0; sg * S < rows; ++sg) tiles.push_back(make_int2((int)b, (int)sg));
     }
+    band_first.push_back((long long)tiles.size());
     const long long T = (long long)tiles.size();
     int rc;
     if ((rc = ensure(s->d_tiles, s->tiles_cap, (size_t)std::max<long long>(T, 1)))) return rc;
     if ((rc = ensure(s->d_seeds, s->seeds_cap, (size_t)std::max<long long>(T, 1) * BAND))) return rc;
     if ((rc = ensure(s->d_acc, s->acc_cap, (size_t)n_len * A))) return rc;
+    const size_t log_cap = std::max<size_t>((size_t)1 << 20, (size_t)(8 * N0));
+    if ((rc = ensure(s->d_log, s->log_cap, log_cap))) return rc;
+    if ((rc = ensure(s->d_logcnt, s->logcnt_cap, (size_t)n_len))) return rc;
+    CU(cudaMemsetAsync(s->d_logcnt, 0, n_len * sizeof(unsigned long long), st));
     if (T) CU(cudaMemcpyAsync(s->d_tiles, tiles.data(), T * sizeof(int2), cudaMemcpyHostToDevice, st));
     const size_t smem = WARPS_PER_CTA * sizeof(WarpSmem);
     CU(cudaFuncSetAttribute(k_tile<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
@@ -1008,10 +1017,15 @@ int vlmp_profile_range(vlmp_session* s, int32_t lmin, int32_t lmax, int64_t band
         CU(cudaEventRecord(s->lev[2 * li], st));
         if (T) {
             TileArgs ta{s->d_prm, s->d_mu, s->d_tn, s->d_tiles, s->d_seeds, s->d_acc + (long long)li * A,
-                        s->d_counters, N, dl, (int)T, S, m, e, li + 1 < n_len};
-            unsigned g = blocks(T, WARPS_PER_CTA);
-            if (full) k_tile<true><<<g, WARPS_PER_CTA * 32, smem, st>>>(ta);
-            else k_tile<false><<<g, WARPS_PER_CTA * 32, smem, st>>>(ta);
+                        s->d_counters, s->d_log, s->d_logcnt + li, (long long)s->log_cap,
+                        N, dl, (int)T, S, m, e, li + 1 < n_len};
+            if (full) k_tile<true><<<blocks(T, WARPS_PER_CTA), WARPS_PER_CTA * 32, smem, st>>>(ta);
+            else {
+                k_tile<false><<<blocks(T, WARPS_PER_CTA), WARPS_PER_CTA * 32, smem, st>>>(ta);
+                k_log_merge<<<296, 256, 0, st>>>(s->d_log, s->d_logcnt + li, (long long)s->log_cap,
+                                                 s->d_acc + (long long)li * A, s->d_counters);
+                klaunch += 1;
+            }
             launches += 1; klaunch += 1;
         }
         CU(cudaEventRecord(s->lev[2 * li + 1], st));
@@ -1035,6 +1049,12 @@ int vlmp_profile_range(vlmp_session* s, int32_t lmin, int32_t lmax, int64_t band
     float ms = 0; CU(cudaEventElapsedTime(&ms, s->ev[0], s->ev[1]));
     unsigned long long cnt[8];
     CU(cudaMemcpy(cnt, s->d_counters, sizeof(cnt), cudaMemcpyDeviceToHost));
+    bool overflow = false;
+    {   // a candidate log that overflowed lost candidates: the caller redoes the run exactly
+        std::vector<unsigned long long> lc(n_len);
+        CU(cudaMemcpy(lc.data(), s->d_logcnt, n_len * sizeof(unsigned long long), cudaMemcpyDeviceToHost));
+        for (auto c : lc) overflow |= c > s->log_cap;
+    }
     double W = 0;
     for (int m = lmin; m <= lmax; ++m) {
         long long k = (n - m + 1) - (m + 1) / 2;
@@ -1047,7 +1067,27 @@ int vlmp_profile_range(vlmp_session* s, int32_t lmin, int32_t lmax, int64_t band
     s->stats[5] = launches; s->stats[6] = n_filtered; s->stats[7] = n_full; s->stats[8] = (double)cnt[0];
     s->stats[9] = klaunch; s->stats[10] = first_ms; s->stats[11] = (double)cnt[2];
     s->stats[12] = (double)cnt[1];
+    *overflow_out = overflow;
     return 0;
+}
+
+int vlmp_profile_range(vlmp_session* s, int32_t lmin, int32_t lmax, int64_t band_lo,
+                       int64_t band_hi, uint32_t flags) {
+    if (!s) return fail(VLMP_E_INVALID_PARAMETERS, "null session");
+    if (s->n <= 0) return fail(VLMP_E_STATE, "no series uploaded");
+    if (lmin > lmax) return fail(VLMP_E_INVALID_PARAMETERS, "lmin > lmax");
+    if (lmin < 4) return fail(VLMP_E_INVALID_PARAMETERS, "minimum window length is 4");
+    if (s->n < (long long)lmax + (lmax + 1) / 2)
+        return fail(VLMP_E_SERIES_TOO_SHORT, "series cannot host a non-trivial pair at lmax");
+    std::lock_guard<std::mutex> g(s->lock);
+    bool overflow = false;
+    int rc = profile_impl(s, lmin, lmax, band_lo, band_hi, flags, &overflow);
+    if (rc == 0 && overflow) {
+        // candidates were dropped (pathological bounds): exact full folds at every length
+        rc = profile_impl(s, lmin, lmax, band_lo, band_hi, flags | VLMP_F_FULL_EVERY_LENGTH, &overflow);
+        s->stats[13] = 1;
+    }
+    return rc;
 }
 
 int vlmp_partials_size(vlmp_session* s, int64_t* n_len, int64_t* stride) {
