@@ -21,7 +21,7 @@ import os
 import numpy as np
 
 from . import _lib, policy
-from .exceptions import AllConstantError, InvalidParametersError, SeriesTooShortError
+from . import exceptions as E
 from .results import (VALMP, DiscordMatrix, DiscordScan, MatrixProfile, ProfileResult,
                       VariableLengthDiscordMatrix, update_variable_length_discords)
 from .series import as_series
@@ -34,12 +34,12 @@ def _device() -> int:
 def validate_range(series, lmin: int, lmax: int):
     """valmod.py:180-189."""
     if lmin > lmax:
-        raise InvalidParametersError(f"lmin {lmin} > lmax {lmax}")
+        raise E.InvalidParametersError(f"lmin {lmin} > lmax {lmax}")
     if lmin < 4:
-        raise InvalidParametersError("minimum window length is 4")
+        raise E.InvalidParametersError("minimum window length is 4")
     need = lmax + policy.exclusion_zone(lmax)
     if series.n < need:
-        raise SeriesTooShortError(
+        raise E.SeriesTooShortError(
             f"series of {series.n} points cannot host a non-trivial pair at length {lmax} "
             f"(needs {need})")
 
@@ -47,10 +47,10 @@ def validate_range(series, lmin: int, lmax: int):
 def _check_profile_length(series, length: int):
     """profile.py:346-355 (the scan at the first length performs these checks)."""
     if length < 4 or 2 * length > series.n:
-        raise SeriesTooShortError(f"need 4 <= length <= n/2 (length={length}, n={series.n})")
+        raise E.SeriesTooShortError(f"need 4 <= length <= n/2 (length={length}, n={series.n})")
     mu, sd = _moving_sd(series, length)
     if not (sd >= series.sigma_floor).any():
-        raise AllConstantError(f"every window of length {length} is constant")
+        raise E.AllConstantError(f"every window of length {length} is constant")
 
 
 def _moving_sd(series, length):
@@ -152,7 +152,7 @@ def valmod(series, lmin: int, lmax: int, p: int, *, ranking=None, trace=None,
     series = as_series(series)
     validate_range(series, lmin, lmax)
     if p < 1:
-        raise InvalidParametersError("p must be at least 1")
+        raise E.InvalidParametersError("p must be at least 1")
     _check_profile_length(series, lmin)
     run = GpuRun(series, lmin, lmax)
     v = run.valmp()
@@ -172,15 +172,15 @@ def topkm_discord_discovery(series, lmin: int, lmax: int, k: int, m: int, p: int
     """Exact top-k m-th discords for every length, merged across lengths (m = 1)."""
     series = as_series(series)
     if m < 1 or k < 1:
-        raise InvalidParametersError("k and m must be at least 1")
+        raise E.InvalidParametersError("k and m must be at least 1")
     if p < m:
-        raise InvalidParametersError(f"p ({p}) must be at least m ({m})")
+        raise E.InvalidParametersError(f"p ({p}) must be at least m ({m})")
     validate_range(series, lmin, lmax)
     if m != 1:
-        raise InvalidParametersError(
+        raise E.InvalidParametersError(
             "the GPU path computes 1st discords (m = 1); m > 1 is not implemented yet")
     if k > 32:
-        raise InvalidParametersError("k must be at most 32 on the GPU path")
+        raise E.InvalidParametersError("k must be at most 32 on the GPU path")
     _check_profile_length(series, lmin)
     run = GpuRun(series, lmin, lmax)
     dist, off = run.discords(k)
@@ -206,11 +206,11 @@ def compute_matrix_profile(series, length: int, p: int, m_track: int = 0,
     """Exact matrix profile at one length (partials are not materialised)."""
     series = as_series(series)
     if length < 4 or 2 * length > series.n:
-        raise SeriesTooShortError(f"need 4 <= length <= n/2 (length={length}, n={series.n})")
+        raise E.SeriesTooShortError(f"need 4 <= length <= n/2 (length={length}, n={series.n})")
     if p < 1:
-        raise InvalidParametersError("p must be at least 1")
+        raise E.InvalidParametersError("p must be at least 1")
     if m_track > 1:
-        raise InvalidParametersError("m_track > 1 is not implemented on the GPU path")
+        raise E.InvalidParametersError("m_track > 1 is not implemented on the GPU path")
     _check_profile_length(series, length)
     run = GpuRun(series, length, length)
     mp, ip = run.profile(length)
@@ -228,7 +228,7 @@ def motifs_per_length(series, lmin: int, lmax: int, k: int):
     validate_range(series, lmin, lmax)
     _check_profile_length(series, lmin)
     if k < 1 or 2 * k > 64:
-        raise InvalidParametersError("k must be in [1, 32]")
+        raise E.InvalidParametersError("k must be in [1, 32]")
     run = GpuRun(series, lmin, lmax)
     return _topk_from_rows(run, k)
 
@@ -254,7 +254,7 @@ def mine(series, lmin: int, lmax: int, k_motif: int = 1, k_discord: int = 1, *,
     validate_range(series, lmin, lmax)
     _check_profile_length(series, lmin)
     if not (1 <= k_motif <= 32) or not (1 <= k_discord <= 32):
-        raise InvalidParametersError("k_motif and k_discord must be in [1, 32]")
+        raise E.InvalidParametersError("k_motif and k_discord must be in [1, 32]")
     run = GpuRun(series, lmin, lmax)
     v = run.valmp()
     motifs = _topk_from_rows(run, k_motif)

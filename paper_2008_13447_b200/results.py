@@ -22,7 +22,7 @@ from dataclasses import dataclass, field
 import numpy as np
 
 from . import policy
-from .exceptions import UnpopulatedError
+from . import exceptions as E
 
 
 class VALMP:
@@ -59,7 +59,7 @@ def top_variable_length_motif(valmp):
     """(offset, neighbour, length, distance, norm) of the smallest normalised entry;
     first minimum wins (smallest offset)."""
     if not np.asarray(valmp.populated).any():
-        raise UnpopulatedError("no populated entries")
+        raise E.UnpopulatedError("no populated entries")
     score = np.where(valmp.populated, valmp.norm_distances, np.inf)
     i = int(np.argmin(score))
     return (i, int(valmp.indices[i]), int(valmp.lengths[i]),

@@ -12,8 +12,7 @@ from __future__ import annotations
 import numpy as np
 
 from . import policy
-from .exceptions import (EmptySeriesError, LengthExceedsSeriesError, NonFiniteError,
-                         OutOfRangeError)
+from . import exceptions as E
 
 
 class DataSeries:
@@ -35,7 +34,7 @@ class DataSeries:
     def moving_stats(self, length: int):
         """Mean/std of every window (reference order of operations)."""
         if length > self.n:
-            raise LengthExceedsSeriesError(f"window length {length} > series length {self.n}")
+            raise E.LengthExceedsSeriesError(f"window length {length} > series length {self.n}")
         s = self._cum[length:] - self._cum[:-length]
         ss = self._cum2[length:] - self._cum2[:-length]
         mu = s / length
@@ -45,7 +44,7 @@ class DataSeries:
 
     def window(self, i: int, length: int):
         if i < 0 or i + length > self.n:
-            raise OutOfRangeError(f"window ({i}, {length}) outside series of {self.n} points")
+            raise E.OutOfRangeError(f"window ({i}, {length}) outside series of {self.n} points")
         return self.values[i:i + length]
 
 
@@ -54,10 +53,10 @@ def ingest(raw) -> DataSeries:
     if v.ndim != 1:
         v = v.reshape(-1)
     if v.size == 0:
-        raise EmptySeriesError("series holds no points")
+        raise E.EmptySeriesError("series holds no points")
     bad = ~np.isfinite(v)
     if bad.any():
-        raise NonFiniteError(int(np.flatnonzero(bad)[0]))
+        raise E.NonFiniteError(int(np.flatnonzero(bad)[0]))
     return DataSeries(v)
 
 
