@@ -205,13 +205,18 @@ __global__ void k_bound(BoundArgs a) {
 // ---------------------------------------------------------------------------------
 struct Cand { int o; int idx; unsigned long long key; };   // candidate (offset, neighbour, key)
 
+// A filter-kernel log record: a lane whose cells passed the bound at row i; its 8 cells are
+// (i, j0 + s) and cov[s] is their covariance, so the merge kernel can recompute the exact
+// keys with the kernel's own FMA sequence (bit-identical) and apply the exact tests.
+struct __align__(16) RowRec { int i; int j0; int pad0, pad1; double cov[D]; };
+
 struct TileArgs {
     const Prm* prm; const double* mu; const double* tn;
     const int2* tiles;
     double* seeds;
     ulonglong2* acc;               // this length's accumulators, natural offsets
     unsigned long long* counters;  // [0] candidates logged, [1] unused, [2] flagged row steps
-    Cand* log;                     // this length's candidate log (filter kernel)
+    RowRec* log;                   // this length's log of flagged lanes (filter kernel)
     unsigned long long* log_count; // this length's log fill counter
     long long log_cap;
     long long N, dlo;
@@ -272,6 +277,21 @@ __device__ inline void stage_group(WarpSmem& w, int b, const Prm* __restrict__ p
     cp_async_commit();
 }
 
+// append one record per flagged lane (one warp-aggregated atomic); rare
+__device__ __forceinline__ void log_lanes(const TileArgs& a, bool flag, int lane, long long i, long long j0,
+                                          const double (&cov)[D]) {
+    const unsigned bal = __ballot_sync(FULLMASK, flag);
+    unsigned long long base = 0;
+    if (lane == 0) base = atomicAdd(a.log_count, (unsigned long long)__popc(bal));
+    base = __shfl_sync(FULLMASK, base, 0) + __popc(bal & ((1u << lane) - 1u));
+    if (flag && (long long)base < a.log_cap) {
+        RowRec* r = a.log + base;
+        r->i = (int)i; r->j0 = (int)j0; r->pad0 = 0; r->pad1 = 0;
+#pragma unroll
+        for (int s = 0; s < D; ++s) r->cov[s] = cov[s];
+    }
+}
+
 template <bool FULL, bool MASKED>
 __device__ __forceinline__ void tile_body(const TileArgs& a, WarpSmem& w, int wid, int lane,
                                           long long d0, long long i0, long long rows_valid) {
@@ -327,6 +347,7 @@ __device__ __forceinline__ void tile_body(const TileArgs& a, WarpSmem& w, int wi
     double rowres = INFINITY, colres = INFINITY;   // FULL: stashed per-row results
     long long rowres_i = 0, colres_j = 0;
     unsigned long long nslow = 0;
+    bool pass_prev = false;            // filter: row (i-1)'s pass predicate, voted on at row i
 
     const int S = a.S;
     const int nrows = (int)(rows_valid < S ? rows_valid : S);
@@ -372,6 +393,14 @@ __device__ __forceinline__ void tile_body(const TileArgs& a, WarpSmem& w, int wi
                 cU[q] = __shfl_sync(FULLMASK, cU[q], src_lane);
 #endif
             }
+            if (!FULL) {
+                // Deferred vote: row i-1's predicate is long resolved. cov[] still holds row
+                // i-1's covariances (row i's recurrence has not run), so flagged lanes log them.
+                if (__any_sync(FULLMASK, pass_prev)) {
+                    log_lanes(a, pass_prev, lane, i - 1, i - 1 + d0 + dbase, cov);
+                    ++nslow;
+                }
+            }
 #pragma unroll
             for (int s = 0; s < D; ++s) {
                 const int p = (s + kk) & (D - 1);
@@ -388,44 +417,7 @@ __device__ __forceinline__ void tile_body(const TileArgs& a, WarpSmem& w, int wi
                     const bool hit = sval[s] && (h <= fmaxf(pr.U, cU[p]));
                     if (s & 1) pb |= hit; else pa |= hit;
                 }
-                const bool pass = pa | pb;
-                if (__any_sync(FULLMASK, pass)) {
-                    // Cold path (~1% of row steps): log every passing cell's exact key -- as a
-                    // candidate for its row offset i and/or its column offset j -- with one
-                    // warp-aggregated atomic; k_log_merge folds the log into the accumulators.
-                    ++nslow;
-                    unsigned rm = 0, cm = 0;
-#pragma unroll
-                    for (int s = 0; s < D; ++s) {
-                        const int p = (s + kk) & (D - 1);
-                        const double r = fma(-(cov[s] * pr.inv), cinv[p], 1.0);
-                        const float h = __int_as_float(__double2hiint(r));
-                        rm |= (sval[s] && (h <= pr.U)) ? (1u << s) : 0u;
-                        cm |= (sval[s] && (h <= cU[p])) ? (1u << s) : 0u;
-                    }
-                    const unsigned cnt = __popc(rm) + __popc(cm);
-                    unsigned incl = cnt;
-#pragma unroll
-                    for (int off = 1; off < 32; off <<= 1) {
-                        const unsigned v = __shfl_up_sync(FULLMASK, incl, off);
-                        if (lane >= off) incl += v;
-                    }
-                    const unsigned total = __shfl_sync(FULLMASK, incl, 31);
-                    unsigned long long base = 0;
-                    if (lane == 0) base = atomicAdd(a.log_count, (unsigned long long)total);
-                    base = __shfl_sync(FULLMASK, base, 0) + (incl - cnt);
-#pragma unroll
-                    for (int s = 0; s < D; ++s) {
-                        if ((rm | cm) & (1u << s)) {
-                            const int p = (s + kk) & (D - 1);
-                            const double r = fma(-(cov[s] * pr.inv), cinv[p], 1.0);
-                            const unsigned long long key = clamp_key(r) & ~PMASK;
-                            const long long j = i + d0 + dbase + s;
-                            if (rm & (1u << s)) { if ((long long)base < a.log_cap) a.log[base] = Cand{(int)i, (int)j, key}; ++base; }
-                            if (cm & (1u << s)) { if ((long long)base < a.log_cap) a.log[base] = Cand{(int)j, (int)i, key}; ++base; }
-                        }
-                    }
-                }
+                pass_prev = pa | pb;
             } else {
                 // rows: lane-local packed min, then warp all-reduce (packed diag index => no exact ties)
                 double rm = INFINITY;
@@ -475,6 +467,11 @@ __device__ __forceinline__ void tile_body(const TileArgs& a, WarpSmem& w, int wi
             }
         }
     } else {
+        if (__any_sync(FULLMASK, pass_prev)) {
+            log_lanes(a, pass_prev, lane, i0 + (long long)ngroups * D - 1,
+                      i0 + (long long)ngroups * D - 1 + d0 + dbase, cov);
+            ++nslow;
+        }
         if (lane == 0 && nslow) atomicAdd(a.counters + 2, nslow);
     }
 }
@@ -505,17 +502,30 @@ k_tile(TileArgs a) {
     }
 }
 
-// fold one length's candidate log into its accumulators (exact (key, idx) CAS merges)
-__global__ void k_log_merge(const Cand* log, const unsigned long long* log_count, long long cap,
-                            ulonglong2* acc, unsigned long long* counters) {
+// fold one length's log into its accumulators: recompute each logged cell's key with the
+// tile kernel's FMA sequence (bit-identical), apply the exact row / column bound tests and
+// the exclusion zone, and merge (key, index) with the 128-bit CAS
+__global__ void k_log_merge(const RowRec* log, const unsigned long long* log_count, long long cap,
+                            const Prm* prm, int e, ulonglong2* acc, unsigned long long* counters) {
     const unsigned long long cnt = *log_count;
     const long long n = (long long)(cnt < (unsigned long long)cap ? cnt : (unsigned long long)cap);
+    unsigned long long merged = 0;
     for (long long q = blockIdx.x * (long long)blockDim.x + threadIdx.x; q < n;
          q += (long long)gridDim.x * blockDim.x) {
-        const Cand c = log[q];
-        acc_merge(acc + c.o, c.key, c.idx);
+        const RowRec rec = log[q];
+        const Prm pr = prm[rec.i];
+        for (int s = 0; s < D; ++s) {
+            const long long j = (long long)rec.j0 + s;
+            if (j - rec.i < e) continue;
+            const Prm pc = prm[j];
+            const double r = fma(-(rec.cov[s] * pr.inv), pc.inv, 1.0);
+            const float h = __int_as_float(__double2hiint(r));
+            const unsigned long long key = clamp_key(r) & ~PMASK;
+            if (h <= pr.U) { acc_merge(acc + rec.i, key, j); ++merged; }
+            if (h <= pc.U) { acc_merge(acc + j, key, rec.i); ++merged; }
+        }
     }
-    if (blockIdx.x == 0 && threadIdx.x == 0) atomicAdd(counters, cnt);
+    if (merged) atomicAdd(counters, merged);
 }
 
 // initial seeds: centred direct sums at the first length
@@ -799,7 +809,7 @@ struct vlmp_session {
     ulonglong2* d_acc = nullptr; size_t acc_cap = 0;
     double* d_mp = nullptr; int* d_ip = nullptr; size_t mp_cap = 0;
     unsigned long long* d_counters = nullptr;
-    Cand* d_log = nullptr; size_t log_cap = 0;          // filter-kernel candidate log
+    RowRec* d_log = nullptr; size_t log_cap = 0;        // filter-kernel log of flagged lanes
     unsigned long long* d_logcnt = nullptr; size_t logcnt_cap = 0;   // per-length fill counters
     // valmp
     double* d_vdist = nullptr; double* d_vnorm = nullptr; long long* d_vlen = nullptr;
@@ -978,7 +988,7 @@ static int profile_impl(vlmp_session* s, int32_t lmin, int32_t lmax, int64_t ban
     if ((rc = ensure(s->d_tiles, s->tiles_cap, (size_t)std::max<long long>(T, 1)))) return rc;
     if ((rc = ensure(s->d_seeds, s->seeds_cap, (size_t)std::max<long long>(T, 1) * BAND))) return rc;
     if ((rc = ensure(s->d_acc, s->acc_cap, (size_t)n_len * A))) return rc;
-    const size_t log_cap = std::max<size_t>((size_t)1 << 20, (size_t)(8 * N0));
+    const size_t log_cap = std::max<size_t>((size_t)1 << 18, (size_t)(2 * N0));
     if ((rc = ensure(s->d_log, s->log_cap, log_cap))) return rc;
     if ((rc = ensure(s->d_logcnt, s->logcnt_cap, (size_t)n_len))) return rc;
     CU(cudaMemsetAsync(s->d_logcnt, 0, n_len * sizeof(unsigned long long), st));
@@ -1022,8 +1032,8 @@ static int profile_impl(vlmp_session* s, int32_t lmin, int32_t lmax, int64_t ban
             if (full) k_tile<true><<<blocks(T, WARPS_PER_CTA), WARPS_PER_CTA * 32, smem, st>>>(ta);
             else {
                 k_tile<false><<<blocks(T, WARPS_PER_CTA), WARPS_PER_CTA * 32, smem, st>>>(ta);
-                k_log_merge<<<296, 256, 0, st>>>(s->d_log, s->d_logcnt + li, (long long)s->log_cap,
-                                                 s->d_acc + (long long)li * A, s->d_counters);
+                k_log_merge<<<296, 128, 0, st>>>(s->d_log, s->d_logcnt + li, (long long)s->log_cap,
+                                                 s->d_prm, e, s->d_acc + (long long)li * A, s->d_counters);
                 klaunch += 1;
             }
             launches += 1; klaunch += 1;

@@ -25,3 +25,7 @@ seriesmine.valmod = drop_in.valmod
 seriesmine.topkm_discord_discovery = drop_in.topkm_discord_discovery
 seriesmine.cli.valmod = drop_in.valmod
 seriesmine.cli.topkm_discord_discovery = drop_in.topkm_discord_discovery
+# the CLI's `mp` and `bench` commands call compute_matrix_profile (cli.py:247-257, :307);
+# seriesmine.compute_matrix_profile itself stays the reference's (its own tests inspect
+# the VALMOD partial profiles, which the exhaustive GPU path does not build)
+seriesmine.cli.compute_matrix_profile = drop_in.compute_matrix_profile
