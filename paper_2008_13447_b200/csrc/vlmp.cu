@@ -160,46 +160,63 @@ struct BoundArgs {
     long long N, Nprev; int m, e; double margin;
 };
 
-__device__ inline double cell_key(const double* __restrict__ tn, long long o, long long c, int m,
-                                  double mo, double mc, double io, double ic) {
-    double cov = 0.0;
-    for (int k = 0; k < m; ++k) cov = fma(tn[o + k] - mo, tn[c + k] - mc, cov);
-    return fma(-(cov * io), ic, 1.0);
-}
 
+// one warp per offset: the (up to 4) candidate dot products are split across the lanes
 __global__ void k_bound(BoundArgs a) {
-    long long o = blockIdx.x * (long long)blockDim.x + threadIdx.x;
+    const int lane = threadIdx.x & 31;
+    const long long o = (blockIdx.x * (long long)blockDim.x + threadIdx.x) >> 5;
     if (o >= a.N) return;
-    float out = -INFINITY;
-    double io = a.prm[o].inv;
-    if (io == io) {   // valid row
-        double mo = a.mu[o];
-        long long cand[4];
-        int nc = 0;
-        long long c1 = (o < a.Nprev) ? a.prev_idx[o] : -1;
-        if (c1 >= 0) { cand[nc++] = c1; cand[nc++] = c1 > o ? c1 + 1 : c1 - 1; }
-        if (o >= 1 && o - 1 < a.Nprev) { long long c = a.prev_idx[o - 1]; if (c >= 0) cand[nc++] = c + 1; }
-        if (o + 1 < a.Nprev) { long long c = a.prev_idx[o + 1]; if (c >= 0) cand[nc++] = c - 1; }
-        double best = INFINITY;
-        for (int q = 0; q < nc; ++q) {
-            long long c = cand[q];
+    const double io = a.prm[o].inv;
+    if (!(io == io)) {   // invalid row: never a candidate
+        if (lane == 0) a.prm[o].U = -INFINITY;
+        return;
+    }
+    long long cand[4];
+    int nc = 0;
+    const long long c1 = (o < a.Nprev) ? a.prev_idx[o] : -1;
+    if (c1 >= 0) { cand[nc++] = c1; cand[nc++] = c1 > o ? c1 + 1 : c1 - 1; }
+    if (o >= 1 && o - 1 < a.Nprev) { const long long c = a.prev_idx[o - 1]; if (c >= 0) cand[nc++] = c + 1; }
+    if (o + 1 < a.Nprev) { const long long c = a.prev_idx[o + 1]; if (c >= 0) cand[nc++] = c - 1; }
+    bool ok[4]; double mc[4], ic[4]; long long cc[4];
+#pragma unroll
+    for (int q = 0; q < 4; ++q) {
+        ok[q] = false; mc[q] = 0.0; ic[q] = 0.0; cc[q] = o;
+        if (q < nc) {
+            const long long c = cand[q];
             bool dup = false;
             for (int r = 0; r < q; ++r) dup |= (cand[r] == c);
-            if (dup || c < 0 || c >= a.N) continue;
-            long long dd = c > o ? c - o : o - c;
-            if (dd < a.e) continue;
-            double ic = a.prm[c].inv;
-            if (!(ic == ic)) continue;
-            best = fmin(best, cell_key(a.tn, o, c, a.m, mo, a.mu[c], io, ic));
-        }
-        if (best < INFINITY) {
-            double U = fmax(best, 0.0) + a.margin;
-            out = __int_as_float(__double2hiint(U));   // x <= U  =>  hi(x) <= hi(U)
-        } else {
-            out = INFINITY;   // no bound: every cell of this offset is a candidate
+            const long long dd = c > o ? c - o : o - c;
+            if (!dup && c >= 0 && c < a.N && dd >= a.e) {
+                ic[q] = a.prm[c].inv;
+                ok[q] = ic[q] == ic[q];
+                mc[q] = a.mu[c];
+                cc[q] = c;
+            }
         }
     }
-    a.prm[o].U = out;
+    const double mo = a.mu[o];
+    double acc[4] = {0.0, 0.0, 0.0, 0.0};
+    for (int k = lane; k < a.m; k += 32) {
+        const double x = a.tn[o + k] - mo;
+#pragma unroll
+        for (int q = 0; q < 4; ++q) acc[q] = fma(x, a.tn[cc[q] + k] - mc[q], acc[q]);
+    }
+    double best = INFINITY;
+#pragma unroll
+    for (int q = 0; q < 4; ++q) {
+        double v = acc[q];
+#pragma unroll
+        for (int off = 16; off >= 1; off >>= 1) v += __shfl_xor_sync(FULLMASK, v, off);
+        if (ok[q]) best = fmin(best, fma(-(v * io), ic[q], 1.0));
+    }
+    if (lane == 0) {
+        float out = INFINITY;   // no bound: every cell of this offset is a candidate
+        if (best < INFINITY) {
+            const double U = fmax(best, 0.0) + a.margin;
+            out = __int_as_float(__double2hiint(U));   // x <= U  =>  hi(x) <= hi(U)
+        }
+        a.prm[o].U = out;
+    }
 }
 
 // ---------------------------------------------------------------------------------
@@ -814,6 +831,10 @@ struct vlmp_session {
     // valmp
     double* d_vdist = nullptr; double* d_vnorm = nullptr; long long* d_vlen = nullptr;
     long long* d_vidx = nullptr; unsigned char* d_vpop = nullptr; size_t v_cap = 0;
+    // read-off scratch (persistent: per-call cudaMallocAsync re-maps pool memory every sync)
+    long long* d_ro_i64 = nullptr; size_t ro_i64_cap = 0;
+    double* d_ro_f64 = nullptr; size_t ro_f64_cap = 0;
+    unsigned long long* d_ro_cnt = nullptr;
     // run state
     int lmin = 0, lmax = 0, n_len = 0; bool have_profile = false, have_final = false;
     double stats[16] = {};
@@ -904,7 +925,7 @@ void vlmp_destroy(vlmp_session* s) {
     cudaStreamSynchronize(s->stream);
     void* ptrs[] = {s->d_tn, s->d_cum, s->d_cum2, s->d_prm, s->d_mu,
                     s->d_previdx, s->d_tiles, s->d_seeds, s->d_acc, s->d_mp, s->d_ip, s->d_counters,
-                    s->d_log, s->d_logcnt, s->d_vdist, s->d_vnorm, s->d_vlen, s->d_vidx, s->d_vpop};
+                    s->d_log, s->d_logcnt, s->d_ro_i64, s->d_ro_f64, s->d_ro_cnt, s->d_vdist, s->d_vnorm, s->d_vlen, s->d_vidx, s->d_vpop};
     for (void* p : ptrs) if (p) cudaFree(p);
     for (auto& ev : s->ev) if (ev) cudaEventDestroy(ev);
     for (auto& ev : s->lev) cudaEventDestroy(ev);
@@ -1018,7 +1039,7 @@ static int profile_impl(vlmp_session* s, int32_t lmin, int32_t lmax, int64_t ban
         if (!full) {
             k_acc_idx<<<blocks(N + 1, 256), 256, 0, st>>>(s->d_acc + (long long)(li - 1) * A, s->d_previdx, N + 1);
             BoundArgs ba{s->d_tn, s->d_mu, s->d_prm, s->d_previdx, N, N + 1, m, e, margin};
-            k_bound<<<blocks(N, 128), 128, 0, st>>>(ba);
+            k_bound<<<blocks(N * 32, 256), 256, 0, st>>>(ba);
             klaunch += 2;
         }
         while (s->lev.size() < (size_t)2 * (li + 1)) {
@@ -1214,17 +1235,16 @@ int vlmp_smallest_rows(vlmp_session* s, int32_t k2, int64_t* out_off, int64_t* o
     std::lock_guard<std::mutex> g(s->lock);
     CU(cudaSetDevice(s->device));
     const long long cnt = (long long)s->n_len * k2;
-    long long* d_off = nullptr; long long* d_nbr = nullptr; double* d_d = nullptr;
-    CU(cudaMallocAsync((void**)&d_off, cnt * 8, s->stream));
-    CU(cudaMallocAsync((void**)&d_nbr, cnt * 8, s->stream));
-    CU(cudaMallocAsync((void**)&d_d, cnt * 8, s->stream));
+    int rc;
+    if ((rc = ensure(s->d_ro_i64, s->ro_i64_cap, (size_t)(2 * cnt)))) return rc;
+    if ((rc = ensure(s->d_ro_f64, s->ro_f64_cap, (size_t)cnt))) return rc;
+    long long* d_off = s->d_ro_i64; long long* d_nbr = s->d_ro_i64 + cnt; double* d_d = s->d_ro_f64;
     SmallArgs sa{s->d_mp, s->d_ip, d_off, d_nbr, d_d, s->n, s->A, s->lmin, k2};
     k_smallest<<<s->n_len, 256, 0, s->stream>>>(sa);
     CU(cudaGetLastError());
     CU(cudaMemcpyAsync(out_off, d_off, cnt * 8, cudaMemcpyDeviceToHost, s->stream));
     CU(cudaMemcpyAsync(out_nbr, d_nbr, cnt * 8, cudaMemcpyDeviceToHost, s->stream));
     CU(cudaMemcpyAsync(out_d, d_d, cnt * 8, cudaMemcpyDeviceToHost, s->stream));
-    CU(cudaFreeAsync(d_off, s->stream)); CU(cudaFreeAsync(d_nbr, s->stream)); CU(cudaFreeAsync(d_d, s->stream));
     CU(cudaStreamSynchronize(s->stream));
     s->stats[9] += 1;
     return 0;
@@ -1236,15 +1256,15 @@ int vlmp_discords(vlmp_session* s, int32_t k, double* out_dist, int64_t* out_off
     std::lock_guard<std::mutex> g(s->lock);
     CU(cudaSetDevice(s->device));
     const long long cnt = (long long)s->n_len * k;
-    double* d_d = nullptr; long long* d_o = nullptr;
-    CU(cudaMallocAsync((void**)&d_d, cnt * 8, s->stream));
-    CU(cudaMallocAsync((void**)&d_o, cnt * 8, s->stream));
+    int rc;
+    if ((rc = ensure(s->d_ro_i64, s->ro_i64_cap, (size_t)cnt))) return rc;
+    if ((rc = ensure(s->d_ro_f64, s->ro_f64_cap, (size_t)cnt))) return rc;
+    double* d_d = s->d_ro_f64; long long* d_o = s->d_ro_i64;
     DiscArgs da{s->d_mp, d_d, d_o, s->n, s->A, s->lmin, s->n_len, k};
     k_discords<<<blocks((long long)s->n_len * 32, 128), 128, 0, s->stream>>>(da);
     CU(cudaGetLastError());
     CU(cudaMemcpyAsync(out_dist, d_d, cnt * 8, cudaMemcpyDeviceToHost, s->stream));
     CU(cudaMemcpyAsync(out_off, d_o, cnt * 8, cudaMemcpyDeviceToHost, s->stream));
-    CU(cudaFreeAsync(d_d, s->stream)); CU(cudaFreeAsync(d_o, s->stream));
     CU(cudaStreamSynchronize(s->stream));
     s->stats[9] += 1;
     return 0;
@@ -1257,10 +1277,13 @@ int vlmp_ranking_events(vlmp_session* s, double tau, int64_t cap, int64_t* ev_of
     CU(cudaSetDevice(s->device));
     cudaStream_t st = s->stream;
     long long c = std::max<long long>(cap, 1);
-    long long *d_o, *d_nb, *d_l; double *d_d, *d_n; unsigned long long* d_c;
-    CU(cudaMallocAsync((void**)&d_o, c * 8, st)); CU(cudaMallocAsync((void**)&d_nb, c * 8, st));
-    CU(cudaMallocAsync((void**)&d_l, c * 8, st)); CU(cudaMallocAsync((void**)&d_d, c * 8, st));
-    CU(cudaMallocAsync((void**)&d_n, c * 8, st)); CU(cudaMallocAsync((void**)&d_c, 8, st));
+    int rc;
+    if ((rc = ensure(s->d_ro_i64, s->ro_i64_cap, (size_t)(3 * c)))) return rc;
+    if ((rc = ensure(s->d_ro_f64, s->ro_f64_cap, (size_t)(2 * c)))) return rc;
+    if (!s->d_ro_cnt) CU(cudaMalloc((void**)&s->d_ro_cnt, 8));
+    long long *d_o = s->d_ro_i64, *d_nb = s->d_ro_i64 + c, *d_l = s->d_ro_i64 + 2 * c;
+    double *d_d = s->d_ro_f64, *d_n = s->d_ro_f64 + c;
+    unsigned long long* d_c = s->d_ro_cnt;
     CU(cudaMemsetAsync(d_c, 0, 8, st));
     const long long n0 = s->n - s->lmin + 1;
     EvArgs ea{s->d_mp, s->d_ip, tau, d_o, d_nb, d_l, d_d, d_n, d_c, cap, s->n, s->A, s->lmin, s->n_len};
@@ -1277,8 +1300,6 @@ int vlmp_ranking_events(vlmp_session* s, double tau, int64_t cap, int64_t* ev_of
         CU(cudaMemcpyAsync(ev_dist, d_d, take * 8, cudaMemcpyDeviceToHost, st));
         CU(cudaMemcpyAsync(ev_norm, d_n, take * 8, cudaMemcpyDeviceToHost, st));
     }
-    CU(cudaFreeAsync(d_o, st)); CU(cudaFreeAsync(d_nb, st)); CU(cudaFreeAsync(d_l, st));
-    CU(cudaFreeAsync(d_d, st)); CU(cudaFreeAsync(d_n, st)); CU(cudaFreeAsync(d_c, st));
     CU(cudaStreamSynchronize(st));
     *count = (int64_t)hc;
     return 0;
