@@ -117,6 +117,17 @@ int vlmp_ranking_events(vlmp_session* s, double tau, int64_t cap, int64_t* ev_of
                         double* ev_norm, int64_t* count);
 
 /*
+ * m-th discords (discords.py:206-247 with m > 1): for every length and offset the m best
+ * neighbours (exact, smallest-index ties), their canonical distances sorted ascending.
+ * Independent of vlmp_profile_range's state. m in [1, 8].
+ */
+int vlmp_profile_mbest(vlmp_session* s, int32_t lmin, int32_t lmax, int32_t m);
+/* dist[N][m] (ascending canonical values), nbr[N][m] (key order; -1 = none). */
+int vlmp_get_profile_m(vlmp_session* s, int32_t length, double* dist, int64_t* nbr);
+/* Top-k m-th discords per length (k x m matrices, discords.py:68-93): [n_len][k][m]. */
+int vlmp_discords_m(vlmp_session* s, int32_t k, double* out_dist, int64_t* out_off);
+
+/*
  * Timings and counters of the last phase-1/phase-2 run:
  * out[0] profile ms (device), out[1] finalize ms, out[2] executed pair updates,
  * out[3] W (non-trivial pair updates), out[4] tile-kernel ms, out[5] tile-kernel

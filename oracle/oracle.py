@@ -45,6 +45,10 @@ def load():
         lib.vlmpo_pair_distance.restype = d
         lib.vlmpo_discords_m1.argtypes = [vp, i64, i64, i64, vp, vp]
         lib.vlmpo_discords_m1.restype = None
+        lib.vlmpo_profile_m.argtypes = [vp, vp, vp, i64, i64, d, i64, i64, vp, vp, i64, vp, vp, C.c_int]
+        lib.vlmpo_profile_m.restype = C.c_int
+        lib.vlmpo_discords_km.argtypes = [vp, i64, i64, i64, i64, vp, vp]
+        lib.vlmpo_discords_km.restype = None
         lib.vlmpo_stats.argtypes = [vp, vp, i64, i64, vp, vp]
         lib.vlmpo_stats.restype = None
         _lib = lib
@@ -74,6 +78,46 @@ def profile(series, m, nthreads=0, row_lo=0, row_hi=None):
                            N if row_hi is None else row_hi, _p(mp), _p(ip), nthreads)
     assert rc == 0
     return mp, ip
+
+
+def profile_m(series, m, mbest, nthreads=0):
+    """MP/IP plus the mbest smallest (distance, index) per row (profile.py:319-326)."""
+    lib = load()
+    t, c1, c2 = _arrays(series)
+    n = t.shape[0]
+    N = n - m + 1
+    mp = np.full(N, np.inf); ip = np.full(N, -1, dtype=np.int64)
+    bm = np.full((N, mbest), np.inf); bmi = np.full((N, mbest), -1, dtype=np.int64)
+    rc = lib.vlmpo_profile_m(_p(t), _p(c1), _p(c2), n, m, float(series.sigma_floor), 0, N,
+                             _p(mp), _p(ip), mbest, _p(bm), _p(bmi), nthreads or os.cpu_count())
+    assert rc == 0
+    return mp, ip, bm, bmi
+
+
+def discords_km(series, lmin, lmax, k, mb, nthreads=0):
+    """Top-k m-th discords per length and merged (discords.py:68-109 replayed on the
+    oracle's exact m best, values via pair_distance, discords.py:126-141)."""
+    lib = load()
+    t, c1, c2 = _arrays(series)
+    fl = float(series.sigma_floor)
+    per = {}
+    merged_d = np.full((k, mb), -np.inf); merged_o = np.full((k, mb), -1, dtype=np.int64)
+    merged_l = np.zeros((k, mb), dtype=np.int64)
+    for length in range(lmin, lmax + 1):
+        _, _, bm, bmi = profile_m(series, length, mb, nthreads)
+        vals = np.full(bm.shape, np.inf)
+        for o in range(bm.shape[0]):
+            if not np.isfinite(bm[o, mb - 1]):
+                continue
+            vals[o] = np.sort([lib.vlmpo_pair_distance(_p(t), _p(c1), _p(c2), o, int(j), length, fl)
+                               for j in bmi[o]])
+        dd = np.empty((k, mb)); do = np.empty((k, mb), dtype=np.int64)
+        lib.vlmpo_discords_km(_p(np.ascontiguousarray(vals)), vals.shape[0], length, k, mb, _p(dd), _p(do))
+        per[length] = (dd, do)
+        score = dd / np.sqrt(length)
+        win = score >= merged_d
+        merged_d[win] = score[win]; merged_o[win] = do[win]; merged_l[win] = length
+    return per, (merged_d, merged_o, merged_l)
 
 
 def pair_distance(series, i, j, m):

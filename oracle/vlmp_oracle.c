@@ -48,6 +48,7 @@ typedef struct {
     const double* t; const double* mu; const double* sd;
     int64_t n, m, n_dp; double floor_;
     double* mp; int64_t* ip;
+    int64_t mbest; double* bm; int64_t* bmi;   /* optional m best per row (profile.py:319-326) */
     int64_t next_chunk, row_lo, row_hi;
     pthread_mutex_t lock;
 } job_t;
@@ -74,12 +75,18 @@ static void scan_chunk(job_t* J, int64_t start, int64_t stop, double* qt, double
             qt[0] = acc;
         }
         if (i < J->row_lo || i >= J->row_hi) continue;
-        if (sd[i] < J->floor_) { J->mp[i] = INFINITY; J->ip[i] = -1; continue; }
+        if (sd[i] < J->floor_) {
+            J->mp[i] = INFINITY; J->ip[i] = -1;
+            for (int64_t q = 0; q < J->mbest; ++q) { J->bm[i * J->mbest + q] = INFINITY; J->bmi[i * J->mbest + q] = -1; }
+            continue;
+        }
         int64_t lo = i - e + 1 > 0 ? i - e + 1 : 0;
         int64_t hi = i + e < n_dp ? i + e : n_dp;
         double a_mu = L * mu[i];
         double a_sd = L * sd[i];
         double best = INFINITY; int64_t bj = -1;
+        double mbd[16]; int64_t mbj[16];
+        for (int64_t q = 0; q < J->mbest; ++q) { mbd[q] = INFINITY; mbj[q] = -1; }
         for (int64_t j = 0; j < n_dp; ++j) {
             if (j >= lo && j < hi) continue;
             if (!(sd[j] >= J->floor_)) continue;
@@ -89,7 +96,13 @@ static void scan_chunk(job_t* J, int64_t start, int64_t stop, double* qt, double
             if (!(rad >= 0.0)) rad = 0.0;     /* np.maximum(rad, 0.0) (NaN stays NaN in numpy; denom>0 here) */
             double d = sqrt(rad);
             if (d < best) { best = d; bj = j; }   /* first argmin */
+            if (J->mbest > 0 && d < mbd[J->mbest - 1]) {   /* m best by (dist, index) */
+                int64_t q = J->mbest - 1;
+                while (q > 0 && d < mbd[q - 1]) { mbd[q] = mbd[q - 1]; mbj[q] = mbj[q - 1]; --q; }
+                mbd[q] = d; mbj[q] = j;
+            }
         }
+        for (int64_t q = 0; q < J->mbest; ++q) { J->bm[i * J->mbest + q] = mbd[q]; J->bmi[i * J->mbest + q] = mbj[q]; }
         J->mp[i] = best; J->ip[i] = (best < INFINITY) ? bj : -1;
         if (!(best < INFINITY)) J->mp[i] = INFINITY;
     }
@@ -118,9 +131,22 @@ static void* worker(void* arg) {
  * mp/ip have n-m+1 entries; rows outside the range are left untouched.
  * Returns 0, or -1 on bad arguments.
  */
+int vlmpo_profile_m(const double* t, const double* cum, const double* cum2, int64_t n,
+                    int64_t m, double sigma_floor, int64_t row_lo, int64_t row_hi,
+                    double* mp, int64_t* ip, int64_t mbest, double* bm, int64_t* bmi, int nthreads);
+
 int vlmpo_profile(const double* t, const double* cum, const double* cum2, int64_t n,
                   int64_t m, double sigma_floor, int64_t row_lo, int64_t row_hi,
                   double* mp, int64_t* ip, int nthreads) {
+    return vlmpo_profile_m(t, cum, cum2, n, m, sigma_floor, row_lo, row_hi, mp, ip, 0, NULL, NULL, nthreads);
+}
+
+/* as vlmpo_profile, plus the mbest (<= 16) smallest (distance, index) per row into
+   bm/bmi [n_dp][mbest] (profile.py:319-326 m_track) */
+int vlmpo_profile_m(const double* t, const double* cum, const double* cum2, int64_t n,
+                    int64_t m, double sigma_floor, int64_t row_lo, int64_t row_hi,
+                    double* mp, int64_t* ip, int64_t mbest, double* bm, int64_t* bmi, int nthreads) {
+    if (mbest < 0 || mbest > 16) return -1;
     if (m < 1 || m > n) return -1;
     int64_t n_dp = n - m + 1;
     if (row_lo < 0) row_lo = 0;
@@ -131,6 +157,7 @@ int vlmpo_profile(const double* t, const double* cum, const double* cum2, int64_
     job_t J;
     J.t = t; J.mu = mu; J.sd = sd; J.n = n; J.m = m; J.n_dp = n_dp; J.floor_ = sigma_floor;
     J.mp = mp; J.ip = ip; J.next_chunk = 0; J.row_lo = row_lo; J.row_hi = row_hi;
+    J.mbest = mbest; J.bm = bm; J.bmi = bmi;
     pthread_mutex_init(&J.lock, NULL);
     if (nthreads < 1) nthreads = 1;
     pthread_t th[256];
@@ -192,6 +219,40 @@ void vlmpo_discords_m1(const double* vals, int64_t n_dp, int64_t m, int64_t k,
                 for (int64_t q = k - 1; q > r; --q) { out_dist[q] = out_dist[q - 1]; out_off[q] = out_off[q - 1]; }
                 out_dist[r] = d; out_off[r] = o;
                 break;
+            }
+        }
+    }
+}
+
+/*
+ * Top-k m-th discords at one length (discords.py:68-93, :48-50): vals[o][mb] are the
+ * owner's canonical match distances ascending; owners whose mb-th value is not finite
+ * are skipped. out_* are [k][mb].
+ */
+void vlmpo_discords_km(const double* vals, int64_t n_dp, int64_t m, int64_t k, int64_t mb,
+                       double* out_dist, int64_t* out_off) {
+    int64_t e = excl_zone(m);
+    for (int64_t r = 0; r < k * mb; ++r) { out_dist[r] = -INFINITY; out_off[r] = -1; }
+    for (int64_t o = 0; o < n_dp; ++o) {
+        const double* b = vals + o * mb;
+        if (!(b[mb - 1] < INFINITY)) continue;
+        int trivial = 0;
+        for (int64_t r = 0; r < k * mb; ++r)
+            if (out_off[r] >= 0 && llabs(o - out_off[r]) < e) { trivial = 1; break; }
+        if (trivial) continue;
+        int done = 0;
+        for (int64_t c = mb - 1; c >= 0 && !done; --c) {
+            double d = b[c];
+            for (int64_t r = 0; r < k; ++r) {
+                if (d > out_dist[r * mb + c]) {
+                    for (int64_t q = k - 1; q > r; --q) {
+                        out_dist[q * mb + c] = out_dist[(q - 1) * mb + c];
+                        out_off[q * mb + c] = out_off[(q - 1) * mb + c];
+                    }
+                    out_dist[r * mb + c] = d; out_off[r * mb + c] = o;
+                    done = 1;
+                    break;
+                }
             }
         }
     }

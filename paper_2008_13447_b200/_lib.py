@@ -36,6 +36,9 @@ SIGNATURES = {
     "vlmp_smallest_rows": (C.c_int, [C.c_void_p, C.c_int32, C.c_void_p, C.c_void_p, C.c_void_p]),
     "vlmp_discords": (C.c_int, [C.c_void_p, C.c_int32, C.c_void_p, C.c_void_p]),
     "vlmp_ranking_events": (C.c_int, [C.c_void_p, C.c_double, C.c_int64] + [C.c_void_p] * 5 + [_c_int64_p]),
+    "vlmp_profile_mbest": (C.c_int, [C.c_void_p, C.c_int32, C.c_int32, C.c_int32]),
+    "vlmp_get_profile_m": (C.c_int, [C.c_void_p, C.c_int32, C.c_void_p, C.c_void_p]),
+    "vlmp_discords_m": (C.c_int, [C.c_void_p, C.c_int32, C.c_void_p, C.c_void_p]),
     "vlmp_stats": (C.c_int, [C.c_void_p, C.c_void_p, C.c_int32]),
     "vlmp_event_record": (C.c_int, [C.c_void_p, C.c_int32]),
     "vlmp_event_elapsed": (C.c_int, [C.c_void_p, C.POINTER(C.c_float)]),
@@ -173,6 +176,23 @@ class Session:
             if cnt.value <= cap:
                 return [b[:cnt.value] for b in bufs]
             cap = int(cnt.value)
+
+    # -- m-best mode (m-th discords) ---------------------------------------------
+    def profile_mbest(self, lmin, lmax, m):
+        self._check(self.lib.vlmp_profile_mbest(self.h, int(lmin), int(lmax), int(m)))
+        self.lmin, self.lmax, self.mbest = int(lmin), int(lmax), int(m)
+
+    def profile_m_arrays(self, length):
+        N = self.n - int(length) + 1
+        d = np.empty((N, self.mbest)); nb = np.empty((N, self.mbest), dtype=np.int64)
+        self._check(self.lib.vlmp_get_profile_m(self.h, int(length), _ptr(d), _ptr(nb)))
+        return d, nb
+
+    def discords_m(self, k):
+        nl = self.lmax - self.lmin + 1
+        d = np.empty((nl, k, self.mbest)); o = np.empty((nl, k, self.mbest), dtype=np.int64)
+        self._check(self.lib.vlmp_discords_m(self.h, int(k), _ptr(d), _ptr(o)))
+        return d, o
 
     def stats(self):
         out = np.zeros(16)

@@ -1,7 +1,7 @@
 """Drop-in entry points: the reference's signatures, results from the B200 path.
 
   valmod                    seriesmine/valmod.py:192-258
-  topkm_discord_discovery   seriesmine/discords.py:206-247
+  topkm_discord_discovery   seriesmine/discords.py:206-247 (m = 1 and m-th discords, m <= 8)
   compute_matrix_profile    seriesmine/profile.py:329-377
   motifs_per_length         BASELINE.md decision 1 (= valmod(series, l, l, p,
                             ranking=PairRanking(k)) for every l)
@@ -176,22 +176,27 @@ def topkm_discord_discovery(series, lmin: int, lmax: int, k: int, m: int, p: int
     if p < m:
         raise E.InvalidParametersError(f"p ({p}) must be at least m ({m})")
     validate_range(series, lmin, lmax)
-    if m != 1:
-        raise E.InvalidParametersError(
-            "the GPU path computes 1st discords (m = 1); m > 1 is not implemented yet")
-    if k > 32:
-        raise E.InvalidParametersError("k must be at most 32 on the GPU path")
+    if m > 8 or k > 32:
+        raise E.InvalidParametersError("the GPU path supports k <= 32 and m <= 8")
     _check_profile_length(series, lmin)
-    run = GpuRun(series, lmin, lmax)
-    dist, off = run.discords(k)
+    if m == 1:
+        run = GpuRun(series, lmin, lmax)
+        dist, off = run.discords(k)
+        dist, off = dist[:, :, None], off[:, :, None]
+    else:
+        sess = _lib.session(_device())
+        with sess.lock:
+            sess.set_series(series.values, series._cum, series._cum2, series.sigma_floor)
+            sess.profile_mbest(lmin, lmax, m)
+            dist, off = sess.discords_m(k)
     merged = VariableLengthDiscordMatrix.empty(k, m)
     per_length = {}
     for li in range(lmax - lmin + 1):
         length = lmin + li
         dkm = DiscordMatrix.empty(k, m, length)
-        dkm.dist[:, 0] = dist[li]
-        dkm.offset[:, 0] = off[li]
-        dkm._occupied = {int(o) for o in off[li] if o >= 0}
+        dkm.dist[:, :] = dist[li]
+        dkm.offset[:, :] = off[li]
+        dkm._occupied = {int(o) for o in off[li].ravel() if o >= 0}
         per_length[length] = dkm
         update_variable_length_discords(dkm, merged, k, m)
         if trace is not None:
@@ -209,8 +214,8 @@ def compute_matrix_profile(series, length: int, p: int, m_track: int = 0,
         raise E.SeriesTooShortError(f"need 4 <= length <= n/2 (length={length}, n={series.n})")
     if p < 1:
         raise E.InvalidParametersError("p must be at least 1")
-    if m_track > 1:
-        raise E.InvalidParametersError("m_track > 1 is not implemented on the GPU path")
+    if m_track > 8:
+        raise E.InvalidParametersError("the GPU path tracks at most m = 8 matches per row")
     _check_profile_length(series, length)
     run = GpuRun(series, length, length)
     mp, ip = run.profile(length)
@@ -218,6 +223,11 @@ def compute_matrix_profile(series, length: int, p: int, m_track: int = 0,
     if m_track == 1:
         best_m = mp[:, None].copy()
         best_nbr = ip[:, None].copy()
+    elif m_track > 1:
+        sess = run.sess
+        with sess.lock:
+            sess.profile_mbest(length, length, m_track)
+            best_m, best_nbr = sess.profile_m_arrays(length)
     return ProfileResult(MatrixProfile(mp, ip, length), None, best_m, best_nbr)
 
 

@@ -802,6 +802,269 @@ __global__ void k_dfma_peak(double* out, int iters, double x) {
     if (s == 12345.678) out[0] = s;
 }
 
+
+// =================================================================================
+// m-th discords (m > 1): per (length, offset) the m best neighbours, exact.
+// The filter tile kernel runs with U = a bound on each offset's m-th best key; passing
+// cells go to per-offset slots; k_select_m keeps the m smallest (key, index); offsets
+// whose slots overflow are recomputed exactly from direct dot products.
+constexpr int MB_MAX = 8;                 // largest supported m
+constexpr int SLOT_CAP = 24;              // candidate slots per offset per length
+
+struct BoundMArgs {
+    const double* tn; const double* mu; Prm* prm;
+    const long long* nn1;      // lmin: full-fold nearest neighbour per offset (or nullptr)
+    const int* prevm;          // > lmin: previous length's m best per offset [A][mb] (or nullptr)
+    long long N, Nprev, A; int m, e, mb; double margin;
+};
+
+// one warp per offset; candidates = previous m-best and their +-1 shifts (or the NN1
+// neighbourhood at the first length); U = m-th smallest candidate key + margin
+__global__ void k_bound_m(BoundMArgs a) {
+    const int lane = threadIdx.x & 31;
+    const long long o = (blockIdx.x * (long long)blockDim.x + threadIdx.x) >> 5;
+    if (o >= a.N) return;
+    const double io = a.prm[o].inv;
+    if (!(io == io)) { if (lane == 0) a.prm[o].U = -INFINITY; return; }
+    long long cand[3 * MB_MAX + 8];
+    int nc = 0;
+    if (a.prevm) {
+        for (int q = 0; q < a.mb; ++q) {
+            const long long c = (o < a.Nprev) ? a.prevm[o * a.mb + q] : -1;
+            if (c >= 0) { cand[nc++] = c; cand[nc++] = c - 1; cand[nc++] = c + 1; }
+        }
+    } else {
+        const long long c1 = a.nn1[o];
+        if (c1 >= 0)
+            for (int t = -(a.mb + 1); t <= a.mb + 1; ++t) cand[nc++] = c1 + t;
+        if (o >= 1) { const long long c = a.nn1[o - 1]; if (c >= 0) cand[nc++] = c + 1; }
+        if (o + 1 < a.N) { const long long c = a.nn1[o + 1]; if (c >= 0) cand[nc++] = c - 1; }
+    }
+    double best[MB_MAX];
+    for (int q = 0; q < MB_MAX; ++q) best[q] = INFINITY;
+    const double mo = a.mu[o];
+    for (int q0 = 0; q0 < nc; q0 += 4) {
+        bool ok[4]; double mc[4], ic[4]; long long cc[4];
+#pragma unroll
+        for (int u = 0; u < 4; ++u) {
+            ok[u] = false; mc[u] = 0.0; ic[u] = 0.0; cc[u] = o;
+            const int q = q0 + u;
+            if (q < nc) {
+                const long long c = cand[q];
+                bool dup = false;
+                for (int r = 0; r < q; ++r) dup |= (cand[r] == c);
+                const long long dd = c > o ? c - o : o - c;
+                if (!dup && c >= 0 && c < a.N && dd >= a.e) {
+                    ic[u] = a.prm[c].inv; ok[u] = ic[u] == ic[u]; mc[u] = a.mu[c]; cc[u] = c;
+                }
+            }
+        }
+        double acc[4] = {0.0, 0.0, 0.0, 0.0};
+        for (int k = lane; k < a.m; k += 32) {
+            const double x = a.tn[o + k] - mo;
+#pragma unroll
+            for (int u = 0; u < 4; ++u) acc[u] = fma(x, a.tn[cc[u] + k] - mc[u], acc[u]);
+        }
+#pragma unroll
+        for (int u = 0; u < 4; ++u) {
+            double v = acc[u];
+#pragma unroll
+            for (int off = 16; off >= 1; off >>= 1) v += __shfl_xor_sync(FULLMASK, v, off);
+            if (ok[u]) {
+                double key = fma(-(v * io), ic[u], 1.0);
+                for (int q = 0; q < a.mb; ++q)            // insertion into the m smallest
+                    if (key < best[q]) { const double t = best[q]; best[q] = key; key = t; }
+            }
+        }
+    }
+    if (lane == 0) {
+        float out = INFINITY;
+        const double bm = best[a.mb - 1];
+        if (bm < INFINITY) out = __int_as_float(__double2hiint(fmax(bm, 0.0) + a.margin));
+        a.prm[o].U = out;
+    }
+}
+
+// filter-kernel log -> per-offset candidate slots (exact keys, exact tests)
+__global__ void k_log_slots(const RowRec* log, const unsigned long long* log_count, long long cap,
+                            const Prm* prm, int e, ulonglong2* slots, int* slot_cnt,
+                            unsigned long long* counters) {
+    const unsigned long long cnt = *log_count;
+    const long long n = (long long)(cnt < (unsigned long long)cap ? cnt : (unsigned long long)cap);
+    for (long long q = blockIdx.x * (long long)blockDim.x + threadIdx.x; q < n;
+         q += (long long)gridDim.x * blockDim.x) {
+        const RowRec rec = log[q];
+        const Prm pr = prm[rec.i];
+        for (int s = 0; s < D; ++s) {
+            const long long j = (long long)rec.j0 + s;
+            if (j - rec.i < e) continue;
+            const Prm pc = prm[j];
+            const double r = fma(-(rec.cov[s] * pr.inv), pc.inv, 1.0);
+            const float h = __int_as_float(__double2hiint(r));
+            const unsigned long long key = clamp_key(r) & ~PMASK;
+            if (h <= pr.U) {
+                const int at = atomicAdd(slot_cnt + rec.i, 1);
+                if (at < SLOT_CAP) slots[(long long)rec.i * SLOT_CAP + at] = make_ulonglong2(key, (unsigned long long)j);
+            }
+            if (h <= pc.U) {
+                const int at = atomicAdd(slot_cnt + j, 1);
+                if (at < SLOT_CAP) slots[j * SLOT_CAP + at] = make_ulonglong2(key, (unsigned long long)rec.i);
+            }
+        }
+    }
+}
+
+// per offset: the m smallest (key, index) of its slots -> out[o][0..mb) (-1 = none);
+// overflowing offsets are queued for an exact recompute; slot counters are reset
+__global__ void k_select_m(ulonglong2* slots, int* slot_cnt, long long N, int mb, int* out,
+                           long long* redo, unsigned long long* redo_cnt) {
+    const long long o = blockIdx.x * (long long)blockDim.x + threadIdx.x;
+    if (o >= N) return;
+    const int c = slot_cnt[o];
+    slot_cnt[o] = 0;
+    unsigned long long bk[MB_MAX]; long long bi[MB_MAX];
+    for (int q = 0; q < MB_MAX; ++q) { bk[q] = KEY_NONE; bi[q] = IDX_NONE; }
+    if (c > SLOT_CAP) {
+        const unsigned long long at = atomicAdd(redo_cnt, 1ull);
+        redo[at] = o;
+    } else {
+        for (int t = 0; t < c; ++t) {
+            const ulonglong2 v = slots[o * SLOT_CAP + t];
+            unsigned long long k = v.x; long long i = (long long)v.y;
+            for (int q = 0; q < mb; ++q)
+                if (key_less(k, i, bk[q], bi[q])) {
+                    const unsigned long long tk = bk[q]; const long long ti = bi[q];
+                    bk[q] = k; bi[q] = i; k = tk; i = ti;
+                }
+        }
+    }
+    for (int q = 0; q < mb; ++q) out[o * mb + q] = bi[q] == IDX_NONE ? -1 : (int)bi[q];
+}
+
+// exact recompute of queued offsets: every valid neighbour's key from a direct centred
+// dot product; block-wide m smallest
+__global__ void k_recompute_m(const double* tn, const double* mu, const Prm* prm, const long long* redo,
+                              const unsigned long long* redo_cnt, long long N, int m, int e, int mb,
+                              int* out) {
+    __shared__ unsigned long long sk[256 * MB_MAX];
+    __shared__ long long si[256 * MB_MAX];
+    const unsigned long long nred = *redo_cnt;
+    for (unsigned long long r = blockIdx.x; r < nred; r += gridDim.x) {
+        const long long o = redo[r];
+        const double io = prm[o].inv, mo = mu[o];
+        unsigned long long bk[MB_MAX]; long long bi[MB_MAX];
+        for (int q = 0; q < MB_MAX; ++q) { bk[q] = KEY_NONE; bi[q] = IDX_NONE; }
+        for (long long j = threadIdx.x; j < N; j += blockDim.x) {
+            const long long dd = j > o ? j - o : o - j;
+            if (dd < e) continue;
+            const double ic = prm[j].inv;
+            if (!(ic == ic) || !(io == io)) continue;
+            const double mc = mu[j];
+            double cv = 0.0;
+            for (int k = 0; k < m; ++k) cv = fma(tn[o + k] - mo, tn[j + k] - mc, cv);
+            unsigned long long key = clamp_key(fma(-(cv * io), ic, 1.0)) & ~PMASK;
+            long long idx = j;
+            for (int q = 0; q < mb; ++q)
+                if (key_less(key, idx, bk[q], bi[q])) {
+                    const unsigned long long tk = bk[q]; const long long ti = bi[q];
+                    bk[q] = key; bi[q] = idx; key = tk; idx = ti;
+                }
+        }
+        for (int q = 0; q < mb; ++q) { sk[threadIdx.x * MB_MAX + q] = bk[q]; si[threadIdx.x * MB_MAX + q] = bi[q]; }
+        __syncthreads();
+        if (threadIdx.x == 0) {
+            unsigned long long fk[MB_MAX]; long long fi[MB_MAX];
+            for (int q = 0; q < MB_MAX; ++q) { fk[q] = KEY_NONE; fi[q] = IDX_NONE; }
+            for (int t = 0; t < (int)blockDim.x; ++t)
+                for (int q0 = 0; q0 < mb; ++q0) {
+                    unsigned long long key = sk[t * MB_MAX + q0]; long long idx = si[t * MB_MAX + q0];
+                    if (idx == IDX_NONE) break;
+                    for (int q = 0; q < mb; ++q)
+                        if (key_less(key, idx, fk[q], fi[q])) {
+                            const unsigned long long tk = fk[q]; const long long ti = fi[q];
+                            fk[q] = key; fi[q] = idx; key = tk; idx = ti;
+                        }
+                }
+            for (int q = 0; q < mb; ++q) out[o * mb + q] = fi[q] == IDX_NONE ? -1 : (int)fi[q];
+        }
+        __syncthreads();
+    }
+}
+
+// canonical distances of the m best, sorted ascending (discords.py:126-141)
+__global__ void k_finalize_m(const double* tn, const double* cum, const double* cum2, const int* ipm,
+                             double* mpm, long long n, long long A, int lmin, int mb, double floor_) {
+    const long long o = blockIdx.x * (long long)blockDim.x + threadIdx.x;
+    const int li = blockIdx.y;
+    const int m = lmin + li;
+    if (o >= n - m + 1) return;
+    const long long base = ((long long)li * A + o) * mb;
+    double v[MB_MAX];
+    for (int q = 0; q < mb; ++q) {
+        const int nb = ipm[base + q];
+        v[q] = nb >= 0 ? pair_distance(tn, cum, cum2, o, nb, m, floor_) : INFINITY;
+    }
+    for (int q = 1; q < mb; ++q)
+        for (int r = q; r > 0 && v[r] < v[r - 1]; --r) { const double t = v[r]; v[r] = v[r - 1]; v[r - 1] = t; }
+    for (int q = 0; q < mb; ++q) mpm[base + q] = v[q];
+}
+
+// top-k m-th discords per length: ascending-offset greedy replay (discords.py:68-93,
+// :48-50) of the canonical sorted distances, exact prefilter "some column beats row k-1";
+// one warp per length, state in shared memory
+__global__ void k_discords_m(const double* mpm, double* out_d, long long* out_o, long long n, long long A,
+                             int lmin, int n_len, int k, int mb) {
+    extern __shared__ unsigned char sm_raw[];
+    const int lane = threadIdx.x & 31, wl = threadIdx.x >> 5;
+    const int li = blockIdx.x * (blockDim.x >> 5) + wl;
+    double* cd = reinterpret_cast<double*>(sm_raw) + (size_t)wl * 32 * MB_MAX * 2;
+    long long* co = reinterpret_cast<long long*>(cd + 32 * MB_MAX);
+    if (li >= n_len) return;
+    const int m = lmin + li;
+    const long long N = n - m + 1, e = (m + 1) / 2;
+    for (int t = lane; t < k * mb; t += 32) { cd[t] = -INFINITY; co[t] = -1; }
+    __syncwarp();
+    for (long long base = 0; base < N; base += 32) {
+        const long long o = base + lane;
+        bool cand = false;
+        if (o < N) {
+            const double* b = mpm + ((long long)li * A + o) * mb;
+            if (b[mb - 1] < INFINITY)
+                for (int c = 0; c < mb; ++c) cand |= b[c] > cd[(k - 1) * mb + c];
+        }
+        unsigned bal = __ballot_sync(FULLMASK, cand);
+        while (bal) {
+            const int src = __ffs(bal) - 1;
+            bal &= bal - 1;
+            if (lane == 0) {
+                const long long ov = base + src;
+                const double* b = mpm + ((long long)li * A + ov) * mb;
+                bool triv = false;
+                for (int t = 0; t < k * mb; ++t) triv |= (co[t] >= 0 && llabs(ov - co[t]) < e);
+                if (!triv) {
+                    bool done = false;
+                    for (int c = mb - 1; c >= 0 && !done; --c) {
+                        const double d = b[c];
+                        for (int r = 0; r < k; ++r) {
+                            if (d > cd[r * mb + c]) {
+                                for (int q = k - 1; q > r; --q) { cd[q * mb + c] = cd[(q - 1) * mb + c]; co[q * mb + c] = co[(q - 1) * mb + c]; }
+                                cd[r * mb + c] = d; co[r * mb + c] = ov;
+                                done = true;
+                                break;
+                            }
+                        }
+                    }
+                }
+            }
+            __syncwarp();
+        }
+    }
+    for (int t = lane; t < k * mb; t += 32) {
+        out_d[(long long)li * k * mb + t] = cd[t];
+        out_o[(long long)li * k * mb + t] = co[t];
+    }
+}
+
 }  // namespace
 
 // =================================================================================
@@ -835,6 +1098,13 @@ struct vlmp_session {
     long long* d_ro_i64 = nullptr; size_t ro_i64_cap = 0;
     double* d_ro_f64 = nullptr; size_t ro_f64_cap = 0;
     unsigned long long* d_ro_cnt = nullptr;
+    // m-best mode (m > 1 discords)
+    int mbest = 1;
+    ulonglong2* d_slots = nullptr; size_t slots_cap = 0;
+    int* d_slotcnt = nullptr; size_t slotcnt_cap = 0;
+    int* d_ipm = nullptr; size_t ipm_cap = 0;
+    double* d_mpm = nullptr; size_t mpm_cap = 0;
+    long long* d_redo = nullptr; size_t redo_cap = 0;
     // run state
     int lmin = 0, lmax = 0, n_len = 0; bool have_profile = false, have_final = false;
     double stats[16] = {};
@@ -860,10 +1130,11 @@ int ensure1(T*& p, size_t count) { size_t cap = 0; if (p) { cudaFree(p); p = nul
 inline unsigned blocks(long long n, int t) { return (unsigned)((n + t - 1) / t); }
 
 int seg_rows(long long n) {
-    // S = 1 + G*D rows per tile; larger for longer series to bound the seed store
+    // S = G*D rows per tile (whole 8-row groups); larger for longer series to bound the
+    // number of tiles and the seed store (config 5: S = 16384, ~1.1M tiles, 2.2 GB of seeds)
     long long G = 128;
-    while ((1 + G * D) * 256 < n && G < 2048) G *= 2;
-    return (int)(1 + G * D);
+    while (G * D * 256 < n && G < 2048) G *= 2;
+    return (int)(G * D);
 }
 
 long long dlo_for(int lmin) { return (lmin + 1) / 2; }
@@ -925,7 +1196,8 @@ void vlmp_destroy(vlmp_session* s) {
     cudaStreamSynchronize(s->stream);
     void* ptrs[] = {s->d_tn, s->d_cum, s->d_cum2, s->d_prm, s->d_mu,
                     s->d_previdx, s->d_tiles, s->d_seeds, s->d_acc, s->d_mp, s->d_ip, s->d_counters,
-                    s->d_log, s->d_logcnt, s->d_ro_i64, s->d_ro_f64, s->d_ro_cnt, s->d_vdist, s->d_vnorm, s->d_vlen, s->d_vidx, s->d_vpop};
+                    s->d_log, s->d_logcnt, s->d_ro_i64, s->d_ro_f64, s->d_ro_cnt,
+                    s->d_slots, s->d_slotcnt, s->d_ipm, s->d_mpm, s->d_redo, s->d_vdist, s->d_vnorm, s->d_vlen, s->d_vidx, s->d_vpop};
     for (void* p : ptrs) if (p) cudaFree(p);
     for (auto& ev : s->ev) if (ev) cudaEventDestroy(ev);
     for (auto& ev : s->lev) cudaEventDestroy(ev);
@@ -1308,6 +1580,148 @@ int vlmp_ranking_events(vlmp_session* s, double tau, int64_t cap, int64_t* ev_of
 int vlmp_stats(vlmp_session* s, double* out, int32_t n_out) {
     if (!s || !out) return fail(VLMP_E_INVALID_PARAMETERS, "null argument");
     for (int q = 0; q < n_out && q < 16; ++q) out[q] = s->stats[q];
+    return 0;
+}
+
+int vlmp_profile_mbest(vlmp_session* s, int32_t lmin, int32_t lmax, int32_t mb) {
+    if (!s) return fail(VLMP_E_INVALID_PARAMETERS, "null session");
+    if (s->n <= 0) return fail(VLMP_E_STATE, "no series uploaded");
+    if (lmin > lmax) return fail(VLMP_E_INVALID_PARAMETERS, "lmin > lmax");
+    if (lmin < 4) return fail(VLMP_E_INVALID_PARAMETERS, "minimum window length is 4");
+    if (mb < 1 || mb > MB_MAX) return fail(VLMP_E_INVALID_PARAMETERS, "m must be in [1, 8]");
+    if (s->n < (long long)lmax + (lmax + 1) / 2)
+        return fail(VLMP_E_SERIES_TOO_SHORT, "series cannot host a non-trivial pair at lmax");
+    std::lock_guard<std::mutex> g(s->lock);
+    CU(cudaSetDevice(s->device));
+    cudaStream_t st = s->stream;
+    const long long n = s->n, A = s->A;
+    const int n_len = lmax - lmin + 1;
+    const long long nb = n_bands_for(n, lmin);
+    const int S = seg_rows(n);
+    const long long N0 = n - lmin + 1, dl = dlo_for(lmin);
+    std::vector<int2> tiles;
+    for (long long b = 0; b < nb; ++b) {
+        long long rows = N0 - (dl + b * BAND);
+        for (long long sg = 0; sg * S < rows; ++sg) tiles.push_back(make_int2((int)b, (int)sg));
+    }
+    const long long T = (long long)tiles.size();
+    int rc;
+    if ((rc = ensure(s->d_tiles, s->tiles_cap, (size_t)std::max<long long>(T, 1)))) return rc;
+    if ((rc = ensure(s->d_seeds, s->seeds_cap, (size_t)std::max<long long>(T, 1) * BAND))) return rc;
+    if ((rc = ensure(s->d_acc, s->acc_cap, (size_t)A))) return rc;
+    const size_t log_cap = std::max<size_t>((size_t)1 << 18, (size_t)(4 * N0));
+    if ((rc = ensure(s->d_log, s->log_cap, log_cap))) return rc;
+    if ((rc = ensure(s->d_logcnt, s->logcnt_cap, (size_t)n_len))) return rc;
+    if ((rc = ensure(s->d_slots, s->slots_cap, (size_t)A * SLOT_CAP))) return rc;
+    if ((rc = ensure(s->d_slotcnt, s->slotcnt_cap, (size_t)A))) return rc;
+    if ((rc = ensure(s->d_ipm, s->ipm_cap, (size_t)n_len * A * mb))) return rc;
+    if ((rc = ensure(s->d_redo, s->redo_cap, (size_t)A))) return rc;
+    if (!s->d_ro_cnt) CU(cudaMalloc((void**)&s->d_ro_cnt, 8));
+    CU(cudaMemsetAsync(s->d_logcnt, 0, n_len * sizeof(unsigned long long), st));
+    CU(cudaMemsetAsync(s->d_slotcnt, 0, A * sizeof(int), st));
+    CU(cudaMemsetAsync(s->d_counters, 0, 8 * sizeof(unsigned long long), st));
+    if (T) CU(cudaMemcpyAsync(s->d_tiles, tiles.data(), T * sizeof(int2), cudaMemcpyHostToDevice, st));
+    const size_t smem = WARPS_PER_CTA * sizeof(WarpSmem);
+    CU(cudaFuncSetAttribute(k_tile<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    CU(cudaFuncSetAttribute(k_tile<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    CU(cudaEventRecord(s->ev[0], st));
+    const double margin = 1.0 / (1 << 26);
+    long long redo_total = 0;
+    for (int li = 0; li < n_len; ++li) {
+        const int m = lmin + li;
+        const long long N = n - m + 1;
+        const int e = (m + 1) / 2;
+        ParamArgs pa{s->d_tn, s->d_cum, s->d_cum2, s->d_prm, s->d_mu, n, N, A, m, s->floor_};
+        k_params<<<blocks(A, 256), 256, 0, st>>>(pa);
+        TileArgs ta{s->d_prm, s->d_mu, s->d_tn, s->d_tiles, s->d_seeds, s->d_acc,
+                    s->d_counters, s->d_log, s->d_logcnt + li, (long long)s->log_cap,
+                    N, dl, (int)T, S, m, e, 0};
+        BoundMArgs bm{s->d_tn, s->d_mu, s->d_prm, nullptr, nullptr, N, N + 1, A, m, e, mb, margin};
+        if (li == 0) {
+            if (T) {
+                SeedArgs sa{s->d_tn, s->d_mu, s->d_tiles, s->d_seeds, dl, (int)T, S, m};
+                k_seed_init<<<blocks(T * 32, WARPS_PER_CTA * 32), WARPS_PER_CTA * 32, 0, st>>>(sa);
+                // nearest neighbours of the first length (seeds untouched) -> bound candidates
+                k_fill_acc<<<blocks(A, 256), 256, 0, st>>>(s->d_acc, A);
+                k_tile<true><<<blocks(T, WARPS_PER_CTA), WARPS_PER_CTA * 32, smem, st>>>(ta);
+            }
+            k_acc_idx<<<blocks(N, 256), 256, 0, st>>>(s->d_acc, s->d_previdx, N);
+            bm.nn1 = s->d_previdx;
+        } else {
+            bm.prevm = s->d_ipm + (long long)(li - 1) * A * mb;
+        }
+        k_bound_m<<<blocks(N * 32, 256), 256, 0, st>>>(bm);
+        if (T) {
+            ta.update_seeds = li + 1 < n_len;
+            k_tile<false><<<blocks(T, WARPS_PER_CTA), WARPS_PER_CTA * 32, smem, st>>>(ta);
+            k_log_slots<<<296, 128, 0, st>>>(s->d_log, s->d_logcnt + li, (long long)s->log_cap, s->d_prm, e,
+                                             s->d_slots, s->d_slotcnt, s->d_counters);
+        }
+        CU(cudaMemsetAsync(s->d_ro_cnt, 0, 8, st));
+        int* out = s->d_ipm + (long long)li * A * mb;
+        k_select_m<<<blocks(N, 256), 256, 0, st>>>(s->d_slots, s->d_slotcnt, N, mb, out, s->d_redo, s->d_ro_cnt);
+        k_recompute_m<<<148, 256, 0, st>>>(s->d_tn, s->d_mu, s->d_prm, s->d_redo, s->d_ro_cnt, N, m, e, mb, out);
+        unsigned long long nred = 0;
+        CU(cudaMemcpyAsync(&nred, s->d_ro_cnt, 8, cudaMemcpyDeviceToHost, st));
+        CU(cudaStreamSynchronize(st));
+        redo_total += (long long)nred;
+        CU(cudaGetLastError());
+    }
+    CU(cudaEventRecord(s->ev[1], st));
+    CU(cudaEventSynchronize(s->ev[1]));
+    float ms = 0; CU(cudaEventElapsedTime(&ms, s->ev[0], s->ev[1]));
+    std::vector<unsigned long long> lc(n_len);
+    CU(cudaMemcpy(lc.data(), s->d_logcnt, n_len * sizeof(unsigned long long), cudaMemcpyDeviceToHost));
+    for (auto c : lc)
+        if (c > s->log_cap) return fail(VLMP_E_CUDA, "m-best candidate log overflow (bounds too weak for this series)");
+    // finalize: canonical sorted distances of the m best; MP/IP (first neighbour) for VALMP
+    if ((rc = ensure(s->d_mpm, s->mpm_cap, (size_t)n_len * A * mb))) return rc;
+    dim3 grid(blocks(N0, 128), n_len);
+    k_finalize_m<<<grid, 128, 0, st>>>(s->d_tn, s->d_cum, s->d_cum2, s->d_ipm, s->d_mpm, n, A, lmin, mb, s->floor_);
+    CU(cudaGetLastError());
+    CU(cudaStreamSynchronize(st));
+    s->lmin = lmin; s->lmax = lmax; s->n_len = n_len; s->mbest = mb;
+    s->have_profile = false; s->have_final = false;
+    memset(s->stats, 0, sizeof(s->stats));
+    s->stats[0] = ms; s->stats[13] = (double)redo_total;
+    return 0;
+}
+
+int vlmp_get_profile_m(vlmp_session* s, int32_t length, double* dist, int64_t* nbr) {
+    if (!s || s->mbest < 1 || !s->d_mpm) return fail(VLMP_E_STATE, "no m-best run");
+    if (length < s->lmin || length > s->lmax) return fail(VLMP_E_INVALID_PARAMETERS, "length outside the run");
+    std::lock_guard<std::mutex> g(s->lock);
+    CU(cudaSetDevice(s->device));
+    const int mb = s->mbest;
+    const long long N = s->n - length + 1;
+    const long long off = (long long)(length - s->lmin) * s->A * mb;
+    std::vector<int> tmp(N * mb);
+    CU(cudaMemcpyAsync(dist, s->d_mpm + off, N * mb * 8, cudaMemcpyDeviceToHost, s->stream));
+    CU(cudaMemcpyAsync(tmp.data(), s->d_ipm + off, N * mb * 4, cudaMemcpyDeviceToHost, s->stream));
+    CU(cudaStreamSynchronize(s->stream));
+    for (long long q = 0; q < N * mb; ++q) nbr[q] = tmp[q];
+    return 0;
+}
+
+int vlmp_discords_m(vlmp_session* s, int32_t k, double* out_dist, int64_t* out_off) {
+    if (!s || !s->d_mpm) return fail(VLMP_E_STATE, "no m-best run");
+    if (k < 1 || k > 32) return fail(VLMP_E_INVALID_PARAMETERS, "k must be in [1, 32]");
+    const int mb = s->mbest;
+    if (k * mb > 32 * MB_MAX) return fail(VLMP_E_INVALID_PARAMETERS, "k*m too large");
+    std::lock_guard<std::mutex> g(s->lock);
+    CU(cudaSetDevice(s->device));
+    const long long cnt = (long long)s->n_len * k * mb;
+    int rc;
+    if ((rc = ensure(s->d_ro_i64, s->ro_i64_cap, (size_t)cnt))) return rc;
+    if ((rc = ensure(s->d_ro_f64, s->ro_f64_cap, (size_t)cnt))) return rc;
+    const int wpb = 4;
+    const size_t sm = (size_t)wpb * 32 * MB_MAX * 16;
+    k_discords_m<<<blocks((long long)s->n_len * 32, wpb * 32), wpb * 32, sm, s->stream>>>(
+        s->d_mpm, s->d_ro_f64, s->d_ro_i64, s->n, s->A, s->lmin, s->n_len, k, mb);
+    CU(cudaGetLastError());
+    CU(cudaMemcpyAsync(out_dist, s->d_ro_f64, cnt * 8, cudaMemcpyDeviceToHost, s->stream));
+    CU(cudaMemcpyAsync(out_off, s->d_ro_i64, cnt * 8, cudaMemcpyDeviceToHost, s->stream));
+    CU(cudaStreamSynchronize(s->stream));
     return 0;
 }
 

@@ -161,5 +161,18 @@ def cfg2():
     print("wrote cfg2 valmod", out2["valmod_seconds"], flush=True)
 
 
+def small_m3():
+    """m-th discords (k = 3, m = 3): reference engine and brute force agree on these."""
+    for seed in (10, 11, 12):
+        t = sm.ingest(random_walk(600, seed=seed))
+        out = {"t": t.values, "lmin": 16, "lmax": 40}
+        scan = sm.topkm_discord_discovery(t, 16, 40, 3, 3, 5)
+        out.update(_discord_fields("k3m3_", scan, 16, 40, 3, 3))
+        per_o, merged_o = sm.brute_force_discords(t, 16, 40, 3, 3)
+        assert all(np.array_equal(per_o[L].offset, scan.per_length[L].offset) for L in per_o)
+        np.savez_compressed(os.path.join(HERE, f"small_m3_walk{seed}.npz"), **out)
+        print("wrote m3", seed, flush=True)
+
+
 if __name__ == "__main__":
-    {"small": small, "cfg1": cfg1, "cfg2": cfg2}[sys.argv[1]]()
+    {"small": small, "small_m3": small_m3, "cfg1": cfg1, "cfg2": cfg2}[sys.argv[1]]()

@@ -251,3 +251,41 @@ def test_symmetric_values_for_mutual_pairs():
         mutual = np.flatnonzero((ip >= 0) & (ip[np.maximum(ip, 0)] == np.arange(ip.shape[0])))
         assert mutual.size > 10
         assert np.array_equal(mp[mutual], mp[ip[mutual]])
+
+
+@pytest.mark.parametrize("seed", [10, 11, 12])
+def test_m_th_discords_match_reference(seed):
+    """Top-k m-th discords (k = 3, m = 3) vs the reference engine (discords.py:206-247)."""
+    g = load_golden(f"small_m3_walk{seed}")
+    s = vl.ingest(g["t"])
+    scan = vl.topkm_discord_discovery(s, 16, 40, 3, 3, 5)
+    for L in range(16, 41):
+        assert np.array_equal(scan.per_length[L].offset, g["k3m3_disc_off"][L - 16]), L
+        fin = np.isfinite(g["k3m3_disc_dist"][L - 16])
+        assert np.allclose(scan.per_length[L].dist[fin], g["k3m3_disc_dist"][L - 16][fin], atol=1e-7)
+    assert np.array_equal(scan.merged.offset, g["k3m3_merged_off"])
+    assert np.array_equal(scan.merged.length, g["k3m3_merged_len"])
+    assert np.allclose(scan.merged.dist, g["k3m3_merged_dist"], atol=1e-7)
+
+
+@pytest.mark.parametrize("mb", [2, 4])
+def test_m_best_rows_against_oracle(mb, oracle_mod):
+    """compute_matrix_profile(m_track = m): the m best neighbours per row, exact, and their
+    canonical distances ascending (profile.py:319-326, discords.py:126-141)."""
+    s = vl.ingest(np.cumsum(np.random.default_rng(31).standard_normal(1500)))
+    for L in (24, 40):
+        res = vl.compute_matrix_profile(s, L, 5, m_track=mb)
+        _, _, bm, bmi = oracle_mod.profile_m(s, L, mb)
+        assert np.array_equal(np.sort(res.best_m_nbr, axis=1), np.sort(bmi, axis=1)), L
+        fin = np.isfinite(bm)
+        canon = np.sort(np.where(fin, bm, np.inf), axis=1)
+        assert np.allclose(res.best_m[fin], canon[fin], atol=1e-7)
+
+
+def test_m_th_discords_config1(oracle_mod):
+    s = vl.ingest(gen.series_for(1))
+    scan = vl.topkm_discord_discovery(s, 32, 40, 2, 3, 5)
+    per, (md, mo, ml) = oracle_mod.discords_km(s, 32, 40, 2, 3)
+    for L in range(32, 41):
+        assert np.array_equal(scan.per_length[L].offset, per[L][1]), L
+    assert np.array_equal(scan.merged.offset, mo)

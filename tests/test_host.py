@@ -37,8 +37,8 @@ def test_discord_parameter_validation():
     assert "p" in str(exc.value) and "m" in str(exc.value)
     with pytest.raises(InvalidParametersError):
         vl.topkm_discord_discovery(t, 16, 24, 0, 1, 5)
-    with pytest.raises(InvalidParametersError):   # m > 1 not on the GPU path (no CPU fallback)
-        vl.topkm_discord_discovery(t, 16, 24, 1, 2, 5)
+    with pytest.raises(InvalidParametersError):   # m > 8 not on the GPU path (no CPU fallback)
+        vl.topkm_discord_discovery(t, 16, 24, 1, 9, 9)
 
 
 def test_all_constant_and_short():

@@ -92,3 +92,16 @@ def test_oracle_kats(oracle_mod):
     # insertion policy: a weaker candidate below everything changes nothing
     d, o = oracle_mod.discords_m1(np.array([5.0, np.inf, 4.0, 3.0]), 4, 2)
     assert list(o) == [0, 2] and list(d) == [5.0, 4.0]   # offset 3 is trivial to 2
+
+
+@pytest.mark.parametrize("seed", [10, 11, 12])
+def test_oracle_m_th_discords_match_reference(seed, oracle_mod):
+    """k = 3, m = 3 discords (discords.py:68-109) vs the reference engine's fixtures."""
+    g = load_golden(f"small_m3_walk{seed}")
+    s = ingest(g["t"])
+    per, (md, mo, ml) = oracle_mod.discords_km(s, 16, 40, 3, 3)
+    for L in range(16, 41):
+        assert np.array_equal(per[L][1], g["k3m3_disc_off"][L - 16]), L
+        fin = np.isfinite(g["k3m3_disc_dist"][L - 16])
+        assert np.allclose(per[L][0][fin], g["k3m3_disc_dist"][L - 16][fin], atol=1e-7)
+    assert np.array_equal(mo, g["k3m3_merged_off"]) and np.array_equal(ml, g["k3m3_merged_len"])
