@@ -398,7 +398,8 @@ __device__ __forceinline__ void tile_body(const TileArgs& a, WarpSmem& w, int wi
                 const int q = (kk + D - 1) & (D - 1);
                 // lane 0's outgoing column leaves the band: overwrite it with the fresh
                 // column, then rotate by one lane so lane 31 receives it
-                if (lane == 0) {
+                // (rows after a group's first: lane 0 loaded it at the end of the previous row)
+                if (lane == 0 && kk == 0) {
                     const Prm f = w.fresh[b][kk];
                     cdf[q] = f.df; cdg[q] = f.dg; cinv[q] = f.inv; cU[q] = f.U;
                 }
@@ -462,6 +463,12 @@ __device__ __forceinline__ void tile_body(const TileArgs& a, WarpSmem& w, int wi
                 const double x0 = __shfl_sync(FULLMASK, x, 0);   // lane 0's exiting column
                 const int slot = (int)((i - i0) & 31);
                 if (lane == slot) { rowres = rm; rowres_i = i; colres = x0; colres_j = i + d0; }
+            }
+            if (kk + 1 < D && lane == 0) {
+                // slot 0's column (phys kk) is dead after this row: lane 0 fetches the next row's
+                // fresh column into it now, so the next rotation's shuffles need not wait
+                const Prm f = w.fresh[b][kk + 1];
+                cdf[kk] = f.df; cdg[kk] = f.dg; cinv[kk] = f.inv; cU[kk] = f.U;
             }
         }
         if (FULL && (g & 3) == 3) flush_full();

@@ -1,0 +1,67 @@
+"""The multi-GPU code path (band sharding + exact two-step MIN merge + finalize) on real
+hardware: two ranks share the one B200 of the pool, exchanging partials with the gloo
+backend (a host-mediated collective: no kernel of one rank waits on the other). The
+merged result must be bit-identical to the single-process run."""
+
+import os
+import socket
+
+import numpy as np
+import pytest
+
+pytestmark = pytest.mark.gpu
+
+
+def _free_port():
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    p = s.getsockname()[1]
+    s.close()
+    return p
+
+
+def _rank(rank, world, port, t, lmin, lmax, out):
+    import torch
+    import torch.distributed as dist
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        from paper_2008_13447_b200 import _lib, distributed, ingest
+        s = ingest(t)
+        sess = _lib.Session(0)
+        distributed.profile_sharded(sess, s, lmin, lmax, rank, world)
+        d, nm, ln, ix, pop = sess.valmp_arrays()
+        off, nbr, dd = sess.smallest_rows(4)
+        disc_d, disc_o = sess.discords(3)
+        if rank == 0:
+            np.savez(out, d=d, nm=nm, ln=ln, ix=ix, pop=pop, off=off, nbr=nbr, dd=dd,
+                     disc_d=disc_d, disc_o=disc_o)
+        sess.close()
+    finally:
+        dist.destroy_process_group()
+
+
+def test_two_ranks_equal_single(tmp_path):
+    import torch.multiprocessing as mp
+    from paper_2008_13447_b200 import _lib, ingest
+    t = np.cumsum(np.random.default_rng(44).standard_normal(6000))
+    lmin, lmax = 48, 64
+    out = str(tmp_path / "sharded.npz")
+    mp.start_processes(_rank, args=(2, _free_port(), t, lmin, lmax, out), nprocs=2, join=True,
+                       start_method="spawn")
+    got = np.load(out)
+    sess = _lib.session(0)
+    with sess.lock:
+        s = ingest(t)
+        sess.set_series(s.values, s._cum, s._cum2, s.sigma_floor)
+        sess.profile(lmin, lmax)
+        sess.finalize()
+        ref = sess.valmp_arrays()
+        rows = sess.smallest_rows(4)
+        disc = sess.discords(3)
+    for a, b in zip(ref, [got["d"], got["nm"], got["ln"], got["ix"], got["pop"]]):
+        assert np.array_equal(a, b)
+    for a, b in zip(rows, [got["off"], got["nbr"], got["dd"]]):
+        assert np.array_equal(a, b)
+    assert np.array_equal(disc[1], got["disc_o"]) and np.array_equal(disc[0], got["disc_d"])
