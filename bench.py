@@ -248,7 +248,7 @@ def run_ours(args):
     tr_path = os.path.join(ROOT, "profiles", "tile_traffic.json")
     if os.path.exists(tr_path):
         try:
-            prof_traffic = json.load(open(tr_path)).get("bytes_per_step")
+            prof_traffic = json.load(open(tr_path)).get("bytes_per_launch")
         except Exception:
             prof_traffic = None
     cpu = None
