@@ -180,7 +180,7 @@ def run_ours(args):
 
     def step():
         if world > 1:
-            distributed.profile_sharded(sess, s, c.lmin, c.lmax, rank, world, group)
+            distributed.profile_sharded(sess, s, c.lmin, c.lmax, rank, world, group, upload=False)
         else:
             with sess.lock:
                 sess.profile(c.lmin, c.lmax, 0, -1, 0)

@@ -77,13 +77,15 @@ def merge_partials(keys, idx, group=None):
     return keys, idx
 
 
-def profile_sharded(sess, series, lmin: int, lmax: int, rank: int, world: int, group=None):
-    """Run this rank's bands on its session's device and merge with the group.
-    Leaves the merged per-length minima imported in ``sess``; call sess.finalize()."""
+def profile_sharded(sess, series, lmin: int, lmax: int, rank: int, world: int, group=None,
+                    upload: bool = True):
+    """Run this rank's bands on its session's device, merge with the group and finalize.
+    ``upload=False`` reuses the series already resident on the device."""
     import torch
     cuts = band_split(series.n, lmin, lmax, world)
     with sess.lock:
-        sess.set_series(series.values, series._cum, series._cum2, series.sigma_floor)
+        if upload:
+            sess.set_series(series.values, series._cum, series._cum2, series.sigma_floor)
         sess.profile(lmin, lmax, int(cuts[rank]), int(cuts[rank + 1]), 0)
         n_len, stride = sess.partials_size()
         dev = torch.device("cuda", sess.device)
