@@ -1088,8 +1088,6 @@ struct vlmp_session {
     double* d_tn = nullptr; double* d_cum = nullptr; double* d_cum2 = nullptr;
     // per-length scratch
     Prm* d_prm = nullptr; double* d_mu = nullptr;
-    Prm* d_prm2 = nullptr; double* d_mu2 = nullptr;     // second buffer: length l+1 prepared during l
-    cudaEvent_t pipe_ev[4] = {};                        // side-stream pipeline events
     long long* d_previdx = nullptr;
     // tiles / seeds
     int2* d_tiles = nullptr; size_t tiles_cap = 0;
@@ -1193,7 +1191,6 @@ int vlmp_create(vlmp_session** out, int device) {
     CU(cudaStreamCreateWithPriority(&s->side, cudaStreamNonBlocking, prio_hi));   // dispatch first
     CU(cudaEventCreateWithFlags(&s->fork_ev, cudaEventDisableTiming));
     CU(cudaEventCreateWithFlags(&s->join_ev, cudaEventDisableTiming));
-    for (auto& ev : s->pipe_ev) CU(cudaEventCreateWithFlags(&ev, cudaEventDisableTiming));
     for (auto& ev : s->ev) CU(cudaEventCreate(&ev));
     CU(cudaMalloc((void**)&s->d_counters, 8 * sizeof(unsigned long long)));
     *out = s;
@@ -1204,7 +1201,7 @@ void vlmp_destroy(vlmp_session* s) {
     if (!s) return;
     cudaSetDevice(s->device);
     cudaStreamSynchronize(s->stream);
-    void* ptrs[] = {s->d_tn, s->d_cum, s->d_cum2, s->d_prm, s->d_mu, s->d_prm2, s->d_mu2,
+    void* ptrs[] = {s->d_tn, s->d_cum, s->d_cum2, s->d_prm, s->d_mu,
                     s->d_previdx, s->d_tiles, s->d_seeds, s->d_acc, s->d_mp, s->d_ip, s->d_counters,
                     s->d_log, s->d_logcnt, s->d_ro_i64, s->d_ro_f64, s->d_ro_cnt,
                     s->d_slots, s->d_slotcnt, s->d_ipm, s->d_mpm, s->d_redo, s->d_vdist, s->d_vnorm, s->d_vlen, s->d_vidx, s->d_vpop};
@@ -1215,7 +1212,6 @@ void vlmp_destroy(vlmp_session* s) {
     if (s->side) cudaStreamDestroy(s->side);
     if (s->fork_ev) cudaEventDestroy(s->fork_ev);
     if (s->join_ev) cudaEventDestroy(s->join_ev);
-    for (auto& ev : s->pipe_ev) if (ev) cudaEventDestroy(ev);
     delete s;
 }
 
@@ -1232,8 +1228,6 @@ int vlmp_set_series(vlmp_session* s, const double* t, const double* cum, const d
     if ((rc = ensure1(s->d_cum, n + 1))) return rc;
     if ((rc = ensure1(s->d_cum2, n + 1))) return rc;
     if ((rc = ensure1(s->d_prm, A))) return rc;
-    if ((rc = ensure1(s->d_prm2, A))) return rc;
-    if ((rc = ensure1(s->d_mu2, A))) return rc;
     if ((rc = ensure1(s->d_mu, A))) return rc;
     if ((rc = ensure1(s->d_previdx, A))) return rc;
     CU(cudaMemsetAsync(s->d_tn, 0, (2 * A + 4096) * sizeof(double), s->stream));
@@ -1308,76 +1302,44 @@ static int profile_impl(vlmp_session* s, int32_t lmin, int32_t lmax, int64_t ban
 
     double executed = 0, launches = 0, n_filtered = 0, n_full = 0, tile_ms = 0, klaunch = 2;
     const double margin = 1.0 / (1 << 26);
-    // Pipeline: the main stream runs tile(l) + log_merge(l); the side stream prepares length
-    // l+1 (parameters into the other buffer, bounds from length l-1's winners -- any valid
-    // cell bounds the minimum, so older winners stay exact) while tile(l) runs.
-    Prm* prm_buf[2] = {s->d_prm, s->d_prm2};
-    double* mu_buf[2] = {s->d_mu, s->d_mu2};
-    cudaStream_t side = s->side;
-    cudaEvent_t& ev_ready = s->pipe_ev[0];   // side: length l+1 prepared
-    cudaEvent_t& ev_done_prev = s->pipe_ev[1];   // main: acc of the length feeding the bound done
-    cudaEvent_t& ev_done = s->pipe_ev[2];
-    auto prepare = [&](int li) -> int {
-        const int m = lmin + li;
-        const long long N = n - m + 1;
-        const int e = (m + 1) / 2;
-        const bool full = (li == 0) || (flags & VLMP_F_FULL_EVERY_LENGTH);
-        ParamArgs pa{s->d_tn, s->d_cum, s->d_cum2, prm_buf[li & 1], mu_buf[li & 1], n, N, A, m, s->floor_};
-        cudaStream_t sx = li == 0 ? st : side;
-        k_params<<<blocks(A, 256), 256, 0, sx>>>(pa);
-        ++klaunch;
-        if (!full) {
-            // winners of length li-2 (li-1 for li == 1, whose only predecessor is the first length)
-            const int src_li = li >= 2 ? li - 2 : 0;
-            const long long Nprev = n - (lmin + src_li) + 1;
-            k_acc_idx<<<blocks(Nprev, 256), 256, 0, sx>>>(s->d_acc + (long long)src_li * A, s->d_previdx, Nprev);
-            BoundArgs ba{s->d_tn, mu_buf[li & 1], prm_buf[li & 1], s->d_previdx, N, Nprev, m, e, margin};
-            k_bound<<<blocks(N * 32, 256), 256, 0, sx>>>(ba);
-            klaunch += 2;
-        }
-        return 0;
-    };
-    prepare(0);
     for (int li = 0; li < n_len; ++li) {
         const int m = lmin + li;
         const long long N = n - m + 1;
         const int e = (m + 1) / 2;
+        ParamArgs pa{s->d_tn, s->d_cum, s->d_cum2, s->d_prm, s->d_mu, n, N, A, m, s->floor_};
+        k_params<<<blocks(A, 256), 256, 0, st>>>(pa);
+        ++klaunch;
         const bool full = (li == 0) || (flags & VLMP_F_FULL_EVERY_LENGTH);
         if (li == 0 && T) {
-            SeedArgs sa{s->d_tn, mu_buf[0], s->d_tiles, s->d_seeds, dl, (int)T, S, m};
+            SeedArgs sa{s->d_tn, s->d_mu, s->d_tiles, s->d_seeds, dl, (int)T, S, m};
             k_seed_init<<<blocks(T * 32, WARPS_PER_CTA * 32), WARPS_PER_CTA * 32, 0, st>>>(sa);
             ++klaunch;
         }
-        if (li > 0) CU(cudaStreamWaitEvent(st, ev_ready, 0));      // length li prepared
+        if (!full) {
+            k_acc_idx<<<blocks(N + 1, 256), 256, 0, st>>>(s->d_acc + (long long)(li - 1) * A, s->d_previdx, N + 1);
+            BoundArgs ba{s->d_tn, s->d_mu, s->d_prm, s->d_previdx, N, N + 1, m, e, margin};
+            k_bound<<<blocks(N * 32, 256), 256, 0, st>>>(ba);
+            klaunch += 2;
+        }
         while (s->lev.size() < (size_t)2 * (li + 1)) {
             cudaEvent_t ev; CU(cudaEventCreate(&ev)); s->lev.push_back(ev);
         }
         CU(cudaEventRecord(s->lev[2 * li], st));
         if (T) {
-            TileArgs ta{prm_buf[li & 1], mu_buf[li & 1], s->d_tn, s->d_tiles, s->d_seeds, s->d_acc + (long long)li * A,
+            TileArgs ta{s->d_prm, s->d_mu, s->d_tn, s->d_tiles, s->d_seeds, s->d_acc + (long long)li * A,
                         s->d_counters, s->d_log, s->d_logcnt + li, (long long)s->log_cap,
                         N, dl, (int)T, S, m, e, li + 1 < n_len};
             if (full) k_tile<true><<<blocks(T, WARPS_PER_CTA), WARPS_PER_CTA * 32, smem, st>>>(ta);
             else {
                 k_tile<false><<<blocks(T, WARPS_PER_CTA), WARPS_PER_CTA * 32, smem, st>>>(ta);
                 k_log_merge<<<296, 128, 0, st>>>(s->d_log, s->d_logcnt + li, (long long)s->log_cap,
-                                                 prm_buf[li & 1], e, s->d_acc + (long long)li * A, s->d_counters);
+                                                 s->d_prm, e, s->d_acc + (long long)li * A, s->d_counters);
                 klaunch += 1;
             }
             launches += 1; klaunch += 1;
         }
         CU(cudaEventRecord(s->lev[2 * li + 1], st));
-        CU(cudaEventRecord(ev_done, st));
         CU(cudaGetLastError());
-        if (li + 1 < n_len) {
-            // the side stream may overwrite buffer (li+1)&1 only after tile(li-1) finished with
-            // it, and needs the winners of length li-1 (li == 0: of length 0 -> wait for it)
-            if (li == 0) CU(cudaStreamWaitEvent(side, ev_done, 0));
-            else CU(cudaStreamWaitEvent(side, ev_done_prev, 0));
-            prepare(li + 1);
-            CU(cudaEventRecord(ev_ready, side));
-        }
-        std::swap(ev_done_prev, ev_done);
         for (long long b = band_lo; b < band_hi; ++b) {
             long long d0 = dl + b * BAND;
             long long rows = N - d0;
