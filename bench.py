@@ -268,7 +268,11 @@ def run_ours(args):
                      "frac": achieved / peak, "traffic": prof_traffic,
                      "peak_source": "measured DFMA microbenchmark (vlmp_measure_fp64_peak); "
                                     "MEASURED_PEAKS.json has no FP64 figure",
-                     "kernel": "k_tile", "avg_tile_ms_per_step": avg_tile_s * 1e3},
+                     "kernel": "k_tile", "avg_tile_ms_per_step": avg_tile_s * 1e3,
+                     "flops_per_update": "8 = the exhaustive cell's 4 FP64 FMA-pipe instr (2 recurrence "
+                                         "DFMA + DMUL + DFMA key); the filter kernel executes the 2 "
+                                         "recurrence DFMA and tests in FP32/INT",
+                     "executed_fp64_frac": achieved / peak / 2},
         "cpu_baseline": cpu,
         "e2e": e2e_line,
         "gpu_launches": launches,

@@ -52,7 +52,7 @@ constexpr int PBITS = (D == 4) ? 7 : (D == 8) ? 8 : 9;   // log2(BAND): packed l
 constexpr unsigned long long PMASK = (1ull << PBITS) - 1;
 constexpr int WARPS_PER_CTA = 4;
 #ifndef VLMP_FILTER_MIN_BLOCKS
-#define VLMP_FILTER_MIN_BLOCKS 4
+#define VLMP_FILTER_MIN_BLOCKS 5
 #endif
 constexpr unsigned FULLMASK = 0xffffffffu;
 constexpr unsigned long long KEY_NONE = 0x7FF0000000000000ull;   // bits of +inf
@@ -220,6 +220,58 @@ __global__ void k_bound(BoundArgs a) {
 }
 
 // ---------------------------------------------------------------------------------
+// Filter thresholds in the covariance domain. A cell (i, j) must reach the exact tests when
+// its key r = 1 - cov inv_i inv_j satisfies hi(r) <= max(U_i, U_j), i.e. r <= R(U) with
+// R(U) the largest double of that high word. With q(U) = 1 - R(U) - 2^-20 and s = 1/inv:
+//   r <= R(U)  =>  cov >= q(U) s_i s_j            (2^-20 >> the FP64 rounding of r)
+// so the tile kernel tests  hi(cov) >= hi(t),  t = a_j * b_i  (FP32, rounded down), with
+// b = s 2^-k (per-session power-of-two scale) and a_j = q(max(U_j, Uwin_i)) b_j -- no
+// per-cell FP64 work beyond the recurrence. q < 2^-20 (a bound at corr ~ 0) is clamped to
+// 0, which still passes every cell of positive covariance; only offsets whose OWN bound is
+// that weak may need non-positive-covariance cells: they are "forced" (1-best: the length
+// falls back to the exact full-fold kernel; m-best: the offset is recomputed exactly).
+constexpr double QSLACK = 1.0 / (1 << 20);
+
+__device__ inline double qfac(float u) {
+    const double R = __hiloint2double(__float_as_int(u), (int)0xFFFFFFFF);
+    const double q = 1.0 - R - QSLACK;
+    return q >= QSLACK ? q : 0.0;      // also 0 for u = +inf / NaN
+}
+
+__device__ inline float qscale(double inv, double sscale) {
+    return __double2float_rd((1.0 / inv) * sscale);   // NaN for an invalid window
+}
+
+// the offset's own bound is too weak for the covariance-domain filter (see above)
+__device__ inline bool q_forced(const Prm& p, double sscale) {
+    if (!(p.inv == p.inv)) return false;
+    const float b = qscale(p.inv, sscale);
+    return qfac(p.U) == 0.0 || !(b >= 0x1p-40f && b <= 0x1p40f);
+}
+
+// colq[o] = (a_o = q(U_o) b_o, b_o) for columns; rowq[o] = (b_o, q(Uwin_o)) for rows, where
+// Uwin_o = max U[o .. o+D-1]: a column entering a lane at row o meets rows o .. o+D-1 there
+__global__ void k_qprep(const Prm* __restrict__ prm, float2* colq, float2* rowq, long long N, long long A,
+                        double sscale, int* forced) {
+    const long long o = blockIdx.x * (long long)blockDim.x + threadIdx.x;
+    if (o >= A) return;
+    const float qnan = __int_as_float(0x7FC00000);
+    if (o >= N) { colq[o] = make_float2(qnan, qnan); rowq[o] = make_float2(qnan, qnan); return; }
+    const Prm p = prm[o];
+    float uw = -INFINITY;
+#pragma unroll
+    for (int k = 0; k < D; ++k)
+        if (o + k < N) uw = fmaxf(uw, prm[o + k].U);
+    const float b = qscale(p.inv, sscale);
+    const double qu = qfac(p.U);
+    const float a = __double2float_rd(qu * (double)b);
+    const float w = uw == -INFINITY ? 3.0e38f : __double2float_rd(qfac(uw));
+    colq[o] = make_float2(a, b);
+    rowq[o] = make_float2(b, w);
+    if (forced && q_forced(p, sscale)) atomicOr(forced, 1);
+}
+
+// ---------------------------------------------------------------------------------
 struct Cand { int o; int idx; unsigned long long key; };   // candidate (offset, neighbour, key)
 
 // A filter-kernel log record: a lane whose cells passed the bound at row i; its 8 cells are
@@ -238,6 +290,10 @@ struct TileArgs {
     long long log_cap;
     long long N, dlo;
     int n_tiles, S, m, e, update_seeds;
+    const float2* colq;            // filter: column factors (a_j, b_j), natural offsets
+    const float2* rowq;            // filter: row factors (b_i, q(Uwin_i))
+    const int* forced;             // filter: nonzero => this length runs the full-fold body
+    int hiC;                       // hi word of 2^(2k) * 2^-127 scaled float -> double bias
 };
 
 __device__ inline bool key_less(unsigned long long k1, long long i1, unsigned long long k2, long long i2) {
@@ -275,9 +331,12 @@ __device__ inline void cp_async_commit() { asm volatile("cp.async.commit_group;\
 __device__ inline void cp_async_wait_all() { asm volatile("cp.async.wait_group 0;\n" ::: "memory"); }
 
 
+constexpr int UCS = 34;      // padded row of float2: conflict-free staging writes and reads
 struct WarpSmem {
     Prm fresh[2][D];         // the column entering lane 31's slot D-1 at each row of a group
     Prm row[2][D];           // the group's row parameters
+    float2 rq[2][D];         // filter: the group's row factors
+    float2 cq[2][D][UCS];    // filter: factors of the column entering lane L's ring at row kk
 };
 
 // stage group g (rows r0 .. r0+7) into buffer b: 8 row structs + 8 fresh columns for lane 31
@@ -292,6 +351,25 @@ __device__ inline void stage_group(WarpSmem& w, int b, const Prm* __restrict__ p
         cp_async16(reinterpret_cast<char*>(dst) + 16 * half, reinterpret_cast<const char*>(src) + 16 * half);
     }
     cp_async_commit();
+}
+
+__device__ inline void cp_async8(void* smem_dst, const void* gmem_src) {
+    unsigned d = (unsigned)__cvta_generic_to_shared(smem_dst);
+    asm volatile("cp.async.ca.shared.global [%0], [%1], 8;\n" :: "r"(d), "l"(gmem_src) : "memory");
+}
+
+// filter: row factors of rows r0 .. r0+7 (64 aligned bytes) and the factors of the columns
+// entering the ring during the group -- lane L at row r0+kk receives column
+// r0 + d0 + D-1 + (D*L + kk); coalesced reads, f = D*L + kk lands at cq[kk][L]
+__device__ inline void stage_q(WarpSmem& w, int b, const float2* __restrict__ colq,
+                               const float2* __restrict__ rowq, long long r0, long long d0, int lane) {
+    if (lane < 4) cp_async16(&w.rq[b][2 * lane], rowq + r0 + 2 * lane);
+    const float2* src = colq + r0 + d0 + D - 1;
+#pragma unroll
+    for (int k = 0; k < D; ++k) {
+        const int f = lane + 32 * k;
+        cp_async8(&w.cq[b][f & (D - 1)][f >> 3], src + f);
+    }
 }
 
 // append one record per flagged lane (one warp-aggregated atomic); rare
@@ -339,12 +417,19 @@ __device__ __forceinline__ void tile_body(const TileArgs& a, WarpSmem& w, int wi
     // The ring starts in its state "after row i0-1": phys p < D-1 holds the column of slot p
     // at row i0, phys D-1 holds the column leaving slot 0 at row i0-1 (cbase - 1), which the
     // first rotation hands to the left neighbour -- so every row, the first included, rotates.
+    // Filter: cA[p] = q(max(U_col, Uwin[row the column entered this lane])) b_col, a lower
+    // bound of q(max(U_i, U_col)) b_col for every row i the column meets in this lane.
     double cdf[D], cdg[D], cinv[D];
-    float cU[D];
+    float cA[D];
+    {
+        const float w0 = FULL ? 0.f : a.rowq[i0].y;
 #pragma unroll
-    for (int s = 0; s < D; ++s) {
-        const Prm pc = a.prm[s < D - 1 ? cbase + s : cbase - 1];
-        cdf[s] = pc.df; cdg[s] = pc.dg; cinv[s] = pc.inv; cU[s] = pc.U;
+        for (int s = 0; s < D; ++s) {
+            const long long c = s < D - 1 ? cbase + s : cbase - 1;
+            const Prm pc = a.prm[c];
+            cdf[s] = pc.df; cdg[s] = pc.dg; if (FULL) cinv[s] = pc.inv;
+            if (!FULL) { const float2 q = a.colq[c]; cA[s] = fminf(q.x, __fmul_rd(w0, q.y)); }
+        }
     }
     {   // pre-adjust so that the uniform recurrence at row i0 reproduces the seed
         const Prm pr = a.prm[i0];
@@ -383,13 +468,17 @@ __device__ __forceinline__ void tile_body(const TileArgs& a, WarpSmem& w, int wi
         rowres = INFINITY; colres = INFINITY;
     };
 
+    if (!FULL) stage_q(w, 0, a.colq, a.rowq, i0, d0, lane);
     stage_group(w, 0, a.prm, i0, d0, lane);
     cp_async_wait_all();
     __syncwarp();
 
     for (int g = 0; g < ngroups; ++g) {
         const int b = g & 1;
-        if (g + 1 < ngroups) stage_group(w, b ^ 1, a.prm, i0 + (long long)(g + 1) * D, d0, lane);
+        if (g + 1 < ngroups) {
+            if (!FULL) stage_q(w, b ^ 1, a.colq, a.rowq, i0 + (long long)(g + 1) * D, d0, lane);
+            stage_group(w, b ^ 1, a.prm, i0 + (long long)(g + 1) * D, d0, lane);
+        }
 #pragma unroll
         for (int kk = 0; kk < D; ++kk) {
             const long long i = i0 + (long long)g * D + kk;
@@ -401,15 +490,18 @@ __device__ __forceinline__ void tile_body(const TileArgs& a, WarpSmem& w, int wi
                 // (rows after a group's first: lane 0 loaded it at the end of the previous row)
                 if (lane == 0 && kk == 0) {
                     const Prm f = w.fresh[b][kk];
-                    cdf[q] = f.df; cdg[q] = f.dg; cinv[q] = f.inv; cU[q] = f.U;
+                    cdf[q] = f.df; cdg[q] = f.dg; if (FULL) cinv[q] = f.inv;
                 }
 #ifndef VLMP_EXP_NOSHFL
                 const int src_lane = (lane + 1) & 31;
                 cdf[q] = __shfl_sync(FULLMASK, cdf[q], src_lane);
                 cdg[q] = __shfl_sync(FULLMASK, cdg[q], src_lane);
-                cinv[q] = __shfl_sync(FULLMASK, cinv[q], src_lane);
-                cU[q] = __shfl_sync(FULLMASK, cU[q], src_lane);
+                if (FULL) cinv[q] = __shfl_sync(FULLMASK, cinv[q], src_lane);
 #endif
+                if (!FULL) {
+                    const float2 cq = w.cq[b][kk][lane];
+                    cA[q] = fminf(cq.x, __fmul_rd(w.rq[b][kk].y, cq.y));
+                }
             }
             if (!FULL) {
                 // Deferred vote: row i-1's predicate is long resolved. cov[] still holds row
@@ -427,12 +519,14 @@ __device__ __forceinline__ void tile_body(const TileArgs& a, WarpSmem& w, int wi
             }
             if (!FULL) {
                 bool pa = false, pb = false;   // two independent predicate chains
+                const float bi = w.rq[b][kk].x;
 #pragma unroll
                 for (int s = 0; s < D; ++s) {
                     const int p = (s + kk) & (D - 1);
-                    const double r = fma(-(cov[s] * pr.inv), cinv[p], 1.0);
-                    const float h = __int_as_float(__double2hiint(r));
-                    const bool hit = sval[s] && (h <= fmaxf(pr.U, cU[p]));
+                    // hi(cov) >= hi((double)t): t's exponent rebiased, mantissa truncated (<= t)
+                    const float t = __fmul_rd(cA[p], bi);
+                    const int ht = (int)(__float_as_uint(t) >> 3) + a.hiC;
+                    const bool hit = sval[s] && (__double2hiint(cov[s]) >= ht);
                     if (s & 1) pb |= hit; else pa |= hit;
                 }
                 pass_prev = pa | pb;
@@ -468,7 +562,7 @@ __device__ __forceinline__ void tile_body(const TileArgs& a, WarpSmem& w, int wi
                 // slot 0's column (phys kk) is dead after this row: lane 0 fetches the next row's
                 // fresh column into it now, so the next rotation's shuffles need not wait
                 const Prm f = w.fresh[b][kk + 1];
-                cdf[kk] = f.df; cdg[kk] = f.dg; cinv[kk] = f.inv; cU[kk] = f.U;
+                cdf[kk] = f.df; cdg[kk] = f.dg; if (FULL) cinv[kk] = f.inv;
             }
         }
         if (FULL && (g & 3) == 3) flush_full();
@@ -501,7 +595,7 @@ __device__ __forceinline__ void tile_body(const TileArgs& a, WarpSmem& w, int wi
 }
 
 template <bool FULL>
-__global__ void __launch_bounds__(WARPS_PER_CTA * 32, VLMP_FILTER_MIN_BLOCKS)
+__global__ void __launch_bounds__(WARPS_PER_CTA * 32, FULL ? 4 : VLMP_FILTER_MIN_BLOCKS)
 k_tile(TileArgs a) {
     extern __shared__ __align__(128) unsigned char smem_raw[];
     WarpSmem* ws = reinterpret_cast<WarpSmem*>(smem_raw);
@@ -517,7 +611,11 @@ k_tile(TileArgs a) {
 #ifdef VLMP_EXP_SKIPBAND0
     if (!FULL && tl.x == 0) return;
 #endif
+#ifdef VLMP_EXP_NOFALLBACK
     if (FULL) {
+#else
+    if (FULL || (a.forced && *a.forced)) {
+#endif
         if (d0 < a.e) tile_body<true, true>(a, ws[wl], wid, lane, d0, i0, rows_valid);
         else tile_body<true, false>(a, ws[wl], wid, lane, d0, i0, rows_valid);
     } else {
@@ -924,14 +1022,14 @@ __global__ void k_log_slots(const RowRec* log, const unsigned long long* log_cou
 // per offset: the m smallest (key, index) of its slots -> out[o][0..mb) (-1 = none);
 // overflowing offsets are queued for an exact recompute; slot counters are reset
 __global__ void k_select_m(ulonglong2* slots, int* slot_cnt, long long N, int mb, int* out,
-                           long long* redo, unsigned long long* redo_cnt) {
+                           long long* redo, unsigned long long* redo_cnt, const Prm* prm, double sscale) {
     const long long o = blockIdx.x * (long long)blockDim.x + threadIdx.x;
     if (o >= N) return;
     const int c = slot_cnt[o];
     slot_cnt[o] = 0;
     unsigned long long bk[MB_MAX]; long long bi[MB_MAX];
     for (int q = 0; q < MB_MAX; ++q) { bk[q] = KEY_NONE; bi[q] = IDX_NONE; }
-    if (c > SLOT_CAP) {
+    if (c > SLOT_CAP || q_forced(prm[o], sscale)) {
         const unsigned long long at = atomicAdd(redo_cnt, 1ull);
         redo[at] = o;
     } else {
@@ -1089,6 +1187,9 @@ struct vlmp_session {
     // per-length scratch
     Prm* d_prm = nullptr; double* d_mu = nullptr;
     long long* d_previdx = nullptr;
+    float2* d_colq = nullptr; float2* d_rowq = nullptr;   // filter factors (k_qprep)
+    int* d_forced = nullptr; size_t forced_cap = 0;      // per-length: full-fold fallback
+    double sscale = 1.0; int hiC = 896 << 20;            // filter: 2^-k scale, hi-word bias
     // tiles / seeds
     int2* d_tiles = nullptr; size_t tiles_cap = 0;
     double* d_seeds = nullptr; size_t seeds_cap = 0;
@@ -1202,7 +1303,7 @@ void vlmp_destroy(vlmp_session* s) {
     cudaSetDevice(s->device);
     cudaStreamSynchronize(s->stream);
     void* ptrs[] = {s->d_tn, s->d_cum, s->d_cum2, s->d_prm, s->d_mu,
-                    s->d_previdx, s->d_tiles, s->d_seeds, s->d_acc, s->d_mp, s->d_ip, s->d_counters,
+                    s->d_previdx, s->d_colq, s->d_rowq, s->d_forced, s->d_tiles, s->d_seeds, s->d_acc, s->d_mp, s->d_ip, s->d_counters,
                     s->d_log, s->d_logcnt, s->d_ro_i64, s->d_ro_f64, s->d_ro_cnt,
                     s->d_slots, s->d_slotcnt, s->d_ipm, s->d_mpm, s->d_redo, s->d_vdist, s->d_vnorm, s->d_vlen, s->d_vidx, s->d_vpop};
     for (void* p : ptrs) if (p) cudaFree(p);
@@ -1230,6 +1331,17 @@ int vlmp_set_series(vlmp_session* s, const double* t, const double* cum, const d
     if ((rc = ensure1(s->d_prm, A))) return rc;
     if ((rc = ensure1(s->d_mu, A))) return rc;
     if ((rc = ensure1(s->d_previdx, A))) return rc;
+    if ((rc = ensure1(s->d_colq, A))) return rc;
+    if ((rc = ensure1(s->d_rowq, A))) return rc;
+    {   // filter scale: b = sigma sqrt(m) 2^-k stays O(1) whatever the series' units
+        double ss = 0.0;
+        for (long long i = 0; i < n; ++i) ss += t[i] * t[i];
+        const double rms = std::sqrt(ss / (double)n);
+        int k = (rms > 0.0 && std::isfinite(rms)) ? std::ilogb(rms) + 4 : 0;
+        k = std::max(-400, std::min(400, k));
+        s->sscale = std::ldexp(1.0, -k);
+        s->hiC = (896 + 2 * k) << 20;
+    }
     CU(cudaMemsetAsync(s->d_tn, 0, (2 * A + 4096) * sizeof(double), s->stream));
     CU(cudaMemcpyAsync(s->d_tn, t, n * sizeof(double), cudaMemcpyHostToDevice, s->stream));
     CU(cudaMemcpyAsync(s->d_cum, cum, (n + 1) * sizeof(double), cudaMemcpyHostToDevice, s->stream));
@@ -1291,7 +1403,9 @@ static int profile_impl(vlmp_session* s, int32_t lmin, int32_t lmax, int64_t ban
     const size_t log_cap = std::max<size_t>((size_t)1 << 18, (size_t)(2 * N0));
     if ((rc = ensure(s->d_log, s->log_cap, log_cap))) return rc;
     if ((rc = ensure(s->d_logcnt, s->logcnt_cap, (size_t)n_len))) return rc;
+    if ((rc = ensure(s->d_forced, s->forced_cap, (size_t)n_len))) return rc;
     CU(cudaMemsetAsync(s->d_logcnt, 0, n_len * sizeof(unsigned long long), st));
+    CU(cudaMemsetAsync(s->d_forced, 0, n_len * sizeof(int), st));
     if (T) CU(cudaMemcpyAsync(s->d_tiles, tiles.data(), T * sizeof(int2), cudaMemcpyHostToDevice, st));
     const size_t smem = WARPS_PER_CTA * sizeof(WarpSmem);
     CU(cudaFuncSetAttribute(k_tile<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
@@ -1319,7 +1433,9 @@ static int profile_impl(vlmp_session* s, int32_t lmin, int32_t lmax, int64_t ban
             k_acc_idx<<<blocks(N + 1, 256), 256, 0, st>>>(s->d_acc + (long long)(li - 1) * A, s->d_previdx, N + 1);
             BoundArgs ba{s->d_tn, s->d_mu, s->d_prm, s->d_previdx, N, N + 1, m, e, margin};
             k_bound<<<blocks(N * 32, 256), 256, 0, st>>>(ba);
-            klaunch += 2;
+            k_qprep<<<blocks(A, 256), 256, 0, st>>>(s->d_prm, s->d_colq, s->d_rowq, N, A, s->sscale,
+                                                    s->d_forced + li);
+            klaunch += 3;
         }
         while (s->lev.size() < (size_t)2 * (li + 1)) {
             cudaEvent_t ev; CU(cudaEventCreate(&ev)); s->lev.push_back(ev);
@@ -1328,7 +1444,8 @@ static int profile_impl(vlmp_session* s, int32_t lmin, int32_t lmax, int64_t ban
         if (T) {
             TileArgs ta{s->d_prm, s->d_mu, s->d_tn, s->d_tiles, s->d_seeds, s->d_acc + (long long)li * A,
                         s->d_counters, s->d_log, s->d_logcnt + li, (long long)s->log_cap,
-                        N, dl, (int)T, S, m, e, li + 1 < n_len};
+                        N, dl, (int)T, S, m, e, li + 1 < n_len,
+                        s->d_colq, s->d_rowq, s->d_forced + li, s->hiC};
             if (full) k_tile<true><<<blocks(T, WARPS_PER_CTA), WARPS_PER_CTA * 32, smem, st>>>(ta);
             else {
                 k_tile<false><<<blocks(T, WARPS_PER_CTA), WARPS_PER_CTA * 32, smem, st>>>(ta);
@@ -1365,6 +1482,12 @@ static int profile_impl(vlmp_session* s, int32_t lmin, int32_t lmax, int64_t ban
         CU(cudaMemcpy(lc.data(), s->d_logcnt, n_len * sizeof(unsigned long long), cudaMemcpyDeviceToHost));
         for (auto c : lc) overflow |= c > s->log_cap;
     }
+    int n_forced = 0;
+    {
+        std::vector<int> fl(n_len);
+        CU(cudaMemcpy(fl.data(), s->d_forced, n_len * sizeof(int), cudaMemcpyDeviceToHost));
+        for (int f : fl) n_forced += f != 0;
+    }
     double W = 0;
     for (int m = lmin; m <= lmax; ++m) {
         long long k = (n - m + 1) - (m + 1) / 2;
@@ -1376,7 +1499,7 @@ static int profile_impl(vlmp_session* s, int32_t lmin, int32_t lmax, int64_t ban
     s->stats[0] = ms; s->stats[2] = executed; s->stats[3] = W; s->stats[4] = tile_ms;
     s->stats[5] = launches; s->stats[6] = n_filtered; s->stats[7] = n_full; s->stats[8] = (double)cnt[0];
     s->stats[9] = klaunch; s->stats[10] = first_ms; s->stats[11] = (double)cnt[2];
-    s->stats[12] = (double)cnt[1];
+    s->stats[12] = (double)cnt[1]; s->stats[14] = n_forced;
     *overflow_out = overflow;
     return 0;
 }
@@ -1642,7 +1765,7 @@ int vlmp_profile_mbest(vlmp_session* s, int32_t lmin, int32_t lmax, int32_t mb) 
         k_params<<<blocks(A, 256), 256, 0, st>>>(pa);
         TileArgs ta{s->d_prm, s->d_mu, s->d_tn, s->d_tiles, s->d_seeds, s->d_acc,
                     s->d_counters, s->d_log, s->d_logcnt + li, (long long)s->log_cap,
-                    N, dl, (int)T, S, m, e, 0};
+                    N, dl, (int)T, S, m, e, 0, s->d_colq, s->d_rowq, nullptr, s->hiC};
         BoundMArgs bm{s->d_tn, s->d_mu, s->d_prm, nullptr, nullptr, N, N + 1, A, m, e, mb, margin};
         if (li == 0) {
             if (T) {
@@ -1658,6 +1781,8 @@ int vlmp_profile_mbest(vlmp_session* s, int32_t lmin, int32_t lmax, int32_t mb) 
             bm.prevm = s->d_ipm + (long long)(li - 1) * A * mb;
         }
         k_bound_m<<<blocks(N * 32, 256), 256, 0, st>>>(bm);
+        // no full-fold fallback here (it folds the 1-best only): forced offsets are recomputed
+        k_qprep<<<blocks(A, 256), 256, 0, st>>>(s->d_prm, s->d_colq, s->d_rowq, N, A, s->sscale, nullptr);
         if (T) {
             ta.update_seeds = li + 1 < n_len;
             k_tile<false><<<blocks(T, WARPS_PER_CTA), WARPS_PER_CTA * 32, smem, st>>>(ta);
@@ -1666,7 +1791,8 @@ int vlmp_profile_mbest(vlmp_session* s, int32_t lmin, int32_t lmax, int32_t mb) 
         }
         CU(cudaMemsetAsync(s->d_ro_cnt, 0, 8, st));
         int* out = s->d_ipm + (long long)li * A * mb;
-        k_select_m<<<blocks(N, 256), 256, 0, st>>>(s->d_slots, s->d_slotcnt, N, mb, out, s->d_redo, s->d_ro_cnt);
+        k_select_m<<<blocks(N, 256), 256, 0, st>>>(s->d_slots, s->d_slotcnt, N, mb, out, s->d_redo, s->d_ro_cnt,
+                                                  s->d_prm, s->sscale);
         k_recompute_m<<<148, 256, 0, st>>>(s->d_tn, s->d_mu, s->d_prm, s->d_redo, s->d_ro_cnt, N, m, e, mb, out);
         unsigned long long nred = 0;
         CU(cudaMemcpyAsync(&nred, s->d_ro_cnt, 8, cudaMemcpyDeviceToHost, st));

@@ -289,3 +289,24 @@ def test_m_th_discords_config1(oracle_mod):
     for L in range(32, 41):
         assert np.array_equal(scan.per_length[L].offset, per[L][1]), L
     assert np.array_equal(scan.merged.offset, mo)
+
+
+def test_weak_bounds_fall_back_exactly(oracle_mod):
+    """Short white noise: some offsets' best correlation is ~0 or negative, so their bound is
+    too weak for the covariance-domain filter: those lengths run the
+    exact full-fold body (1-best) and those offsets are recomputed exactly (m-best)."""
+    s = vl.ingest(np.random.default_rng(5).standard_normal(61))
+    lmin, lmax = 30, 40
+    run = api.GpuRun(s, lmin, lmax)
+    assert run.stats["fallback_lengths"] > 0
+    ref = oracle_mod.run(s, lmin, lmax, k_discord=1, keep_profiles=True)
+    for L in range(lmin, lmax + 1):
+        mp, ip = run.profile(L)
+        omp, oip = ref["profiles"][L]
+        assert np.array_equal(ip, oip), L
+        fin = np.isfinite(omp)
+        assert np.allclose(mp[fin], omp[fin], rtol=1e-6, atol=1e-7)
+    for L in (24, 30):
+        res = vl.compute_matrix_profile(s, L, 5, m_track=3)
+        _, _, bm, bmi = oracle_mod.profile_m(s, L, 3)
+        assert np.array_equal(np.sort(res.best_m_nbr, axis=1), np.sort(bmi, axis=1)), L
