@@ -133,7 +133,7 @@ int vlmp_discords_m(vlmp_session* s, int32_t k, double* out_dist, int64_t* out_o
  * out[3] W (non-trivial pair updates), out[4] tile-kernel ms, out[5] tile-kernel
  * launches, out[6] filtered lengths, out[7] full lengths, out[8] slow-path
  * candidate merges, out[9] total kernel launches, out[10] first-length tile ms,
- * out[11] flagged filter row steps, out[12] unused, out[13] exact redo count (1-best:
+ * out[11] flagged filter lane-rows (log records), out[12] offsets whose bound needed a direct dot product, out[13] exact redo count (1-best:
  * 1 = the run was redone with full folds after a log overflow; m-best: offsets
  * recomputed), out[14] lengths that fell back to full folds (an offset's own bound
  * too weak for the covariance-domain filter).

@@ -153,69 +153,95 @@ __global__ void k_params(ParamArgs a) {
 }
 
 // ---------------------------------------------------------------------------------
-// bound U[o] >= the kernel's key of o's best cell, from the previous length's winners
-struct BoundArgs {
-    const double* tn; const double* mu; Prm* prm;
-    const long long* prev_idx;
+// O(1)-per-offset bound from the previous length's winners (1-best mode). Candidates:
+// o's own winner c1 and its neighbours' winners shifted along their diagonals,
+// (o, nn(o-1)+1) and (o, nn(o+1)-1). Their covariance at length m-1 comes from the stored
+// key, cov = (1 - r) / (inv_o inv_c) (r kept to 2^-44), plus / minus one step of the
+// diagonal recurrence; the Welford co-moment step carries it to length m. Any valid cell's
+// key bounds the minimum; the reconstruction error (~1e-13) is far below the margin.
+struct Bound2Args {
+    const double* tn; const Prm* prm; const Prm* pprev; const double* mu_prev;
+    const ulonglong2* acc_prev; Prm* out;
     long long N, Nprev; int m, e; double margin;
+    long long* fix; unsigned long long* fix_cnt;   // offsets left without a bound
 };
 
-
-// one warp per offset: the (up to 4) candidate dot products are split across the lanes
-__global__ void k_bound(BoundArgs a) {
-    const int lane = threadIdx.x & 31;
-    const long long o = (blockIdx.x * (long long)blockDim.x + threadIdx.x) >> 5;
+__global__ void k_bound2(Bound2Args a) {
+    const long long o = blockIdx.x * (long long)blockDim.x + threadIdx.x;
     if (o >= a.N) return;
     const double io = a.prm[o].inv;
-    if (!(io == io)) {   // invalid row: never a candidate
-        if (lane == 0) a.prm[o].U = -INFINITY;
-        return;
-    }
-    long long cand[4];
-    int nc = 0;
-    const long long c1 = (o < a.Nprev) ? a.prev_idx[o] : -1;
-    if (c1 >= 0) { cand[nc++] = c1; cand[nc++] = c1 > o ? c1 + 1 : c1 - 1; }
-    if (o >= 1 && o - 1 < a.Nprev) { const long long c = a.prev_idx[o - 1]; if (c >= 0) cand[nc++] = c + 1; }
-    if (o + 1 < a.Nprev) { const long long c = a.prev_idx[o + 1]; if (c >= 0) cand[nc++] = c - 1; }
-    bool ok[4]; double mc[4], ic[4]; long long cc[4];
-#pragma unroll
-    for (int q = 0; q < 4; ++q) {
-        ok[q] = false; mc[q] = 0.0; ic[q] = 0.0; cc[q] = o;
-        if (q < nc) {
-            const long long c = cand[q];
-            bool dup = false;
-            for (int r = 0; r < q; ++r) dup |= (cand[r] == c);
-            const long long dd = c > o ? c - o : o - c;
-            if (!dup && c >= 0 && c < a.N && dd >= a.e) {
-                ic[q] = a.prm[c].inv;
-                ok[q] = ic[q] == ic[q];
-                mc[q] = a.mu[c];
-                cc[q] = c;
-            }
-        }
-    }
-    const double mo = a.mu[o];
-    double acc[4] = {0.0, 0.0, 0.0, 0.0};
-    for (int k = lane; k < a.m; k += 32) {
-        const double x = a.tn[o + k] - mo;
-#pragma unroll
-        for (int q = 0; q < 4; ++q) acc[q] = fma(x, a.tn[cc[q] + k] - mc[q], acc[q]);
-    }
+    if (!(io == io)) { a.out[o].U = -INFINITY; return; }
+    const int m = a.m;
+    const double wgt = (double)(m - 1) / (double)m;
+    const double xo = a.tn[o + m - 1] - a.mu_prev[o];
     double best = INFINITY;
-#pragma unroll
-    for (int q = 0; q < 4; ++q) {
-        double v = acc[q];
-#pragma unroll
-        for (int off = 16; off >= 1; off >>= 1) v += __shfl_xor_sync(FULLMASK, v, off);
-        if (ok[q]) best = fmin(best, fma(-(v * io), ic[q], 1.0));
+    auto eval = [&](long long c, double covp) {
+        const long long dd = c > o ? c - o : o - c;
+        if (c < 0 || c >= a.N || dd < a.e) return;
+        const double ic = a.prm[c].inv;
+        if (!(ic == ic)) return;
+        const double covm = fma(wgt * xo, a.tn[c + m - 1] - a.mu_prev[c], covp);
+        best = fmin(best, fma(-(covm * io), ic, 1.0));
+    };
+    auto cov_of = [&](long long i, const ulonglong2& v) {   // winner's covariance at m-1
+        const double r = __longlong_as_double((long long)v.x);
+        return (1.0 - r) / (a.pprev[i].inv * a.pprev[(long long)v.y].inv);
+    };
+    if (o < a.Nprev) {
+        const ulonglong2 v = a.acc_prev[o];
+        if (v.x != KEY_NONE) eval((long long)v.y, cov_of(o, v));
     }
-    if (lane == 0) {
-        float out = INFINITY;   // no bound: every cell of this offset is a candidate
-        if (best < INFINITY) {
-            const double U = fmax(best, 0.0) + a.margin;
-            out = __int_as_float(__double2hiint(U));   // x <= U  =>  hi(x) <= hi(U)
+    if (o >= 1 && o - 1 < a.Nprev) {
+        const ulonglong2 v = a.acc_prev[o - 1];
+        if (v.x != KEY_NONE) {   // (o, c0+1) follows (o-1, c0) on its diagonal
+            const long long c = (long long)v.y + 1;
+            const Prm po = a.pprev[o], pc = a.pprev[c];
+            eval(c, cov_of(o - 1, v) + po.df * pc.dg + pc.df * po.dg);
         }
-        a.prm[o].U = out;
+    }
+    if (o + 1 < a.Nprev) {
+        const ulonglong2 v = a.acc_prev[o + 1];
+        if (v.x != KEY_NONE && v.y >= 1) {   // (o, c0-1) precedes (o+1, c0) on its diagonal
+            const long long c0 = (long long)v.y;
+            const Prm po = a.pprev[o + 1], pc = a.pprev[c0];
+            eval(c0 - 1, cov_of(o + 1, v) - po.df * pc.dg - pc.df * po.dg);
+        }
+    }
+    float out = INFINITY;   // no bound: every cell of this offset is a candidate
+    if (best < INFINITY) out = __int_as_float(__double2hiint(fmax(best, 0.0) + a.margin));
+    else if (o < a.Nprev && a.acc_prev[o].x != KEY_NONE) {
+        // the winner fell into the grown exclusion zone (|c1 - o| = e_{m-1} < e_m): queue the
+        // cell one step further out, (o, c1 +- 1), for a direct dot product (k_bound_fix)
+        const unsigned long long at = atomicAdd(a.fix_cnt, 1ull);
+        a.fix[at] = o;
+    }
+    a.out[o].U = out;
+}
+
+// direct centred dot product for the queued offsets (one warp each), cell (o, c1 +- 1)
+__global__ void k_bound_fix(const double* __restrict__ tn, const double* __restrict__ mu, Prm* prm,
+                            const ulonglong2* __restrict__ acc_prev, const long long* fix,
+                            const unsigned long long* fix_cnt, long long N, int m, int e, double margin) {
+    const int lane = threadIdx.x & 31;
+    const unsigned long long cnt = *fix_cnt;
+    for (unsigned long long w = (blockIdx.x * (unsigned long long)blockDim.x + threadIdx.x) >> 5; w < cnt;
+         w += ((unsigned long long)gridDim.x * blockDim.x) >> 5) {
+        const long long o = fix[w];
+        const long long c1 = (long long)acc_prev[o].y;
+        const long long c = c1 > o ? c1 + 1 : c1 - 1;
+        const long long dd = c > o ? c - o : o - c;
+        if (c < 0 || c >= N || dd < e) continue;
+        const double io = prm[o].inv, ic = prm[c].inv;
+        if (!(ic == ic)) continue;
+        const double mo = mu[o], mc = mu[c];
+        double acc = 0.0;
+        for (int k = lane; k < m; k += 32) acc = fma(tn[o + k] - mo, tn[c + k] - mc, acc);
+#pragma unroll
+        for (int off = 16; off >= 1; off >>= 1) acc += __shfl_xor_sync(FULLMASK, acc, off);
+        if (lane == 0) {
+            const double r = fma(-(acc * io), ic, 1.0);
+            prm[o].U = __int_as_float(__double2hiint(fmax(r, 0.0) + margin));
+        }
     }
 }
 
@@ -372,15 +398,11 @@ __device__ inline void stage_q(WarpSmem& w, int b, const float2* __restrict__ co
     }
 }
 
-// append one record per flagged lane (one warp-aggregated atomic); rare
-__device__ __forceinline__ void log_lanes(const TileArgs& a, bool flag, int lane, long long i, long long j0,
-                                          const double (&cov)[D]) {
-    const unsigned bal = __ballot_sync(FULLMASK, flag);
-    unsigned long long base = 0;
-    if (lane == 0) base = atomicAdd(a.log_count, (unsigned long long)__popc(bal));
-    base = __shfl_sync(FULLMASK, base, 0) + __popc(bal & ((1u << lane) - 1u));
-    if (flag && (long long)base < a.log_cap) {
-        RowRec* r = a.log + base;
+// one flagged lane's record (per-lane atomic; the caller diverges)
+__device__ __forceinline__ void log_one(const TileArgs& a, long long i, long long j0, const double (&cov)[D]) {
+    const unsigned long long at = atomicAdd(a.log_count, 1ull);
+    if ((long long)at < a.log_cap) {
+        RowRec* r = a.log + at;
         r->i = (int)i; r->j0 = (int)j0; r->pad0 = 0; r->pad1 = 0;
 #pragma unroll
         for (int s = 0; s < D; ++s) r->cov[s] = cov[s];
@@ -449,7 +471,7 @@ __device__ __forceinline__ void tile_body(const TileArgs& a, WarpSmem& w, int wi
     double rowres = INFINITY, colres = INFINITY;   // FULL: stashed per-row results
     long long rowres_i = 0, colres_j = 0;
     unsigned long long nslow = 0;
-    bool pass_prev = false;            // filter: row (i-1)'s pass predicate, voted on at row i
+    bool pass_prev = false;            // filter: row (i-1)'s pass predicate, acted on at row i
 
     const int S = a.S;
     const int nrows = (int)(rows_valid < S ? rows_valid : S);
@@ -504,10 +526,11 @@ __device__ __forceinline__ void tile_body(const TileArgs& a, WarpSmem& w, int wi
                 }
             }
             if (!FULL) {
-                // Deferred vote: row i-1's predicate is long resolved. cov[] still holds row
+                // Deferred test: row i-1's predicate is long resolved. cov[] still holds row
                 // i-1's covariances (row i's recurrence has not run), so flagged lanes log them.
-                if (__any_sync(FULLMASK, pass_prev)) {
-                    log_lanes(a, pass_prev, lane, i - 1, i - 1 + d0 + dbase, cov);
+                // divergent per-lane slow path: no warp vote on the fast path
+                if (pass_prev) {
+                    log_one(a, i - 1, i - 1 + d0 + dbase, cov);
                     ++nslow;
                 }
             }
@@ -585,12 +608,11 @@ __device__ __forceinline__ void tile_body(const TileArgs& a, WarpSmem& w, int wi
             }
         }
     } else {
-        if (__any_sync(FULLMASK, pass_prev)) {
-            log_lanes(a, pass_prev, lane, i0 + (long long)ngroups * D - 1,
-                      i0 + (long long)ngroups * D - 1 + d0 + dbase, cov);
+        if (pass_prev) {
+            log_one(a, i0 + (long long)ngroups * D - 1, i0 + (long long)ngroups * D - 1 + d0 + dbase, cov);
             ++nslow;
         }
-        if (lane == 0 && nslow) atomicAdd(a.counters + 2, nslow);
+        if (nslow) atomicAdd(a.counters + 2, nslow);
     }
 }
 
@@ -630,22 +652,36 @@ k_tile(TileArgs a) {
 __global__ void k_log_merge(const RowRec* log, const unsigned long long* log_count, long long cap,
                             const Prm* prm, int e, ulonglong2* acc, unsigned long long* counters) {
     const unsigned long long cnt = *log_count;
-    const long long n = (long long)(cnt < (unsigned long long)cap ? cnt : (unsigned long long)cap);
+    const long long nrec = (long long)(cnt < (unsigned long long)cap ? cnt : (unsigned long long)cap);
+    const int s = threadIdx.x & (D - 1);   // D consecutive lanes share one record, one cell each
     unsigned long long merged = 0;
-    for (long long q = blockIdx.x * (long long)blockDim.x + threadIdx.x; q < n;
-         q += (long long)gridDim.x * blockDim.x) {
-        const RowRec rec = log[q];
-        const Prm pr = prm[rec.i];
-        for (int s = 0; s < D; ++s) {
-            const long long j = (long long)rec.j0 + s;
-            if (j - rec.i < e) continue;
-            const Prm pc = prm[j];
-            const double r = fma(-(rec.cov[s] * pr.inv), pc.inv, 1.0);
-            const float h = __int_as_float(__double2hiint(r));
-            const unsigned long long key = clamp_key(r) & ~PMASK;
-            if (h <= pr.U) { acc_merge(acc + rec.i, key, j); ++merged; }
-            if (h <= pc.U) { acc_merge(acc + j, key, rec.i); ++merged; }
+    const long long stride = ((long long)gridDim.x * blockDim.x) / D;
+    const long long q_end = (nrec + stride - 1) / stride * stride;   // whole groups iterate together
+    for (long long q = (blockIdx.x * (long long)blockDim.x + threadIdx.x) / D; q < q_end; q += stride) {
+        unsigned long long rk = KEY_NONE; long long rj = IDX_NONE;
+        long long i = 0;
+        if (q < nrec) {
+            const RowRec* rec = log + q;
+            const int2 ij = *reinterpret_cast<const int2*>(rec);
+            i = ij.x;
+            const long long j = (long long)ij.y + s;
+            if (j - i >= e) {
+                const Prm pr = prm[i], pc = prm[j];
+                const double r = fma(-(rec->cov[s] * pr.inv), pc.inv, 1.0);
+                const float h = __int_as_float(__double2hiint(r));
+                const unsigned long long key = clamp_key(r) & ~PMASK;
+                if (h <= pr.U) { rk = key; rj = j; }
+                if (h <= pc.U) { acc_merge(acc + j, key, i); ++merged; }
+            }
         }
+        // the record's row-side candidates: one (key, index) minimum, one CAS
+#pragma unroll
+        for (int off = 1; off < D; off <<= 1) {
+            const unsigned long long ok = __shfl_xor_sync(FULLMASK, rk, off);
+            const long long oj = __shfl_xor_sync(FULLMASK, rj, off);
+            if (key_less(ok, oj, rk, rj)) { rk = ok; rj = oj; }
+        }
+        if (s == 0 && rj != IDX_NONE) { acc_merge(acc + i, rk, rj); ++merged; }
     }
     if (merged) atomicAdd(counters, merged);
 }
@@ -808,6 +844,8 @@ struct DiscArgs {
 };
 
 __global__ void k_discords(DiscArgs a) {
+    // one warp per length replays the reference's ascending-offset greedy insertion; lane r
+    // holds list entry r (sorted descending), 8 chunks of the profile are loaded ahead
     const int lane = threadIdx.x & 31;
     const int li = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
     if (li >= a.n_len) return;
@@ -815,36 +853,39 @@ __global__ void k_discords(DiscArgs a) {
     const long long N = a.n - m + 1;
     const long long e = (m + 1) / 2;
     const double* mp = a.mp + (long long)li * a.A;
-    constexpr int KMAX = 32;
-    double cd[KMAX]; long long co[KMAX];
-    const int k = a.k;
-    for (int r = 0; r < k; ++r) { cd[r] = -INFINITY; co[r] = -1; }
-    for (long long base = 0; base < N; base += 32) {
-        const long long o = base + lane;
-        const double d = o < N ? mp[o] : INFINITY;
-        const double thr = cd[k - 1];
-        bool cand = (d < INFINITY) && (d > thr);
-        unsigned bal = __ballot_sync(FULLMASK, cand);
-        while (bal) {
-            const int src = __ffs(bal) - 1;
-            bal &= bal - 1;
-            const double dv = __shfl_sync(FULLMASK, d, src);
-            const long long ov = base + src;
-            bool triv = false;
-            for (int r = 0; r < k; ++r) triv |= (co[r] >= 0 && llabs(ov - co[r]) < e);
-            if (triv) continue;
-            for (int r = 0; r < k; ++r) {
-                if (dv > cd[r]) {
-                    for (int q = k - 1; q > r; --q) { cd[q] = cd[q - 1]; co[q] = co[q - 1]; }
-                    cd[r] = dv; co[r] = ov;
-                    break;
-                }
+    constexpr int AHEAD = 8;
+    const int k = a.k;                       // <= 32
+    double cd = -INFINITY; long long co = -1;
+    for (long long base = 0; base < N; base += 32 * AHEAD) {
+        double dv8[AHEAD];
+#pragma unroll
+        for (int u = 0; u < AHEAD; ++u) {
+            const long long o = base + 32 * u + lane;
+            dv8[u] = o < N ? mp[o] : INFINITY;
+        }
+#pragma unroll
+        for (int u = 0; u < AHEAD; ++u) {
+            const double thr = __shfl_sync(FULLMASK, cd, k - 1);
+            const double d = dv8[u];
+            unsigned bal = __ballot_sync(FULLMASK, (d < INFINITY) && (d > thr));
+            while (bal) {
+                const int src = __ffs(bal) - 1;
+                bal &= bal - 1;
+                const double dv = __shfl_sync(FULLMASK, d, src);
+                const long long ov = base + 32 * u + src;
+                const bool mine = lane < k;
+                if (__any_sync(FULLMASK, mine && co >= 0 && llabs(ov - co) < e)) continue;   // trivial match
+                // before the first strictly smaller entry
+                const int at = __popc(__ballot_sync(FULLMASK, mine && !(dv > cd)));
+                if (at >= k) continue;
+                const double ud = __shfl_up_sync(FULLMASK, cd, 1);
+                const long long uo = __shfl_up_sync(FULLMASK, co, 1);
+                if (mine && lane > at) { cd = ud; co = uo; }
+                if (lane == at) { cd = dv; co = ov; }
             }
         }
     }
-    if (lane == 0) {
-        for (int r = 0; r < k; ++r) { a.out_d[(long long)li * k + r] = cd[r]; a.out_o[(long long)li * k + r] = co[r]; }
-    }
+    if (lane < k) { a.out_d[(long long)li * k + lane] = cd; a.out_o[(long long)li * k + lane] = co; }
 }
 
 // VALMP improvement events with norm <= tau (motifsets.py:105-117 stream)
@@ -1186,9 +1227,11 @@ struct vlmp_session {
     double* d_tn = nullptr; double* d_cum = nullptr; double* d_cum2 = nullptr;
     // per-length scratch
     Prm* d_prm = nullptr; double* d_mu = nullptr;
+    Prm* d_prm2 = nullptr; double* d_mu2 = nullptr;     // previous length's (1-best bound)
     long long* d_previdx = nullptr;
     float2* d_colq = nullptr; float2* d_rowq = nullptr;   // filter factors (k_qprep)
     int* d_forced = nullptr; size_t forced_cap = 0;      // per-length: full-fold fallback
+    unsigned long long* d_fixcnt = nullptr; size_t fixcnt_cap = 0;   // per-length k_bound_fix queue
     double sscale = 1.0; int hiC = 896 << 20;            // filter: 2^-k scale, hi-word bias
     // tiles / seeds
     int2* d_tiles = nullptr; size_t tiles_cap = 0;
@@ -1302,8 +1345,8 @@ void vlmp_destroy(vlmp_session* s) {
     if (!s) return;
     cudaSetDevice(s->device);
     cudaStreamSynchronize(s->stream);
-    void* ptrs[] = {s->d_tn, s->d_cum, s->d_cum2, s->d_prm, s->d_mu,
-                    s->d_previdx, s->d_colq, s->d_rowq, s->d_forced, s->d_tiles, s->d_seeds, s->d_acc, s->d_mp, s->d_ip, s->d_counters,
+    void* ptrs[] = {s->d_tn, s->d_cum, s->d_cum2, s->d_prm, s->d_mu, s->d_prm2, s->d_mu2,
+                    s->d_previdx, s->d_colq, s->d_rowq, s->d_forced, s->d_fixcnt, s->d_tiles, s->d_seeds, s->d_acc, s->d_mp, s->d_ip, s->d_counters,
                     s->d_log, s->d_logcnt, s->d_ro_i64, s->d_ro_f64, s->d_ro_cnt,
                     s->d_slots, s->d_slotcnt, s->d_ipm, s->d_mpm, s->d_redo, s->d_vdist, s->d_vnorm, s->d_vlen, s->d_vidx, s->d_vpop};
     for (void* p : ptrs) if (p) cudaFree(p);
@@ -1330,6 +1373,8 @@ int vlmp_set_series(vlmp_session* s, const double* t, const double* cum, const d
     if ((rc = ensure1(s->d_cum2, n + 1))) return rc;
     if ((rc = ensure1(s->d_prm, A))) return rc;
     if ((rc = ensure1(s->d_mu, A))) return rc;
+    if ((rc = ensure1(s->d_prm2, A))) return rc;
+    if ((rc = ensure1(s->d_mu2, A))) return rc;
     if ((rc = ensure1(s->d_previdx, A))) return rc;
     if ((rc = ensure1(s->d_colq, A))) return rc;
     if ((rc = ensure1(s->d_rowq, A))) return rc;
@@ -1404,6 +1449,9 @@ static int profile_impl(vlmp_session* s, int32_t lmin, int32_t lmax, int64_t ban
     if ((rc = ensure(s->d_log, s->log_cap, log_cap))) return rc;
     if ((rc = ensure(s->d_logcnt, s->logcnt_cap, (size_t)n_len))) return rc;
     if ((rc = ensure(s->d_forced, s->forced_cap, (size_t)n_len))) return rc;
+    if ((rc = ensure(s->d_fixcnt, s->fixcnt_cap, (size_t)n_len))) return rc;
+    if ((rc = ensure(s->d_redo, s->redo_cap, (size_t)A))) return rc;
+    CU(cudaMemsetAsync(s->d_fixcnt, 0, n_len * sizeof(unsigned long long), st));
     CU(cudaMemsetAsync(s->d_logcnt, 0, n_len * sizeof(unsigned long long), st));
     CU(cudaMemsetAsync(s->d_forced, 0, n_len * sizeof(int), st));
     if (T) CU(cudaMemcpyAsync(s->d_tiles, tiles.data(), T * sizeof(int2), cudaMemcpyHostToDevice, st));
@@ -1420,37 +1468,44 @@ static int profile_impl(vlmp_session* s, int32_t lmin, int32_t lmax, int64_t ban
         const int m = lmin + li;
         const long long N = n - m + 1;
         const int e = (m + 1) / 2;
-        ParamArgs pa{s->d_tn, s->d_cum, s->d_cum2, s->d_prm, s->d_mu, n, N, A, m, s->floor_};
+        // window parameters ping-pong between two buffers: the bound reads length m-1's
+        Prm* prm = (li & 1) ? s->d_prm2 : s->d_prm;
+        double* mu = (li & 1) ? s->d_mu2 : s->d_mu;
+        const Prm* prm_prev = (li & 1) ? s->d_prm : s->d_prm2;
+        const double* mu_prev = (li & 1) ? s->d_mu : s->d_mu2;
+        ParamArgs pa{s->d_tn, s->d_cum, s->d_cum2, prm, mu, n, N, A, m, s->floor_};
         k_params<<<blocks(A, 256), 256, 0, st>>>(pa);
         ++klaunch;
         const bool full = (li == 0) || (flags & VLMP_F_FULL_EVERY_LENGTH);
         if (li == 0 && T) {
-            SeedArgs sa{s->d_tn, s->d_mu, s->d_tiles, s->d_seeds, dl, (int)T, S, m};
+            SeedArgs sa{s->d_tn, mu, s->d_tiles, s->d_seeds, dl, (int)T, S, m};
             k_seed_init<<<blocks(T * 32, WARPS_PER_CTA * 32), WARPS_PER_CTA * 32, 0, st>>>(sa);
             ++klaunch;
         }
         if (!full) {
-            k_acc_idx<<<blocks(N + 1, 256), 256, 0, st>>>(s->d_acc + (long long)(li - 1) * A, s->d_previdx, N + 1);
-            BoundArgs ba{s->d_tn, s->d_mu, s->d_prm, s->d_previdx, N, N + 1, m, e, margin};
-            k_bound<<<blocks(N * 32, 256), 256, 0, st>>>(ba);
-            k_qprep<<<blocks(A, 256), 256, 0, st>>>(s->d_prm, s->d_colq, s->d_rowq, N, A, s->sscale,
+            Bound2Args ba{s->d_tn, prm, prm_prev, mu_prev, s->d_acc + (long long)(li - 1) * A, prm,
+                          N, N + 1, m, e, margin, s->d_redo, s->d_fixcnt + li};
+            k_bound2<<<blocks(N, 256), 256, 0, st>>>(ba);
+            k_bound_fix<<<148 * 4, 256, 0, st>>>(s->d_tn, mu, prm, s->d_acc + (long long)(li - 1) * A, s->d_redo,
+                                                  s->d_fixcnt + li, N, m, e, margin);
+            k_qprep<<<blocks(A, 256), 256, 0, st>>>(prm, s->d_colq, s->d_rowq, N, A, s->sscale,
                                                     s->d_forced + li);
-            klaunch += 3;
+            klaunch += 2;
         }
         while (s->lev.size() < (size_t)2 * (li + 1)) {
             cudaEvent_t ev; CU(cudaEventCreate(&ev)); s->lev.push_back(ev);
         }
         CU(cudaEventRecord(s->lev[2 * li], st));
         if (T) {
-            TileArgs ta{s->d_prm, s->d_mu, s->d_tn, s->d_tiles, s->d_seeds, s->d_acc + (long long)li * A,
+            TileArgs ta{prm, mu, s->d_tn, s->d_tiles, s->d_seeds, s->d_acc + (long long)li * A,
                         s->d_counters, s->d_log, s->d_logcnt + li, (long long)s->log_cap,
                         N, dl, (int)T, S, m, e, li + 1 < n_len,
                         s->d_colq, s->d_rowq, s->d_forced + li, s->hiC};
             if (full) k_tile<true><<<blocks(T, WARPS_PER_CTA), WARPS_PER_CTA * 32, smem, st>>>(ta);
             else {
                 k_tile<false><<<blocks(T, WARPS_PER_CTA), WARPS_PER_CTA * 32, smem, st>>>(ta);
-                k_log_merge<<<296, 128, 0, st>>>(s->d_log, s->d_logcnt + li, (long long)s->log_cap,
-                                                 s->d_prm, e, s->d_acc + (long long)li * A, s->d_counters);
+                k_log_merge<<<148 * 8, 256, 0, st>>>(s->d_log, s->d_logcnt + li, (long long)s->log_cap,
+                                                     prm, e, s->d_acc + (long long)li * A, s->d_counters);
                 klaunch += 1;
             }
             launches += 1; klaunch += 1;
@@ -1483,10 +1538,14 @@ static int profile_impl(vlmp_session* s, int32_t lmin, int32_t lmax, int64_t ban
         for (auto c : lc) overflow |= c > s->log_cap;
     }
     int n_forced = 0;
+    double n_fix = 0;
     {
         std::vector<int> fl(n_len);
         CU(cudaMemcpy(fl.data(), s->d_forced, n_len * sizeof(int), cudaMemcpyDeviceToHost));
         for (int f : fl) n_forced += f != 0;
+        std::vector<unsigned long long> fx(n_len);
+        CU(cudaMemcpy(fx.data(), s->d_fixcnt, n_len * sizeof(unsigned long long), cudaMemcpyDeviceToHost));
+        for (auto f : fx) n_fix += (double)f;
     }
     double W = 0;
     for (int m = lmin; m <= lmax; ++m) {
@@ -1499,7 +1558,7 @@ static int profile_impl(vlmp_session* s, int32_t lmin, int32_t lmax, int64_t ban
     s->stats[0] = ms; s->stats[2] = executed; s->stats[3] = W; s->stats[4] = tile_ms;
     s->stats[5] = launches; s->stats[6] = n_filtered; s->stats[7] = n_full; s->stats[8] = (double)cnt[0];
     s->stats[9] = klaunch; s->stats[10] = first_ms; s->stats[11] = (double)cnt[2];
-    s->stats[12] = (double)cnt[1]; s->stats[14] = n_forced;
+    s->stats[12] = n_fix; s->stats[14] = n_forced;
     *overflow_out = overflow;
     return 0;
 }
@@ -1663,7 +1722,7 @@ int vlmp_discords(vlmp_session* s, int32_t k, double* out_dist, int64_t* out_off
     if ((rc = ensure(s->d_ro_f64, s->ro_f64_cap, (size_t)cnt))) return rc;
     double* d_d = s->d_ro_f64; long long* d_o = s->d_ro_i64;
     DiscArgs da{s->d_mp, d_d, d_o, s->n, s->A, s->lmin, s->n_len, k};
-    k_discords<<<blocks((long long)s->n_len * 32, 128), 128, 0, s->stream>>>(da);
+    k_discords<<<s->n_len, 32, 0, s->stream>>>(da);
     CU(cudaGetLastError());
     CU(cudaMemcpyAsync(out_dist, d_d, cnt * 8, cudaMemcpyDeviceToHost, s->stream));
     CU(cudaMemcpyAsync(out_off, d_o, cnt * 8, cudaMemcpyDeviceToHost, s->stream));
