@@ -50,10 +50,15 @@ constexpr int D = VLMP_D;         // diagonals per lane (power of two)
 constexpr int BAND = 32 * D;      // diagonals per warp tile
 constexpr int PBITS = (D == 4) ? 7 : (D == 8) ? 8 : 9;   // log2(BAND): packed local index bits
 constexpr unsigned long long PMASK = (1ull << PBITS) - 1;
-constexpr int WARPS_PER_CTA = 4;
-#ifndef VLMP_FILTER_MIN_BLOCKS
-#define VLMP_FILTER_MIN_BLOCKS 5
+#ifndef VLMP_WARPS_PER_CTA
+#define VLMP_WARPS_PER_CTA 1
 #endif
+#ifndef VLMP_FILTER_WARPS_PER_SM
+#define VLMP_FILTER_WARPS_PER_SM 20   // 96 registers
+#endif
+constexpr int WARPS_PER_CTA = VLMP_WARPS_PER_CTA;
+constexpr int FILTER_MIN_BLOCKS = VLMP_FILTER_WARPS_PER_SM / WARPS_PER_CTA;
+constexpr int FULL_MIN_BLOCKS = 16 / WARPS_PER_CTA;               // 128 registers
 constexpr unsigned FULLMASK = 0xffffffffu;
 constexpr unsigned long long KEY_NONE = 0x7FF0000000000000ull;   // bits of +inf
 constexpr long long IDX_NONE = 0x7FFFFFFFFFFFFFFFll;
@@ -349,10 +354,6 @@ __device__ inline double pack_low(double v, unsigned idx) {
     return __hiloint2double(hi, lo);
 }
 
-__device__ inline void cp_async16(void* smem_dst, const void* gmem_src) {
-    unsigned d = (unsigned)__cvta_generic_to_shared(smem_dst);
-    asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" :: "r"(d), "l"(gmem_src) : "memory");
-}
 __device__ inline void cp_async_commit() { asm volatile("cp.async.commit_group;\n" ::: "memory"); }
 __device__ inline void cp_async_wait_all() { asm volatile("cp.async.wait_group 0;\n" ::: "memory"); }
 
@@ -365,37 +366,68 @@ struct WarpSmem {
     float2 cq[2][D][UCS];    // filter: factors of the column entering lane L's ring at row kk
 };
 
-// stage group g (rows r0 .. r0+7) into buffer b: 8 row structs + 8 fresh columns for lane 31
-__device__ inline void stage_group(WarpSmem& w, int b, const Prm* __restrict__ prm, long long r0,
-                                   long long d0, int lane) {
-#pragma unroll
-    for (int it = lane; it < 4 * D; it += 32) {   // 2 halves x (D rows + D fresh columns)
-        const int q = it >> 1, half = it & 1;
-        const Prm* src = (q < D) ? prm + r0 + q                          // row r0 + q
-                                 : prm + r0 + (q - D) + d0 + BAND - 1;   // fresh column at row r0+q-D
-        Prm* dst = (q < D) ? &w.row[b][q] : &w.fresh[b][q - D];
-        cp_async16(reinterpret_cast<char*>(dst) + 16 * half, reinterpret_cast<const char*>(src) + 16 * half);
+// Per-group staging by cp.async, planned once per tile: every lane's global source advances
+// by a fixed stride per 8-row group and its shared destination alternates between two
+// buffers, so a group costs ~10 LDGSTS with immediate offsets and a few adds.
+//   row structs / fresh columns: lanes 0-15 copy half q = lane/2 of row r0+q, lanes 16-31
+//     half of the fresh column r0+q+d0+BAND-1 entering lane 31 at row r0+q (q = lane/2 - 8);
+//   filter row factors (b_i, q(Uwin_i)) of rows r0..r0+7: lanes 0-3, 16 B each;
+//   filter column factors: lane L at row r0+kk receives column r0 + d0 + D-1 + (D*L + kk);
+//     entry f = lane + 32k (coalesced reads) lands at cq[f & 7][f >> 3] = cq[lane & 7][lane >> 3
+//     + 4k]: a fixed per-lane base + 32 B * k.
+struct StagePlan {
+    const char* src_pr; unsigned dst_pr;      // Prm halves (+256 B per group)
+    const char* src_rq; unsigned dst_rq;      // rowq (+64 B per group), lanes < 4
+    const char* src_cq; unsigned dst_cq;      // colq (+64 B per group)
+};
+constexpr unsigned PR_BUF = sizeof(Prm) * D;             // fresh[b] / row[b] stride
+constexpr unsigned RQ_BUF = sizeof(float2) * D;
+constexpr unsigned CQ_BUF = sizeof(float2) * D * UCS;
+
+template <int OFF_D, int OFF_S, int BYTES>
+__device__ __forceinline__ void cp_async_imm(unsigned d, const char* s) {
+    if (BYTES == 16)
+        asm volatile("cp.async.cg.shared.global [%0+%2], [%1+%3], 16;\n" :: "r"(d), "l"(s), "n"(OFF_D), "n"(OFF_S) : "memory");
+    else
+        asm volatile("cp.async.ca.shared.global [%0+%2], [%1+%3], 8;\n" :: "r"(d), "l"(s), "n"(OFF_D), "n"(OFF_S) : "memory");
+}
+
+template <bool FILTER>
+__device__ __forceinline__ StagePlan make_plan(WarpSmem& w, const TileArgs& a, long long i0, long long d0,
+                                               int lane) {
+    StagePlan p;
+    const int q = (lane & 15) >> 1, half = lane & 1;
+    const long long prow = lane < 16 ? i0 + q : i0 + q + d0 + BAND - 1;
+    p.src_pr = reinterpret_cast<const char*>(a.prm + prow) + 16 * half;
+    p.dst_pr = (unsigned)__cvta_generic_to_shared(lane < 16 ? &w.row[0][q] : &w.fresh[0][q]) + 16 * half;
+    if (FILTER) {
+        p.src_rq = reinterpret_cast<const char*>(a.rowq + i0 + 2 * (lane & 3));
+        p.dst_rq = (unsigned)__cvta_generic_to_shared(&w.rq[0][2 * (lane & 3)]);
+        p.src_cq = reinterpret_cast<const char*>(a.colq + i0 + d0 + D - 1 + lane);
+        p.dst_cq = (unsigned)__cvta_generic_to_shared(&w.cq[0][lane & (D - 1)][lane >> 3]);
+    }
+    return p;
+}
+
+// stage group g (rows i0 + 8g ..) into buffer b
+template <bool FILTER>
+__device__ __forceinline__ void stage(const StagePlan& p, int g, int b, int lane) {
+    const unsigned bsel = (unsigned)b;
+    cp_async_imm<0, 0, 16>(p.dst_pr + bsel * PR_BUF, p.src_pr + (long long)g * (D * sizeof(Prm)));
+    if (FILTER) {
+        if (lane < 4) cp_async_imm<0, 0, 16>(p.dst_rq + bsel * RQ_BUF, p.src_rq + (long long)g * (D * 8));
+        const unsigned dc = p.dst_cq + bsel * CQ_BUF;
+        const char* sc = p.src_cq + (long long)g * (D * 8);
+        cp_async_imm<0, 0, 8>(dc, sc);
+        cp_async_imm<32, 256, 8>(dc, sc);
+        cp_async_imm<64, 512, 8>(dc, sc);
+        cp_async_imm<96, 768, 8>(dc, sc);
+        cp_async_imm<128, 1024, 8>(dc, sc);
+        cp_async_imm<160, 1280, 8>(dc, sc);
+        cp_async_imm<192, 1536, 8>(dc, sc);
+        cp_async_imm<224, 1792, 8>(dc, sc);
     }
     cp_async_commit();
-}
-
-__device__ inline void cp_async8(void* smem_dst, const void* gmem_src) {
-    unsigned d = (unsigned)__cvta_generic_to_shared(smem_dst);
-    asm volatile("cp.async.ca.shared.global [%0], [%1], 8;\n" :: "r"(d), "l"(gmem_src) : "memory");
-}
-
-// filter: row factors of rows r0 .. r0+7 (64 aligned bytes) and the factors of the columns
-// entering the ring during the group -- lane L at row r0+kk receives column
-// r0 + d0 + D-1 + (D*L + kk); coalesced reads, f = D*L + kk lands at cq[kk][L]
-__device__ inline void stage_q(WarpSmem& w, int b, const float2* __restrict__ colq,
-                               const float2* __restrict__ rowq, long long r0, long long d0, int lane) {
-    if (lane < 4) cp_async16(&w.rq[b][2 * lane], rowq + r0 + 2 * lane);
-    const float2* src = colq + r0 + d0 + D - 1;
-#pragma unroll
-    for (int k = 0; k < D; ++k) {
-        const int f = lane + 32 * k;
-        cp_async8(&w.cq[b][f & (D - 1)][f >> 3], src + f);
-    }
 }
 
 // one flagged lane's record (per-lane atomic; the caller diverges)
@@ -490,17 +522,14 @@ __device__ __forceinline__ void tile_body(const TileArgs& a, WarpSmem& w, int wi
         rowres = INFINITY; colres = INFINITY;
     };
 
-    if (!FULL) stage_q(w, 0, a.colq, a.rowq, i0, d0, lane);
-    stage_group(w, 0, a.prm, i0, d0, lane);
+    const StagePlan plan = make_plan<!FULL>(w, a, i0, d0, lane);
+    stage<!FULL>(plan, 0, 0, lane);
     cp_async_wait_all();
     __syncwarp();
 
     for (int g = 0; g < ngroups; ++g) {
         const int b = g & 1;
-        if (g + 1 < ngroups) {
-            if (!FULL) stage_q(w, b ^ 1, a.colq, a.rowq, i0 + (long long)(g + 1) * D, d0, lane);
-            stage_group(w, b ^ 1, a.prm, i0 + (long long)(g + 1) * D, d0, lane);
-        }
+        if (g + 1 < ngroups) stage<!FULL>(plan, g + 1, b ^ 1, lane);
 #pragma unroll
         for (int kk = 0; kk < D; ++kk) {
             const long long i = i0 + (long long)g * D + kk;
@@ -617,7 +646,7 @@ __device__ __forceinline__ void tile_body(const TileArgs& a, WarpSmem& w, int wi
 }
 
 template <bool FULL>
-__global__ void __launch_bounds__(WARPS_PER_CTA * 32, FULL ? 4 : VLMP_FILTER_MIN_BLOCKS)
+__global__ void __launch_bounds__(WARPS_PER_CTA * 32, FULL ? FULL_MIN_BLOCKS : FILTER_MIN_BLOCKS)
 k_tile(TileArgs a) {
     extern __shared__ __align__(128) unsigned char smem_raw[];
     WarpSmem* ws = reinterpret_cast<WarpSmem*>(smem_raw);
@@ -1283,7 +1312,10 @@ inline unsigned blocks(long long n, int t) { return (unsigned)((n + t - 1) / t);
 int seg_rows(long long n) {
     // S = G*D rows per tile (whole 8-row groups); larger for longer series to bound the
     // number of tiles and the seed store (config 5: S = 16384, ~1.1M tiles, 2.2 GB of seeds)
-    long long G = 128;
+#ifndef VLMP_SEG_G0
+#define VLMP_SEG_G0 128
+#endif
+    long long G = VLMP_SEG_G0;
     while (G * D * 256 < n && G < 2048) G *= 2;
     return (int)(G * D);
 }
