@@ -430,6 +430,11 @@ __device__ __forceinline__ void stage(const StagePlan& p, int g, int b, int lane
     cp_async_commit();
 }
 
+// high word of (double)(a*b rounded down): exponent rebiased, mantissa truncated (<= a*b)
+__device__ __forceinline__ int q_hi(float a, float b, int hiC) {
+    return (int)(__float_as_uint(__fmul_rd(a, b)) >> 3) + hiC;
+}
+
 // one flagged lane's record (per-lane atomic; the caller diverges)
 __device__ __forceinline__ void log_one(const TileArgs& a, long long i, long long j0, const double (&cov)[D]) {
     const unsigned long long at = atomicAdd(a.log_count, 1ull);
@@ -576,8 +581,7 @@ __device__ __forceinline__ void tile_body(const TileArgs& a, WarpSmem& w, int wi
                 for (int s = 0; s < D; ++s) {
                     const int p = (s + kk) & (D - 1);
                     // hi(cov) >= hi((double)t): t's exponent rebiased, mantissa truncated (<= t)
-                    const float t = __fmul_rd(cA[p], bi);
-                    const int ht = (int)(__float_as_uint(t) >> 3) + a.hiC;
+                    const int ht = q_hi(cA[p], bi, a.hiC);
                     const bool hit = sval[s] && (__double2hiint(cov[s]) >= ht);
                     if (s & 1) pb |= hit; else pa |= hit;
                 }
@@ -680,39 +684,63 @@ k_tile(TileArgs a) {
 // the exclusion zone, and merge (key, index) with the 128-bit CAS
 __global__ void k_log_merge(const RowRec* log, const unsigned long long* log_count, long long cap,
                             const Prm* prm, int e, ulonglong2* acc, unsigned long long* counters) {
+    // D consecutive lanes share one record (one cell each); every group takes R records at
+    // once so the dependent loads (record -> window params -> accumulator) overlap
+    constexpr int R = 4;
     const unsigned long long cnt = *log_count;
     const long long nrec = (long long)(cnt < (unsigned long long)cap ? cnt : (unsigned long long)cap);
-    const int s = threadIdx.x & (D - 1);   // D consecutive lanes share one record, one cell each
+    const int s = threadIdx.x & (D - 1);
     unsigned long long merged = 0;
-    const long long stride = ((long long)gridDim.x * blockDim.x) / D;
+    const long long groups = ((long long)gridDim.x * blockDim.x) / D;
+    const long long stride = groups * R;
     const long long q_end = (nrec + stride - 1) / stride * stride;   // whole groups iterate together
-    for (long long q = (blockIdx.x * (long long)blockDim.x + threadIdx.x) / D; q < q_end; q += stride) {
-        unsigned long long rk = KEY_NONE; long long rj = IDX_NONE;
-        long long i = 0;
-        if (q < nrec) {
-            const RowRec* rec = log + q;
-            const int2 ij = *reinterpret_cast<const int2*>(rec);
-            i = ij.x;
-            const long long j = (long long)ij.y + s;
-            if (j - i >= e) {
-                const Prm pr = prm[i], pc = prm[j];
-                const double r = fma(-(rec->cov[s] * pr.inv), pc.inv, 1.0);
-                const float h = __int_as_float(__double2hiint(r));
-                const unsigned long long key = clamp_key(r) & ~PMASK;
-                if (h <= pr.U) { rk = key; rj = j; }
-                if (h <= pc.U) { acc_merge(acc + j, key, i); ++merged; }
+    for (long long q0 = (blockIdx.x * (long long)blockDim.x + threadIdx.x) / D; q0 < q_end; q0 += stride) {
+        long long iv[R], jv[R]; double cv[R];
+        bool ok[R];
+#pragma unroll
+        for (int u = 0; u < R; ++u) {
+            const long long q = q0 + u * groups;
+            ok[u] = q < nrec;
+            iv[u] = 0; jv[u] = 0; cv[u] = 0.0;
+            if (ok[u]) {
+                const RowRec* rec = log + q;
+                const int2 ij = *reinterpret_cast<const int2*>(rec);
+                iv[u] = ij.x; jv[u] = (long long)ij.y + s; cv[u] = rec->cov[s];
+                ok[u] = jv[u] - iv[u] >= e;
             }
         }
-        // the record's row-side candidates: one (key, index) minimum, one CAS
+        double ii[R], ij_[R]; float ui[R], uj[R];
 #pragma unroll
-        for (int off = 1; off < D; off <<= 1) {
-            const unsigned long long ok = __shfl_xor_sync(FULLMASK, rk, off);
-            const long long oj = __shfl_xor_sync(FULLMASK, rj, off);
-            if (key_less(ok, oj, rk, rj)) { rk = ok; rj = oj; }
+        for (int u = 0; u < R; ++u) {
+            ii[u] = 0.0; ij_[u] = 0.0; ui[u] = -INFINITY; uj[u] = -INFINITY;
+            if (ok[u]) {
+                const Prm pr = prm[iv[u]], pc = prm[jv[u]];
+                ii[u] = pr.inv; ij_[u] = pc.inv; ui[u] = pr.U; uj[u] = pc.U;
+            }
         }
-        if (s == 0 && rj != IDX_NONE) { acc_merge(acc + i, rk, rj); ++merged; }
+#pragma unroll
+        for (int u = 0; u < R; ++u) {
+            unsigned long long rk = KEY_NONE; long long rj = IDX_NONE;
+            if (ok[u]) {
+                const double r = fma(-(cv[u] * ii[u]), ij_[u], 1.0);
+                const float h = __int_as_float(__double2hiint(r));
+                const unsigned long long key = clamp_key(r) & ~PMASK;
+                if (h <= ui[u]) { rk = key; rj = jv[u]; }
+                if (h <= uj[u]) { acc_merge(acc + jv[u], key, iv[u]); ++merged; }
+            }
+            // the record's row-side candidates: one (key, index) minimum, one CAS
+#pragma unroll
+            for (int off = 1; off < D; off <<= 1) {
+                const unsigned long long ok2 = __shfl_xor_sync(FULLMASK, rk, off);
+                const long long oj = __shfl_xor_sync(FULLMASK, rj, off);
+                if (key_less(ok2, oj, rk, rj)) { rk = ok2; rj = oj; }
+            }
+            if (s == 0 && rj != IDX_NONE) { acc_merge(acc + iv[u], rk, rj); ++merged; }
+        }
     }
-    if (merged) atomicAdd(counters, merged);
+#pragma unroll
+    for (int off = 16; off >= 1; off >>= 1) merged += __shfl_xor_sync(FULLMASK, merged, off);
+    if ((threadIdx.x & 31) == 0 && merged) atomicAdd(counters, merged);
 }
 
 // initial seeds: centred direct sums at the first length
