@@ -136,7 +136,7 @@ int vlmp_discords_m(vlmp_session* s, int32_t k, double* out_dist, int64_t* out_o
  * out[11] flagged filter lane-rows (log records), out[12] offsets whose bound needed a direct dot product, out[13] exact redo count (1-best:
  * 1 = the run was redone with full folds after a log overflow; m-best: offsets
  * recomputed), out[14] lengths that fell back to full folds (an offset's own bound
- * too weak for the covariance-domain filter).
+ * too weak for the covariance-domain filter), out[15] largest per-length log fill.
  */
 int vlmp_stats(vlmp_session* s, double* out, int32_t n_out);
 

@@ -199,7 +199,7 @@ class Session:
         self._check(self.lib.vlmp_stats(self.h, _ptr(out), 16))
         keys = ["profile_ms", "finalize_ms", "executed_updates", "W", "tile_ms", "tile_launches",
                 "filtered_lengths", "full_lengths", "slow_merges", "kernel_launches", "first_tile_ms",
-                "slow_rowsteps", "bound_fixes", "exact_redo", "fallback_lengths"]
+                "slow_rowsteps", "bound_fixes", "exact_redo", "fallback_lengths", "max_log_records"]
         return {k: float(out[i]) for i, k in enumerate(keys)}
 
     def event_record(self, slot):

@@ -1337,6 +1337,18 @@ int ensure1(T*& p, size_t count) { size_t cap = 0; if (p) { cudaFree(p); p = nul
 
 inline unsigned blocks(long long n, int t) { return (unsigned)((n + t - 1) / t); }
 
+// filter log records per length: 8 per offset (quasi-periodic series flag many near-minimum
+// cells), at most a quarter of the free device memory; an overflow re-runs exactly
+size_t log_capacity(long long N0) {
+    size_t want = std::max<size_t>((size_t)1 << 20, (size_t)(8 * N0));
+    size_t free_b = 0, total_b = 0;
+    if (cudaMemGetInfo(&free_b, &total_b) == cudaSuccess) {
+        const size_t lim = free_b / 4 / sizeof(RowRec);
+        if (want > lim) want = std::max<size_t>(lim, (size_t)1 << 18);
+    }
+    return want;
+}
+
 int seg_rows(long long n) {
     // S = G*D rows per tile (whole 8-row groups); larger for longer series to bound the
     // number of tiles and the seed store (config 5: S = 16384, ~1.1M tiles, 2.2 GB of seeds)
@@ -1505,7 +1517,7 @@ static int profile_impl(vlmp_session* s, int32_t lmin, int32_t lmax, int64_t ban
     if ((rc = ensure(s->d_tiles, s->tiles_cap, (size_t)std::max<long long>(T, 1)))) return rc;
     if ((rc = ensure(s->d_seeds, s->seeds_cap, (size_t)std::max<long long>(T, 1) * BAND))) return rc;
     if ((rc = ensure(s->d_acc, s->acc_cap, (size_t)n_len * A))) return rc;
-    const size_t log_cap = std::max<size_t>((size_t)1 << 18, (size_t)(2 * N0));
+    const size_t log_cap = log_capacity(N0);
     if ((rc = ensure(s->d_log, s->log_cap, log_cap))) return rc;
     if ((rc = ensure(s->d_logcnt, s->logcnt_cap, (size_t)n_len))) return rc;
     if ((rc = ensure(s->d_forced, s->forced_cap, (size_t)n_len))) return rc;
@@ -1592,10 +1604,11 @@ static int profile_impl(vlmp_session* s, int32_t lmin, int32_t lmax, int64_t ban
     unsigned long long cnt[8];
     CU(cudaMemcpy(cnt, s->d_counters, sizeof(cnt), cudaMemcpyDeviceToHost));
     bool overflow = false;
+    double max_log = 0;
     {   // a candidate log that overflowed lost candidates: the caller redoes the run exactly
         std::vector<unsigned long long> lc(n_len);
         CU(cudaMemcpy(lc.data(), s->d_logcnt, n_len * sizeof(unsigned long long), cudaMemcpyDeviceToHost));
-        for (auto c : lc) overflow |= c > s->log_cap;
+        for (auto c : lc) { overflow |= c > s->log_cap; max_log = std::max(max_log, (double)c); }
     }
     int n_forced = 0;
     double n_fix = 0;
@@ -1618,7 +1631,7 @@ static int profile_impl(vlmp_session* s, int32_t lmin, int32_t lmax, int64_t ban
     s->stats[0] = ms; s->stats[2] = executed; s->stats[3] = W; s->stats[4] = tile_ms;
     s->stats[5] = launches; s->stats[6] = n_filtered; s->stats[7] = n_full; s->stats[8] = (double)cnt[0];
     s->stats[9] = klaunch; s->stats[10] = first_ms; s->stats[11] = (double)cnt[2];
-    s->stats[12] = n_fix; s->stats[14] = n_forced;
+    s->stats[12] = n_fix; s->stats[14] = n_forced; s->stats[15] = max_log;
     *overflow_out = overflow;
     return 0;
 }
@@ -1858,7 +1871,7 @@ int vlmp_profile_mbest(vlmp_session* s, int32_t lmin, int32_t lmax, int32_t mb) 
     if ((rc = ensure(s->d_tiles, s->tiles_cap, (size_t)std::max<long long>(T, 1)))) return rc;
     if ((rc = ensure(s->d_seeds, s->seeds_cap, (size_t)std::max<long long>(T, 1) * BAND))) return rc;
     if ((rc = ensure(s->d_acc, s->acc_cap, (size_t)A))) return rc;
-    const size_t log_cap = std::max<size_t>((size_t)1 << 18, (size_t)(4 * N0));
+    const size_t log_cap = log_capacity(N0);
     if ((rc = ensure(s->d_log, s->log_cap, log_cap))) return rc;
     if ((rc = ensure(s->d_logcnt, s->logcnt_cap, (size_t)n_len))) return rc;
     if ((rc = ensure(s->d_slots, s->slots_cap, (size_t)A * SLOT_CAP))) return rc;

@@ -15,7 +15,9 @@ st = sess.stats()
 W = gen.pair_updates(c.n, c.lmin, c.lmax)
 out = {"config": cfg, "n": c.n, "lengths": c.lmax - c.lmin + 1, "W": W, "wall_s": wall,
        "profile_ms": st["profile_ms"], "tile_ms": st["tile_ms"], "updates_per_s": W / (st["profile_ms"] * 1e-3),
-       "slow_merges": st["slow_merges"], "flagged_rowsteps": st["slow_rowsteps"]}
+       "slow_merges": st["slow_merges"], "flagged_lane_rows": st["slow_rowsteps"],
+       "max_log_records": st.get("max_log_records"), "exact_redo": st.get("exact_redo"),
+       "fallback_lengths": st.get("fallback_lengths"), "bound_fixes": st.get("bound_fixes")}
 rng = np.random.default_rng(cfg)
 bad = 0; checked = 0; maxrel = 0.0
 for L in sorted({c.lmin, (c.lmin + c.lmax) // 2, c.lmax}):
