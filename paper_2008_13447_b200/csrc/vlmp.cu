@@ -46,9 +46,12 @@ namespace {
 #ifndef VLMP_D
 #define VLMP_D 8
 #endif
-constexpr int D = VLMP_D;         // diagonals per lane (power of two)
+constexpr int D = VLMP_D;         // diagonals per lane (even, <= 16)
 constexpr int BAND = 32 * D;      // diagonals per warp tile
-constexpr int PBITS = (D == 4) ? 7 : (D == 8) ? 8 : 9;   // log2(BAND): packed local index bits
+constexpr int ceil_log2(int v) { int b = 0; while ((1 << b) < v) ++b; return b; }
+constexpr int PBITS = ceil_log2(BAND);   // packed local index bits (full-fold keys)
+constexpr int MG = 1 << ceil_log2(D);    // lanes per log record in k_log_merge
+static_assert(D % 2 == 0 && D <= 16, "D: even, at most 16");
 constexpr unsigned long long PMASK = (1ull << PBITS) - 1;
 #ifndef VLMP_WARPS_PER_CTA
 #define VLMP_WARPS_PER_CTA 1
@@ -358,7 +361,7 @@ __device__ inline void cp_async_commit() { asm volatile("cp.async.commit_group;\
 __device__ inline void cp_async_wait_all() { asm volatile("cp.async.wait_group 0;\n" ::: "memory"); }
 
 
-constexpr int UCS = 34;      // padded row of float2: conflict-free staging writes and reads
+constexpr int UCS = 34;      // padded cq row: conflict-free (D = 8) / 2-way (D = 10, 12) staging writes
 struct WarpSmem {
     Prm fresh[2][D];         // the column entering lane 31's slot D-1 at each row of a group
     Prm row[2][D];           // the group's row parameters
@@ -367,18 +370,19 @@ struct WarpSmem {
 };
 
 // Per-group staging by cp.async, planned once per tile: every lane's global source advances
-// by a fixed stride per 8-row group and its shared destination alternates between two
-// buffers, so a group costs ~10 LDGSTS with immediate offsets and a few adds.
-//   row structs / fresh columns: lanes 0-15 copy half q = lane/2 of row r0+q, lanes 16-31
-//     half of the fresh column r0+q+d0+BAND-1 entering lane 31 at row r0+q (q = lane/2 - 8);
-//   filter row factors (b_i, q(Uwin_i)) of rows r0..r0+7: lanes 0-3, 16 B each;
+// by a fixed stride per D-row group and its shared destination alternates between two
+// buffers, so a group costs a few LDGSTS with immediate offsets and a few adds.
+//   row structs / fresh columns: lane l < 2D copies half l%2 of row r0 + l/2 and of the fresh
+//     column r0 + l/2 + d0 + BAND-1 that enters lane 31 at row r0 + l/2;
+//   filter row factors (b_i, q(Uwin_i)) of rows r0..r0+D-1: lanes < D/2, 16 B each;
 //   filter column factors: lane L at row r0+kk receives column r0 + d0 + D-1 + (D*L + kk);
-//     entry f = lane + 32k (coalesced reads) lands at cq[f & 7][f >> 3] = cq[lane & 7][lane >> 3
-//     + 4k]: a fixed per-lane base + 32 B * k.
+//     entry f = lane + 32k (coalesced reads) goes to cq[f % D][f / D] (conflict-free reads by
+//     lane). f % D repeats with period P = D / gcd(D, 32) in k, f / D then advances by 32P/D,
+//     so P destination bases per group plus immediate offsets cover all D entries.
 struct StagePlan {
-    const char* src_pr; unsigned dst_pr;      // Prm halves (+256 B per group)
-    const char* src_rq; unsigned dst_rq;      // rowq (+64 B per group), lanes < 4
-    const char* src_cq; unsigned dst_cq;      // colq (+64 B per group)
+    const char* src_pr; const char* src_fr; unsigned dst_pr, dst_fr;   // +D*32 B per group
+    const char* src_rq; unsigned dst_rq;      // rowq (+8D B per group), lanes < D/2
+    const char* src_cq; unsigned dst_cq;      // colq (+8D B per group)
 };
 constexpr unsigned PR_BUF = sizeof(Prm) * D;             // fresh[b] / row[b] stride
 constexpr unsigned RQ_BUF = sizeof(float2) * D;
@@ -396,36 +400,57 @@ template <bool FILTER>
 __device__ __forceinline__ StagePlan make_plan(WarpSmem& w, const TileArgs& a, long long i0, long long d0,
                                                int lane) {
     StagePlan p;
-    const int q = (lane & 15) >> 1, half = lane & 1;
-    const long long prow = lane < 16 ? i0 + q : i0 + q + d0 + BAND - 1;
-    p.src_pr = reinterpret_cast<const char*>(a.prm + prow) + 16 * half;
-    p.dst_pr = (unsigned)__cvta_generic_to_shared(lane < 16 ? &w.row[0][q] : &w.fresh[0][q]) + 16 * half;
+    const int q = (lane >> 1) % D, half = lane & 1;
+    p.src_pr = reinterpret_cast<const char*>(a.prm + i0 + q) + 16 * half;
+    p.src_fr = reinterpret_cast<const char*>(a.prm + i0 + q + d0 + BAND - 1) + 16 * half;
+    p.dst_pr = (unsigned)__cvta_generic_to_shared(&w.row[0][q]) + 16 * half;
+    p.dst_fr = (unsigned)__cvta_generic_to_shared(&w.fresh[0][q]) + 16 * half;
+    if (4 * D <= 32 && lane >= 16) { p.src_pr = p.src_fr; p.dst_pr = p.dst_fr; }   // one instruction
     if (FILTER) {
-        p.src_rq = reinterpret_cast<const char*>(a.rowq + i0 + 2 * (lane & 3));
-        p.dst_rq = (unsigned)__cvta_generic_to_shared(&w.rq[0][2 * (lane & 3)]);
+        const int r2 = lane % (D / 2);
+        p.src_rq = reinterpret_cast<const char*>(a.rowq + i0 + 2 * r2);
+        p.dst_rq = (unsigned)__cvta_generic_to_shared(&w.rq[0][2 * r2]);
         p.src_cq = reinterpret_cast<const char*>(a.colq + i0 + d0 + D - 1 + lane);
-        p.dst_cq = (unsigned)__cvta_generic_to_shared(&w.cq[0][lane & (D - 1)][lane >> 3]);
+        p.dst_cq = (unsigned)__cvta_generic_to_shared(&w.cq[0][0][0]);
     }
     return p;
 }
 
-// stage group g (rows i0 + 8g ..) into buffer b
+constexpr int gcd_c(int a, int b) { return b == 0 ? a : gcd_c(b, a % b); }
+constexpr int CQ_P = D / gcd_c(D, 32);        // period of (lane + 32k) % D in k
+constexpr int CQ_STEPL = 32 * CQ_P / D;       // f / D advance per period
+
+template <int M>
+__device__ __forceinline__ void stage_cq_run(unsigned d, const char* sc) {
+    if constexpr (M < D / CQ_P) {
+        cp_async_imm<M * CQ_STEPL * 8, M * CQ_P * 256, 8>(d, sc);
+        stage_cq_run<M + 1>(d, sc);
+    }
+}
+
+template <int R>
+__device__ __forceinline__ void stage_cq(unsigned dc, const char* sc, int lane) {
+    if constexpr (R < CQ_P) {
+        const int f = lane + 32 * R;
+        stage_cq_run<0>(dc + (unsigned)(((f % D) * UCS + f / D) * 8), sc + 256 * R);
+        stage_cq<R + 1>(dc, sc, lane);
+    }
+}
+
+// stage group g (rows i0 + D*g ..) into buffer b
 template <bool FILTER>
 __device__ __forceinline__ void stage(const StagePlan& p, int g, int b, int lane) {
     const unsigned bsel = (unsigned)b;
-    cp_async_imm<0, 0, 16>(p.dst_pr + bsel * PR_BUF, p.src_pr + (long long)g * (D * sizeof(Prm)));
+    const long long gs = (long long)g * (D * sizeof(Prm));
+    if constexpr (4 * D <= 32) {   // one instruction: lanes < 2D rows, lanes >= 16 fresh columns
+        if ((lane & 15) < 2 * D) cp_async_imm<0, 0, 16>(p.dst_pr + bsel * PR_BUF, p.src_pr + gs);
+    } else if (lane < 2 * D) {
+        cp_async_imm<0, 0, 16>(p.dst_pr + bsel * PR_BUF, p.src_pr + gs);
+        cp_async_imm<0, 0, 16>(p.dst_fr + bsel * PR_BUF, p.src_fr + gs);
+    }
     if (FILTER) {
-        if (lane < 4) cp_async_imm<0, 0, 16>(p.dst_rq + bsel * RQ_BUF, p.src_rq + (long long)g * (D * 8));
-        const unsigned dc = p.dst_cq + bsel * CQ_BUF;
-        const char* sc = p.src_cq + (long long)g * (D * 8);
-        cp_async_imm<0, 0, 8>(dc, sc);
-        cp_async_imm<32, 256, 8>(dc, sc);
-        cp_async_imm<64, 512, 8>(dc, sc);
-        cp_async_imm<96, 768, 8>(dc, sc);
-        cp_async_imm<128, 1024, 8>(dc, sc);
-        cp_async_imm<160, 1280, 8>(dc, sc);
-        cp_async_imm<192, 1536, 8>(dc, sc);
-        cp_async_imm<224, 1792, 8>(dc, sc);
+        if (lane < D / 2) cp_async_imm<0, 0, 16>(p.dst_rq + bsel * RQ_BUF, p.src_rq + (long long)g * (D * 8));
+        stage_cq<0>(p.dst_cq + bsel * CQ_BUF, p.src_cq + (long long)g * (D * 8), lane);
     }
     cp_async_commit();
 }
@@ -540,7 +565,7 @@ __device__ __forceinline__ void tile_body(const TileArgs& a, WarpSmem& w, int wi
             const long long i = i0 + (long long)g * D + kk;
             const Prm pr = w.row[b][kk];
             {   // ring rotation: phys (kk-1) mod D receives lane+1's outgoing column
-                const int q = (kk + D - 1) & (D - 1);
+                const int q = (kk + D - 1) % D;
                 // lane 0's outgoing column leaves the band: overwrite it with the fresh
                 // column, then rotate by one lane so lane 31 receives it
                 // (rows after a group's first: lane 0 loaded it at the end of the previous row)
@@ -570,7 +595,7 @@ __device__ __forceinline__ void tile_body(const TileArgs& a, WarpSmem& w, int wi
             }
 #pragma unroll
             for (int s = 0; s < D; ++s) {
-                const int p = (s + kk) & (D - 1);
+                const int p = (s + kk) % D;
                 cov[s] = fma(pr.df, cdg[p], cov[s]);
                 cov[s] = fma(cdf[p], pr.dg, cov[s]);
             }
@@ -579,7 +604,7 @@ __device__ __forceinline__ void tile_body(const TileArgs& a, WarpSmem& w, int wi
                 const float bi = w.rq[b][kk].x;
 #pragma unroll
                 for (int s = 0; s < D; ++s) {
-                    const int p = (s + kk) & (D - 1);
+                    const int p = (s + kk) % D;
                     // hi(cov) >= hi((double)t): t's exponent rebiased, mantissa truncated (<= t)
                     const int ht = q_hi(cA[p], bi, a.hiC);
                     const bool hit = sval[s] && (__double2hiint(cov[s]) >= ht);
@@ -591,7 +616,7 @@ __device__ __forceinline__ void tile_body(const TileArgs& a, WarpSmem& w, int wi
                 double rm = INFINITY;
 #pragma unroll
                 for (int s = 0; s < D; ++s) {
-                    const int p = (s + kk) & (D - 1);
+                    const int p = (s + kk) % D;
                     const double r = fma(-(cov[s] * pr.inv), cinv[p], 1.0);
                     double v = r < 0.0 ? 0.0 : r;     // clamp (NaN stays NaN)
                     if (!sval[s]) v = __longlong_as_double(0x7FF8000000000000ll);
@@ -613,6 +638,7 @@ __device__ __forceinline__ void tile_body(const TileArgs& a, WarpSmem& w, int wi
                 const double x0 = __shfl_sync(FULLMASK, x, 0);   // lane 0's exiting column
                 const int slot = (int)((i - i0) & 31);
                 if (lane == slot) { rowres = rm; rowres_i = i; colres = x0; colres_j = i + d0; }
+                if (32 % D != 0 && slot == 31) flush_full();   // every lane holds a stashed row
             }
             if (kk + 1 < D && lane == 0) {
                 // slot 0's column (phys kk) is dead after this row: lane 0 fetches the next row's
@@ -621,7 +647,7 @@ __device__ __forceinline__ void tile_body(const TileArgs& a, WarpSmem& w, int wi
                 cdf[kk] = f.df; cdg[kk] = f.dg; if (FULL) cinv[kk] = f.inv;
             }
         }
-        if (FULL && (g & 3) == 3) flush_full();
+        if (FULL && 32 % D == 0 && ((g + 1) * D) % 32 == 0) flush_full();   // 32 rows stashed
         cp_async_wait_all();
         __syncwarp();
     }
@@ -684,23 +710,23 @@ k_tile(TileArgs a) {
 // the exclusion zone, and merge (key, index) with the 128-bit CAS
 __global__ void k_log_merge(const RowRec* log, const unsigned long long* log_count, long long cap,
                             const Prm* prm, int e, ulonglong2* acc, unsigned long long* counters) {
-    // D consecutive lanes share one record (one cell each); every group takes R records at
-    // once so the dependent loads (record -> window params -> accumulator) overlap
+    // MG consecutive lanes share one record (cells s < D, one each); every group takes R
+    // records at once so the dependent loads (record -> window params -> accumulator) overlap
     constexpr int R = 4;
     const unsigned long long cnt = *log_count;
     const long long nrec = (long long)(cnt < (unsigned long long)cap ? cnt : (unsigned long long)cap);
-    const int s = threadIdx.x & (D - 1);
+    const int s = threadIdx.x & (MG - 1);
     unsigned long long merged = 0;
-    const long long groups = ((long long)gridDim.x * blockDim.x) / D;
+    const long long groups = ((long long)gridDim.x * blockDim.x) / MG;
     const long long stride = groups * R;
     const long long q_end = (nrec + stride - 1) / stride * stride;   // whole groups iterate together
-    for (long long q0 = (blockIdx.x * (long long)blockDim.x + threadIdx.x) / D; q0 < q_end; q0 += stride) {
+    for (long long q0 = (blockIdx.x * (long long)blockDim.x + threadIdx.x) / MG; q0 < q_end; q0 += stride) {
         long long iv[R], jv[R]; double cv[R];
         bool ok[R];
 #pragma unroll
         for (int u = 0; u < R; ++u) {
             const long long q = q0 + u * groups;
-            ok[u] = q < nrec;
+            ok[u] = q < nrec && s < D;
             iv[u] = 0; jv[u] = 0; cv[u] = 0.0;
             if (ok[u]) {
                 const RowRec* rec = log + q;
@@ -730,7 +756,7 @@ __global__ void k_log_merge(const RowRec* log, const unsigned long long* log_cou
             }
             // the record's row-side candidates: one (key, index) minimum, one CAS
 #pragma unroll
-            for (int off = 1; off < D; off <<= 1) {
+            for (int off = 1; off < MG; off <<= 1) {
                 const unsigned long long ok2 = __shfl_xor_sync(FULLMASK, rk, off);
                 const long long oj = __shfl_xor_sync(FULLMASK, rj, off);
                 if (key_less(ok2, oj, rk, rj)) { rk = ok2; rj = oj; }

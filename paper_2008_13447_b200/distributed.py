@@ -21,7 +21,7 @@ from __future__ import annotations
 
 import numpy as np
 
-BAND = 256
+BAND = 256   # = 32 * VLMP_D of libvlmp (diagonals per warp tile)
 IDX_NONE = np.iinfo(np.int64).max
 
 
