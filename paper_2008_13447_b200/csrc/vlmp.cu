@@ -168,10 +168,10 @@ __global__ void k_params(ParamArgs a) {
 // diagonal recurrence; the Welford co-moment step carries it to length m. Any valid cell's
 // key bounds the minimum; the reconstruction error (~1e-13) is far below the margin.
 struct Bound2Args {
-    const double* tn; const Prm* prm; const Prm* pprev; const double* mu_prev;
+    const double* tn; const Prm* prm; const Prm* pprev; const double* mu_prev; const double* mu;
     const ulonglong2* acc_prev; Prm* out;
     long long N, Nprev; int m, e; double margin;
-    long long* fix; unsigned long long* fix_cnt;   // offsets left without a bound
+    unsigned long long* fix_cnt;   // offsets re-bounded by a direct dot product
 };
 
 __global__ void k_bound2(Bound2Args a) {
@@ -215,43 +215,28 @@ __global__ void k_bound2(Bound2Args a) {
             eval(c0 - 1, cov_of(o + 1, v) - po.df * pc.dg - pc.df * po.dg);
         }
     }
+    if (!(best < INFINITY) && o < a.Nprev && a.acc_prev[o].x != KEY_NONE) {
+        // the winner fell into the grown exclusion zone (|c1 - o| = e_{m-1} < e_m): the cell
+        // one step further out, (o, c1 +- 1), by a direct centred dot product (rare)
+        const long long c1 = (long long)a.acc_prev[o].y;
+        const long long c = c1 > o ? c1 + 1 : c1 - 1;
+        const long long dd = c > o ? c - o : o - c;
+        if (c >= 0 && c < a.N && dd >= a.e) {
+            const double ic = a.prm[c].inv;
+            if (ic == ic) {
+                const double mo = a.mu[o], mc = a.mu[c];
+                double cv = 0.0;
+                for (int k = 0; k < m; ++k) cv = fma(a.tn[o + k] - mo, a.tn[c + k] - mc, cv);
+                best = fma(-(cv * io), ic, 1.0);
+                atomicAdd(a.fix_cnt, 1ull);
+            }
+        }
+    }
     float out = INFINITY;   // no bound: every cell of this offset is a candidate
     if (best < INFINITY) out = __int_as_float(__double2hiint(fmax(best, 0.0) + a.margin));
-    else if (o < a.Nprev && a.acc_prev[o].x != KEY_NONE) {
-        // the winner fell into the grown exclusion zone (|c1 - o| = e_{m-1} < e_m): queue the
-        // cell one step further out, (o, c1 +- 1), for a direct dot product (k_bound_fix)
-        const unsigned long long at = atomicAdd(a.fix_cnt, 1ull);
-        a.fix[at] = o;
-    }
     a.out[o].U = out;
 }
 
-// direct centred dot product for the queued offsets (one warp each), cell (o, c1 +- 1)
-__global__ void k_bound_fix(const double* __restrict__ tn, const double* __restrict__ mu, Prm* prm,
-                            const ulonglong2* __restrict__ acc_prev, const long long* fix,
-                            const unsigned long long* fix_cnt, long long N, int m, int e, double margin) {
-    const int lane = threadIdx.x & 31;
-    const unsigned long long cnt = *fix_cnt;
-    for (unsigned long long w = (blockIdx.x * (unsigned long long)blockDim.x + threadIdx.x) >> 5; w < cnt;
-         w += ((unsigned long long)gridDim.x * blockDim.x) >> 5) {
-        const long long o = fix[w];
-        const long long c1 = (long long)acc_prev[o].y;
-        const long long c = c1 > o ? c1 + 1 : c1 - 1;
-        const long long dd = c > o ? c - o : o - c;
-        if (c < 0 || c >= N || dd < e) continue;
-        const double io = prm[o].inv, ic = prm[c].inv;
-        if (!(ic == ic)) continue;
-        const double mo = mu[o], mc = mu[c];
-        double acc = 0.0;
-        for (int k = lane; k < m; k += 32) acc = fma(tn[o + k] - mo, tn[c + k] - mc, acc);
-#pragma unroll
-        for (int off = 16; off >= 1; off >>= 1) acc += __shfl_xor_sync(FULLMASK, acc, off);
-        if (lane == 0) {
-            const double r = fma(-(acc * io), ic, 1.0);
-            prm[o].U = __int_as_float(__double2hiint(fmax(r, 0.0) + margin));
-        }
-    }
-}
 
 // ---------------------------------------------------------------------------------
 // Filter thresholds in the covariance domain. A cell (i, j) must reach the exact tests when
@@ -289,14 +274,14 @@ __global__ void k_qprep(const Prm* __restrict__ prm, float2* colq, float2* rowq,
                         double sscale, int* forced) {
     const long long o = blockIdx.x * (long long)blockDim.x + threadIdx.x;
     if (o >= A) return;
-    const float qnan = __int_as_float(0x7FC00000);
-    if (o >= N) { colq[o] = make_float2(qnan, qnan); rowq[o] = make_float2(qnan, qnan); return; }
+    // invalid windows / past the end: factors +inf, so every threshold is +inf (never passes)
+    if (o >= N) { colq[o] = make_float2(INFINITY, INFINITY); rowq[o] = make_float2(INFINITY, INFINITY); return; }
     const Prm p = prm[o];
     float uw = -INFINITY;
 #pragma unroll
     for (int k = 0; k < D; ++k)
         if (o + k < N) uw = fmaxf(uw, prm[o + k].U);
-    const float b = qscale(p.inv, sscale);
+    const float b = p.inv == p.inv ? qscale(p.inv, sscale) : INFINITY;
     const double qu = qfac(p.U);
     const float a = __double2float_rd(qu * (double)b);
     const float w = uw == -INFINITY ? 3.0e38f : __double2float_rd(qfac(uw));
@@ -1314,7 +1299,7 @@ struct vlmp_session {
     long long* d_previdx = nullptr;
     float2* d_colq = nullptr; float2* d_rowq = nullptr;   // filter factors (k_qprep)
     int* d_forced = nullptr; size_t forced_cap = 0;      // per-length: full-fold fallback
-    unsigned long long* d_fixcnt = nullptr; size_t fixcnt_cap = 0;   // per-length k_bound_fix queue
+    unsigned long long* d_fixcnt = nullptr; size_t fixcnt_cap = 0;   // per-length re-bounded offsets
     double sscale = 1.0; int hiC = 896 << 20;            // filter: 2^-k scale, hi-word bias
     // tiles / seeds
     int2* d_tiles = nullptr; size_t tiles_cap = 0;
@@ -1373,6 +1358,20 @@ size_t log_capacity(long long N0) {
         if (want > lim) want = std::max<size_t>(lim, (size_t)1 << 18);
     }
     return want;
+}
+
+// launch order: longest tiles first (LPT), so the partial last segments of the bands fill
+// the tail of each length's launch instead of leaving SMs idle behind full-size tiles
+#ifndef VLMP_TILE_LPT
+#define VLMP_TILE_LPT 1
+#endif
+void order_tiles(std::vector<int2>& tiles, long long N0, long long dl, int S) {
+    if (!VLMP_TILE_LPT) return;
+    auto rows = [&](const int2& t) {
+        const long long r = N0 - (dl + (long long)t.x * BAND) - (long long)t.y * S;
+        return r < S ? r : (long long)S;
+    };
+    std::stable_sort(tiles.begin(), tiles.end(), [&](const int2& a, const int2& b) { return rows(a) > rows(b); });
 }
 
 int seg_rows(long long n) {
@@ -1528,16 +1527,14 @@ static int profile_impl(vlmp_session* s, int32_t lmin, int32_t lmax, int64_t ban
     if (band_lo < 0) band_lo = 0;
     const int S = seg_rows(n);
     const long long N0 = n - lmin + 1, dl = dlo_for(lmin);
-    // tile list (band-major: the near-diagonal, candidate-heavy bands start first),
-    // using N at lmin (a superset of every later length's tiles)
+    // tile list using N at lmin (a superset of every later length's tiles), launched
+    // longest-first (order_tiles)
     std::vector<int2> tiles;
-    std::vector<long long> band_first;   // first tile of each band of the shard
     for (long long b = band_lo; b < band_hi; ++b) {
-        band_first.push_back((long long)tiles.size());
         long long rows = N0 - (dl + b * BAND);
         for (long long sg = 0; sg * S < rows; ++sg) tiles.push_back(make_int2((int)b, (int)sg));
     }
-    band_first.push_back((long long)tiles.size());
+    order_tiles(tiles, N0, dl, S);
     const long long T = (long long)tiles.size();
     int rc;
     if ((rc = ensure(s->d_tiles, s->tiles_cap, (size_t)std::max<long long>(T, 1)))) return rc;
@@ -1548,7 +1545,6 @@ static int profile_impl(vlmp_session* s, int32_t lmin, int32_t lmax, int64_t ban
     if ((rc = ensure(s->d_logcnt, s->logcnt_cap, (size_t)n_len))) return rc;
     if ((rc = ensure(s->d_forced, s->forced_cap, (size_t)n_len))) return rc;
     if ((rc = ensure(s->d_fixcnt, s->fixcnt_cap, (size_t)n_len))) return rc;
-    if ((rc = ensure(s->d_redo, s->redo_cap, (size_t)A))) return rc;
     CU(cudaMemsetAsync(s->d_fixcnt, 0, n_len * sizeof(unsigned long long), st));
     CU(cudaMemsetAsync(s->d_logcnt, 0, n_len * sizeof(unsigned long long), st));
     CU(cudaMemsetAsync(s->d_forced, 0, n_len * sizeof(int), st));
@@ -1581,11 +1577,9 @@ static int profile_impl(vlmp_session* s, int32_t lmin, int32_t lmax, int64_t ban
             ++klaunch;
         }
         if (!full) {
-            Bound2Args ba{s->d_tn, prm, prm_prev, mu_prev, s->d_acc + (long long)(li - 1) * A, prm,
-                          N, N + 1, m, e, margin, s->d_redo, s->d_fixcnt + li};
+            Bound2Args ba{s->d_tn, prm, prm_prev, mu_prev, mu, s->d_acc + (long long)(li - 1) * A, prm,
+                          N, N + 1, m, e, margin, s->d_fixcnt + li};
             k_bound2<<<blocks(N, 256), 256, 0, st>>>(ba);
-            k_bound_fix<<<148 * 4, 256, 0, st>>>(s->d_tn, mu, prm, s->d_acc + (long long)(li - 1) * A, s->d_redo,
-                                                  s->d_fixcnt + li, N, m, e, margin);
             k_qprep<<<blocks(A, 256), 256, 0, st>>>(prm, s->d_colq, s->d_rowq, N, A, s->sscale,
                                                     s->d_forced + li);
             klaunch += 2;
@@ -1892,6 +1886,7 @@ int vlmp_profile_mbest(vlmp_session* s, int32_t lmin, int32_t lmax, int32_t mb) 
         long long rows = N0 - (dl + b * BAND);
         for (long long sg = 0; sg * S < rows; ++sg) tiles.push_back(make_int2((int)b, (int)sg));
     }
+    order_tiles(tiles, N0, dl, S);
     const long long T = (long long)tiles.size();
     int rc;
     if ((rc = ensure(s->d_tiles, s->tiles_cap, (size_t)std::max<long long>(T, 1)))) return rc;
