@@ -128,6 +128,16 @@ int vlmp_get_profile_m(vlmp_session* s, int32_t length, double* dist, int64_t* n
 int vlmp_discords_m(vlmp_session* s, int32_t k, double* out_dist, int64_t* out_off);
 
 /*
+ * Motif-set range queries (motifsets.py:158-165, the row_profile path of _range_members):
+ * for query q, every offset j with dist(owners[q], j) < radii[q] at length lengths[q],
+ * from the owner's full row with the reference formula (profile.py:235-260); trivial
+ * matches and constant windows excluded. Needs only vlmp_set_series. members is
+ * [n_q][cap] (unordered); counts[q] may exceed cap (then only cap were stored).
+ */
+int vlmp_range_query(vlmp_session* s, int64_t n_q, const int64_t* owners, const int32_t* lengths,
+                     const double* radii, int64_t cap, int64_t* members, int64_t* counts);
+
+/*
  * Timings and counters of the last phase-1/phase-2 run:
  * out[0] profile ms (device), out[1] finalize ms, out[2] executed pair updates,
  * out[3] W (non-trivial pair updates), out[4] tile-kernel ms, out[5] tile-kernel

@@ -12,6 +12,7 @@ scan) and its read-offs, each following the reference line for line in numpy:
   discord replay (m = 1)          discords.py:68-93 + :48-50, oracle.py:137-145,
                                   values via pair_distance (discords.py:126-141)
   merged discords                 discords.py:96-109
+  motif-set range rows            motifsets.py:158-165 row_profile branch, profile.py:235-269
 Pinned against tests/golden/*.npz, which were produced by the real reference.
 """
 
@@ -136,6 +137,33 @@ def canonical_values(series, ip, m):
     for o in np.flatnonzero(ip >= 0):
         out[o] = lib.vlmpo_pair_distance(_p(t), _p(c1), _p(c2), int(o), int(ip[o]), int(m), fl)
     return out
+
+
+def range_row(series, owner, m, r):
+    """Offsets j with dist(owner, j) < r at length m: the full row of profile.py:235-260
+    (owner-first formula, trivial zone [i-e+1, i+e) and constant windows -> +inf), with
+    direct dot products in place of the FFT (sliding_dot_product, series.py:124-138)."""
+    t = np.asarray(series.values, dtype=np.float64)
+    n = t.shape[0]
+    N = n - m + 1
+    c1, c2 = series._cum, series._cum2
+    s = c1[m:] - c1[:-m]
+    ss = c2[m:] - c2[:-m]
+    mu = s / m
+    var = ss / m - mu * mu
+    np.maximum(var, 0.0, out=var)
+    sd = np.sqrt(var)
+    from numpy.lib.stride_tricks import sliding_window_view
+    qt = sliding_window_view(t, m)[:N] @ t[owner:owner + m]
+    with np.errstate(invalid="ignore", divide="ignore"):
+        q_raw = (qt - m * mu[owner] * mu) / (m * sd[owner] * sd)
+        rad = 2.0 * m * (1.0 - q_raw)
+    np.maximum(rad, 0.0, out=rad)
+    dist = np.sqrt(rad)
+    dist[~(sd >= series.sigma_floor)] = np.inf
+    e = (m + 1) // 2
+    dist[max(0, owner - e + 1):min(N, owner + e)] = np.inf
+    return np.flatnonzero(dist < r)
 
 
 def discords_m1(vals, m, k):

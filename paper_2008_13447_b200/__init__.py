@@ -18,6 +18,7 @@ from .results import (VALMP, DiscordMatrix, DiscordScan, LengthTrace, MatrixProf
                       update_variable_length_discords)
 from .api import (MiningResult, compute_matrix_profile, mine, motifs_per_length,
                   topkm_discord_discovery, validate_range, valmod)
+from .motifsets import MotifSet, compute_var_length_motif_sets, validate_disjoint
 
 __version__ = "0.1.0"
 
@@ -27,7 +28,7 @@ __all__ = [
     "VariableLengthDiscordMatrix", "top_variable_length_motif",
     "update_fixed_length_discords", "update_valmp", "update_variable_length_discords",
     "compute_matrix_profile", "mine", "MiningResult", "motifs_per_length", "topkm_discord_discovery",
-    "validate_range", "valmod",
+    "validate_range", "valmod", "MotifSet", "compute_var_length_motif_sets", "validate_disjoint",
     "SeriesMineError", "EmptySeriesError", "NonFiniteError", "LengthExceedsSeriesError",
     "OutOfRangeError", "ZeroVarianceError", "SeriesTooShortError", "AllConstantError",
     "NoValidNeighborError", "InvalidParametersError", "UnpopulatedError",

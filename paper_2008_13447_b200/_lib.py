@@ -36,6 +36,8 @@ SIGNATURES = {
     "vlmp_smallest_rows": (C.c_int, [C.c_void_p, C.c_int32, C.c_void_p, C.c_void_p, C.c_void_p]),
     "vlmp_discords": (C.c_int, [C.c_void_p, C.c_int32, C.c_void_p, C.c_void_p]),
     "vlmp_ranking_events": (C.c_int, [C.c_void_p, C.c_double, C.c_int64] + [C.c_void_p] * 5 + [_c_int64_p]),
+    "vlmp_range_query": (C.c_int, [C.c_void_p, C.c_int64, C.c_void_p, C.c_void_p, C.c_void_p, C.c_int64,
+                                   C.c_void_p, C.c_void_p]),
     "vlmp_profile_mbest": (C.c_int, [C.c_void_p, C.c_int32, C.c_int32, C.c_int32]),
     "vlmp_get_profile_m": (C.c_int, [C.c_void_p, C.c_int32, C.c_void_p, C.c_void_p]),
     "vlmp_discords_m": (C.c_int, [C.c_void_p, C.c_int32, C.c_void_p, C.c_void_p]),
@@ -176,6 +178,21 @@ class Session:
             if cnt.value <= cap:
                 return [b[:cnt.value] for b in bufs]
             cap = int(cnt.value)
+
+    def range_query(self, owners, lengths, radii, cap=256):
+        """Sorted member offsets per query (see vlmp_range_query)."""
+        owners = np.ascontiguousarray(owners, dtype=np.int64)
+        lengths = np.ascontiguousarray(lengths, dtype=np.int32)
+        radii = np.ascontiguousarray(radii, dtype=np.float64)
+        nq = owners.shape[0]
+        while True:
+            mem = np.empty((nq, cap), dtype=np.int64)
+            cnt = np.zeros(nq, dtype=np.int64)
+            self._check(self.lib.vlmp_range_query(self.h, nq, _ptr(owners), _ptr(lengths), _ptr(radii),
+                                                  int(cap), _ptr(mem), _ptr(cnt)))
+            if nq == 0 or int(cnt.max()) <= cap:
+                return [np.sort(mem[q, :cnt[q]]) for q in range(nq)]
+            cap = int(cnt.max())
 
     # -- m-best mode (m-th discords) ---------------------------------------------
     def profile_mbest(self, lmin, lmax, m):

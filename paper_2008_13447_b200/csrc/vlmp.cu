@@ -801,6 +801,7 @@ struct FinArgs {
     long long n, A; int lmin, n_len; double floor_;
 };
 
+#ifdef VLMP_FINALIZE_GRID   // one thread per (length, offset): the full sum every time
 __global__ void k_finalize(FinArgs a) {
     const long long o = blockIdx.x * (long long)blockDim.x + threadIdx.x;
     const int li = blockIdx.y;
@@ -815,6 +816,48 @@ __global__ void k_finalize(FinArgs a) {
     }
     a.mp[(long long)li * a.A + o] = d;
     a.ip[(long long)li * a.A + o] = j;
+}
+#endif
+
+// Same values, one thread per offset walking the lengths upward: pair_distance's dot
+// product is a sequential left-to-right sum over k < m, so when an offset keeps the same
+// canonical pair (a, b) from length m-1 to m its sum at m is the sum at m-1 plus one term
+// -- bit-identical to recomputing it. Only neighbour changes pay the O(m) sum.
+__global__ void k_finalize_walk(FinArgs a) {
+    const long long o = blockIdx.x * (long long)blockDim.x + threadIdx.x;
+    if (o >= a.n - a.lmin + 1) return;
+    long long pa = -1, pb = -1; int pm = -1;
+    double qt = 0.0;
+    for (int li = 0; li < a.n_len; ++li) {
+        const int m = a.lmin + li;
+        if (o > a.n - m) break;
+        const ulonglong2 v = a.acc[(long long)li * a.A + o];
+        double d = INFINITY; int j = -1;
+        if (v.x != KEY_NONE) {
+            j = (int)v.y;
+            const long long lo = o <= j ? o : j, hi = o <= j ? j : o;
+            double mua, sda, mub, sdb;
+            win_stats_pd(a.cum, a.cum2, lo, m, mua, sda);
+            win_stats_pd(a.cum, a.cum2, hi, m, mub, sdb);
+            if (lo == pa && hi == pb && m == pm + 1) {
+                qt = __dadd_rn(qt, __dmul_rn(a.tn[lo + m - 1], a.tn[hi + m - 1]));
+            } else {
+                qt = 0.0;
+#pragma unroll 8
+                for (int k = 0; k < m; ++k) qt = __dadd_rn(qt, __dmul_rn(a.tn[lo + k], a.tn[hi + k]));
+            }
+            pa = lo; pb = hi; pm = m;
+            if (sda >= a.floor_ && sdb >= a.floor_) {
+                const double L = (double)m;
+                const double num = __dsub_rn(qt, __dmul_rn(__dmul_rn(L, mua), mub));
+                const double den = __dmul_rn(__dmul_rn(L, sda), sdb);
+                const double rad = __dmul_rn(__dmul_rn(2.0, L), __dsub_rn(1.0, __ddiv_rn(num, den)));
+                d = rad > 0.0 ? __dsqrt_rn(rad) : 0.0;
+            }
+        }
+        a.mp[(long long)li * a.A + o] = d;
+        a.ip[(long long)li * a.A + o] = j;
+    }
 }
 
 struct ValmpArgs {
@@ -954,6 +997,44 @@ __global__ void k_discords(DiscArgs a) {
         }
     }
     if (lane < k) { a.out_d[(long long)li * k + lane] = cd; a.out_o[(long long)li * k + lane] = co; }
+}
+
+// Motif-set range queries (motifsets.py:158-165 row_profile path, profile.py:235-260):
+// offsets j with dist(owner, j) < radius at the query's length, the owner's full row with
+// the reference's formula and evaluation order; trivial zone and constant windows excluded.
+struct RangeArgs {
+    const double* tn; const double* cum; const double* cum2;
+    const long long* owner; const int* len; const double* radius;
+    long long* members; unsigned long long* counts; long long cap;
+    long long n; double floor_;
+};
+
+__global__ void k_range_query(RangeArgs a) {
+    const int q = blockIdx.y;
+    const long long j = blockIdx.x * (long long)blockDim.x + threadIdx.x;
+    const int m = a.len[q];
+    const long long N = a.n - m + 1;
+    if (j >= N) return;
+    const long long i = a.owner[q];
+    const long long e = (m + 1) / 2;
+    const long long lo = i - e + 1 > 0 ? i - e + 1 : 0, hi = i + e < N ? i + e : N;
+    if (j >= lo && j < hi) return;
+    double mui, sdi, muj, sdj;
+    win_stats_pd(a.cum, a.cum2, i, m, mui, sdi);
+    win_stats_pd(a.cum, a.cum2, j, m, muj, sdj);
+    if (!(sdj >= a.floor_)) return;
+    double qt = 0.0;
+    for (int k = 0; k < m; ++k) qt = fma(a.tn[i + k], a.tn[j + k], qt);
+    const double L = (double)m;
+    const double qraw = __ddiv_rn(__dsub_rn(qt, __dmul_rn(__dmul_rn(L, mui), muj)),
+                                  __dmul_rn(__dmul_rn(L, sdi), sdj));
+    double rad = __dmul_rn(__dmul_rn(2.0, L), __dsub_rn(1.0, qraw));
+    if (rad < 0.0) rad = 0.0;                    // np.maximum(rad, 0): NaN stays NaN
+    const double d = __dsqrt_rn(rad);
+    if (d < a.radius[q]) {
+        const unsigned long long at = atomicAdd(a.counts + q, 1ull);
+        if ((long long)at < a.cap) a.members[(long long)q * a.cap + (long long)at] = j;
+    }
 }
 
 // VALMP improvement events with norm <= tau (motifsets.py:105-117 stream)
@@ -1739,8 +1820,12 @@ int vlmp_finalize(vlmp_session* s) {
     }
     CU(cudaEventRecord(s->ev[4], st));
     FinArgs fa{s->d_tn, s->d_cum, s->d_cum2, s->d_acc, s->d_mp, s->d_ip, n, A, s->lmin, s->n_len, s->floor_};
+#ifdef VLMP_FINALIZE_GRID
     dim3 grid(blocks(n0, 128), s->n_len);
     k_finalize<<<grid, 128, 0, st>>>(fa);
+#else
+    k_finalize_walk<<<blocks(n0, 64), 64, 0, st>>>(fa);
+#endif
     ValmpArgs va{s->d_mp, s->d_ip, s->d_vdist, s->d_vnorm, s->d_vlen, s->d_vidx, s->d_vpop, n, A, s->lmin, s->n_len};
     k_valmp<<<blocks(n0, 256), 256, 0, st>>>(va);
     CU(cudaEventRecord(s->ev[5], st));
@@ -1856,6 +1941,49 @@ int vlmp_ranking_events(vlmp_session* s, double tau, int64_t cap, int64_t* ev_of
     }
     CU(cudaStreamSynchronize(st));
     *count = (int64_t)hc;
+    return 0;
+}
+
+int vlmp_range_query(vlmp_session* s, int64_t n_q, const int64_t* owners, const int32_t* lengths,
+                     const double* radii, int64_t cap, int64_t* members, int64_t* counts) {
+    if (!s || (n_q > 0 && (!owners || !lengths || !radii || !members || !counts)) || n_q < 0 || cap < 0)
+        return fail(VLMP_E_INVALID_PARAMETERS, "bad range query arguments");
+    if (s->n <= 0) return fail(VLMP_E_STATE, "no series uploaded");
+    if (n_q == 0) return 0;
+    long long max_n = 0;
+    for (long long q = 0; q < n_q; ++q) {
+        if (lengths[q] < 4 || lengths[q] > s->n || owners[q] < 0 || owners[q] > s->n - lengths[q])
+            return fail(VLMP_E_INVALID_PARAMETERS, "range query owner/length outside the series");
+        max_n = std::max<long long>(max_n, s->n - lengths[q] + 1);
+    }
+    std::lock_guard<std::mutex> g(s->lock);
+    CU(cudaSetDevice(s->device));
+    cudaStream_t st = s->stream;
+    const long long c = std::max<long long>(cap, 1);
+    long long* d_own = nullptr; int* d_len = nullptr; double* d_rad = nullptr;
+    long long* d_mem = nullptr; unsigned long long* d_cnt = nullptr;
+    CU(cudaMallocAsync((void**)&d_own, n_q * 8, st));
+    CU(cudaMallocAsync((void**)&d_len, n_q * 4, st));
+    CU(cudaMallocAsync((void**)&d_rad, n_q * 8, st));
+    CU(cudaMallocAsync((void**)&d_mem, n_q * c * 8, st));
+    CU(cudaMallocAsync((void**)&d_cnt, n_q * 8, st));
+    CU(cudaMemcpyAsync(d_own, owners, n_q * 8, cudaMemcpyHostToDevice, st));
+    CU(cudaMemcpyAsync(d_len, lengths, n_q * 4, cudaMemcpyHostToDevice, st));
+    CU(cudaMemcpyAsync(d_rad, radii, n_q * 8, cudaMemcpyHostToDevice, st));
+    CU(cudaMemsetAsync(d_cnt, 0, n_q * 8, st));
+    RangeArgs ra{s->d_tn, s->d_cum, s->d_cum2, d_own, d_len, d_rad, d_mem, d_cnt, c, s->n, s->floor_};
+    dim3 grid((unsigned)((max_n + 255) / 256), (unsigned)n_q);
+    k_range_query<<<grid, 256, 0, st>>>(ra);
+    CU(cudaGetLastError());
+    std::vector<unsigned long long> hc(n_q);
+    CU(cudaMemcpyAsync(hc.data(), d_cnt, n_q * 8, cudaMemcpyDeviceToHost, st));
+    if (cap > 0) CU(cudaMemcpyAsync(members, d_mem, n_q * cap * 8, cudaMemcpyDeviceToHost, st));
+    CU(cudaStreamSynchronize(st));
+    for (long long q = 0; q < n_q; ++q) counts[q] = (int64_t)hc[q];
+    cudaFreeAsync(d_own, st); cudaFreeAsync(d_len, st); cudaFreeAsync(d_rad, st);
+    cudaFreeAsync(d_mem, st); cudaFreeAsync(d_cnt, st);
+    CU(cudaStreamSynchronize(st));
+    s->stats[9] += 1;
     return 0;
 }
 

@@ -29,3 +29,6 @@ seriesmine.cli.topkm_discord_discovery = drop_in.topkm_discord_discovery
 # seriesmine.compute_matrix_profile itself stays the reference's (its own tests inspect
 # the VALMOD partial profiles, which the exhaustive GPU path does not build)
 seriesmine.cli.compute_matrix_profile = drop_in.compute_matrix_profile
+# motif-set expansion (motifsets.py:168-203): GPU range queries + the reference's admission rule
+seriesmine.compute_var_length_motif_sets = drop_in.compute_var_length_motif_sets
+seriesmine.cli.compute_var_length_motif_sets = drop_in.compute_var_length_motif_sets

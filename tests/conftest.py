@@ -30,3 +30,22 @@ def oracle_mod():
     from oracle import oracle
     oracle.load()
     return oracle
+
+
+MOTIFSET_CASES = ["cluster", "walk4"]
+MOTIFSET_RF = {"rf1em09": 1e-9, "rf2": 2.0, "rf4": 4.0}
+
+
+def golden_pairs(g):
+    """The reference ranking stored in a motif-set fixture, as RankedPair objects."""
+    from paper_2008_13447_b200.results import RankedPair
+    return [RankedPair(int(a), int(b), float(d), int(L), float(nm)) for a, b, L, d, nm in g["pairs"]]
+
+
+def golden_sets(g, tag):
+    """[(anchor, length, radius, members)] of a fixture's expanded sets."""
+    out, at = [], 0
+    for (a, b, L, f), r in zip(g[f"{tag}_head"], g[f"{tag}_radius"]):
+        out.append(((int(a), int(b)), int(L), float(r), g[f"{tag}_members"][at:at + f].tolist()))
+        at += f
+    return out

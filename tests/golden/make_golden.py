@@ -174,5 +174,31 @@ def small_m3():
         print("wrote m3", seed, flush=True)
 
 
+def motifsets():
+    """Motif sets (motifsets.py:168-203) from the reference's own rankings: the pairs and
+    the expanded sets, so the GPU expansion can be fed the identical ranking."""
+    from seriesmine.synthetic import planted_cluster_series
+    cases = [("cluster", planted_cluster_series(1800, 48, (200, 500, 800, 1100, 1400),
+                                                jitter=0.02, seed=0), 32, 48, 8, 40),
+             ("walk4", random_walk(900, seed=4), 16, 40, 5, 12)]
+    for name, values, lmin, lmax, p, K in cases:
+        t = sm.ingest(values)
+        ranking = PairRanking(K)
+        sm.valmod(t, lmin, lmax, p, ranking=ranking)
+        pairs = np.array([(q.off1, q.off2, q.length, q.distance, q.norm_distance) for q in ranking])
+        out = {"t": t.values, "lmin": lmin, "lmax": lmax, "pairs": pairs}
+        for rf in (1e-9, 2.0, 4.0):
+            sets = sm.compute_var_length_motif_sets(t, ranking, radius_factor=rf)
+            tag = f"rf{rf:g}".replace(".", "p").replace("-", "m")
+            out[f"{tag}_head"] = np.array([(s.anchor[0], s.anchor[1], s.length, s.frequency)
+                                           for s in sets], dtype=np.int64).reshape(-1, 4)
+            out[f"{tag}_radius"] = np.array([s.radius for s in sets])
+            out[f"{tag}_members"] = (np.concatenate([s.members for s in sets]) if sets
+                                     else np.zeros(0, dtype=np.int64))
+        np.savez_compressed(os.path.join(HERE, f"motifsets_{name}.npz"), **out)
+        print("wrote motifsets", name, flush=True)
+
+
 if __name__ == "__main__":
-    {"small": small, "small_m3": small_m3, "cfg1": cfg1, "cfg2": cfg2}[sys.argv[1]]()
+    {"small": small, "small_m3": small_m3, "cfg1": cfg1, "cfg2": cfg2,
+     "motifsets": motifsets}[sys.argv[1]]()

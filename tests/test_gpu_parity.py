@@ -310,3 +310,49 @@ def test_weak_bounds_fall_back_exactly(oracle_mod):
         res = vl.compute_matrix_profile(s, L, 5, m_track=3)
         _, _, bm, bmi = oracle_mod.profile_m(s, L, 3)
         assert np.array_equal(np.sort(res.best_m_nbr, axis=1), np.sort(bmi, axis=1)), L
+
+
+@pytest.mark.parametrize("name", ["cluster", "walk4"])
+def test_motif_sets_match_reference(name):
+    """compute_var_length_motif_sets with GPU range queries, fed the reference's own
+    ranking, reproduces the reference's sets (anchors, radius, members) exactly."""
+    from conftest import MOTIFSET_RF, golden_pairs, golden_sets
+    g = load_golden(f"motifsets_{name}")
+    s = vl.ingest(g["t"])
+    pairs = golden_pairs(g)
+    for tag, rf in MOTIFSET_RF.items():
+        sets = vl.compute_var_length_motif_sets(s, pairs, radius_factor=rf)
+        got = [(st.anchor, st.length, st.radius, st.members.tolist()) for st in sets]
+        assert got == golden_sets(g, tag), (name, tag)
+        assert vl.validate_disjoint(sets)
+
+
+def test_range_query_rows_against_oracle(oracle_mod):
+    """vlmp_range_query rows equal the oracle's full-row range queries (several lengths,
+    owners near both ends, radii around the row's own distance quantiles)."""
+    from paper_2008_13447_b200.motifsets import range_members
+    s = vl.ingest(np.cumsum(np.random.default_rng(41).standard_normal(3000)))
+    rng = np.random.default_rng(3)
+    owners, lengths, radii = [], [], []
+    for L in (16, 57, 200):
+        for o in (0, 1, 3000 - L, int(rng.integers(0, 3000 - L))):
+            for rad in (1.0, 3.0, 6.0):
+                owners.append(o); lengths.append(L); radii.append(rad * np.sqrt(L / 16.0))
+    rows = range_members(s, owners, lengths, radii)
+    for q in range(len(owners)):
+        want = oracle_mod.range_row(s, owners[q], lengths[q], radii[q])
+        assert np.array_equal(rows[q], want), (owners[q], lengths[q], radii[q])
+
+
+def test_planted_cluster_motif_set_end_to_end():
+    """GPU ranking (valmod) + GPU expansion on the reference's planted-cluster workload."""
+    from conftest import golden_sets
+    g = load_golden("motifsets_cluster")
+    s = vl.ingest(g["t"])
+    ranking = vl.PairRanking(10)
+    vl.valmod(s, 32, 48, 8, ranking=ranking)
+    sets = vl.compute_var_length_motif_sets(s, ranking, radius_factor=4.0)
+    top = sorted(map(int, sets[0].members))
+    assert sets[0].frequency == 5 and np.all(np.diff(top) == 300)   # the five planted copies
+    ref_top = golden_sets(g, "rf4")[0]                               # the reference's own run
+    assert (sets[0].anchor, sets[0].length, top) == (ref_top[0], ref_top[1], ref_top[3])

@@ -105,3 +105,23 @@ def test_oracle_m_th_discords_match_reference(seed, oracle_mod):
         fin = np.isfinite(g["k3m3_disc_dist"][L - 16])
         assert np.allclose(per[L][0][fin], g["k3m3_disc_dist"][L - 16][fin], atol=1e-7)
     assert np.array_equal(mo, g["k3m3_merged_off"]) and np.array_equal(ml, g["k3m3_merged_len"])
+
+
+@pytest.mark.parametrize("name", ["cluster", "walk4"])
+def test_motif_sets_oracle_rows_match_reference(name, oracle_mod):
+    """The oracle's full-row range query + the package's admission pass (host code)
+    reproduce the reference's compute_var_length_motif_sets on its own ranking."""
+    from conftest import MOTIFSET_RF, golden_pairs, golden_sets
+    from paper_2008_13447_b200.motifsets import expand_sets
+    g = load_golden(f"motifsets_{name}")
+    s = ingest(g["t"])
+    pairs = golden_pairs(g)
+    for tag, rf in MOTIFSET_RF.items():
+        rows = []
+        for p in pairs:
+            r = p.distance * rf
+            rows += [oracle_mod.range_row(s, p.off1, p.length, r),
+                     oracle_mod.range_row(s, p.off2, p.length, r)]
+        got = [(st.anchor, st.length, st.radius, st.members.tolist())
+               for st in expand_sets(pairs, rows, rf)]
+        assert got == golden_sets(g, tag), (name, tag)
