@@ -276,7 +276,7 @@ def run_ours(args):
     peak_dfma = sess.measure_fp64_peak()
     avg_tile_s = tile_ms * 1e-3 / args.steps
     achieved = W * 4 * 2 / avg_tile_s / 1e12          # TFLOP/s (2 flops per FMA-pipe instr)
-    peak = peak_dfma * 2 / 1e12
+    peak = peak_dfma * 2 / 1e12 * world            # aggregate over the N GPUs of the job
     prof_traffic = None
     tr_path = os.path.join(ROOT, "profiles", "tile_traffic.json")
     if os.path.exists(tr_path):
