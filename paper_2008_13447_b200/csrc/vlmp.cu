@@ -6,27 +6,34 @@
 // reference's per-length STOMP scan (profile.py:288-377) and its drivers
 // (valmod.py:192-289, discords.py:144-247). See DESIGN.md for the derivations.
 //
-// Layout and kernels (all FP64, CUDA cores; no tensor cores -- not a contraction):
+// Kernels (FP64 arithmetic on the CUDA cores; no tensor cores -- not a contraction):
 //   k_params      per length: window mean/std from the host's prefix sums with the
-//                 reference's exact op order (series.py:91-100), and the SCAMP-style
+//                 reference's exact op order (series.py:91-100) and the SCAMP-style
 //                 recurrence factors df, dg, inv = 1/(sigma*sqrt(m)) (NaN = invalid),
-//                 stored D-interleaved ("permuted") so a warp's per-lane column
-//                 streams are coalesced.
-//   k_bound       per length > first: an upper bound U[o] on offset o's exact key
-//                 r' = 1 - corr, from the previous length's neighbours (+margin).
-//   k_tile<FULL>  one warp = one tile: 256 consecutive diagonals x S rows. Each lane
-//                 owns D=8 diagonals, walks rows with the covariance recurrence
-//                 cov(i,j) = cov(i-1,j-1) + df_i dg_j + df_j dg_i   (2 DFMA)
-//                 r' = 1 - cov * inv_i * inv_j                     (DMUL + DFMA)
-//                 FULL=false: a cell only needs 2 FSETP against U's high word
-//                 (ALU pipe); the rare passing cells merge (key,index) exactly with
-//                 a 128-bit CAS. FULL=true (first length): exact folds with packed
-//                 8-bit diagonal indices, warp-reduced rows, lane-travelling columns.
-//                 Seeds (cov at the tile's first row) are extended to the next
-//                 length with the Welford co-moment update.
-//   k_finalize    exact canonical pair distance of each winner (series.py:169-194).
-//   k_valmp, k_smallest, k_discords, k_events: read-offs (valmod.py:57-73,170-177;
-//                 discords.py:68-93; motifsets.py:105-117).
+//                 a 32-byte struct per offset (natural order; two buffers ping-pong
+//                 so the bound can read the previous length's).
+//   k_bound2      per length > first: an upper bound U[o] on offset o's key
+//                 r = 1 - corr from the previous length's winners, O(1) per offset
+//                 (stored keys -> covariances, one diagonal step, Welford to length m).
+//   k_qprep       the filter's FP32 factors: b = sigma sqrt(m) 2^-k per offset and
+//                 a = q(U) b, q(U) = 1 - R(U) - 2^-20, windowed over a lane's 8 rows.
+//   k_tile<FULL>  one warp (one CTA) = one tile: 256 consecutive diagonals x S rows.
+//                 Each lane owns D=8 diagonals and walks rows with the recurrence
+//                 cov(i,j) = cov(i-1,j-1) + df_i dg_j + df_j dg_i   (2 DFMA per cell)
+//                 over a register ring of column factors rotated lane to lane.
+//                 FULL=false (filter): cell test hi(cov) >= hi(a_j b_i) (FMUL, LEA,
+//                 ISETP); a passing lane logs its row's 8 covariances. FULL=true
+//                 (first length, fallback, self-check): r = 1 - cov inv_i inv_j for
+//                 every cell, exact folds with packed diagonal indices, warp-reduced
+//                 rows, lane-travelling columns. Seeds (cov at each tile's first row)
+//                 are carried to the next length with the Welford co-moment update.
+//   k_log_merge   logged cells: bit-identical keys, exact row/column tests against U,
+//                 lexicographic (key, index) minimum by 128-bit CAS.
+//   k_finalize_walk  canonical pair distance of each winner (series.py:169-194).
+//   k_valmp, k_smallest, k_discords, k_events, k_range_query: read-offs
+//                 (valmod.py:57-73,170-177; discords.py:68-93; motifsets.py:105-165).
+//   m-best mode (m-th discords): k_bound_m, k_log_slots, k_select_m, k_recompute_m,
+//                 k_finalize_m, k_discords_m.
 
 #include <cuda_runtime.h>
 #include <stdint.h>
@@ -558,12 +565,10 @@ __device__ __forceinline__ void tile_body(const TileArgs& a, WarpSmem& w, int wi
                     const Prm f = w.fresh[b][kk];
                     cdf[q] = f.df; cdg[q] = f.dg; if (FULL) cinv[q] = f.inv;
                 }
-#ifndef VLMP_EXP_NOSHFL
                 const int src_lane = (lane + 1) & 31;
                 cdf[q] = __shfl_sync(FULLMASK, cdf[q], src_lane);
                 cdg[q] = __shfl_sync(FULLMASK, cdg[q], src_lane);
                 if (FULL) cinv[q] = __shfl_sync(FULLMASK, cinv[q], src_lane);
-#endif
                 if (!FULL) {
                     const float2 cq = w.cq[b][kk][lane];
                     cA[q] = fminf(cq.x, __fmul_rd(w.rq[b][kk].y, cq.y));
@@ -674,14 +679,7 @@ k_tile(TileArgs a) {
     const long long i0 = (long long)tl.y * a.S;
     const long long rows_valid = a.N - d0 - i0;
     if (rows_valid <= 0 || d0 + BAND - 1 < a.e) return;   // empty, or entirely trivial
-#ifdef VLMP_EXP_SKIPBAND0
-    if (!FULL && tl.x == 0) return;
-#endif
-#ifdef VLMP_EXP_NOFALLBACK
-    if (FULL) {
-#else
     if (FULL || (a.forced && *a.forced)) {
-#endif
         if (d0 < a.e) tile_body<true, true>(a, ws[wl], wid, lane, d0, i0, rows_valid);
         else tile_body<true, false>(a, ws[wl], wid, lane, d0, i0, rows_valid);
     } else {
@@ -801,23 +799,6 @@ struct FinArgs {
     long long n, A; int lmin, n_len; double floor_;
 };
 
-#ifdef VLMP_FINALIZE_GRID   // one thread per (length, offset): the full sum every time
-__global__ void k_finalize(FinArgs a) {
-    const long long o = blockIdx.x * (long long)blockDim.x + threadIdx.x;
-    const int li = blockIdx.y;
-    const int m = a.lmin + li;
-    const long long N = a.n - m + 1;
-    if (o >= N) return;
-    const ulonglong2 v = a.acc[(long long)li * a.A + o];
-    double d = INFINITY; int j = -1;
-    if (v.x != KEY_NONE) {
-        j = (int)v.y;
-        d = pair_distance(a.tn, a.cum, a.cum2, o, j, m, a.floor_);
-    }
-    a.mp[(long long)li * a.A + o] = d;
-    a.ip[(long long)li * a.A + o] = j;
-}
-#endif
 
 // Same values, one thread per offset walking the lengths upward: pair_distance's dot
 // product is a sequential left-to-right sum over k < m, so when an offset keeps the same
@@ -1820,12 +1801,7 @@ int vlmp_finalize(vlmp_session* s) {
     }
     CU(cudaEventRecord(s->ev[4], st));
     FinArgs fa{s->d_tn, s->d_cum, s->d_cum2, s->d_acc, s->d_mp, s->d_ip, n, A, s->lmin, s->n_len, s->floor_};
-#ifdef VLMP_FINALIZE_GRID
-    dim3 grid(blocks(n0, 128), s->n_len);
-    k_finalize<<<grid, 128, 0, st>>>(fa);
-#else
     k_finalize_walk<<<blocks(n0, 64), 64, 0, st>>>(fa);
-#endif
     ValmpArgs va{s->d_mp, s->d_ip, s->d_vdist, s->d_vnorm, s->d_vlen, s->d_vidx, s->d_vpop, n, A, s->lmin, s->n_len};
     k_valmp<<<blocks(n0, 256), 256, 0, st>>>(va);
     CU(cudaEventRecord(s->ev[5], st));
