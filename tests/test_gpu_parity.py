@@ -356,3 +356,24 @@ def test_planted_cluster_motif_set_end_to_end():
     assert sets[0].frequency == 5 and np.all(np.diff(top) == 300)   # the five planted copies
     ref_top = golden_sets(g, "rf4")[0]                               # the reference's own run
     assert (sets[0].anchor, sets[0].length, top) == (ref_top[0], ref_top[1], ref_top[3])
+
+
+@pytest.mark.parametrize("scale", [1e-12, 1e-3, 1e6, 1e15])
+def test_series_scale_invariance_against_oracle(scale, oracle_mod):
+    """The filter's FP32 factors carry a per-series power-of-two scale (hi-word bias):
+    profiles at extreme magnitudes still equal the oracle's exactly (indices) and use
+    the filtered path (no full-fold fallback)."""
+    t = scale * np.cumsum(np.random.default_rng(19).standard_normal(2500))
+    s = vl.ingest(t)
+    lmin, lmax = 24, 40
+    run = api.GpuRun(s, lmin, lmax)
+    assert run.stats["fallback_lengths"] == 0 and run.stats["exact_redo"] == 0
+    ref = oracle_mod.run(s, lmin, lmax, k_discord=2, keep_profiles=True)
+    for L in range(lmin, lmax + 1):
+        mp, ip = run.profile(L)
+        omp, oip = ref["profiles"][L]
+        assert np.array_equal(ip, oip), (scale, L)
+        fin = np.isfinite(omp)
+        assert np.allclose(mp[fin], omp[fin], rtol=1e-7, atol=1e-9)
+    d, o = run.discords(2)
+    assert np.array_equal(o, ref["disc_off"])
