@@ -48,13 +48,19 @@ def _check_profile_length(series, length: int):
     """profile.py:346-355 (the scan at the first length performs these checks)."""
     if length < 4 or 2 * length > series.n:
         raise E.SeriesTooShortError(f"need 4 <= length <= n/2 (length={length}, n={series.n})")
-    mu, sd = _moving_sd(series, length)
-    if not (sd >= series.sigma_floor).any():
-        raise E.AllConstantError(f"every window of length {length} is constant")
+    # any non-constant window will do: a short prefix first, the whole series only when
+    # that prefix is entirely constant
+    for span in (min(series.n, length + 4096), series.n):
+        _, sd = _moving_sd(series, length, span)
+        if (sd >= series.sigma_floor).any():
+            return
+    raise E.AllConstantError(f"every window of length {length} is constant")
 
 
-def _moving_sd(series, length):
+def _moving_sd(series, length, span=None):
     cum, cum2 = series._cum, series._cum2
+    if span is not None:
+        cum, cum2 = cum[:span + 1], cum2[:span + 1]
     s = cum[length:] - cum[:-length]
     ss = cum2[length:] - cum2[:-length]
     mu = s / length
@@ -292,16 +298,26 @@ def mine(series, lmin: int, lmax: int, k_motif: int = 1, k_discord: int = 1, *,
 
 
 def _topk_from_rows(run: GpuRun, k: int):
+    """Per length, the k best distinct canonical pairs (min, max) among the 2k smallest
+    rows, keyed (d, a, b) (motifsets.py:78-95 semantics, BASELINE.md decision 1);
+    vectorised over lengths."""
     off, nbr, d = run.smallest_rows(2 * k)
+    nl, K = off.shape
+    valid = np.cumprod((off >= 0) & np.isfinite(d), axis=1).astype(bool)   # rows stop at the first gap
+    li = np.broadcast_to(np.arange(nl)[:, None], (nl, K))[valid]
+    a = np.minimum(off, nbr)[valid]
+    b = np.maximum(off, nbr)[valid]
+    dv = d[valid]
+    o = np.lexsort((dv, b, a, li))                         # per (length, pair): best distance first
+    li, a, b, dv = li[o], a[o], b[o], dv[o]
+    first = np.ones(li.shape[0], dtype=bool)
+    first[1:] = (li[1:] != li[:-1]) | (a[1:] != a[:-1]) | (b[1:] != b[:-1])
+    li, a, b, dv = li[first], a[first], b[first], dv[first]
+    o = np.lexsort((b, a, dv, li))                         # per length: (d, a, b) ascending
+    li, a, b, dv = li[o], a[o], b[o], dv[o]
+    starts = np.searchsorted(li, np.arange(nl + 1))
     out = {}
-    for li in range(run.lmax - run.lmin + 1):
-        best = {}
-        for q in range(off.shape[1]):
-            if off[li, q] < 0 or not np.isfinite(d[li, q]):
-                break
-            a, b = sorted((int(off[li, q]), int(nbr[li, q])))
-            if (a, b) not in best or d[li, q] < best[(a, b)]:
-                best[(a, b)] = float(d[li, q])
-        items = sorted(((dv, a, b) for (a, b), dv in best.items()))
-        out[run.lmin + li] = [(a, b, dv) for dv, a, b in items[:k]]
+    for q in range(nl):
+        lo, hi = starts[q], min(starts[q + 1], starts[q] + k)
+        out[run.lmin + q] = [(int(x), int(y), float(z)) for x, y, z in zip(a[lo:hi], b[lo:hi], dv[lo:hi])]
     return out
