@@ -187,7 +187,7 @@ def run_ours(args):
 
     def step():
         if world > 1:
-            distributed.profile_sharded(sess, s, c.lmin, c.lmax, rank, world, group, upload=False)
+            distributed.profile_length_sharded(sess, s, c.lmin, c.lmax, rank, world, group, upload=False)
         else:
             with sess.lock:
                 sess.profile(c.lmin, c.lmax, 0, -1, 0)
@@ -234,7 +234,7 @@ def run_ours(args):
         import torch.distributed as dist
 
         def e2e_step():
-            distributed.profile_sharded(sess, s, c.lmin, c.lmax, rank, world, group, upload=True)
+            distributed.profile_length_sharded(sess, s, c.lmin, c.lmax, rank, world, group, upload=True)
             with sess.lock:
                 rows = sess.smallest_rows(k2)
                 disc = sess.discords(kd)
@@ -253,7 +253,7 @@ def run_ours(args):
         e2e_line = {"value": W / e2e_s, "unit": UNIT,
                     "h2d_bytes_per_step": int(8 * (s.n + 2 * (s.n + 1))),
                     "d2h_bytes_per_step": int(n0 * 33 + nl * (k2 * 24 + kd * 16)),
-                    "ms_per_step": e2e_s * 1e3, "api": "distributed.profile_sharded + session read-offs"}
+                    "ms_per_step": e2e_s * 1e3, "api": "distributed.profile_length_sharded + session read-offs"}
     if rank == 0 and world == 1:
         from paper_2008_13447_b200 import mine
         for _ in range(2):
@@ -294,7 +294,7 @@ def run_ours(args):
         "scaling": "strong", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
         "config": {"workload": f"config {args.config}: {c.note}", "n": c.n, "lmin": c.lmin,
                    "lmax": c.lmax, "k_motif": c.k_motif, "k_discord": c.k_discord,
-                   "W_updates": W, "parallelism": f"diagonal bands x{world}",
+                   "W_updates": W, "parallelism": f"length shards x{world}",
                    "l2": "working set (series + per-length params, 2.6 MB) is L2-resident by design; "
                          "no flush: the kernel is FP64-bound, not memory-bound"},
         "roofline": {"bound": "fp64_fma", "achieved": achieved, "peak": peak, "unit": "TFLOP/s",

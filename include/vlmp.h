@@ -67,6 +67,17 @@ int vlmp_set_series(vlmp_session* s, const double* t, const double* cum,
 int vlmp_profile_range(vlmp_session* s, int32_t lmin, int32_t lmax,
                        int64_t band_lo, int64_t band_hi, uint32_t flags);
 
+/*
+ * Length shard for multi-GPU runs: phase 1 for length indices li_lo..li_hi of
+ * [lmin, lmax] (all bands). Seeds are carried from lmin to li_lo by the tile kernel's
+ * own Welford step (bit-identical to a single run), li_lo is walked with full folds,
+ * later lengths are filtered; accumulators of other lengths stay empty, so an
+ * all-reduce MIN of the partials (vlmp_partials_*) over the shards reproduces the
+ * single-GPU partials exactly.
+ */
+int vlmp_profile_lengths(vlmp_session* s, int32_t lmin, int32_t lmax, int32_t li_lo, int32_t li_hi,
+                         uint32_t flags);
+
 /* Number of 256-diagonal bands and a work-balanced contiguous split of them. */
 int vlmp_band_count(vlmp_session* s, int32_t lmin, int64_t* n_bands);
 int vlmp_band_split(vlmp_session* s, int32_t lmin, int32_t lmax, int32_t parts,

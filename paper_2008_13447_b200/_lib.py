@@ -24,6 +24,7 @@ SIGNATURES = {
     "vlmp_last_error": (C.c_char_p, []),
     "vlmp_set_series": (C.c_int, [C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p, C.c_int64, C.c_double]),
     "vlmp_profile_range": (C.c_int, [C.c_void_p, C.c_int32, C.c_int32, C.c_int64, C.c_int64, C.c_uint32]),
+    "vlmp_profile_lengths": (C.c_int, [C.c_void_p, C.c_int32, C.c_int32, C.c_int32, C.c_int32, C.c_uint32]),
     "vlmp_band_count": (C.c_int, [C.c_void_p, C.c_int32, _c_int64_p]),
     "vlmp_band_split": (C.c_int, [C.c_void_p, C.c_int32, C.c_int32, C.c_int32, C.c_void_p]),
     "vlmp_partials_size": (C.c_int, [C.c_void_p, _c_int64_p, _c_int64_p]),
@@ -112,6 +113,11 @@ class Session:
         self._check(self.lib.vlmp_set_series(self.h, _ptr(t), _ptr(c1), _ptr(c2), t.shape[0],
                                              float(sigma_floor)))
         self.n = int(t.shape[0])
+
+    def profile_lengths(self, lmin, lmax, li_lo, li_hi, flags=0):
+        self._check(self.lib.vlmp_profile_lengths(self.h, int(lmin), int(lmax), int(li_lo), int(li_hi),
+                                                  int(flags)))
+        self.lmin, self.lmax = int(lmin), int(lmax)
 
     def profile(self, lmin, lmax, band_lo=0, band_hi=-1, flags=0):
         self._check(self.lib.vlmp_profile_range(self.h, int(lmin), int(lmax), int(band_lo),

@@ -780,6 +780,23 @@ __global__ void k_seed_init(SeedArgs a) {
     for (int s = 0; s < D; ++s) sp[s] = acc[s];
 }
 
+// carry every tile's seeds from length m to m+1 without walking the tile: the tile kernel's
+// own Welford step, same expressions (bit-identical), for lengths a length shard skips
+__global__ void k_seed_step(SeedArgs a) {
+    const int lane = threadIdx.x & 31;
+    const int wid = blockIdx.x * WARPS_PER_CTA + (threadIdx.x >> 5);
+    if (wid >= a.n_tiles) return;
+    const int2 tl = a.tiles[wid];
+    const long long d0 = a.dlo + (long long)tl.x * BAND;
+    const long long i0 = (long long)tl.y * a.S;
+    const long long cbase = i0 + d0 + lane * D;
+    const double wgt = (double)a.m / (double)(a.m + 1);
+    const double xi = (a.tn[i0 + a.m] - a.mu[i0]) * wgt;
+    double* seedp = a.seeds + (long long)wid * BAND + lane * D;
+#pragma unroll
+    for (int s = 0; s < D; ++s) seedp[s] = fma(xi, a.tn[cbase + s + a.m] - a.mu[cbase + s], seedp[s]);
+}
+
 __global__ void k_fill_acc(ulonglong2* acc, long long n) {
     long long o = blockIdx.x * (long long)blockDim.x + threadIdx.x;
     if (o < n) acc[o] = make_ulonglong2(KEY_NONE, (unsigned long long)IDX_NONE);
@@ -1578,8 +1595,12 @@ int vlmp_band_split(vlmp_session* s, int32_t lmin, int32_t lmax, int32_t parts, 
     return 0;
 }
 
+// Lengths li_lo..li_hi (indices into [lmin, lmax]) of bands [band_lo, band_hi): a length
+// shard starts with a full-fold pass at li_lo on seeds carried there from lmin (bit-identical
+// to the single-run chain); accumulators of other lengths stay empty.
 static int profile_impl(vlmp_session* s, int32_t lmin, int32_t lmax, int64_t band_lo,
-                        int64_t band_hi, uint32_t flags, bool* overflow_out) {
+                        int64_t band_hi, uint32_t flags, bool* overflow_out, int li_lo = 0,
+                        int li_hi = -1) {
     CU(cudaSetDevice(s->device));
     cudaStream_t st = s->stream;
     const long long n = s->n, A = s->A;
@@ -1620,7 +1641,11 @@ static int profile_impl(vlmp_session* s, int32_t lmin, int32_t lmax, int64_t ban
 
     double executed = 0, launches = 0, n_filtered = 0, n_full = 0, tile_ms = 0, klaunch = 2;
     const double margin = 1.0 / (1 << 26);
-    for (int li = 0; li < n_len; ++li) {
+    if (li_lo < 0) li_lo = 0;
+    if (li_hi >= n_len || (li_hi < 0 && li_lo == 0)) li_hi = n_len - 1;   // default: every length
+    if (li_hi < li_lo) li_hi = -1;                                        // empty shard: no work
+    std::vector<int> timed;   // lengths whose tile pass ran (event pairs)
+    for (int li = 0; li <= li_hi; ++li) {
         const int m = lmin + li;
         const long long N = n - m + 1;
         const int e = (m + 1) / 2;
@@ -1632,11 +1657,19 @@ static int profile_impl(vlmp_session* s, int32_t lmin, int32_t lmax, int64_t ban
         ParamArgs pa{s->d_tn, s->d_cum, s->d_cum2, prm, mu, n, N, A, m, s->floor_};
         k_params<<<blocks(A, 256), 256, 0, st>>>(pa);
         ++klaunch;
-        const bool full = (li == 0) || (flags & VLMP_F_FULL_EVERY_LENGTH);
+        const bool full = (li == li_lo) || (flags & VLMP_F_FULL_EVERY_LENGTH);
         if (li == 0 && T) {
             SeedArgs sa{s->d_tn, mu, s->d_tiles, s->d_seeds, dl, (int)T, S, m};
             k_seed_init<<<blocks(T * 32, WARPS_PER_CTA * 32), WARPS_PER_CTA * 32, 0, st>>>(sa);
             ++klaunch;
+        }
+        if (li < li_lo) {   // before this shard's lengths: only the seeds move on
+            if (T) {
+                SeedArgs sa{s->d_tn, mu, s->d_tiles, s->d_seeds, dl, (int)T, S, m};
+                k_seed_step<<<blocks(T * 32, WARPS_PER_CTA * 32), WARPS_PER_CTA * 32, 0, st>>>(sa);
+                ++klaunch;
+            }
+            continue;
         }
         if (!full) {
             Bound2Args ba{s->d_tn, prm, prm_prev, mu_prev, mu, s->d_acc + (long long)(li - 1) * A, prm,
@@ -1649,11 +1682,12 @@ static int profile_impl(vlmp_session* s, int32_t lmin, int32_t lmax, int64_t ban
         while (s->lev.size() < (size_t)2 * (li + 1)) {
             cudaEvent_t ev; CU(cudaEventCreate(&ev)); s->lev.push_back(ev);
         }
+        timed.push_back(li);
         CU(cudaEventRecord(s->lev[2 * li], st));
         if (T) {
             TileArgs ta{prm, mu, s->d_tn, s->d_tiles, s->d_seeds, s->d_acc + (long long)li * A,
                         s->d_counters, s->d_log, s->d_logcnt + li, (long long)s->log_cap,
-                        N, dl, (int)T, S, m, e, li + 1 < n_len,
+                        N, dl, (int)T, S, m, e, li + 1 <= li_hi,
                         s->d_colq, s->d_rowq, s->d_forced + li, s->hiC};
             if (full) k_tile<true><<<blocks(T, WARPS_PER_CTA), WARPS_PER_CTA * 32, smem, st>>>(ta);
             else {
@@ -1677,10 +1711,10 @@ static int profile_impl(vlmp_session* s, int32_t lmin, int32_t lmax, int64_t ban
     CU(cudaEventRecord(s->ev[1], st));
     CU(cudaEventSynchronize(s->ev[1]));
     double first_ms = 0;
-    for (int li = 0; li < n_len; ++li) {
+    for (int li : timed) {
         float lm = 0; CU(cudaEventElapsedTime(&lm, s->lev[2 * li], s->lev[2 * li + 1]));
         tile_ms += lm;
-        if (li == 0) first_ms = lm;
+        if (li == li_lo) first_ms = lm;
     }
     float ms = 0; CU(cudaEventElapsedTime(&ms, s->ev[0], s->ev[1]));
     unsigned long long cnt[8];
@@ -1732,6 +1766,27 @@ int vlmp_profile_range(vlmp_session* s, int32_t lmin, int32_t lmax, int64_t band
     if (rc == 0 && overflow) {
         // candidates were dropped (pathological bounds): exact full folds at every length
         rc = profile_impl(s, lmin, lmax, band_lo, band_hi, flags | VLMP_F_FULL_EVERY_LENGTH, &overflow);
+        s->stats[13] = 1;
+    }
+    return rc;
+}
+
+int vlmp_profile_lengths(vlmp_session* s, int32_t lmin, int32_t lmax, int32_t li_lo, int32_t li_hi,
+                         uint32_t flags) {
+    if (!s) return fail(VLMP_E_INVALID_PARAMETERS, "null session");
+    if (s->n <= 0) return fail(VLMP_E_STATE, "no series uploaded");
+    if (lmin > lmax) return fail(VLMP_E_INVALID_PARAMETERS, "lmin > lmax");
+    if (lmin < 4) return fail(VLMP_E_INVALID_PARAMETERS, "minimum window length is 4");
+    if (li_lo < 0 || li_hi < li_lo - 1 || li_hi > lmax - lmin)   // li_hi = li_lo - 1: empty shard
+        return fail(VLMP_E_INVALID_PARAMETERS, "length shard outside [0, lmax - lmin]");
+    if (s->n < (long long)lmax + (lmax + 1) / 2)
+        return fail(VLMP_E_SERIES_TOO_SHORT, "series cannot host a non-trivial pair at lmax");
+    std::lock_guard<std::mutex> g(s->lock);
+    bool overflow = false;
+    if (li_hi < li_lo) { li_lo = lmax - lmin + 1; li_hi = -1; }   // empty shard: setup only
+    int rc = profile_impl(s, lmin, lmax, 0, -1, flags, &overflow, li_lo, li_hi);
+    if (rc == 0 && overflow) {
+        rc = profile_impl(s, lmin, lmax, 0, -1, flags | VLMP_F_FULL_EVERY_LENGTH, &overflow, li_lo, li_hi);
         s->stats[13] = 1;
     }
     return rc;

@@ -1,5 +1,16 @@
-"""Multi-GPU sharding: one process per GPU, diagonal bands split by work,
-per-(length, offset) minima merged exactly with two NCCL MIN all-reduces.
+"""Multi-GPU sharding: one process per GPU; per-(length, offset) minima merged exactly with
+two NCCL MIN all-reduces.
+
+Length shards (default, `profile_length_sharded`). Each rank owns a contiguous run of
+lengths of equal work and computes the complete profile of those lengths on its GPU, with
+no exchange while it runs: its seeds are carried from lmin to its first length by the
+tile kernel's own Welford step (bit-identical to a single run), its first length is
+walked with full folds (the filter needs the previous length's winners), the rest are
+filtered. Every length's whole triangle runs on one GPU, so every GPU stays fully
+occupied at any world size. The partials of the other lengths stay empty, and the MIN
+merge below reproduces the single-GPU partials bit for bit.
+
+Band shards (`profile_sharded`), kept for very long lengths ranges per GPU:
 
 Partition. The pair triangle at length l holds cells (i, i+d), d >= ceil(l/2).
 Bands of 256 consecutive diagonals are the unit (one warp tile wide); band b's
@@ -64,6 +75,39 @@ def band_split(n: int, lmin: int, lmax: int, parts: int) -> np.ndarray:
     return cuts
 
 
+def length_work(n: int, m: int) -> float:
+    """Non-trivial pairs at length m: (N - e)(N - e + 1) / 2."""
+    k = (n - m + 1) - (m + 1) // 2
+    return k * (k + 1) / 2.0 if k > 0 else 0.0
+
+
+# a shard's first length is walked with full folds: ~1.6x a filtered length (config 2)
+FULL_PASS_FACTOR = 1.6
+
+
+def length_split(n: int, lmin: int, lmax: int, parts: int) -> np.ndarray:
+    """Contiguous length-index cuts [c_r, c_{r+1}) of [0, lmax - lmin + 1) with equal work,
+    each shard's first (full-fold) length counted at FULL_PASS_FACTOR; cuts are placed at
+    the nearest length boundary. More shards than lengths leave the extra shards empty."""
+    nl = lmax - lmin + 1
+    w = np.array([length_work(n, lmin + li) for li in range(nl)])
+    extra = (FULL_PASS_FACTOR - 1.0) * (w.mean() if nl else 0.0)
+    live = max(1, min(parts, nl))
+    target = (w.sum() + live * extra) / live
+    cuts = [0]
+    acc = extra
+    for li in range(nl):
+        if len(cuts) < live and li > cuts[-1] and acc + w[li] / 2.0 > target \
+                and nl - li >= live - len(cuts):
+            cuts.append(li)
+            acc = extra
+        acc += w[li]
+    while len(cuts) < live:
+        cuts.append(cuts[-1] + 1)
+    cuts += [nl] * (parts + 1 - len(cuts))
+    return np.array(cuts, dtype=np.int64)
+
+
 def merge_partials(keys, idx, group=None):
     """Exact (key, smallest idx) merge of torch int64 tensors across the group,
     in place. Works for any backend (NCCL on GPU tensors, gloo on CPU tensors)."""
@@ -75,6 +119,43 @@ def merge_partials(keys, idx, group=None):
     dist.all_reduce(idx, op=dist.ReduceOp.MIN, group=group)
     keys.copy_(merged)
     return keys, idx
+
+
+def _exchange_and_finalize(sess, rank, world, group):
+    import torch
+    with sess.lock:
+        n_len, stride = sess.partials_size()
+        dev = torch.device("cuda", sess.device)
+        keys = torch.empty(n_len * stride, dtype=torch.int64, device=dev)
+        idx = torch.empty(n_len * stride, dtype=torch.int64, device=dev)
+        sess.partials_export(keys.data_ptr(), idx.data_ptr())
+    if world > 1:
+        import torch.distributed as dist
+        merged = keys.clone()
+        dist.all_reduce(merged, op=dist.ReduceOp.MIN, group=group)
+        torch.cuda.synchronize(dev)
+        with sess.lock:
+            sess.partials_mask_idx(merged.data_ptr(), keys.data_ptr(), idx.data_ptr())
+        dist.all_reduce(idx, op=dist.ReduceOp.MIN, group=group)
+        torch.cuda.synchronize(dev)
+        keys = merged
+    with sess.lock:
+        sess.partials_import(keys.data_ptr(), idx.data_ptr())
+        sess.finalize()
+
+
+def profile_length_sharded(sess, series, lmin: int, lmax: int, rank: int, world: int, group=None,
+                           upload: bool = True):
+    """This rank's lengths on its session's device, then the exact merge and finalize.
+    ``upload=False`` reuses the series already resident on the device."""
+    cuts = length_split(series.n, lmin, lmax, world)
+    with sess.lock:
+        if upload:
+            sess.set_series(series.values, series._cum, series._cum2, series.sigma_floor)
+        # an empty shard (more ranks than lengths) still joins the merge with empty partials
+        sess.profile_lengths(lmin, lmax, int(cuts[rank]), int(cuts[rank + 1]) - 1)
+    _exchange_and_finalize(sess, rank, world, group)
+    return cuts
 
 
 def profile_sharded(sess, series, lmin: int, lmax: int, rank: int, world: int, group=None,

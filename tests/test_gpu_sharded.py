@@ -20,7 +20,7 @@ def _free_port():
     return p
 
 
-def _rank(rank, world, port, t, lmin, lmax, out):
+def _rank(rank, world, port, t, lmin, lmax, out, mode="bands"):
     import torch
     import torch.distributed as dist
     os.environ["MASTER_ADDR"] = "127.0.0.1"
@@ -30,7 +30,10 @@ def _rank(rank, world, port, t, lmin, lmax, out):
         from paper_2008_13447_b200 import _lib, distributed, ingest
         s = ingest(t)
         sess = _lib.Session(0)
-        distributed.profile_sharded(sess, s, lmin, lmax, rank, world)
+        if mode == "lengths":
+            distributed.profile_length_sharded(sess, s, lmin, lmax, rank, world)
+        else:
+            distributed.profile_sharded(sess, s, lmin, lmax, rank, world)
         d, nm, ln, ix, pop = sess.valmp_arrays()
         off, nbr, dd = sess.smallest_rows(4)
         disc_d, disc_o = sess.discords(3)
@@ -42,14 +45,12 @@ def _rank(rank, world, port, t, lmin, lmax, out):
         dist.destroy_process_group()
 
 
-def test_two_ranks_equal_single(tmp_path):
+def _sharded_equals_single(tmp_path, world, mode, t, lmin, lmax):
     import torch.multiprocessing as mp
     from paper_2008_13447_b200 import _lib, ingest
-    t = np.cumsum(np.random.default_rng(44).standard_normal(6000))
-    lmin, lmax = 48, 64
-    out = str(tmp_path / "sharded.npz")
-    mp.start_processes(_rank, args=(2, _free_port(), t, lmin, lmax, out), nprocs=2, join=True,
-                       start_method="spawn")
+    out = str(tmp_path / f"sharded_{mode}_{world}.npz")
+    mp.start_processes(_rank, args=(world, _free_port(), t, lmin, lmax, out, mode), nprocs=world,
+                       join=True, start_method="spawn")
     got = np.load(out)
     sess = _lib.session(0)
     with sess.lock:
@@ -65,3 +66,17 @@ def test_two_ranks_equal_single(tmp_path):
     for a, b in zip(rows, [got["off"], got["nbr"], got["dd"]]):
         assert np.array_equal(a, b)
     assert np.array_equal(disc[1], got["disc_o"]) and np.array_equal(disc[0], got["disc_d"])
+
+
+def test_two_ranks_equal_single(tmp_path):
+    """Band shards: bit-identical to one process."""
+    t = np.cumsum(np.random.default_rng(44).standard_normal(6000))
+    _sharded_equals_single(tmp_path, 2, "bands", t, 48, 64)
+
+
+@pytest.mark.parametrize("world", [2, 3])
+def test_length_shards_equal_single(tmp_path, world):
+    """Length shards (each rank: seeds carried to its first length, a full-fold pass, then
+    filtered lengths): bit-identical to one process."""
+    t = np.cumsum(np.random.default_rng(45).standard_normal(6000))
+    _sharded_equals_single(tmp_path, world, "lengths", t, 48, 64)

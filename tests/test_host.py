@@ -161,3 +161,17 @@ def test_band_split_balances_work():
     w = [sum(distributed.band_work(65536, 256, 384, b) for b in range(cuts[p], cuts[p + 1]))
          for p in range(4)]
     assert max(w) / min(w) < 1.05
+
+
+def test_length_split_balances_and_covers():
+    from paper_2008_13447_b200 import distributed as D
+    for n, lmin, lmax in ((65536, 256, 384), (1 << 22, 1000, 1256), (6000, 48, 64)):
+        nl = lmax - lmin + 1
+        for parts in (1, 2, 3, 4, 8):
+            c = D.length_split(n, lmin, lmax, parts)
+            assert len(c) == parts + 1 and c[0] == 0 and c[-1] == nl and np.all(np.diff(c) >= 1)
+            if nl >= 16 * parts:   # enough lengths per shard for the granularity to even out
+                w = [sum(D.length_work(n, lmin + li) for li in range(c[p], c[p + 1])) for p in range(parts)]
+                assert max(w) / min(w) < 1.1
+    c = D.length_split(100, 10, 12, 8)          # more ranks than lengths: empty tail shards
+    assert c.tolist() == [0, 1, 2, 3, 3, 3, 3, 3, 3]
