@@ -353,32 +353,41 @@ __device__ inline void cp_async_commit() { asm volatile("cp.async.commit_group;\
 __device__ inline void cp_async_wait_all() { asm volatile("cp.async.wait_group 0;\n" ::: "memory"); }
 
 
-constexpr int UCS = 34;      // padded cq row: conflict-free (D = 8) / 2-way (D = 10, 12) staging writes
+// Staging groups of GR rows. Over a group, lane L's ring receives columns
+// c0 + D*L + kk (kk < GR, c0 = r0 + d0 + D - 1): NCOL = 31 D + GR distinct columns, staged
+// once each (coalesced) into a linear buffer with one pad slot per 8 entries, so lane L's
+// read of entry D*L + kk is bank-conflict free (D = 8: word 18 L + 2 kk' spans 32 banks).
+#ifndef VLMP_GR
+#define VLMP_GR 8
+#endif
+constexpr int GR = VLMP_GR;
+static_assert(GR % D == 0 && GR <= 16, "a group must return the ring to its phase; 2 GR row halves <= 32 lanes");
+constexpr int NCOL = 31 * D + GR;
+__host__ __device__ constexpr int cpad(int f) { return f + (f >> 3); }
+constexpr int CQN = cpad(NCOL - 1) + 1;
 struct WarpSmem {
-    Prm fresh[2][D];         // the column entering lane 31's slot D-1 at each row of a group
-    Prm row[2][D];           // the group's row parameters
-    float2 rq[2][D];         // filter: the group's row factors
-    float2 cq[2][D][UCS];    // filter: factors of the column entering lane L's ring at row kk
+    Prm fresh[2][GR];        // the column entering lane 31's slot D-1 at each row of a group
+    Prm row[2][GR];          // the group's row parameters
+    float2 rq[2][GR];        // filter: the group's row factors
+    float2 cq[2][CQN];       // filter: factors of the columns entering the lanes' rings (padded)
 };
 
 // Per-group staging by cp.async, planned once per tile: every lane's global source advances
-// by a fixed stride per D-row group and its shared destination alternates between two
+// by a fixed stride per GR-row group and its shared destination alternates between two
 // buffers, so a group costs a few LDGSTS with immediate offsets and a few adds.
-//   row structs / fresh columns: lane l < 2D copies half l%2 of row r0 + l/2 and of the fresh
-//     column r0 + l/2 + d0 + BAND-1 that enters lane 31 at row r0 + l/2;
-//   filter row factors (b_i, q(Uwin_i)) of rows r0..r0+D-1: lanes < D/2, 16 B each;
-//   filter column factors: lane L at row r0+kk receives column r0 + d0 + D-1 + (D*L + kk);
-//     entry f = lane + 32k (coalesced reads) goes to cq[f % D][f / D] (conflict-free reads by
-//     lane). f % D repeats with period P = D / gcd(D, 32) in k, f / D then advances by 32P/D,
-//     so P destination bases per group plus immediate offsets cover all D entries.
+//   row structs / fresh columns: GR rows, two 16-B halves each, plus the fresh column
+//     r0 + q + d0 + BAND-1 that enters lane 31 at row r0 + q;
+//   filter row factors of rows r0..r0+GR-1: 16-B chunks, lanes < GR/2;
+//   filter column factors: the NCOL entering columns, entry f = lane + 32k (coalesced) to
+//     cq[cpad(f)] = per-lane base + 36 k entries.
 struct StagePlan {
-    const char* src_pr; const char* src_fr; unsigned dst_pr, dst_fr;   // +D*32 B per group
-    const char* src_rq; unsigned dst_rq;      // rowq (+8D B per group), lanes < D/2
-    const char* src_cq; unsigned dst_cq;      // colq (+8D B per group)
+    const char* src_pr; const char* src_fr; unsigned dst_pr, dst_fr;   // +GR*32 B per group
+    const char* src_rq; unsigned dst_rq;      // rowq (+8 GR B per group), lanes < GR/2
+    const char* src_cq; unsigned dst_cq;      // colq (+8 GR B per group)
 };
-constexpr unsigned PR_BUF = sizeof(Prm) * D;             // fresh[b] / row[b] stride
-constexpr unsigned RQ_BUF = sizeof(float2) * D;
-constexpr unsigned CQ_BUF = sizeof(float2) * D * UCS;
+constexpr unsigned PR_BUF = sizeof(Prm) * GR;            // fresh[b] / row[b] stride
+constexpr unsigned RQ_BUF = sizeof(float2) * GR;
+constexpr unsigned CQ_BUF = sizeof(float2) * CQN;
 
 template <int OFF_D, int OFF_S, int BYTES>
 __device__ __forceinline__ void cp_async_imm(unsigned d, const char* s) {
@@ -392,57 +401,45 @@ template <bool FILTER>
 __device__ __forceinline__ StagePlan make_plan(WarpSmem& w, const TileArgs& a, long long i0, long long d0,
                                                int lane) {
     StagePlan p;
-    const int q = (lane >> 1) % D, half = lane & 1;
+    const int q = (lane >> 1) % GR, half = lane & 1;
     p.src_pr = reinterpret_cast<const char*>(a.prm + i0 + q) + 16 * half;
     p.src_fr = reinterpret_cast<const char*>(a.prm + i0 + q + d0 + BAND - 1) + 16 * half;
     p.dst_pr = (unsigned)__cvta_generic_to_shared(&w.row[0][q]) + 16 * half;
     p.dst_fr = (unsigned)__cvta_generic_to_shared(&w.fresh[0][q]) + 16 * half;
-    if (4 * D <= 32 && lane >= 16) { p.src_pr = p.src_fr; p.dst_pr = p.dst_fr; }   // one instruction
+    if (4 * GR <= 32 && lane >= 16) { p.src_pr = p.src_fr; p.dst_pr = p.dst_fr; }   // one instruction
     if (FILTER) {
-        const int r2 = lane % (D / 2);
+        const int r2 = lane % (GR / 2);
         p.src_rq = reinterpret_cast<const char*>(a.rowq + i0 + 2 * r2);
         p.dst_rq = (unsigned)__cvta_generic_to_shared(&w.rq[0][2 * r2]);
         p.src_cq = reinterpret_cast<const char*>(a.colq + i0 + d0 + D - 1 + lane);
-        p.dst_cq = (unsigned)__cvta_generic_to_shared(&w.cq[0][0][0]);
+        p.dst_cq = (unsigned)__cvta_generic_to_shared(&w.cq[0][cpad(lane)]);
     }
     return p;
 }
 
-constexpr int gcd_c(int a, int b) { return b == 0 ? a : gcd_c(b, a % b); }
-constexpr int CQ_P = D / gcd_c(D, 32);        // period of (lane + 32k) % D in k
-constexpr int CQ_STEPL = 32 * CQ_P / D;       // f / D advance per period
-
-template <int M>
-__device__ __forceinline__ void stage_cq_run(unsigned d, const char* sc) {
-    if constexpr (M < D / CQ_P) {
-        cp_async_imm<M * CQ_STEPL * 8, M * CQ_P * 256, 8>(d, sc);
-        stage_cq_run<M + 1>(d, sc);
-    }
-}
-
-template <int R>
+template <int K>
 __device__ __forceinline__ void stage_cq(unsigned dc, const char* sc, int lane) {
-    if constexpr (R < CQ_P) {
-        const int f = lane + 32 * R;
-        stage_cq_run<0>(dc + (unsigned)(((f % D) * UCS + f / D) * 8), sc + 256 * R);
-        stage_cq<R + 1>(dc, sc, lane);
+    if constexpr (32 * K < NCOL) {
+        // entry f = lane + 32 K lands at cpad(f) = cpad(lane) + 36 K (lane + 32 K keeps lane's low bits)
+        if (32 * (K + 1) <= NCOL || lane + 32 * K < NCOL) cp_async_imm<K * 36 * 8, K * 256, 8>(dc, sc);
+        stage_cq<K + 1>(dc, sc, lane);
     }
 }
 
-// stage group g (rows i0 + D*g ..) into buffer b
+// stage group g (rows i0 + GR*g ..) into buffer b
 template <bool FILTER>
 __device__ __forceinline__ void stage(const StagePlan& p, int g, int b, int lane) {
     const unsigned bsel = (unsigned)b;
-    const long long gs = (long long)g * (D * sizeof(Prm));
-    if constexpr (4 * D <= 32) {   // one instruction: lanes < 2D rows, lanes >= 16 fresh columns
-        if ((lane & 15) < 2 * D) cp_async_imm<0, 0, 16>(p.dst_pr + bsel * PR_BUF, p.src_pr + gs);
-    } else if (lane < 2 * D) {
+    const long long gs = (long long)g * (GR * sizeof(Prm));
+    if constexpr (4 * GR <= 32) {   // one instruction: lanes < 2GR rows, lanes >= 16 fresh columns
+        if ((lane & 15) < 2 * GR) cp_async_imm<0, 0, 16>(p.dst_pr + bsel * PR_BUF, p.src_pr + gs);
+    } else if (lane < 2 * GR) {
         cp_async_imm<0, 0, 16>(p.dst_pr + bsel * PR_BUF, p.src_pr + gs);
         cp_async_imm<0, 0, 16>(p.dst_fr + bsel * PR_BUF, p.src_fr + gs);
     }
     if (FILTER) {
-        if (lane < D / 2) cp_async_imm<0, 0, 16>(p.dst_rq + bsel * RQ_BUF, p.src_rq + (long long)g * (D * 8));
-        stage_cq<0>(p.dst_cq + bsel * CQ_BUF, p.src_cq + (long long)g * (D * 8), lane);
+        if (lane < GR / 2) cp_async_imm<0, 0, 16>(p.dst_rq + bsel * RQ_BUF, p.src_rq + (long long)g * (GR * 8));
+        stage_cq<0>(p.dst_cq + bsel * CQ_BUF, p.src_cq + (long long)g * (GR * 8), lane);
     }
     cp_async_commit();
 }
@@ -529,7 +526,7 @@ __device__ __forceinline__ void tile_body(const TileArgs& a, WarpSmem& w, int wi
 
     const int S = a.S;
     const int nrows = (int)(rows_valid < S ? rows_valid : S);
-    const int ngroups = (nrows + D - 1) / D;
+    const int ngroups = (nrows + GR - 1) / GR;
 
     auto flush_full = [&]() {
         if (rowres < INFINITY) {
@@ -553,8 +550,8 @@ __device__ __forceinline__ void tile_body(const TileArgs& a, WarpSmem& w, int wi
         const int b = g & 1;
         if (g + 1 < ngroups) stage<!FULL>(plan, g + 1, b ^ 1, lane);
 #pragma unroll
-        for (int kk = 0; kk < D; ++kk) {
-            const long long i = i0 + (long long)g * D + kk;
+        for (int kk = 0; kk < GR; ++kk) {
+            const long long i = i0 + (long long)g * GR + kk;
             const Prm pr = w.row[b][kk];
             {   // ring rotation: phys (kk-1) mod D receives lane+1's outgoing column
                 const int q = (kk + D - 1) % D;
@@ -570,7 +567,7 @@ __device__ __forceinline__ void tile_body(const TileArgs& a, WarpSmem& w, int wi
                 cdg[q] = __shfl_sync(FULLMASK, cdg[q], src_lane);
                 if (FULL) cinv[q] = __shfl_sync(FULLMASK, cinv[q], src_lane);
                 if (!FULL) {
-                    const float2 cq = w.cq[b][kk][lane];
+                    const float2 cq = w.cq[b][cpad(dbase + kk)];
                     cA[q] = fminf(cq.x, __fmul_rd(w.rq[b][kk].y, cq.y));
                 }
             }
@@ -621,31 +618,31 @@ __device__ __forceinline__ void tile_body(const TileArgs& a, WarpSmem& w, int wi
                     rm = o < rm ? o : rm;
                 }
                 // the exiting column (logical slot 0, phys kk) travels to lane-1's slot D-1
-                const double x = colacc[kk];
+                const double x = colacc[kk % D];
                 double y = __shfl_down_sync(FULLMASK, x, 1);
                 if (lane == 31) y = INFINITY;
-                colacc[kk] = y;
+                colacc[kk % D] = y;
                 const double x0 = __shfl_sync(FULLMASK, x, 0);   // lane 0's exiting column
                 const int slot = (int)((i - i0) & 31);
                 if (lane == slot) { rowres = rm; rowres_i = i; colres = x0; colres_j = i + d0; }
-                if (32 % D != 0 && slot == 31) flush_full();   // every lane holds a stashed row
+                if (32 % GR != 0 && slot == 31) flush_full();   // every lane holds a stashed row
             }
-            if (kk + 1 < D && lane == 0) {
+            if (kk + 1 < GR && lane == 0) {
                 // slot 0's column (phys kk) is dead after this row: lane 0 fetches the next row's
                 // fresh column into it now, so the next rotation's shuffles need not wait
                 const Prm f = w.fresh[b][kk + 1];
-                cdf[kk] = f.df; cdg[kk] = f.dg; if (FULL) cinv[kk] = f.inv;
+                cdf[kk % D] = f.df; cdg[kk % D] = f.dg; if (FULL) cinv[kk % D] = f.inv;
             }
         }
-        if (FULL && 32 % D == 0 && ((g + 1) * D) % 32 == 0) flush_full();   // 32 rows stashed
+        if (FULL && 32 % GR == 0 && ((g + 1) * GR) % 32 == 0) flush_full();   // 32 rows stashed
         cp_async_wait_all();
         __syncwarp();
     }
     if (FULL) {
         flush_full();
         // after the last row (kk = D-1) and its rotate, phys p holds the column of logical
-        // slot p at row i_end = i0 + 8*ngroups
-        const long long i_end = i0 + (long long)ngroups * D;
+        // slot p at row i_end = i0 + GR*ngroups (GR is a multiple of D)
+        const long long i_end = i0 + (long long)ngroups * GR;
 #pragma unroll
         for (int p = 0; p < D; ++p) {
             const double v = colacc[p];
@@ -658,7 +655,7 @@ __device__ __forceinline__ void tile_body(const TileArgs& a, WarpSmem& w, int wi
         }
     } else {
         if (pass_prev) {
-            log_one(a, i0 + (long long)ngroups * D - 1, i0 + (long long)ngroups * D - 1 + d0 + dbase, cov);
+            log_one(a, i0 + (long long)ngroups * GR - 1, i0 + (long long)ngroups * GR - 1 + d0 + dbase, cov);
             ++nslow;
         }
         if (nslow) atomicAdd(a.counters + 2, nslow);
@@ -1454,7 +1451,7 @@ void order_tiles(std::vector<int2>& tiles, long long N0, long long dl, int S) {
 }
 
 int seg_rows(long long n) {
-    // S = G*D rows per tile (whole 8-row groups); larger for longer series to bound the
+    // S = G*D rows per tile (whole GR-row groups); larger for longer series to bound the
     // number of tiles and the seed store (config 5: S = 16384, ~1.1M tiles, 2.2 GB of seeds)
 #ifndef VLMP_SEG_G0
 #define VLMP_SEG_G0 128
