@@ -104,6 +104,16 @@ int vlmp_partials_import(vlmp_session* s, const void* keys, const void* idx);
  */
 int vlmp_finalize(vlmp_session* s);
 
+/*
+ * Phase 2 split for length shards: profile values of length indices li_lo..li_hi only
+ * ((+inf, -1) for the others, neutral for a MIN / MAX all-reduce), the device buffers
+ * MP [n_len][stride] (double) and IP [n_len][stride] (int32) for the collective, then
+ * the read-off state (VALMP fold) from whatever the buffers hold.
+ */
+int vlmp_finalize_lengths(vlmp_session* s, int32_t li_lo, int32_t li_hi);
+int vlmp_final_buffers(vlmp_session* s, void** mp, void** ip, int64_t* n_len, int64_t* stride);
+int vlmp_finalize_readoffs(vlmp_session* s);
+
 /* Read-offs (all after vlmp_finalize). */
 int vlmp_get_valmp(vlmp_session* s, double* dist, double* norm, int64_t* lengths,
                    int64_t* indices, uint8_t* populated /* n - lmin + 1 each */);

@@ -32,6 +32,10 @@ SIGNATURES = {
     "vlmp_partials_mask_idx": (C.c_int, [C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p]),
     "vlmp_partials_import": (C.c_int, [C.c_void_p, C.c_void_p, C.c_void_p]),
     "vlmp_finalize": (C.c_int, [C.c_void_p]),
+    "vlmp_finalize_lengths": (C.c_int, [C.c_void_p, C.c_int32, C.c_int32]),
+    "vlmp_final_buffers": (C.c_int, [C.c_void_p, C.POINTER(C.c_void_p), C.POINTER(C.c_void_p), _c_int64_p,
+                                     _c_int64_p]),
+    "vlmp_finalize_readoffs": (C.c_int, [C.c_void_p]),
     "vlmp_get_valmp": (C.c_int, [C.c_void_p] + [C.c_void_p] * 5),
     "vlmp_get_profile": (C.c_int, [C.c_void_p, C.c_int32, C.c_void_p, C.c_void_p]),
     "vlmp_smallest_rows": (C.c_int, [C.c_void_p, C.c_int32, C.c_void_p, C.c_void_p, C.c_void_p]),
@@ -146,6 +150,19 @@ class Session:
 
     def finalize(self):
         self._check(self.lib.vlmp_finalize(self.h))
+
+    def finalize_lengths(self, li_lo, li_hi):
+        self._check(self.lib.vlmp_finalize_lengths(self.h, int(li_lo), int(li_hi)))
+
+    def final_buffers(self):
+        """(mp_ptr, ip_ptr, n_len, stride): device buffers of the finalized values."""
+        mp, ip = C.c_void_p(), C.c_void_p()
+        nl, st = C.c_int64(), C.c_int64()
+        self._check(self.lib.vlmp_final_buffers(self.h, C.byref(mp), C.byref(ip), C.byref(nl), C.byref(st)))
+        return mp.value, ip.value, nl.value, st.value
+
+    def finalize_readoffs(self):
+        self._check(self.lib.vlmp_finalize_readoffs(self.h))
 
     # -- read-offs -------------------------------------------------------------
     def valmp_arrays(self):

@@ -811,6 +811,7 @@ struct FinArgs {
     const ulonglong2* acc;      // [n_len][A]
     double* mp; int* ip;        // [n_len][A]
     long long n, A; int lmin, n_len; double floor_;
+    int li_lo, li_hi;           // lengths finalized here; others get (+inf, -1) (length shards)
 };
 
 
@@ -826,6 +827,11 @@ __global__ void k_finalize_walk(FinArgs a) {
     for (int li = 0; li < a.n_len; ++li) {
         const int m = a.lmin + li;
         if (o > a.n - m) break;
+        if (li < a.li_lo || li > a.li_hi) {   // another shard's length: neutral for MIN / MAX
+            a.mp[(long long)li * a.A + o] = INFINITY;
+            a.ip[(long long)li * a.A + o] = -1;
+            continue;
+        }
         const ulonglong2 v = a.acc[(long long)li * a.A + o];
         double d = INFINITY; int j = -1;
         if (v.x != KEY_NONE) {
@@ -1401,7 +1407,7 @@ struct vlmp_session {
     double* d_mpm = nullptr; size_t mpm_cap = 0;
     long long* d_redo = nullptr; size_t redo_cap = 0;
     // run state
-    int lmin = 0, lmax = 0, n_len = 0; bool have_profile = false, have_final = false;
+    int lmin = 0, lmax = 0, n_len = 0; bool have_profile = false, have_final = false, have_finals = false;
     double stats[16] = {};
     std::vector<cudaEvent_t> lev;   // 2 per length: tile-kernel start/stop
 };
@@ -1565,7 +1571,7 @@ int vlmp_set_series(vlmp_session* s, const double* t, const double* cum, const d
     CU(cudaMemcpyAsync(s->d_cum, cum, (n + 1) * sizeof(double), cudaMemcpyHostToDevice, s->stream));
     CU(cudaMemcpyAsync(s->d_cum2, cum2, (n + 1) * sizeof(double), cudaMemcpyHostToDevice, s->stream));
     CU(cudaStreamSynchronize(s->stream));
-    s->have_profile = s->have_final = false;
+    s->have_profile = s->have_final = s->have_finals = false;
     return 0;
 }
 
@@ -1739,7 +1745,7 @@ static int profile_impl(vlmp_session* s, int32_t lmin, int32_t lmax, int64_t ban
         if (k > 0) W += (double)k * (double)(k + 1) / 2.0;
     }
     s->lmin = lmin; s->lmax = lmax; s->n_len = n_len;
-    s->have_profile = true; s->have_final = false;
+    s->have_profile = true; s->have_final = false; s->have_finals = false;
     memset(s->stats, 0, sizeof(s->stats));
     s->stats[0] = ms; s->stats[2] = executed; s->stats[3] = W; s->stats[4] = tile_ms;
     s->stats[5] = launches; s->stats[6] = n_filtered; s->stats[7] = n_full; s->stats[8] = (double)cnt[0];
@@ -1829,9 +1835,7 @@ int vlmp_partials_import(vlmp_session* s, const void* keys, const void* idx) {
     return 0;
 }
 
-int vlmp_finalize(vlmp_session* s) {
-    if (!s || !s->have_profile) return fail(VLMP_E_STATE, "no profile run");
-    std::lock_guard<std::mutex> g(s->lock);
+static int finalize_impl(vlmp_session* s, int li_lo, int li_hi, bool readoffs) {
     CU(cudaSetDevice(s->device));
     cudaStream_t st = s->stream;
     const long long A = s->A, n = s->n;
@@ -1852,18 +1856,52 @@ int vlmp_finalize(vlmp_session* s) {
         s->v_cap = n0;
     }
     CU(cudaEventRecord(s->ev[4], st));
-    FinArgs fa{s->d_tn, s->d_cum, s->d_cum2, s->d_acc, s->d_mp, s->d_ip, n, A, s->lmin, s->n_len, s->floor_};
-    k_finalize_walk<<<blocks(n0, 64), 64, 0, st>>>(fa);
-    ValmpArgs va{s->d_mp, s->d_ip, s->d_vdist, s->d_vnorm, s->d_vlen, s->d_vidx, s->d_vpop, n, A, s->lmin, s->n_len};
-    k_valmp<<<blocks(n0, 256), 256, 0, st>>>(va);
+    if (li_lo <= li_hi) {
+        FinArgs fa{s->d_tn, s->d_cum, s->d_cum2, s->d_acc, s->d_mp, s->d_ip, n, A, s->lmin, s->n_len, s->floor_,
+                   li_lo, li_hi};
+        k_finalize_walk<<<blocks(n0, 64), 64, 0, st>>>(fa);
+        s->stats[9] += 1;
+    }
+    if (readoffs) {
+        ValmpArgs va{s->d_mp, s->d_ip, s->d_vdist, s->d_vnorm, s->d_vlen, s->d_vidx, s->d_vpop, n, A, s->lmin, s->n_len};
+        k_valmp<<<blocks(n0, 256), 256, 0, st>>>(va);
+        s->stats[9] += 1;
+    }
     CU(cudaEventRecord(s->ev[5], st));
     CU(cudaGetLastError());
     CU(cudaEventSynchronize(s->ev[5]));
     float ms = 0; CU(cudaEventElapsedTime(&ms, s->ev[4], s->ev[5]));
     s->stats[1] = ms;
-    s->stats[9] += 2;
-    s->have_final = true;
+    s->have_final = readoffs;
+    s->have_finals = true;
     return 0;
+}
+
+int vlmp_finalize(vlmp_session* s) {
+    if (!s || !s->have_profile) return fail(VLMP_E_STATE, "no profile run");
+    std::lock_guard<std::mutex> g(s->lock);
+    return finalize_impl(s, 0, s->n_len - 1, true);
+}
+
+int vlmp_finalize_lengths(vlmp_session* s, int32_t li_lo, int32_t li_hi) {
+    if (!s || !s->have_profile) return fail(VLMP_E_STATE, "no profile run");
+    if (li_lo < 0 || li_hi < li_lo - 1 || li_hi >= s->n_len)
+        return fail(VLMP_E_INVALID_PARAMETERS, "length range outside the profiled range");
+    std::lock_guard<std::mutex> g(s->lock);
+    return finalize_impl(s, li_lo, li_hi, false);
+}
+
+int vlmp_final_buffers(vlmp_session* s, void** mp, void** ip, int64_t* n_len, int64_t* stride) {
+    if (!s || !s->have_finals) return fail(VLMP_E_STATE, "no finalized values");
+    if (!mp || !ip || !n_len || !stride) return fail(VLMP_E_INVALID_PARAMETERS, "null argument");
+    *mp = s->d_mp; *ip = s->d_ip; *n_len = s->n_len; *stride = s->A;
+    return 0;
+}
+
+int vlmp_finalize_readoffs(vlmp_session* s) {
+    if (!s || !s->have_finals) return fail(VLMP_E_STATE, "no finalized values");
+    std::lock_guard<std::mutex> g(s->lock);
+    return finalize_impl(s, 0, -1, true);
 }
 
 int vlmp_get_valmp(vlmp_session* s, double* dist, double* norm, int64_t* lengths, int64_t* indices,
@@ -2123,7 +2161,7 @@ int vlmp_profile_mbest(vlmp_session* s, int32_t lmin, int32_t lmax, int32_t mb) 
     CU(cudaGetLastError());
     CU(cudaStreamSynchronize(st));
     s->lmin = lmin; s->lmax = lmax; s->n_len = n_len; s->mbest = mb;
-    s->have_profile = false; s->have_final = false;
+    s->have_profile = false; s->have_final = false; s->have_finals = false;
     memset(s->stats, 0, sizeof(s->stats));
     s->stats[0] = ms; s->stats[13] = (double)redo_total;
     return 0;

@@ -144,17 +144,40 @@ def _exchange_and_finalize(sess, rank, world, group):
         sess.finalize()
 
 
+class _DeviceArray:
+    """__cuda_array_interface__ view of a library-owned device buffer (no copy)."""
+
+    def __init__(self, ptr, count, typestr):
+        self.__cuda_array_interface__ = {"shape": (count,), "typestr": typestr, "data": (ptr, False),
+                                         "version": 3, "strides": None}
+
+
 def profile_length_sharded(sess, series, lmin: int, lmax: int, rank: int, world: int, group=None,
                            upload: bool = True):
-    """This rank's lengths on its session's device, then the exact merge and finalize.
+    """This rank's lengths on its session's device, finalized there; the per-length profile
+    values are then combined across ranks (every (length, offset) is owned by exactly one
+    rank: MIN over distances, MAX over neighbours) and every rank builds the read-offs.
     ``upload=False`` reuses the series already resident on the device."""
+    import torch
     cuts = length_split(series.n, lmin, lmax, world)
+    lo, hi = int(cuts[rank]), int(cuts[rank + 1]) - 1
     with sess.lock:
         if upload:
             sess.set_series(series.values, series._cum, series._cum2, series.sigma_floor)
-        # an empty shard (more ranks than lengths) still joins the merge with empty partials
-        sess.profile_lengths(lmin, lmax, int(cuts[rank]), int(cuts[rank + 1]) - 1)
-    _exchange_and_finalize(sess, rank, world, group)
+        # an empty shard (more ranks than lengths) still joins with neutral values
+        sess.profile_lengths(lmin, lmax, lo, hi)
+        sess.finalize_lengths(lo, hi)
+    if world > 1:
+        import torch.distributed as dist
+        mp_ptr, ip_ptr, n_len, stride = sess.final_buffers()
+        dev = torch.device("cuda", sess.device)
+        mp = torch.as_tensor(_DeviceArray(mp_ptr, n_len * stride, "<f8"), device=dev)
+        ip = torch.as_tensor(_DeviceArray(ip_ptr, n_len * stride, "<i4"), device=dev)
+        dist.all_reduce(mp, op=dist.ReduceOp.MIN, group=group)
+        dist.all_reduce(ip, op=dist.ReduceOp.MAX, group=group)
+        torch.cuda.synchronize(dev)
+    with sess.lock:
+        sess.finalize_readoffs()
     return cuts
 
 
