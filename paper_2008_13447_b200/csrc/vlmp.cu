@@ -777,21 +777,34 @@ __global__ void k_seed_init(SeedArgs a) {
     for (int s = 0; s < D; ++s) sp[s] = acc[s];
 }
 
-// carry every tile's seeds from length m to m+1 without walking the tile: the tile kernel's
-// own Welford step, same expressions (bit-identical), for lengths a length shard skips
-__global__ void k_seed_step(SeedArgs a) {
+// Carry every tile's seeds from length m_from to m_to without walking the tiles (a length
+// shard's lengths before its first): the tile kernel's own Welford step per length, with
+// the means recomputed in k_params' arithmetic (win_stats) -- bit-identical seeds.
+__global__ void k_seed_forward(SeedArgs a, const double* __restrict__ cum, int m_to) {
     const int lane = threadIdx.x & 31;
-    const int wid = blockIdx.x * WARPS_PER_CTA + (threadIdx.x >> 5);
+    const int wid = (int)((blockIdx.x * (long long)blockDim.x + threadIdx.x) >> 5);
     if (wid >= a.n_tiles) return;
     const int2 tl = a.tiles[wid];
     const long long d0 = a.dlo + (long long)tl.x * BAND;
     const long long i0 = (long long)tl.y * a.S;
     const long long cbase = i0 + d0 + lane * D;
-    const double wgt = (double)a.m / (double)(a.m + 1);
-    const double xi = (a.tn[i0 + a.m] - a.mu[i0]) * wgt;
     double* seedp = a.seeds + (long long)wid * BAND + lane * D;
+    double sd[D];
 #pragma unroll
-    for (int s = 0; s < D; ++s) seedp[s] = fma(xi, a.tn[cbase + s + a.m] - a.mu[cbase + s], seedp[s]);
+    for (int s = 0; s < D; ++s) sd[s] = seedp[s];
+    for (int m = a.m; m < m_to; ++m) {
+        const double L = (double)m;
+        const double wgt = (double)m / (double)(m + 1);
+        const double mi = __ddiv_rn(__dsub_rn(cum[i0 + m], cum[i0]), L);
+        const double xi = (a.tn[i0 + m] - mi) * wgt;
+#pragma unroll
+        for (int s = 0; s < D; ++s) {
+            const double mc = __ddiv_rn(__dsub_rn(cum[cbase + s + m], cum[cbase + s]), L);
+            sd[s] = fma(xi, a.tn[cbase + s + m] - mc, sd[s]);
+        }
+    }
+#pragma unroll
+    for (int s = 0; s < D; ++s) seedp[s] = sd[s];
 }
 
 __global__ void k_fill_acc(ulonglong2* acc, long long n) {
@@ -1648,7 +1661,16 @@ static int profile_impl(vlmp_session* s, int32_t lmin, int32_t lmax, int64_t ban
     if (li_hi >= n_len || (li_hi < 0 && li_lo == 0)) li_hi = n_len - 1;   // default: every length
     if (li_hi < li_lo) li_hi = -1;                                        // empty shard: no work
     std::vector<int> timed;   // lengths whose tile pass ran (event pairs)
-    for (int li = 0; li <= li_hi; ++li) {
+    if (li_lo > 0 && li_lo <= li_hi && T) {
+        // a later length shard: seeds at lmin (direct sums), carried to its first length
+        ParamArgs pa{s->d_tn, s->d_cum, s->d_cum2, s->d_prm, s->d_mu, n, n - lmin + 1, A, lmin, s->floor_};
+        k_params<<<blocks(A, 256), 256, 0, st>>>(pa);
+        SeedArgs sa{s->d_tn, s->d_mu, s->d_tiles, s->d_seeds, dl, (int)T, S, lmin};
+        k_seed_init<<<blocks(T * 32, WARPS_PER_CTA * 32), WARPS_PER_CTA * 32, 0, st>>>(sa);
+        k_seed_forward<<<blocks(T * 32, 128), 128, 0, st>>>(sa, s->d_cum, lmin + li_lo);
+        klaunch += 3;
+    }
+    for (int li = (li_lo <= li_hi ? li_lo : 0); li <= li_hi; ++li) {
         const int m = lmin + li;
         const long long N = n - m + 1;
         const int e = (m + 1) / 2;
@@ -1665,14 +1687,6 @@ static int profile_impl(vlmp_session* s, int32_t lmin, int32_t lmax, int64_t ban
             SeedArgs sa{s->d_tn, mu, s->d_tiles, s->d_seeds, dl, (int)T, S, m};
             k_seed_init<<<blocks(T * 32, WARPS_PER_CTA * 32), WARPS_PER_CTA * 32, 0, st>>>(sa);
             ++klaunch;
-        }
-        if (li < li_lo) {   // before this shard's lengths: only the seeds move on
-            if (T) {
-                SeedArgs sa{s->d_tn, mu, s->d_tiles, s->d_seeds, dl, (int)T, S, m};
-                k_seed_step<<<blocks(T * 32, WARPS_PER_CTA * 32), WARPS_PER_CTA * 32, 0, st>>>(sa);
-                ++klaunch;
-            }
-            continue;
         }
         if (!full) {
             Bound2Args ba{s->d_tn, prm, prm_prev, mu_prev, mu, s->d_acc + (long long)(li - 1) * A, prm,

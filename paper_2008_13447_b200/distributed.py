@@ -4,7 +4,7 @@ two NCCL MIN all-reduces.
 Length shards (default, `profile_length_sharded`). Each rank owns a contiguous run of
 lengths of equal work and computes the complete profile of those lengths on its GPU, with
 no exchange while it runs: its seeds are carried from lmin to its first length by the
-tile kernel's own Welford step (bit-identical to a single run), its first length is
+tile kernel's own Welford step with the same arithmetic (bit-identical to a single run), its first length is
 walked with full folds (the filter needs the previous length's winners), the rest are
 filtered. Every length's whole triangle runs on one GPU, so every GPU stays fully
 occupied at any world size. The partials of the other lengths stay empty, and the MIN
