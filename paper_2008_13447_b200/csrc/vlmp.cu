@@ -38,6 +38,7 @@
 #include <cuda_runtime.h>
 #include <stdint.h>
 #include <stdio.h>
+#include <stdlib.h>
 #include <string.h>
 #include <math.h>
 
@@ -1657,6 +1658,10 @@ static int profile_impl(vlmp_session* s, int32_t lmin, int32_t lmax, int64_t ban
 
     double executed = 0, launches = 0, n_filtered = 0, n_full = 0, tile_ms = 0, klaunch = 2;
     const double margin = 1.0 / (1 << 26);
+    // VLMP_LOG_CAP (records) lowers the effective log capacity: a test hook that forces the
+    // overflow -> exact full-fold re-run path
+    long long eff_cap = (long long)s->log_cap;
+    if (const char* env = getenv("VLMP_LOG_CAP")) eff_cap = std::max(1LL, std::min(eff_cap, atoll(env)));
     if (li_lo < 0) li_lo = 0;
     if (li_hi >= n_len || (li_hi < 0 && li_lo == 0)) li_hi = n_len - 1;   // default: every length
     if (li_hi < li_lo) li_hi = -1;                                        // empty shard: no work
@@ -1703,13 +1708,13 @@ static int profile_impl(vlmp_session* s, int32_t lmin, int32_t lmax, int64_t ban
         CU(cudaEventRecord(s->lev[2 * li], st));
         if (T) {
             TileArgs ta{prm, mu, s->d_tn, s->d_tiles, s->d_seeds, s->d_acc + (long long)li * A,
-                        s->d_counters, s->d_log, s->d_logcnt + li, (long long)s->log_cap,
+                        s->d_counters, s->d_log, s->d_logcnt + li, eff_cap,
                         N, dl, (int)T, S, m, e, li + 1 <= li_hi,
                         s->d_colq, s->d_rowq, s->d_forced + li, s->hiC};
             if (full) k_tile<true><<<blocks(T, WARPS_PER_CTA), WARPS_PER_CTA * 32, smem, st>>>(ta);
             else {
                 k_tile<false><<<blocks(T, WARPS_PER_CTA), WARPS_PER_CTA * 32, smem, st>>>(ta);
-                k_log_merge<<<148 * 8, 256, 0, st>>>(s->d_log, s->d_logcnt + li, (long long)s->log_cap,
+                k_log_merge<<<148 * 8, 256, 0, st>>>(s->d_log, s->d_logcnt + li, eff_cap,
                                                      prm, e, s->d_acc + (long long)li * A, s->d_counters);
                 klaunch += 1;
             }
@@ -1741,7 +1746,7 @@ static int profile_impl(vlmp_session* s, int32_t lmin, int32_t lmax, int64_t ban
     {   // a candidate log that overflowed lost candidates: the caller redoes the run exactly
         std::vector<unsigned long long> lc(n_len);
         CU(cudaMemcpy(lc.data(), s->d_logcnt, n_len * sizeof(unsigned long long), cudaMemcpyDeviceToHost));
-        for (auto c : lc) { overflow |= c > s->log_cap; max_log = std::max(max_log, (double)c); }
+        for (auto c : lc) { overflow |= (long long)c > eff_cap; max_log = std::max(max_log, (double)c); }
     }
     int n_forced = 0;
     double n_fix = 0;

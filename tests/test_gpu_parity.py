@@ -377,3 +377,18 @@ def test_series_scale_invariance_against_oracle(scale, oracle_mod):
         assert np.allclose(mp[fin], omp[fin], rtol=1e-7, atol=1e-9)
     d, o = run.discords(2)
     assert np.array_equal(o, ref["disc_off"])
+
+
+def test_log_overflow_reruns_exactly(monkeypatch):
+    """A candidate log too small for a length (forced with the VLMP_LOG_CAP test hook) drops
+    candidates; the run is redone with full folds and the profiles equal the normal run."""
+    s = vl.ingest(np.cumsum(np.random.default_rng(23).standard_normal(3000)))
+    ref = api.GpuRun(s, 32, 48)
+    want = [ref.profile(L) for L in range(32, 49)]
+    assert ref.stats["exact_redo"] == 0
+    monkeypatch.setenv("VLMP_LOG_CAP", "16")
+    run = api.GpuRun(s, 32, 48)
+    assert run.stats["exact_redo"] == 1
+    for L, (mp, ip) in zip(range(32, 49), want):
+        got = run.profile(L)
+        assert np.array_equal(got[1], ip) and np.array_equal(got[0], mp), L
