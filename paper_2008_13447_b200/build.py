@@ -7,7 +7,9 @@ import subprocess
 
 HERE = os.path.dirname(os.path.abspath(__file__))
 ROOT = os.path.dirname(HERE)
-SRC = os.path.join(HERE, "csrc", "vlmp.cu")
+SRCS = [os.path.join(HERE, "csrc", f) for f in ("profile.cu", "readout.cu", "session.cu")]
+SRC = SRCS[0]   # the tile kernels (variant builds)
+HDRS = [os.path.join(HERE, "csrc", "vlmp_internal.cuh")]
 OUT = os.path.join(HERE, "libvlmp.so")
 
 NVCC_FLAGS = ["-gencode", "arch=compute_100a,code=sm_100a", "-O3", "-lineinfo", "-std=c++17",
@@ -22,10 +24,10 @@ def nvcc() -> str:
 
 
 def build(force: bool = False, verbose: bool = False) -> str:
-    deps = [SRC, os.path.join(ROOT, "include", "vlmp.h")]
+    deps = SRCS + HDRS + [os.path.join(ROOT, "include", "vlmp.h")]
     if not force and os.path.exists(OUT) and all(os.path.getmtime(OUT) >= os.path.getmtime(d) for d in deps):
         return OUT
-    cmd = [nvcc(), *NVCC_FLAGS, "-o", OUT, SRC]
+    cmd = [nvcc(), *NVCC_FLAGS, "-o", OUT, *SRCS]
     if verbose:
         cmd.insert(1, "-Xptxas=-v")
     subprocess.run(cmd, check=True)

@@ -1,4 +1,4 @@
-// vlmp.cu -- B200 (sm_100a) variable-length z-normalised matrix profile.
+// profile.cu -- B200 (sm_100a) variable-length z-normalised matrix profile, phase 1.
 //
 // Hot path of arxiv 2008.13447 (MAD/VALMOD), rebuilt for the GPU: the exact
 // matrix profile of one series at every window length in [lmin, lmax], from
@@ -35,111 +35,9 @@
 //   m-best mode (m-th discords): k_bound_m, k_log_slots, k_select_m, k_recompute_m,
 //                 k_finalize_m, k_discords_m.
 
-#include <cuda_runtime.h>
-#include <stdint.h>
-#include <stdio.h>
-#include <stdlib.h>
-#include <string.h>
-#include <math.h>
+#include "vlmp_internal.cuh"
 
-#include <algorithm>
-#include <mutex>
-#include <string>
-#include <vector>
-
-#include "../../include/vlmp.h"
-
-namespace {
-
-#ifndef VLMP_D
-#define VLMP_D 8
-#endif
-constexpr int D = VLMP_D;         // diagonals per lane (even, <= 16)
-constexpr int BAND = 32 * D;      // diagonals per warp tile
-constexpr int ceil_log2(int v) { int b = 0; while ((1 << b) < v) ++b; return b; }
-constexpr int PBITS = ceil_log2(BAND);   // packed local index bits (full-fold keys)
-constexpr int MG = 1 << ceil_log2(D);    // lanes per log record in k_log_merge
-static_assert(D % 2 == 0 && D <= 16, "D: even, at most 16");
-constexpr unsigned long long PMASK = (1ull << PBITS) - 1;
-#ifndef VLMP_WARPS_PER_CTA
-#define VLMP_WARPS_PER_CTA 1
-#endif
-#ifndef VLMP_FILTER_WARPS_PER_SM
-#define VLMP_FILTER_WARPS_PER_SM 20   // 96 registers
-#endif
-constexpr int WARPS_PER_CTA = VLMP_WARPS_PER_CTA;
-constexpr int FILTER_MIN_BLOCKS = VLMP_FILTER_WARPS_PER_SM / WARPS_PER_CTA;
-constexpr int FULL_MIN_BLOCKS = 16 / WARPS_PER_CTA;               // 128 registers
-constexpr unsigned FULLMASK = 0xffffffffu;
-constexpr unsigned long long KEY_NONE = 0x7FF0000000000000ull;   // bits of +inf
-constexpr long long IDX_NONE = 0x7FFFFFFFFFFFFFFFll;
-
-thread_local std::string g_err;
-
-int fail(int code, const std::string& msg) { g_err = msg; return code; }
-
-#define CU(call)                                                                   \
-    do {                                                                           \
-        cudaError_t e_ = (call);                                                   \
-        if (e_ != cudaSuccess)                                                     \
-            return fail(VLMP_E_CUDA, std::string(#call) + ": " + cudaGetErrorString(e_)); \
-    } while (0)
-
-
-// ---------------------------------------------------------------------------------
-// exact window statistics (series.py:91-100): no contraction, numpy op order
-__device__ inline void win_stats(const double* __restrict__ cum, const double* __restrict__ cum2,
-                                 long long o, int m, double& mu, double& sd) {
-    double s = __dsub_rn(cum[o + m], cum[o]);
-    double ss = __dsub_rn(cum2[o + m], cum2[o]);
-    double L = (double)m;
-    double u = __ddiv_rn(s, L);
-    double var = __dsub_rn(__ddiv_rn(ss, L), __dmul_rn(u, u));
-    if (!(var >= 0.0)) var = 0.0;
-    mu = u;
-    sd = __dsqrt_rn(var);
-}
-
-// series.py:81-89 (stats: sigma = sqrt(var) if var > 0 else 0) -- used by pair_distance
-__device__ inline void win_stats_pd(const double* __restrict__ cum, const double* __restrict__ cum2,
-                                    long long o, int m, double& mu, double& sd) {
-    double s = __dsub_rn(cum[o + m], cum[o]);
-    double ss = __dsub_rn(cum2[o + m], cum2[o]);
-    double L = (double)m;
-    double u = __ddiv_rn(s, L);
-    double var = __dsub_rn(__ddiv_rn(ss, L), __dmul_rn(u, u));
-    mu = u;
-    sd = var > 0.0 ? __dsqrt_rn(var) : 0.0;
-}
-
-// canonical pair distance (series.py:169-194): dot in (min,max) order, sequential sum
-__device__ double pair_distance(const double* __restrict__ t, const double* __restrict__ cum,
-                                const double* __restrict__ cum2, long long i, long long j, int m,
-                                double floor_) {
-    long long a = i <= j ? i : j, b = i <= j ? j : i;
-    double mua, sda, mub, sdb;
-    win_stats_pd(cum, cum2, a, m, mua, sda);
-    win_stats_pd(cum, cum2, b, m, mub, sdb);
-    if (sda < floor_ || sdb < floor_) return INFINITY;
-    double qt = 0.0;
-    for (int k = 0; k < m; ++k) qt = __dadd_rn(qt, __dmul_rn(t[a + k], t[b + k]));
-    double L = (double)m;
-    double num = __dsub_rn(qt, __dmul_rn(__dmul_rn(L, mua), mub));
-    double den = __dmul_rn(__dmul_rn(L, sda), sdb);
-    double rad = __dmul_rn(__dmul_rn(2.0, L), __dsub_rn(1.0, __ddiv_rn(num, den)));
-    return rad > 0.0 ? __dsqrt_rn(rad) : 0.0;
-}
-
-// ---------------------------------------------------------------------------------
-// Per-length window parameters, natural layout, 32-byte AoS so one warp-contiguous
-// run of offsets is a coalesced 1 KB read (and two 16-byte cp.async per entry).
-struct __align__(32) Prm {
-    double df;    // (t[o+m-1] - t[o-1]) / 2                       (0 at o = 0)
-    double dg;    // (t[o+m-1] - mu_o) + (t[o-1] - mu_{o-1})        (0 at o = 0)
-    double inv;   // 1 / (sigma_o sqrt(m)); NaN = invalid window (constant / past the end)
-    float U;      // bound on the offset's best key, high word as float (filter kernel)
-    float pad;
-};
+namespace vlmp_impl {
 
 struct ParamArgs {
     const double* tn; const double* cum; const double* cum2;
@@ -301,10 +199,6 @@ __global__ void k_qprep(const Prm* __restrict__ prm, float2* colq, float2* rowq,
 // ---------------------------------------------------------------------------------
 struct Cand { int o; int idx; unsigned long long key; };   // candidate (offset, neighbour, key)
 
-// A filter-kernel log record: a lane whose cells passed the bound at row i; its 8 cells are
-// (i, j0 + s) and cov[s] is their covariance, so the merge kernel can recompute the exact
-// keys with the kernel's own FMA sequence (bit-identical) and apply the exact tests.
-struct __align__(16) RowRec { int i; int j0; int pad0, pad1; double cov[D]; };
 
 struct TileArgs {
     const Prm* prm; const double* mu; const double* tn;
@@ -819,270 +713,6 @@ __global__ void k_acc_idx(const ulonglong2* acc, long long* idx, long long n) {
     if (o < n) { ulonglong2 v = acc[o]; idx[o] = v.x == KEY_NONE ? -1 : (long long)v.y; }
 }
 
-// ---------------------------------------------------------------------------------
-struct FinArgs {
-    const double* tn; const double* cum; const double* cum2;
-    const ulonglong2* acc;      // [n_len][A]
-    double* mp; int* ip;        // [n_len][A]
-    long long n, A; int lmin, n_len; double floor_;
-    int li_lo, li_hi;           // lengths finalized here; others get (+inf, -1) (length shards)
-};
-
-
-// Same values, one thread per offset walking the lengths upward: pair_distance's dot
-// product is a sequential left-to-right sum over k < m, so when an offset keeps the same
-// canonical pair (a, b) from length m-1 to m its sum at m is the sum at m-1 plus one term
-// -- bit-identical to recomputing it. Only neighbour changes pay the O(m) sum.
-__global__ void k_finalize_walk(FinArgs a) {
-    const long long o = blockIdx.x * (long long)blockDim.x + threadIdx.x;
-    if (o >= a.n - a.lmin + 1) return;
-    long long pa = -1, pb = -1; int pm = -1;
-    double qt = 0.0;
-    for (int li = 0; li < a.n_len; ++li) {
-        const int m = a.lmin + li;
-        if (o > a.n - m) break;
-        if (li < a.li_lo || li > a.li_hi) {   // another shard's length: neutral for MIN / MAX
-            a.mp[(long long)li * a.A + o] = INFINITY;
-            a.ip[(long long)li * a.A + o] = -1;
-            continue;
-        }
-        const ulonglong2 v = a.acc[(long long)li * a.A + o];
-        double d = INFINITY; int j = -1;
-        if (v.x != KEY_NONE) {
-            j = (int)v.y;
-            const long long lo = o <= j ? o : j, hi = o <= j ? j : o;
-            double mua, sda, mub, sdb;
-            win_stats_pd(a.cum, a.cum2, lo, m, mua, sda);
-            win_stats_pd(a.cum, a.cum2, hi, m, mub, sdb);
-            if (lo == pa && hi == pb && m == pm + 1) {
-                qt = __dadd_rn(qt, __dmul_rn(a.tn[lo + m - 1], a.tn[hi + m - 1]));
-            } else {
-                qt = 0.0;
-#pragma unroll 8
-                for (int k = 0; k < m; ++k) qt = __dadd_rn(qt, __dmul_rn(a.tn[lo + k], a.tn[hi + k]));
-            }
-            pa = lo; pb = hi; pm = m;
-            if (sda >= a.floor_ && sdb >= a.floor_) {
-                const double L = (double)m;
-                const double num = __dsub_rn(qt, __dmul_rn(__dmul_rn(L, mua), mub));
-                const double den = __dmul_rn(__dmul_rn(L, sda), sdb);
-                const double rad = __dmul_rn(__dmul_rn(2.0, L), __dsub_rn(1.0, __ddiv_rn(num, den)));
-                d = rad > 0.0 ? __dsqrt_rn(rad) : 0.0;
-            }
-        }
-        a.mp[(long long)li * a.A + o] = d;
-        a.ip[(long long)li * a.A + o] = j;
-    }
-}
-
-struct ValmpArgs {
-    const double* mp; const int* ip;
-    double* dist; double* norm; long long* len; long long* idx; unsigned char* pop;
-    long long n, A; int lmin, n_len;
-};
-
-// valmod.py:57-73: lnorm = mp * sqrt(1/length); strict improvement, ascending lengths
-__global__ void k_valmp(ValmpArgs a) {
-    const long long o = blockIdx.x * (long long)blockDim.x + threadIdx.x;
-    const long long n0 = a.n - a.lmin + 1;
-    if (o >= n0) return;
-    double bd = INFINITY, bn = INFINITY; long long bl = 0, bi = -1; bool pop = false;
-    for (int li = 0; li < a.n_len; ++li) {
-        const int m = a.lmin + li;
-        if (o > a.n - m) break;
-        const double mpv = a.mp[(long long)li * a.A + o];
-        const double ln = __dmul_rn(mpv, __dsqrt_rn(__ddiv_rn(1.0, (double)m)));
-        if (ln < INFINITY && (!pop || bn > ln)) {
-            bd = mpv; bn = ln; bl = m; bi = a.ip[(long long)li * a.A + o]; pop = true;
-        }
-    }
-    a.dist[o] = bd; a.norm[o] = bn; a.len[o] = bl; a.idx[o] = bi; a.pop[o] = pop ? 1 : 0;
-}
-
-// per length: the K smallest (mp, offset) rows (K <= 64), block-wide selection
-struct SmallArgs {
-    const double* mp; const int* ip; long long* off; long long* nbr; double* d;
-    long long n, A; int lmin, K;
-};
-
-__device__ inline bool row_less(double d1, long long o1, double d2, long long o2) {
-    return d1 < d2 || (d1 == d2 && o1 < o2);
-}
-
-__global__ void k_smallest(SmallArgs a) {
-    constexpr int T = 256, KMAX = 64;
-    const int li = blockIdx.x;
-    const int m = a.lmin + li;
-    const long long N = a.n - m + 1;
-    const double* mp = a.mp + (long long)li * a.A;
-    // each thread: local sorted list of K
-    double ld[KMAX]; long long lo[KMAX];
-    const int K = a.K;
-    for (int q = 0; q < K; ++q) { ld[q] = INFINITY; lo[q] = -1; }
-    for (long long o = threadIdx.x; o < N; o += T) {
-        const double v = mp[o];
-        if (!(v < INFINITY)) continue;
-        if (!row_less(v, o, ld[K - 1], lo[K - 1] < 0 ? (1ll << 62) : lo[K - 1])) continue;
-        int q = K - 1;
-        while (q > 0 && row_less(v, o, ld[q - 1], lo[q - 1] < 0 ? (1ll << 62) : lo[q - 1])) {
-            ld[q] = ld[q - 1]; lo[q] = lo[q - 1]; --q;
-        }
-        ld[q] = v; lo[q] = o;
-    }
-    __shared__ double sd[T];
-    __shared__ long long so[T];
-    // merge: repeated K rounds of block argmin over heads (K small)
-    __shared__ int head[T];
-    head[threadIdx.x] = 0;
-    __syncthreads();
-    for (int q = 0; q < K; ++q) {
-        const int h = head[threadIdx.x];
-        double v = h < K ? ld[h] : INFINITY;
-        long long ov = h < K ? lo[h] : -1;
-        if (ov < 0) v = INFINITY;
-        sd[threadIdx.x] = v; so[threadIdx.x] = ov < 0 ? (1ll << 62) : ov;
-        __syncthreads();
-        for (int w = T / 2; w >= 1; w >>= 1) {
-            if (threadIdx.x < w) {
-                if (row_less(sd[threadIdx.x + w], so[threadIdx.x + w], sd[threadIdx.x], so[threadIdx.x])) {
-                    sd[threadIdx.x] = sd[threadIdx.x + w]; so[threadIdx.x] = so[threadIdx.x + w];
-                }
-            }
-            __syncthreads();
-        }
-        const double bv = sd[0]; const long long bo = so[0];
-        __syncthreads();
-        if (bv < INFINITY && ov == bo) head[threadIdx.x] = h + 1;
-        if (threadIdx.x == 0) {
-            const long long dst = (long long)li * K + q;
-            if (bv < INFINITY) { a.off[dst] = bo; a.nbr[dst] = a.ip[(long long)li * a.A + bo]; a.d[dst] = bv; }
-            else { a.off[dst] = -1; a.nbr[dst] = -1; a.d[dst] = INFINITY; }
-        }
-        __syncthreads();
-    }
-}
-
-// per length: top-k 1st discords, ascending-offset greedy replay (discords.py:68-93,
-// :48-50, oracle.py:137-145) with the exact prefilter d > dist[k-1]; one warp per length
-struct DiscArgs {
-    const double* mp; double* out_d; long long* out_o;
-    long long n, A; int lmin, n_len, k;
-};
-
-__global__ void k_discords(DiscArgs a) {
-    // one warp per length replays the reference's ascending-offset greedy insertion; lane r
-    // holds list entry r (sorted descending), 8 chunks of the profile are loaded ahead
-    const int lane = threadIdx.x & 31;
-    const int li = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
-    if (li >= a.n_len) return;
-    const int m = a.lmin + li;
-    const long long N = a.n - m + 1;
-    const long long e = (m + 1) / 2;
-    const double* mp = a.mp + (long long)li * a.A;
-    constexpr int AHEAD = 8;
-    const int k = a.k;                       // <= 32
-    double cd = -INFINITY; long long co = -1;
-    for (long long base = 0; base < N; base += 32 * AHEAD) {
-        double dv8[AHEAD];
-#pragma unroll
-        for (int u = 0; u < AHEAD; ++u) {
-            const long long o = base + 32 * u + lane;
-            dv8[u] = o < N ? mp[o] : INFINITY;
-        }
-#pragma unroll
-        for (int u = 0; u < AHEAD; ++u) {
-            const double thr = __shfl_sync(FULLMASK, cd, k - 1);
-            const double d = dv8[u];
-            unsigned bal = __ballot_sync(FULLMASK, (d < INFINITY) && (d > thr));
-            while (bal) {
-                const int src = __ffs(bal) - 1;
-                bal &= bal - 1;
-                const double dv = __shfl_sync(FULLMASK, d, src);
-                const long long ov = base + 32 * u + src;
-                const bool mine = lane < k;
-                if (__any_sync(FULLMASK, mine && co >= 0 && llabs(ov - co) < e)) continue;   // trivial match
-                // before the first strictly smaller entry
-                const int at = __popc(__ballot_sync(FULLMASK, mine && !(dv > cd)));
-                if (at >= k) continue;
-                const double ud = __shfl_up_sync(FULLMASK, cd, 1);
-                const long long uo = __shfl_up_sync(FULLMASK, co, 1);
-                if (mine && lane > at) { cd = ud; co = uo; }
-                if (lane == at) { cd = dv; co = ov; }
-            }
-        }
-    }
-    if (lane < k) { a.out_d[(long long)li * k + lane] = cd; a.out_o[(long long)li * k + lane] = co; }
-}
-
-// Motif-set range queries (motifsets.py:158-165 row_profile path, profile.py:235-260):
-// offsets j with dist(owner, j) < radius at the query's length, the owner's full row with
-// the reference's formula and evaluation order; trivial zone and constant windows excluded.
-struct RangeArgs {
-    const double* tn; const double* cum; const double* cum2;
-    const long long* owner; const int* len; const double* radius;
-    long long* members; unsigned long long* counts; long long cap;
-    long long n; double floor_;
-};
-
-__global__ void k_range_query(RangeArgs a) {
-    const int q = blockIdx.y;
-    const long long j = blockIdx.x * (long long)blockDim.x + threadIdx.x;
-    const int m = a.len[q];
-    const long long N = a.n - m + 1;
-    if (j >= N) return;
-    const long long i = a.owner[q];
-    const long long e = (m + 1) / 2;
-    const long long lo = i - e + 1 > 0 ? i - e + 1 : 0, hi = i + e < N ? i + e : N;
-    if (j >= lo && j < hi) return;
-    double mui, sdi, muj, sdj;
-    win_stats_pd(a.cum, a.cum2, i, m, mui, sdi);
-    win_stats_pd(a.cum, a.cum2, j, m, muj, sdj);
-    if (!(sdj >= a.floor_)) return;
-    double qt = 0.0;
-    for (int k = 0; k < m; ++k) qt = fma(a.tn[i + k], a.tn[j + k], qt);
-    const double L = (double)m;
-    const double qraw = __ddiv_rn(__dsub_rn(qt, __dmul_rn(__dmul_rn(L, mui), muj)),
-                                  __dmul_rn(__dmul_rn(L, sdi), sdj));
-    double rad = __dmul_rn(__dmul_rn(2.0, L), __dsub_rn(1.0, qraw));
-    if (rad < 0.0) rad = 0.0;                    // np.maximum(rad, 0): NaN stays NaN
-    const double d = __dsqrt_rn(rad);
-    if (d < a.radius[q]) {
-        const unsigned long long at = atomicAdd(a.counts + q, 1ull);
-        if ((long long)at < a.cap) a.members[(long long)q * a.cap + (long long)at] = j;
-    }
-}
-
-// VALMP improvement events with norm <= tau (motifsets.py:105-117 stream)
-struct EvArgs {
-    const double* mp; const int* ip; double tau;
-    long long* ev_off; long long* ev_nbr; long long* ev_len; double* ev_d; double* ev_n;
-    unsigned long long* count; long long cap;
-    long long n, A; int lmin, n_len;
-};
-
-__global__ void k_events(EvArgs a) {
-    const long long o = blockIdx.x * (long long)blockDim.x + threadIdx.x;
-    const long long n0 = a.n - a.lmin + 1;
-    if (o >= n0) return;
-    double bn = INFINITY; bool pop = false;
-    for (int li = 0; li < a.n_len; ++li) {
-        const int m = a.lmin + li;
-        if (o > a.n - m) break;
-        const double mpv = a.mp[(long long)li * a.A + o];
-        const double ln = __dmul_rn(mpv, __dsqrt_rn(__ddiv_rn(1.0, (double)m)));
-        if (ln < INFINITY && (!pop || bn > ln)) {
-            bn = ln; pop = true;
-            if (ln <= a.tau) {
-                const unsigned long long q = atomicAdd(a.count, 1ull);
-                if ((long long)q < a.cap) {
-                    a.ev_off[q] = o; a.ev_nbr[q] = a.ip[(long long)li * a.A + o]; a.ev_len[q] = m;
-                    a.ev_d[q] = mpv; a.ev_n[q] = ln;
-                }
-            }
-        }
-    }
-}
-
 // partial export / mask / import for the multi-GPU exact merge
 __global__ void k_export(const ulonglong2* acc, unsigned long long* keys, long long* idx, long long total) {
     long long q = blockIdx.x * (long long)blockDim.x + threadIdx.x;
@@ -1096,22 +726,6 @@ __global__ void k_import(ulonglong2* acc, const unsigned long long* keys, const 
     long long q = blockIdx.x * (long long)blockDim.x + threadIdx.x;
     if (q < total) acc[q] = make_ulonglong2(keys[q], (unsigned long long)idx[q]);
 }
-
-// FP64 FMA peak: 8 independent chains per thread
-__global__ void k_dfma_peak(double* out, int iters, double x) {
-    double a0 = x, a1 = x + 1, a2 = x + 2, a3 = x + 3, a4 = x + 4, a5 = x + 5, a6 = x + 6, a7 = x + 7;
-    const double b = 0.999999, c = 1e-9;
-    for (int it = 0; it < iters; ++it) {
-#pragma unroll
-        for (int u = 0; u < 16; ++u) {
-            a0 = fma(a0, b, c); a1 = fma(a1, b, c); a2 = fma(a2, b, c); a3 = fma(a3, b, c);
-            a4 = fma(a4, b, c); a5 = fma(a5, b, c); a6 = fma(a6, b, c); a7 = fma(a7, b, c);
-        }
-    }
-    double s = a0 + a1 + a2 + a3 + a4 + a5 + a6 + a7;
-    if (s == 12345.678) out[0] = s;
-}
-
 
 // =================================================================================
 // m-th discords (m > 1): per (length, offset) the m best neighbours, exact.
@@ -1375,74 +989,7 @@ __global__ void k_discords_m(const double* mpm, double* out_d, long long* out_o,
     }
 }
 
-}  // namespace
 
-// =================================================================================
-struct vlmp_session {
-    int device = 0;
-    cudaStream_t stream = nullptr;
-    cudaStream_t side = nullptr;       // near-diagonal (masked) bands, overlapped with the main launch
-    cudaEvent_t fork_ev = nullptr, join_ev = nullptr;
-    cudaEvent_t ev[8] = {};
-    std::mutex lock;
-    // series
-    long long n = 0, A = 0;
-    double floor_ = 0.0;
-    double* d_tn = nullptr; double* d_cum = nullptr; double* d_cum2 = nullptr;
-    // per-length scratch
-    Prm* d_prm = nullptr; double* d_mu = nullptr;
-    Prm* d_prm2 = nullptr; double* d_mu2 = nullptr;     // previous length's (1-best bound)
-    long long* d_previdx = nullptr;
-    float2* d_colq = nullptr; float2* d_rowq = nullptr;   // filter factors (k_qprep)
-    int* d_forced = nullptr; size_t forced_cap = 0;      // per-length: full-fold fallback
-    unsigned long long* d_fixcnt = nullptr; size_t fixcnt_cap = 0;   // per-length re-bounded offsets
-    double sscale = 1.0; int hiC = 896 << 20;            // filter: 2^-k scale, hi-word bias
-    // tiles / seeds
-    int2* d_tiles = nullptr; size_t tiles_cap = 0;
-    double* d_seeds = nullptr; size_t seeds_cap = 0;
-    // accumulators [n_len][A]
-    ulonglong2* d_acc = nullptr; size_t acc_cap = 0;
-    double* d_mp = nullptr; int* d_ip = nullptr; size_t mp_cap = 0;
-    unsigned long long* d_counters = nullptr;
-    RowRec* d_log = nullptr; size_t log_cap = 0;        // filter-kernel log of flagged lanes
-    unsigned long long* d_logcnt = nullptr; size_t logcnt_cap = 0;   // per-length fill counters
-    // valmp
-    double* d_vdist = nullptr; double* d_vnorm = nullptr; long long* d_vlen = nullptr;
-    long long* d_vidx = nullptr; unsigned char* d_vpop = nullptr; size_t v_cap = 0;
-    // read-off scratch (persistent: per-call cudaMallocAsync re-maps pool memory every sync)
-    long long* d_ro_i64 = nullptr; size_t ro_i64_cap = 0;
-    double* d_ro_f64 = nullptr; size_t ro_f64_cap = 0;
-    unsigned long long* d_ro_cnt = nullptr;
-    // m-best mode (m > 1 discords)
-    int mbest = 1;
-    ulonglong2* d_slots = nullptr; size_t slots_cap = 0;
-    int* d_slotcnt = nullptr; size_t slotcnt_cap = 0;
-    int* d_ipm = nullptr; size_t ipm_cap = 0;
-    double* d_mpm = nullptr; size_t mpm_cap = 0;
-    long long* d_redo = nullptr; size_t redo_cap = 0;
-    // run state
-    int lmin = 0, lmax = 0, n_len = 0; bool have_profile = false, have_final = false, have_finals = false;
-    double stats[16] = {};
-    std::vector<cudaEvent_t> lev;   // 2 per length: tile-kernel start/stop
-};
-
-namespace {
-
-template <class T>
-int ensure(T*& p, size_t& cap, size_t count) {
-    if (count <= cap && p) return 0;
-    if (p) cudaFree(p);
-    p = nullptr; cap = 0;
-    cudaError_t e = cudaMalloc((void**)&p, std::max<size_t>(count, 1) * sizeof(T));
-    if (e != cudaSuccess) return fail(VLMP_E_NOMEM, std::string("cudaMalloc: ") + cudaGetErrorString(e));
-    cap = count;
-    return 0;
-}
-
-template <class T>
-int ensure1(T*& p, size_t count) { size_t cap = 0; if (p) { cudaFree(p); p = nullptr; } return ensure(p, cap, count); }
-
-inline unsigned blocks(long long n, int t) { return (unsigned)((n + t - 1) / t); }
 
 // filter log records per length: 8 per offset (quasi-periodic series flag many near-minimum
 // cells), at most a quarter of the free device memory; an overflow re-runs exactly
@@ -1503,91 +1050,10 @@ double band_work(long long n, int lmin, int lmax, long long b) {
     return w;
 }
 
-}  // namespace
+
+}  // namespace vlmp_impl
 
 extern "C" {
-
-const char* vlmp_last_error(void) { return g_err.c_str(); }
-
-int vlmp_create(vlmp_session** out, int device) {
-    if (!out) return fail(VLMP_E_INVALID_PARAMETERS, "null out");
-    int ndev = 0;
-    cudaError_t e = cudaGetDeviceCount(&ndev);
-    if (e != cudaSuccess || ndev == 0)
-        return fail(VLMP_E_CUDA, std::string("no CUDA device: ") + cudaGetErrorString(e));
-    if (device < 0 || device >= ndev) return fail(VLMP_E_INVALID_PARAMETERS, "bad device id");
-    CU(cudaSetDevice(device));
-    cudaDeviceProp prop;
-    CU(cudaGetDeviceProperties(&prop, device));
-    if (prop.major != 10) return fail(VLMP_E_CUDA, "libvlmp is built for sm_100a (B200) only");
-    vlmp_session* s = new vlmp_session();
-    s->device = device;
-    CU(cudaStreamCreateWithFlags(&s->stream, cudaStreamNonBlocking));
-    int prio_lo = 0, prio_hi = 0;
-    CU(cudaDeviceGetStreamPriorityRange(&prio_lo, &prio_hi));
-    CU(cudaStreamCreateWithPriority(&s->side, cudaStreamNonBlocking, prio_hi));   // dispatch first
-    CU(cudaEventCreateWithFlags(&s->fork_ev, cudaEventDisableTiming));
-    CU(cudaEventCreateWithFlags(&s->join_ev, cudaEventDisableTiming));
-    for (auto& ev : s->ev) CU(cudaEventCreate(&ev));
-    CU(cudaMalloc((void**)&s->d_counters, 8 * sizeof(unsigned long long)));
-    *out = s;
-    return 0;
-}
-
-void vlmp_destroy(vlmp_session* s) {
-    if (!s) return;
-    cudaSetDevice(s->device);
-    cudaStreamSynchronize(s->stream);
-    void* ptrs[] = {s->d_tn, s->d_cum, s->d_cum2, s->d_prm, s->d_mu, s->d_prm2, s->d_mu2,
-                    s->d_previdx, s->d_colq, s->d_rowq, s->d_forced, s->d_fixcnt, s->d_tiles, s->d_seeds, s->d_acc, s->d_mp, s->d_ip, s->d_counters,
-                    s->d_log, s->d_logcnt, s->d_ro_i64, s->d_ro_f64, s->d_ro_cnt,
-                    s->d_slots, s->d_slotcnt, s->d_ipm, s->d_mpm, s->d_redo, s->d_vdist, s->d_vnorm, s->d_vlen, s->d_vidx, s->d_vpop};
-    for (void* p : ptrs) if (p) cudaFree(p);
-    for (auto& ev : s->ev) if (ev) cudaEventDestroy(ev);
-    for (auto& ev : s->lev) cudaEventDestroy(ev);
-    if (s->stream) cudaStreamDestroy(s->stream);
-    if (s->side) cudaStreamDestroy(s->side);
-    if (s->fork_ev) cudaEventDestroy(s->fork_ev);
-    if (s->join_ev) cudaEventDestroy(s->join_ev);
-    delete s;
-}
-
-int vlmp_set_series(vlmp_session* s, const double* t, const double* cum, const double* cum2,
-                    int64_t n, double sigma_floor) {
-    if (!s || !t || !cum || !cum2) return fail(VLMP_E_INVALID_PARAMETERS, "null argument");
-    if (n <= 0) return fail(VLMP_E_EMPTY_SERIES, "series holds no points");
-    std::lock_guard<std::mutex> g(s->lock);
-    CU(cudaSetDevice(s->device));
-    long long A = ((n + 1024 + 255) / 256) * 256 + 256;
-    s->n = n; s->A = A; s->floor_ = sigma_floor;
-    int rc;
-    if ((rc = ensure1(s->d_tn, 2 * A + 4096))) return rc;
-    if ((rc = ensure1(s->d_cum, n + 1))) return rc;
-    if ((rc = ensure1(s->d_cum2, n + 1))) return rc;
-    if ((rc = ensure1(s->d_prm, A))) return rc;
-    if ((rc = ensure1(s->d_mu, A))) return rc;
-    if ((rc = ensure1(s->d_prm2, A))) return rc;
-    if ((rc = ensure1(s->d_mu2, A))) return rc;
-    if ((rc = ensure1(s->d_previdx, A))) return rc;
-    if ((rc = ensure1(s->d_colq, A))) return rc;
-    if ((rc = ensure1(s->d_rowq, A))) return rc;
-    {   // filter scale: b = sigma sqrt(m) 2^-k stays O(1) whatever the series' units
-        double ss = 0.0;
-        for (long long i = 0; i < n; ++i) ss += t[i] * t[i];
-        const double rms = std::sqrt(ss / (double)n);
-        int k = (rms > 0.0 && std::isfinite(rms)) ? std::ilogb(rms) + 4 : 0;
-        k = std::max(-400, std::min(400, k));
-        s->sscale = std::ldexp(1.0, -k);
-        s->hiC = (896 + 2 * k) << 20;
-    }
-    CU(cudaMemsetAsync(s->d_tn, 0, (2 * A + 4096) * sizeof(double), s->stream));
-    CU(cudaMemcpyAsync(s->d_tn, t, n * sizeof(double), cudaMemcpyHostToDevice, s->stream));
-    CU(cudaMemcpyAsync(s->d_cum, cum, (n + 1) * sizeof(double), cudaMemcpyHostToDevice, s->stream));
-    CU(cudaMemcpyAsync(s->d_cum2, cum2, (n + 1) * sizeof(double), cudaMemcpyHostToDevice, s->stream));
-    CU(cudaStreamSynchronize(s->stream));
-    s->have_profile = s->have_final = s->have_finals = false;
-    return 0;
-}
 
 int vlmp_band_count(vlmp_session* s, int32_t lmin, int64_t* n_bands) {
     if (!s || !n_bands) return fail(VLMP_E_INVALID_PARAMETERS, "null argument");
@@ -1854,230 +1320,6 @@ int vlmp_partials_import(vlmp_session* s, const void* keys, const void* idx) {
     return 0;
 }
 
-static int finalize_impl(vlmp_session* s, int li_lo, int li_hi, bool readoffs) {
-    CU(cudaSetDevice(s->device));
-    cudaStream_t st = s->stream;
-    const long long A = s->A, n = s->n;
-    int rc;
-    if ((size_t)s->n_len * A > s->mp_cap || !s->d_mp || !s->d_ip) {
-        if ((rc = ensure1(s->d_mp, (size_t)s->n_len * A))) return rc;
-        if ((rc = ensure1(s->d_ip, (size_t)s->n_len * A))) return rc;
-        s->mp_cap = (size_t)s->n_len * A;
-    }
-    const long long n0 = n - s->lmin + 1;
-    size_t vc = s->v_cap;
-    if (vc < (size_t)n0 || !s->d_vdist) {
-        if ((rc = ensure1(s->d_vdist, n0))) return rc;
-        if ((rc = ensure1(s->d_vnorm, n0))) return rc;
-        if ((rc = ensure1(s->d_vlen, n0))) return rc;
-        if ((rc = ensure1(s->d_vidx, n0))) return rc;
-        if ((rc = ensure1(s->d_vpop, n0))) return rc;
-        s->v_cap = n0;
-    }
-    CU(cudaEventRecord(s->ev[4], st));
-    if (li_lo <= li_hi) {
-        FinArgs fa{s->d_tn, s->d_cum, s->d_cum2, s->d_acc, s->d_mp, s->d_ip, n, A, s->lmin, s->n_len, s->floor_,
-                   li_lo, li_hi};
-        k_finalize_walk<<<blocks(n0, 64), 64, 0, st>>>(fa);
-        s->stats[9] += 1;
-    }
-    if (readoffs) {
-        ValmpArgs va{s->d_mp, s->d_ip, s->d_vdist, s->d_vnorm, s->d_vlen, s->d_vidx, s->d_vpop, n, A, s->lmin, s->n_len};
-        k_valmp<<<blocks(n0, 256), 256, 0, st>>>(va);
-        s->stats[9] += 1;
-    }
-    CU(cudaEventRecord(s->ev[5], st));
-    CU(cudaGetLastError());
-    CU(cudaEventSynchronize(s->ev[5]));
-    float ms = 0; CU(cudaEventElapsedTime(&ms, s->ev[4], s->ev[5]));
-    s->stats[1] = ms;
-    s->have_final = readoffs;
-    s->have_finals = true;
-    return 0;
-}
-
-int vlmp_finalize(vlmp_session* s) {
-    if (!s || !s->have_profile) return fail(VLMP_E_STATE, "no profile run");
-    std::lock_guard<std::mutex> g(s->lock);
-    return finalize_impl(s, 0, s->n_len - 1, true);
-}
-
-int vlmp_finalize_lengths(vlmp_session* s, int32_t li_lo, int32_t li_hi) {
-    if (!s || !s->have_profile) return fail(VLMP_E_STATE, "no profile run");
-    if (li_lo < 0 || li_hi < li_lo - 1 || li_hi >= s->n_len)
-        return fail(VLMP_E_INVALID_PARAMETERS, "length range outside the profiled range");
-    std::lock_guard<std::mutex> g(s->lock);
-    return finalize_impl(s, li_lo, li_hi, false);
-}
-
-int vlmp_final_buffers(vlmp_session* s, void** mp, void** ip, int64_t* n_len, int64_t* stride) {
-    if (!s || !s->have_finals) return fail(VLMP_E_STATE, "no finalized values");
-    if (!mp || !ip || !n_len || !stride) return fail(VLMP_E_INVALID_PARAMETERS, "null argument");
-    *mp = s->d_mp; *ip = s->d_ip; *n_len = s->n_len; *stride = s->A;
-    return 0;
-}
-
-int vlmp_finalize_readoffs(vlmp_session* s) {
-    if (!s || !s->have_finals) return fail(VLMP_E_STATE, "no finalized values");
-    std::lock_guard<std::mutex> g(s->lock);
-    return finalize_impl(s, 0, -1, true);
-}
-
-int vlmp_get_valmp(vlmp_session* s, double* dist, double* norm, int64_t* lengths, int64_t* indices,
-                   uint8_t* populated) {
-    if (!s || !s->have_final) return fail(VLMP_E_STATE, "not finalized");
-    std::lock_guard<std::mutex> g(s->lock);
-    CU(cudaSetDevice(s->device));
-    const long long n0 = s->n - s->lmin + 1;
-    CU(cudaMemcpyAsync(dist, s->d_vdist, n0 * 8, cudaMemcpyDeviceToHost, s->stream));
-    CU(cudaMemcpyAsync(norm, s->d_vnorm, n0 * 8, cudaMemcpyDeviceToHost, s->stream));
-    CU(cudaMemcpyAsync(lengths, s->d_vlen, n0 * 8, cudaMemcpyDeviceToHost, s->stream));
-    CU(cudaMemcpyAsync(indices, s->d_vidx, n0 * 8, cudaMemcpyDeviceToHost, s->stream));
-    CU(cudaMemcpyAsync(populated, s->d_vpop, n0, cudaMemcpyDeviceToHost, s->stream));
-    CU(cudaStreamSynchronize(s->stream));
-    return 0;
-}
-
-int vlmp_get_profile(vlmp_session* s, int32_t length, double* mp, int64_t* ip) {
-    if (!s || !s->have_final) return fail(VLMP_E_STATE, "not finalized");
-    if (length < s->lmin || length > s->lmax) return fail(VLMP_E_INVALID_PARAMETERS, "length outside the run");
-    std::lock_guard<std::mutex> g(s->lock);
-    CU(cudaSetDevice(s->device));
-    const long long N = s->n - length + 1;
-    const long long off = (long long)(length - s->lmin) * s->A;
-    std::vector<int> tmp(N);
-    CU(cudaMemcpyAsync(mp, s->d_mp + off, N * 8, cudaMemcpyDeviceToHost, s->stream));
-    CU(cudaMemcpyAsync(tmp.data(), s->d_ip + off, N * 4, cudaMemcpyDeviceToHost, s->stream));
-    CU(cudaStreamSynchronize(s->stream));
-    for (long long o = 0; o < N; ++o) ip[o] = tmp[o];
-    return 0;
-}
-
-int vlmp_smallest_rows(vlmp_session* s, int32_t k2, int64_t* out_off, int64_t* out_nbr, double* out_d) {
-    if (!s || !s->have_final) return fail(VLMP_E_STATE, "not finalized");
-    if (k2 < 1 || k2 > 64) return fail(VLMP_E_INVALID_PARAMETERS, "k2 must be in [1, 64]");
-    std::lock_guard<std::mutex> g(s->lock);
-    CU(cudaSetDevice(s->device));
-    const long long cnt = (long long)s->n_len * k2;
-    int rc;
-    if ((rc = ensure(s->d_ro_i64, s->ro_i64_cap, (size_t)(2 * cnt)))) return rc;
-    if ((rc = ensure(s->d_ro_f64, s->ro_f64_cap, (size_t)cnt))) return rc;
-    long long* d_off = s->d_ro_i64; long long* d_nbr = s->d_ro_i64 + cnt; double* d_d = s->d_ro_f64;
-    SmallArgs sa{s->d_mp, s->d_ip, d_off, d_nbr, d_d, s->n, s->A, s->lmin, k2};
-    k_smallest<<<s->n_len, 256, 0, s->stream>>>(sa);
-    CU(cudaGetLastError());
-    CU(cudaMemcpyAsync(out_off, d_off, cnt * 8, cudaMemcpyDeviceToHost, s->stream));
-    CU(cudaMemcpyAsync(out_nbr, d_nbr, cnt * 8, cudaMemcpyDeviceToHost, s->stream));
-    CU(cudaMemcpyAsync(out_d, d_d, cnt * 8, cudaMemcpyDeviceToHost, s->stream));
-    CU(cudaStreamSynchronize(s->stream));
-    s->stats[9] += 1;
-    return 0;
-}
-
-int vlmp_discords(vlmp_session* s, int32_t k, double* out_dist, int64_t* out_off) {
-    if (!s || !s->have_final) return fail(VLMP_E_STATE, "not finalized");
-    if (k < 1 || k > 32) return fail(VLMP_E_INVALID_PARAMETERS, "k must be in [1, 32]");
-    std::lock_guard<std::mutex> g(s->lock);
-    CU(cudaSetDevice(s->device));
-    const long long cnt = (long long)s->n_len * k;
-    int rc;
-    if ((rc = ensure(s->d_ro_i64, s->ro_i64_cap, (size_t)cnt))) return rc;
-    if ((rc = ensure(s->d_ro_f64, s->ro_f64_cap, (size_t)cnt))) return rc;
-    double* d_d = s->d_ro_f64; long long* d_o = s->d_ro_i64;
-    DiscArgs da{s->d_mp, d_d, d_o, s->n, s->A, s->lmin, s->n_len, k};
-    k_discords<<<s->n_len, 32, 0, s->stream>>>(da);
-    CU(cudaGetLastError());
-    CU(cudaMemcpyAsync(out_dist, d_d, cnt * 8, cudaMemcpyDeviceToHost, s->stream));
-    CU(cudaMemcpyAsync(out_off, d_o, cnt * 8, cudaMemcpyDeviceToHost, s->stream));
-    CU(cudaStreamSynchronize(s->stream));
-    s->stats[9] += 1;
-    return 0;
-}
-
-int vlmp_ranking_events(vlmp_session* s, double tau, int64_t cap, int64_t* ev_off, int64_t* ev_nbr,
-                        int64_t* ev_len, double* ev_dist, double* ev_norm, int64_t* count) {
-    if (!s || !s->have_final) return fail(VLMP_E_STATE, "not finalized");
-    std::lock_guard<std::mutex> g(s->lock);
-    CU(cudaSetDevice(s->device));
-    cudaStream_t st = s->stream;
-    long long c = std::max<long long>(cap, 1);
-    int rc;
-    if ((rc = ensure(s->d_ro_i64, s->ro_i64_cap, (size_t)(3 * c)))) return rc;
-    if ((rc = ensure(s->d_ro_f64, s->ro_f64_cap, (size_t)(2 * c)))) return rc;
-    if (!s->d_ro_cnt) CU(cudaMalloc((void**)&s->d_ro_cnt, 8));
-    long long *d_o = s->d_ro_i64, *d_nb = s->d_ro_i64 + c, *d_l = s->d_ro_i64 + 2 * c;
-    double *d_d = s->d_ro_f64, *d_n = s->d_ro_f64 + c;
-    unsigned long long* d_c = s->d_ro_cnt;
-    CU(cudaMemsetAsync(d_c, 0, 8, st));
-    const long long n0 = s->n - s->lmin + 1;
-    EvArgs ea{s->d_mp, s->d_ip, tau, d_o, d_nb, d_l, d_d, d_n, d_c, cap, s->n, s->A, s->lmin, s->n_len};
-    k_events<<<blocks(n0, 256), 256, 0, st>>>(ea);
-    CU(cudaGetLastError());
-    unsigned long long hc = 0;
-    CU(cudaMemcpyAsync(&hc, d_c, 8, cudaMemcpyDeviceToHost, st));
-    CU(cudaStreamSynchronize(st));
-    long long take = std::min<long long>((long long)hc, cap);
-    if (take > 0) {
-        CU(cudaMemcpyAsync(ev_off, d_o, take * 8, cudaMemcpyDeviceToHost, st));
-        CU(cudaMemcpyAsync(ev_nbr, d_nb, take * 8, cudaMemcpyDeviceToHost, st));
-        CU(cudaMemcpyAsync(ev_len, d_l, take * 8, cudaMemcpyDeviceToHost, st));
-        CU(cudaMemcpyAsync(ev_dist, d_d, take * 8, cudaMemcpyDeviceToHost, st));
-        CU(cudaMemcpyAsync(ev_norm, d_n, take * 8, cudaMemcpyDeviceToHost, st));
-    }
-    CU(cudaStreamSynchronize(st));
-    *count = (int64_t)hc;
-    return 0;
-}
-
-int vlmp_range_query(vlmp_session* s, int64_t n_q, const int64_t* owners, const int32_t* lengths,
-                     const double* radii, int64_t cap, int64_t* members, int64_t* counts) {
-    if (!s || (n_q > 0 && (!owners || !lengths || !radii || !members || !counts)) || n_q < 0 || cap < 0)
-        return fail(VLMP_E_INVALID_PARAMETERS, "bad range query arguments");
-    if (s->n <= 0) return fail(VLMP_E_STATE, "no series uploaded");
-    if (n_q == 0) return 0;
-    long long max_n = 0;
-    for (long long q = 0; q < n_q; ++q) {
-        if (lengths[q] < 4 || lengths[q] > s->n || owners[q] < 0 || owners[q] > s->n - lengths[q])
-            return fail(VLMP_E_INVALID_PARAMETERS, "range query owner/length outside the series");
-        max_n = std::max<long long>(max_n, s->n - lengths[q] + 1);
-    }
-    std::lock_guard<std::mutex> g(s->lock);
-    CU(cudaSetDevice(s->device));
-    cudaStream_t st = s->stream;
-    const long long c = std::max<long long>(cap, 1);
-    long long* d_own = nullptr; int* d_len = nullptr; double* d_rad = nullptr;
-    long long* d_mem = nullptr; unsigned long long* d_cnt = nullptr;
-    CU(cudaMallocAsync((void**)&d_own, n_q * 8, st));
-    CU(cudaMallocAsync((void**)&d_len, n_q * 4, st));
-    CU(cudaMallocAsync((void**)&d_rad, n_q * 8, st));
-    CU(cudaMallocAsync((void**)&d_mem, n_q * c * 8, st));
-    CU(cudaMallocAsync((void**)&d_cnt, n_q * 8, st));
-    CU(cudaMemcpyAsync(d_own, owners, n_q * 8, cudaMemcpyHostToDevice, st));
-    CU(cudaMemcpyAsync(d_len, lengths, n_q * 4, cudaMemcpyHostToDevice, st));
-    CU(cudaMemcpyAsync(d_rad, radii, n_q * 8, cudaMemcpyHostToDevice, st));
-    CU(cudaMemsetAsync(d_cnt, 0, n_q * 8, st));
-    RangeArgs ra{s->d_tn, s->d_cum, s->d_cum2, d_own, d_len, d_rad, d_mem, d_cnt, c, s->n, s->floor_};
-    dim3 grid((unsigned)((max_n + 255) / 256), (unsigned)n_q);
-    k_range_query<<<grid, 256, 0, st>>>(ra);
-    CU(cudaGetLastError());
-    std::vector<unsigned long long> hc(n_q);
-    CU(cudaMemcpyAsync(hc.data(), d_cnt, n_q * 8, cudaMemcpyDeviceToHost, st));
-    if (cap > 0) CU(cudaMemcpyAsync(members, d_mem, n_q * cap * 8, cudaMemcpyDeviceToHost, st));
-    CU(cudaStreamSynchronize(st));
-    for (long long q = 0; q < n_q; ++q) counts[q] = (int64_t)hc[q];
-    cudaFreeAsync(d_own, st); cudaFreeAsync(d_len, st); cudaFreeAsync(d_rad, st);
-    cudaFreeAsync(d_mem, st); cudaFreeAsync(d_cnt, st);
-    CU(cudaStreamSynchronize(st));
-    s->stats[9] += 1;
-    return 0;
-}
-
-int vlmp_stats(vlmp_session* s, double* out, int32_t n_out) {
-    if (!s || !out) return fail(VLMP_E_INVALID_PARAMETERS, "null argument");
-    for (int q = 0; q < n_out && q < 16; ++q) out[q] = s->stats[q];
-    return 0;
-}
-
 int vlmp_profile_mbest(vlmp_session* s, int32_t lmin, int32_t lmax, int32_t mb) {
     if (!s) return fail(VLMP_E_INVALID_PARAMETERS, "null session");
     if (s->n <= 0) return fail(VLMP_E_STATE, "no series uploaded");
@@ -2221,43 +1463,6 @@ int vlmp_discords_m(vlmp_session* s, int32_t k, double* out_dist, int64_t* out_o
     CU(cudaMemcpyAsync(out_dist, s->d_ro_f64, cnt * 8, cudaMemcpyDeviceToHost, s->stream));
     CU(cudaMemcpyAsync(out_off, s->d_ro_i64, cnt * 8, cudaMemcpyDeviceToHost, s->stream));
     CU(cudaStreamSynchronize(s->stream));
-    return 0;
-}
-
-int vlmp_event_record(vlmp_session* s, int32_t slot) {
-    if (!s || slot < 0 || slot > 1) return fail(VLMP_E_INVALID_PARAMETERS, "slot must be 0 or 1");
-    CU(cudaSetDevice(s->device));
-    CU(cudaEventRecord(s->ev[6 + slot], s->stream));
-    return 0;
-}
-
-int vlmp_event_elapsed(vlmp_session* s, float* ms) {
-    if (!s || !ms) return fail(VLMP_E_INVALID_PARAMETERS, "null argument");
-    CU(cudaSetDevice(s->device));
-    CU(cudaEventSynchronize(s->ev[7]));
-    CU(cudaEventElapsedTime(ms, s->ev[6], s->ev[7]));
-    return 0;
-}
-
-int vlmp_measure_fp64_peak(vlmp_session* s, double* fma_per_s) {
-    if (!s || !fma_per_s) return fail(VLMP_E_INVALID_PARAMETERS, "null argument");
-    std::lock_guard<std::mutex> g(s->lock);
-    CU(cudaSetDevice(s->device));
-    int sms = 0;
-    CU(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, s->device));
-    double* d_out = nullptr;
-    CU(cudaMalloc((void**)&d_out, 8));
-    const int threads = 512, per_sm = 4, iters = 2048;
-    const unsigned grid = sms * per_sm;
-    k_dfma_peak<<<grid, threads, 0, s->stream>>>(d_out, 16, 1.0);   // warm-up
-    CU(cudaEventRecord(s->ev[6], s->stream));
-    k_dfma_peak<<<grid, threads, 0, s->stream>>>(d_out, iters, 1.0);
-    CU(cudaEventRecord(s->ev[7], s->stream));
-    CU(cudaEventSynchronize(s->ev[7]));
-    float ms = 0; CU(cudaEventElapsedTime(&ms, s->ev[6], s->ev[7]));
-    CU(cudaFree(d_out));
-    const double fmas = (double)grid * threads * iters * 16.0 * 8.0;
-    *fma_per_s = fmas / (ms * 1e-3);
     return 0;
 }
 

@@ -1,0 +1,183 @@
+// vlmp_internal.cuh -- shared declarations of the libvlmp translation units
+// (profile.cu: phase 1 kernels + host; readout.cu: phase 2 / read-offs; session.cu:
+// sessions, series upload, timing). See profile.cu for the kernel map.
+#pragma once
+
+#include <cuda_runtime.h>
+#include <stdint.h>
+#include <stdio.h>
+#include <stdlib.h>
+#include <string.h>
+#include <math.h>
+#include <algorithm>
+#include <mutex>
+#include <string>
+#include <vector>
+#include "../../include/vlmp.h"
+
+namespace vlmp_impl {
+
+#ifndef VLMP_D
+#define VLMP_D 8
+#endif
+constexpr int D = VLMP_D;         // diagonals per lane (even, <= 16)
+constexpr int BAND = 32 * D;      // diagonals per warp tile
+constexpr int ceil_log2(int v) { int b = 0; while ((1 << b) < v) ++b; return b; }
+constexpr int PBITS = ceil_log2(BAND);   // packed local index bits (full-fold keys)
+constexpr int MG = 1 << ceil_log2(D);    // lanes per log record in k_log_merge
+static_assert(D % 2 == 0 && D <= 16, "D: even, at most 16");
+constexpr unsigned long long PMASK = (1ull << PBITS) - 1;
+#ifndef VLMP_WARPS_PER_CTA
+#define VLMP_WARPS_PER_CTA 1
+#endif
+#ifndef VLMP_FILTER_WARPS_PER_SM
+#define VLMP_FILTER_WARPS_PER_SM 20   // 96 registers
+#endif
+constexpr int WARPS_PER_CTA = VLMP_WARPS_PER_CTA;
+constexpr int FILTER_MIN_BLOCKS = VLMP_FILTER_WARPS_PER_SM / WARPS_PER_CTA;
+constexpr int FULL_MIN_BLOCKS = 16 / WARPS_PER_CTA;               // 128 registers
+constexpr unsigned FULLMASK = 0xffffffffu;
+constexpr unsigned long long KEY_NONE = 0x7FF0000000000000ull;   // bits of +inf
+constexpr long long IDX_NONE = 0x7FFFFFFFFFFFFFFFll;
+
+extern thread_local std::string g_err;   // session.cu
+
+inline int fail(int code, const std::string& msg) { g_err = msg; return code; }
+
+#define CU(call)                                                                   \
+    do {                                                                           \
+        cudaError_t e_ = (call);                                                   \
+        if (e_ != cudaSuccess)                                                     \
+            return fail(VLMP_E_CUDA, std::string(#call) + ": " + cudaGetErrorString(e_)); \
+    } while (0)
+
+
+// ---------------------------------------------------------------------------------
+// exact window statistics (series.py:91-100): no contraction, numpy op order
+__device__ inline void win_stats(const double* __restrict__ cum, const double* __restrict__ cum2,
+                                 long long o, int m, double& mu, double& sd) {
+    double s = __dsub_rn(cum[o + m], cum[o]);
+    double ss = __dsub_rn(cum2[o + m], cum2[o]);
+    double L = (double)m;
+    double u = __ddiv_rn(s, L);
+    double var = __dsub_rn(__ddiv_rn(ss, L), __dmul_rn(u, u));
+    if (!(var >= 0.0)) var = 0.0;
+    mu = u;
+    sd = __dsqrt_rn(var);
+}
+
+// series.py:81-89 (stats: sigma = sqrt(var) if var > 0 else 0) -- used by pair_distance
+__device__ inline void win_stats_pd(const double* __restrict__ cum, const double* __restrict__ cum2,
+                                    long long o, int m, double& mu, double& sd) {
+    double s = __dsub_rn(cum[o + m], cum[o]);
+    double ss = __dsub_rn(cum2[o + m], cum2[o]);
+    double L = (double)m;
+    double u = __ddiv_rn(s, L);
+    double var = __dsub_rn(__ddiv_rn(ss, L), __dmul_rn(u, u));
+    mu = u;
+    sd = var > 0.0 ? __dsqrt_rn(var) : 0.0;
+}
+
+// canonical pair distance (series.py:169-194): dot in (min,max) order, sequential sum
+__device__ inline double pair_distance(const double* __restrict__ t, const double* __restrict__ cum,
+                                const double* __restrict__ cum2, long long i, long long j, int m,
+                                double floor_) {
+    long long a = i <= j ? i : j, b = i <= j ? j : i;
+    double mua, sda, mub, sdb;
+    win_stats_pd(cum, cum2, a, m, mua, sda);
+    win_stats_pd(cum, cum2, b, m, mub, sdb);
+    if (sda < floor_ || sdb < floor_) return INFINITY;
+    double qt = 0.0;
+    for (int k = 0; k < m; ++k) qt = __dadd_rn(qt, __dmul_rn(t[a + k], t[b + k]));
+    double L = (double)m;
+    double num = __dsub_rn(qt, __dmul_rn(__dmul_rn(L, mua), mub));
+    double den = __dmul_rn(__dmul_rn(L, sda), sdb);
+    double rad = __dmul_rn(__dmul_rn(2.0, L), __dsub_rn(1.0, __ddiv_rn(num, den)));
+    return rad > 0.0 ? __dsqrt_rn(rad) : 0.0;
+}
+
+// ---------------------------------------------------------------------------------
+// Per-length window parameters, natural layout, 32-byte AoS so one warp-contiguous
+// run of offsets is a coalesced 1 KB read (and two 16-byte cp.async per entry).
+struct __align__(32) Prm {
+    double df;    // (t[o+m-1] - t[o-1]) / 2                       (0 at o = 0)
+    double dg;    // (t[o+m-1] - mu_o) + (t[o-1] - mu_{o-1})        (0 at o = 0)
+    double inv;   // 1 / (sigma_o sqrt(m)); NaN = invalid window (constant / past the end)
+    float U;      // bound on the offset's best key, high word as float (filter kernel)
+    float pad;
+};
+
+// A filter-kernel log record: a lane whose cells passed the bound at row i; its 8 cells are
+// (i, j0 + s) and cov[s] is their covariance, so the merge kernel can recompute the exact
+// keys with the kernel's own FMA sequence (bit-identical) and apply the exact tests.
+struct __align__(16) RowRec { int i; int j0; int pad0, pad1; double cov[D]; };
+
+
+template <class T>
+int ensure(T*& p, size_t& cap, size_t count) {
+    if (count <= cap && p) return 0;
+    if (p) cudaFree(p);
+    p = nullptr; cap = 0;
+    cudaError_t e = cudaMalloc((void**)&p, std::max<size_t>(count, 1) * sizeof(T));
+    if (e != cudaSuccess) return fail(VLMP_E_NOMEM, std::string("cudaMalloc: ") + cudaGetErrorString(e));
+    cap = count;
+    return 0;
+}
+
+template <class T>
+int ensure1(T*& p, size_t count) { size_t cap = 0; if (p) { cudaFree(p); p = nullptr; } return ensure(p, cap, count); }
+
+inline unsigned blocks(long long n, int t) { return (unsigned)((n + t - 1) / t); }
+
+}  // namespace vlmp_impl
+
+using namespace vlmp_impl;
+
+// =================================================================================
+struct vlmp_session {
+    int device = 0;
+    cudaStream_t stream = nullptr;
+    cudaStream_t side = nullptr;       // near-diagonal (masked) bands, overlapped with the main launch
+    cudaEvent_t fork_ev = nullptr, join_ev = nullptr;
+    cudaEvent_t ev[8] = {};
+    std::mutex lock;
+    // series
+    long long n = 0, A = 0;
+    double floor_ = 0.0;
+    double* d_tn = nullptr; double* d_cum = nullptr; double* d_cum2 = nullptr;
+    // per-length scratch
+    Prm* d_prm = nullptr; double* d_mu = nullptr;
+    Prm* d_prm2 = nullptr; double* d_mu2 = nullptr;     // previous length's (1-best bound)
+    long long* d_previdx = nullptr;
+    float2* d_colq = nullptr; float2* d_rowq = nullptr;   // filter factors (k_qprep)
+    int* d_forced = nullptr; size_t forced_cap = 0;      // per-length: full-fold fallback
+    unsigned long long* d_fixcnt = nullptr; size_t fixcnt_cap = 0;   // per-length re-bounded offsets
+    double sscale = 1.0; int hiC = 896 << 20;            // filter: 2^-k scale, hi-word bias
+    // tiles / seeds
+    int2* d_tiles = nullptr; size_t tiles_cap = 0;
+    double* d_seeds = nullptr; size_t seeds_cap = 0;
+    // accumulators [n_len][A]
+    ulonglong2* d_acc = nullptr; size_t acc_cap = 0;
+    double* d_mp = nullptr; int* d_ip = nullptr; size_t mp_cap = 0;
+    unsigned long long* d_counters = nullptr;
+    RowRec* d_log = nullptr; size_t log_cap = 0;        // filter-kernel log of flagged lanes
+    unsigned long long* d_logcnt = nullptr; size_t logcnt_cap = 0;   // per-length fill counters
+    // valmp
+    double* d_vdist = nullptr; double* d_vnorm = nullptr; long long* d_vlen = nullptr;
+    long long* d_vidx = nullptr; unsigned char* d_vpop = nullptr; size_t v_cap = 0;
+    // read-off scratch (persistent: per-call cudaMallocAsync re-maps pool memory every sync)
+    long long* d_ro_i64 = nullptr; size_t ro_i64_cap = 0;
+    double* d_ro_f64 = nullptr; size_t ro_f64_cap = 0;
+    unsigned long long* d_ro_cnt = nullptr;
+    // m-best mode (m > 1 discords)
+    int mbest = 1;
+    ulonglong2* d_slots = nullptr; size_t slots_cap = 0;
+    int* d_slotcnt = nullptr; size_t slotcnt_cap = 0;
+    int* d_ipm = nullptr; size_t ipm_cap = 0;
+    double* d_mpm = nullptr; size_t mpm_cap = 0;
+    long long* d_redo = nullptr; size_t redo_cap = 0;
+    // run state
+    int lmin = 0, lmax = 0, n_len = 0; bool have_profile = false, have_final = false, have_finals = false;
+    double stats[16] = {};
+    std::vector<cudaEvent_t> lev;   // 2 per length: tile-kernel start/stop
+};
