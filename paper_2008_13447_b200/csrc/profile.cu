@@ -197,7 +197,6 @@ __global__ void k_qprep(const Prm* __restrict__ prm, float2* colq, float2* rowq,
 }
 
 // ---------------------------------------------------------------------------------
-struct Cand { int o; int idx; unsigned long long key; };   // candidate (offset, neighbour, key)
 
 
 struct TileArgs {

@@ -42,11 +42,6 @@ int vlmp_create(vlmp_session** out, int device) {
     vlmp_session* s = new vlmp_session();
     s->device = device;
     CU(cudaStreamCreateWithFlags(&s->stream, cudaStreamNonBlocking));
-    int prio_lo = 0, prio_hi = 0;
-    CU(cudaDeviceGetStreamPriorityRange(&prio_lo, &prio_hi));
-    CU(cudaStreamCreateWithPriority(&s->side, cudaStreamNonBlocking, prio_hi));   // dispatch first
-    CU(cudaEventCreateWithFlags(&s->fork_ev, cudaEventDisableTiming));
-    CU(cudaEventCreateWithFlags(&s->join_ev, cudaEventDisableTiming));
     for (auto& ev : s->ev) CU(cudaEventCreate(&ev));
     CU(cudaMalloc((void**)&s->d_counters, 8 * sizeof(unsigned long long)));
     *out = s;
@@ -65,9 +60,6 @@ void vlmp_destroy(vlmp_session* s) {
     for (auto& ev : s->ev) if (ev) cudaEventDestroy(ev);
     for (auto& ev : s->lev) cudaEventDestroy(ev);
     if (s->stream) cudaStreamDestroy(s->stream);
-    if (s->side) cudaStreamDestroy(s->side);
-    if (s->fork_ev) cudaEventDestroy(s->fork_ev);
-    if (s->join_ev) cudaEventDestroy(s->join_ev);
     delete s;
 }
 

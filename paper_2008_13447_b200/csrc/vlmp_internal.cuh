@@ -137,8 +137,6 @@ using namespace vlmp_impl;
 struct vlmp_session {
     int device = 0;
     cudaStream_t stream = nullptr;
-    cudaStream_t side = nullptr;       // near-diagonal (masked) bands, overlapped with the main launch
-    cudaEvent_t fork_ev = nullptr, join_ev = nullptr;
     cudaEvent_t ev[8] = {};
     std::mutex lock;
     // series
