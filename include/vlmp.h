@@ -165,8 +165,8 @@ int vlmp_range_query(vlmp_session* s, int64_t n_q, const int64_t* owners, const 
  * launches, out[6] filtered lengths, out[7] full lengths, out[8] slow-path
  * candidate merges, out[9] total kernel launches, out[10] first-length tile ms,
  * out[11] flagged filter lane-rows (log records), out[12] offsets whose bound needed a direct dot product, out[13] exact redo count (1-best:
- * 1 = the run was redone with full folds after a log overflow; m-best: offsets
- * recomputed), out[14] lengths that fell back to full folds (an offset's own bound
+ * 1 = redone without the sampled first-length start after a log overflow, 2 = redone
+ * with full folds at every length; m-best: offsets recomputed), out[14] lengths that fell back to full folds (an offset's own bound
  * too weak for the covariance-domain filter), out[15] largest per-length log fill.
  */
 int vlmp_stats(vlmp_session* s, double* out, int32_t n_out);

@@ -144,6 +144,22 @@ __global__ void k_bound2(Bound2Args a) {
 }
 
 
+// Bound of a shard's first length from its own partial minima (a full-fold pass over a
+// sample of the bands): any folded cell is a valid cell of this length.
+__global__ void k_bound_self(const ulonglong2* __restrict__ acc, Prm* prm, long long N, double margin) {
+    const long long o = blockIdx.x * (long long)blockDim.x + threadIdx.x;
+    if (o >= N) return;
+    const double io = prm[o].inv;
+    float u = -INFINITY;
+    if (io == io) {
+        const ulonglong2 v = acc[o];
+        u = INFINITY;
+        if (v.x != KEY_NONE)
+            u = __int_as_float(__double2hiint(fmax(__longlong_as_double((long long)v.x), 0.0) + margin));
+    }
+    prm[o].U = u;
+}
+
 // ---------------------------------------------------------------------------------
 // Filter thresholds in the covariance domain. A cell (i, j) must reach the exact tests when
 // its key r = 1 - cov inv_i inv_j satisfies hi(r) <= max(U_i, U_j), i.e. r <= R(U) with
@@ -214,6 +230,7 @@ struct TileArgs {
     const float2* rowq;            // filter: row factors (b_i, q(Uwin_i))
     const int* forced;             // filter: nonzero => this length runs the full-fold body
     int hiC;                       // hi word of 2^(2k) * 2^-127 scaled float -> double bias
+    const int* seed_map;           // tile list subset: seed slot of each listed tile (or nullptr)
 };
 
 __device__ inline bool key_less(unsigned long long k1, long long i1, unsigned long long k2, long long i2) {
@@ -566,16 +583,17 @@ k_tile(TileArgs a) {
     const int wid = blockIdx.x * WARPS_PER_CTA + wl;
     if (wid >= a.n_tiles) return;
     const int2 tl = a.tiles[wid];
+    const int sw = a.seed_map ? a.seed_map[wid] : wid;   // seed slot of this tile
     const long long d0 = a.dlo + (long long)tl.x * BAND;
     const long long i0 = (long long)tl.y * a.S;
     const long long rows_valid = a.N - d0 - i0;
     if (rows_valid <= 0 || d0 + BAND - 1 < a.e) return;   // empty, or entirely trivial
     if (FULL || (a.forced && *a.forced)) {
-        if (d0 < a.e) tile_body<true, true>(a, ws[wl], wid, lane, d0, i0, rows_valid);
-        else tile_body<true, false>(a, ws[wl], wid, lane, d0, i0, rows_valid);
+        if (d0 < a.e) tile_body<true, true>(a, ws[wl], sw, lane, d0, i0, rows_valid);
+        else tile_body<true, false>(a, ws[wl], sw, lane, d0, i0, rows_valid);
     } else {
-        if (d0 < a.e) tile_body<false, true>(a, ws[wl], wid, lane, d0, i0, rows_valid);
-        else tile_body<false, false>(a, ws[wl], wid, lane, d0, i0, rows_valid);
+        if (d0 < a.e) tile_body<false, true>(a, ws[wl], sw, lane, d0, i0, rows_valid);
+        else tile_body<false, false>(a, ws[wl], sw, lane, d0, i0, rows_valid);
     }
 }
 
@@ -990,10 +1008,10 @@ __global__ void k_discords_m(const double* mpm, double* out_d, long long* out_o,
 
 
 
-// filter log records per length: 8 per offset (quasi-periodic series flag many near-minimum
+// filter log records per length: 16 per offset (quasi-periodic series flag many near-minimum
 // cells), at most a quarter of the free device memory; an overflow re-runs exactly
 size_t log_capacity(long long N0) {
-    size_t want = std::max<size_t>((size_t)1 << 20, (size_t)(8 * N0));
+    size_t want = std::max<size_t>((size_t)1 << 20, (size_t)(16 * N0));
     size_t free_b = 0, total_b = 0;
     if (cudaMemGetInfo(&free_b, &total_b) == cudaSuccess) {
         const size_t lim = free_b / 4 / sizeof(RowRec);
@@ -1080,9 +1098,11 @@ int vlmp_band_split(vlmp_session* s, int32_t lmin, int32_t lmax, int32_t parts, 
 // Lengths li_lo..li_hi (indices into [lmin, lmax]) of bands [band_lo, band_hi): a length
 // shard starts with a full-fold pass at li_lo on seeds carried there from lmin (bit-identical
 // to the single-run chain); accumulators of other lengths stay empty.
+constexpr uint32_t F_NO_SAMPLED_START = 1u << 30;   // internal: first length by full folds
+
 static int profile_impl(vlmp_session* s, int32_t lmin, int32_t lmax, int64_t band_lo,
-                        int64_t band_hi, uint32_t flags, bool* overflow_out, int li_lo = 0,
-                        int li_hi = -1) {
+                        int64_t band_hi, uint32_t flags, bool* overflow_out, bool* used_sampled,
+                        int li_lo = 0, int li_hi = -1) {
     CU(cudaSetDevice(s->device));
     cudaStream_t st = s->stream;
     const long long n = s->n, A = s->A;
@@ -1100,6 +1120,19 @@ static int profile_impl(vlmp_session* s, int32_t lmin, int32_t lmax, int64_t ban
         for (long long sg = 0; sg * S < rows; ++sg) tiles.push_back(make_int2((int)b, (int)sg));
     }
     order_tiles(tiles, N0, dl, S);
+    // a shard's first length: full folds over every SAMPLE-th band first (cheap), whose minima
+    // bound the filtered pass over all bands -- instead of full folds everywhere
+#ifndef VLMP_FIRST_SAMPLE
+#define VLMP_FIRST_SAMPLE 4
+#endif
+    constexpr int SAMPLE = VLMP_FIRST_SAMPLE;
+    std::vector<int2> tiles_s;
+    std::vector<int> smap;
+    for (size_t k = 0; k < tiles.size(); ++k)
+        if ((tiles[k].x - band_lo) % SAMPLE == 0) { tiles_s.push_back(tiles[k]); smap.push_back((int)k); }
+    const bool sampled_start = SAMPLE > 1 && (band_hi - band_lo) >= 8 * SAMPLE &&
+                               !(flags & (VLMP_F_FULL_EVERY_LENGTH | F_NO_SAMPLED_START));
+    *used_sampled = sampled_start;
     const long long T = (long long)tiles.size();
     int rc;
     if ((rc = ensure(s->d_tiles, s->tiles_cap, (size_t)std::max<long long>(T, 1)))) return rc;
@@ -1114,6 +1147,13 @@ static int profile_impl(vlmp_session* s, int32_t lmin, int32_t lmax, int64_t ban
     CU(cudaMemsetAsync(s->d_logcnt, 0, n_len * sizeof(unsigned long long), st));
     CU(cudaMemsetAsync(s->d_forced, 0, n_len * sizeof(int), st));
     if (T) CU(cudaMemcpyAsync(s->d_tiles, tiles.data(), T * sizeof(int2), cudaMemcpyHostToDevice, st));
+    const long long Ts = (long long)tiles_s.size();
+    if (sampled_start && Ts) {
+        if ((rc = ensure(s->d_tiles_s, s->tiles_s_cap, (size_t)Ts))) return rc;
+        if ((rc = ensure(s->d_smap, s->smap_cap, (size_t)Ts))) return rc;
+        CU(cudaMemcpyAsync(s->d_tiles_s, tiles_s.data(), Ts * sizeof(int2), cudaMemcpyHostToDevice, st));
+        CU(cudaMemcpyAsync(s->d_smap, smap.data(), Ts * sizeof(int), cudaMemcpyHostToDevice, st));
+    }
     const size_t smem = WARPS_PER_CTA * sizeof(WarpSmem);
     CU(cudaFuncSetAttribute(k_tile<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
     CU(cudaFuncSetAttribute(k_tile<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
@@ -1176,7 +1216,19 @@ static int profile_impl(vlmp_session* s, int32_t lmin, int32_t lmax, int64_t ban
                         s->d_counters, s->d_log, s->d_logcnt + li, eff_cap,
                         N, dl, (int)T, S, m, e, li + 1 <= li_hi,
                         s->d_colq, s->d_rowq, s->d_forced + li, s->hiC};
-            if (full) k_tile<true><<<blocks(T, WARPS_PER_CTA), WARPS_PER_CTA * 32, smem, st>>>(ta);
+            if (full && li == li_lo && sampled_start && Ts) {
+                // sampled full folds (seeds untouched) -> bounds -> filtered pass over all bands
+                TileArgs tsa = ta;
+                tsa.tiles = s->d_tiles_s; tsa.n_tiles = (int)Ts; tsa.seed_map = s->d_smap; tsa.update_seeds = 0;
+                k_tile<true><<<blocks(Ts, WARPS_PER_CTA), WARPS_PER_CTA * 32, smem, st>>>(tsa);
+                k_bound_self<<<blocks(N, 256), 256, 0, st>>>(s->d_acc + (long long)li * A, prm, N, margin);
+                k_qprep<<<blocks(A, 256), 256, 0, st>>>(prm, s->d_colq, s->d_rowq, N, A, s->sscale,
+                                                        s->d_forced + li);
+                k_tile<false><<<blocks(T, WARPS_PER_CTA), WARPS_PER_CTA * 32, smem, st>>>(ta);
+                k_log_merge<<<148 * 8, 256, 0, st>>>(s->d_log, s->d_logcnt + li, eff_cap,
+                                                     prm, e, s->d_acc + (long long)li * A, s->d_counters);
+                klaunch += 4;
+            } else if (full) k_tile<true><<<blocks(T, WARPS_PER_CTA), WARPS_PER_CTA * 32, smem, st>>>(ta);
             else {
                 k_tile<false><<<blocks(T, WARPS_PER_CTA), WARPS_PER_CTA * 32, smem, st>>>(ta);
                 k_log_merge<<<148 * 8, 256, 0, st>>>(s->d_log, s->d_logcnt + li, eff_cap,
@@ -1239,6 +1291,25 @@ static int profile_impl(vlmp_session* s, int32_t lmin, int32_t lmax, int64_t ban
     return 0;
 }
 
+// A candidate log that overflowed lost candidates: redo the run exactly -- first without the
+// sampled start (its bounds are the loosest), then with full folds at every length.
+static int profile_retrying(vlmp_session* s, int32_t lmin, int32_t lmax, int64_t band_lo, int64_t band_hi,
+                            uint32_t flags, int li_lo, int li_hi) {
+    bool overflow = false, sampled = false;
+    int rc = profile_impl(s, lmin, lmax, band_lo, band_hi, flags, &overflow, &sampled, li_lo, li_hi);
+    if (rc == 0 && overflow && sampled) {
+        rc = profile_impl(s, lmin, lmax, band_lo, band_hi, flags | F_NO_SAMPLED_START, &overflow, &sampled,
+                          li_lo, li_hi);
+        s->stats[13] = 1;
+    }
+    if (rc == 0 && overflow) {
+        rc = profile_impl(s, lmin, lmax, band_lo, band_hi, flags | VLMP_F_FULL_EVERY_LENGTH, &overflow, &sampled,
+                          li_lo, li_hi);
+        s->stats[13] = 2;
+    }
+    return rc;
+}
+
 int vlmp_profile_range(vlmp_session* s, int32_t lmin, int32_t lmax, int64_t band_lo,
                        int64_t band_hi, uint32_t flags) {
     if (!s) return fail(VLMP_E_INVALID_PARAMETERS, "null session");
@@ -1248,14 +1319,7 @@ int vlmp_profile_range(vlmp_session* s, int32_t lmin, int32_t lmax, int64_t band
     if (s->n < (long long)lmax + (lmax + 1) / 2)
         return fail(VLMP_E_SERIES_TOO_SHORT, "series cannot host a non-trivial pair at lmax");
     std::lock_guard<std::mutex> g(s->lock);
-    bool overflow = false;
-    int rc = profile_impl(s, lmin, lmax, band_lo, band_hi, flags, &overflow);
-    if (rc == 0 && overflow) {
-        // candidates were dropped (pathological bounds): exact full folds at every length
-        rc = profile_impl(s, lmin, lmax, band_lo, band_hi, flags | VLMP_F_FULL_EVERY_LENGTH, &overflow);
-        s->stats[13] = 1;
-    }
-    return rc;
+    return profile_retrying(s, lmin, lmax, band_lo, band_hi, flags, 0, -1);
 }
 
 int vlmp_profile_lengths(vlmp_session* s, int32_t lmin, int32_t lmax, int32_t li_lo, int32_t li_hi,
@@ -1269,14 +1333,8 @@ int vlmp_profile_lengths(vlmp_session* s, int32_t lmin, int32_t lmax, int32_t li
     if (s->n < (long long)lmax + (lmax + 1) / 2)
         return fail(VLMP_E_SERIES_TOO_SHORT, "series cannot host a non-trivial pair at lmax");
     std::lock_guard<std::mutex> g(s->lock);
-    bool overflow = false;
     if (li_hi < li_lo) { li_lo = lmax - lmin + 1; li_hi = -1; }   // empty shard: setup only
-    int rc = profile_impl(s, lmin, lmax, 0, -1, flags, &overflow, li_lo, li_hi);
-    if (rc == 0 && overflow) {
-        rc = profile_impl(s, lmin, lmax, 0, -1, flags | VLMP_F_FULL_EVERY_LENGTH, &overflow, li_lo, li_hi);
-        s->stats[13] = 1;
-    }
-    return rc;
+    return profile_retrying(s, lmin, lmax, 0, -1, flags, li_lo, li_hi);
 }
 
 int vlmp_partials_size(vlmp_session* s, int64_t* n_len, int64_t* stride) {

@@ -153,6 +153,8 @@ struct vlmp_session {
     double sscale = 1.0; int hiC = 896 << 20;            // filter: 2^-k scale, hi-word bias
     // tiles / seeds
     int2* d_tiles = nullptr; size_t tiles_cap = 0;
+    int2* d_tiles_s = nullptr; size_t tiles_s_cap = 0;   // sampled bands of a shard's first length
+    int* d_smap = nullptr; size_t smap_cap = 0;          // their seed slots
     double* d_seeds = nullptr; size_t seeds_cap = 0;
     // accumulators [n_len][A]
     ulonglong2* d_acc = nullptr; size_t acc_cap = 0;

@@ -388,7 +388,7 @@ def test_log_overflow_reruns_exactly(monkeypatch):
     assert ref.stats["exact_redo"] == 0
     monkeypatch.setenv("VLMP_LOG_CAP", "16")
     run = api.GpuRun(s, 32, 48)
-    assert run.stats["exact_redo"] == 1
+    assert run.stats["exact_redo"] >= 1
     for L, (mp, ip) in zip(range(32, 49), want):
         got = run.profile(L)
         assert np.array_equal(got[1], ip) and np.array_equal(got[0], mp), L
