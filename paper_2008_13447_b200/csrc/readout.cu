@@ -157,7 +157,7 @@ struct DiscArgs {
 
 __global__ void k_discords(DiscArgs a) {
     // one warp per length replays the reference's ascending-offset greedy insertion; lane r
-    // holds list entry r (sorted descending), 8 chunks of the profile are loaded ahead
+    // holds list entry r (sorted descending), 32 chunks of the profile are loaded ahead
     const int lane = threadIdx.x & 31;
     const int li = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
     if (li >= a.n_len) return;
@@ -165,7 +165,7 @@ __global__ void k_discords(DiscArgs a) {
     const long long N = a.n - m + 1;
     const long long e = (m + 1) / 2;
     const double* mp = a.mp + (long long)li * a.A;
-    constexpr int AHEAD = 8;
+    constexpr int AHEAD = 32;
     const int k = a.k;                       // <= 32
     double cd = -INFINITY; long long co = -1;
     for (long long base = 0; base < N; base += 32 * AHEAD) {
@@ -177,23 +177,36 @@ __global__ void k_discords(DiscArgs a) {
         }
 #pragma unroll
         for (int u = 0; u < AHEAD; ++u) {
-            const double thr = __shfl_sync(FULLMASK, cd, k - 1);
+            double thr = __shfl_sync(FULLMASK, cd, k - 1);
             const double d = dv8[u];
+            const long long ol = base + 32 * u + lane;
             unsigned bal = __ballot_sync(FULLMASK, (d < INFINITY) && (d > thr));
             while (bal) {
-                const int src = __ffs(bal) - 1;
-                bal &= bal - 1;
+                // every pending candidate against the current list at once: those below the
+                // first non-trivial one are trivial matches of an unchanged list (rejected as
+                // in the sequential replay); the rest are re-checked after each insertion
+                bool triv = false;
+                for (int r = 0; r < k; ++r) {
+                    const long long cr = __shfl_sync(FULLMASK, co, r);
+                    triv |= cr >= 0 && llabs(ol - cr) < e;
+                }
+                const unsigned live = bal & __ballot_sync(FULLMASK, !triv);
+                if (!live) break;
+                const int src = __ffs(live) - 1;
+                bal &= ~((2u << src) - 1u);          // src and every (trivial) candidate before it
                 const double dv = __shfl_sync(FULLMASK, d, src);
                 const long long ov = base + 32 * u + src;
                 const bool mine = lane < k;
-                if (__any_sync(FULLMASK, mine && co >= 0 && llabs(ov - co) < e)) continue;   // trivial match
                 // before the first strictly smaller entry
                 const int at = __popc(__ballot_sync(FULLMASK, mine && !(dv > cd)));
-                if (at >= k) continue;
-                const double ud = __shfl_up_sync(FULLMASK, cd, 1);
-                const long long uo = __shfl_up_sync(FULLMASK, co, 1);
-                if (mine && lane > at) { cd = ud; co = uo; }
-                if (lane == at) { cd = dv; co = ov; }
+                if (at < k) {
+                    const double ud = __shfl_up_sync(FULLMASK, cd, 1);
+                    const long long uo = __shfl_up_sync(FULLMASK, co, 1);
+                    if (mine && lane > at) { cd = ud; co = uo; }
+                    if (lane == at) { cd = dv; co = ov; }
+                    thr = __shfl_sync(FULLMASK, cd, k - 1);
+                    bal &= __ballot_sync(FULLMASK, d > thr);
+                }
             }
         }
     }
