@@ -61,9 +61,14 @@ int vlmp_set_series(vlmp_session* s, const double* t, const double* cum,
  * (vlmp_band_split) and merge the partial per-length minima with
  * vlmp_partials_* + an NCCL min all-reduce before phase 2.
  * flags: VLMP_F_FULL_EVERY_LENGTH forces the exact full-fold kernel at every
- * length (no bound filter) -- a self-check mode, slower.
+ * length (no bound filter) -- a self-check mode, slower. VLMP_F_FP64_FILTER walks the
+ * filtered lengths with the FP64 recurrence and covariance log (profile.cu k_tile<false> +
+ * k_log_merge) instead of the default FP32 walk + exact FP64 run evaluation (filter32.cu);
+ * both are exact, the flag exists for A/B checks and is the fallback the library takes
+ * itself when the FP32 run log overflows or a bound is too weak for it.
  */
 #define VLMP_F_FULL_EVERY_LENGTH 1u
+#define VLMP_F_FP64_FILTER 2u
 int vlmp_profile_range(vlmp_session* s, int32_t lmin, int32_t lmax,
                        int64_t band_lo, int64_t band_hi, uint32_t flags);
 
@@ -167,7 +172,9 @@ int vlmp_range_query(vlmp_session* s, int64_t n_q, const int64_t* owners, const 
  * out[11] flagged filter lane-rows (log records), out[12] offsets whose bound needed a direct dot product, out[13] exact redo count (1-best:
  * 1 = redone without the sampled first-length start after a log overflow, 2 = redone
  * with full folds at every length; m-best: offsets recomputed), out[14] lengths that fell back to full folds (an offset's own bound
- * too weak for the covariance-domain filter), out[15] largest per-length log fill.
+ * too weak for the covariance-domain filter), out[15] largest per-length log fill,
+ * out[16] 1 if the filtered lengths ran the FP32 walk (filter32.cu), out[17] largest
+ * per-length run count of that walk, out[18] cells evaluated exactly in its runs (n_out <= 20).
  */
 int vlmp_stats(vlmp_session* s, double* out, int32_t n_out);
 

@@ -53,6 +53,7 @@ SIGNATURES = {
 }
 
 FLAG_FULL_EVERY_LENGTH = 1
+FLAG_FP64_FILTER = 2
 
 _lib = None
 _lib_lock = threading.Lock()
@@ -235,11 +236,12 @@ class Session:
         return d, o
 
     def stats(self):
-        out = np.zeros(16)
-        self._check(self.lib.vlmp_stats(self.h, _ptr(out), 16))
+        out = np.zeros(20)
+        self._check(self.lib.vlmp_stats(self.h, _ptr(out), 20))
         keys = ["profile_ms", "finalize_ms", "executed_updates", "W", "tile_ms", "tile_launches",
                 "filtered_lengths", "full_lengths", "slow_merges", "kernel_launches", "first_tile_ms",
-                "slow_rowsteps", "bound_fixes", "exact_redo", "fallback_lengths", "max_log_records"]
+                "slow_rowsteps", "bound_fixes", "exact_redo", "fallback_lengths", "max_log_records",
+                "fp32_walk", "max_runs", "run_cells", "reserved"]
         return {k: float(out[i]) for i, k in enumerate(keys)}
 
     def event_record(self, slot):

@@ -1,0 +1,471 @@
+// filter32.cu -- the per-length tile walk with an FP32 bound filter, and the exact FP64
+// evaluation of the cells it passes (1-best mode, lengths after a run's first).
+//
+// Same job as profile.cu's k_tile<false> + k_log_merge: every non-trivial cell (i, j) whose key
+// r = 1 - cov(i,j) inv_i inv_j could beat the bound U of its row or its column must be folded
+// into acc with its exact key. The walk needs only an approximate covariance to decide that,
+// so it runs the diagonal recurrence (SCAMP form)
+//     cov(i,j) = cov(i-1,j-1) + df_i dg_j + df_j dg_i
+// in FP32 from each tile's FP64 seed, with a rigorous error slack eps folded into the seed:
+//   |cov32 - cov| <= (4 S + 16) 2^-24 * 1.05 * max_rows(mag) * max_cols(mag)  (mag >= ||x||, |df|, |dg|)
+// (two roundings per FFMA, the FP32 inputs, the seed conversion; |cov| <= s_i s_j by
+// Cauchy-Schwarz). A cell passes when cov32 + eps >= cA_j b_i, where cA_j b_i <= q(max(U_i,U_j))
+// s_i s_j (profile.cu's covariance-domain threshold, in FP32 rounded down): one FFMA per cell,
+// its sign bit ANDed over the lane's cells. Passing cells are grouped into runs along their
+// diagonals (the lane tracks which of its diagonals passed at its previous flagged row) and
+// logged; k_runs evaluates each run exactly: a centred FP64 dot product at the run's first cell,
+// the FP64 recurrence (as an ordered warp scan) along the run, the reference key formula, the
+// exact hi(r) <= U tests and the 128-bit CAS fold. Nothing approximate reaches acc.
+//
+// Lane geometry: each lane owns D2 consecutive diagonals; a tile is 32 D2 diagonals x S rows
+// (D2 = 16: two neighbouring FP64 tiles of the same row segment, whose FP64 seeds it reads and
+// carries to the next length with the FP64 kernel's own Welford step -- bit-identical seeds).
+
+#include "vlmp_internal.cuh"
+
+namespace vlmp_impl {
+
+#ifndef VLMP_D2
+#define VLMP_D2 16
+#endif
+constexpr int D2 = VLMP_D2;                 // diagonals per lane (FP32 walk)
+constexpr int BAND2 = 32 * D2;              // diagonals per FP32 tile
+constexpr int LPT = BAND / D2;              // lanes per FP64 tile (16 or 32)
+constexpr int GR2 = D2;                     // rows per staging group (ring returns to phase)
+constexpr int CQS = 33;                     // staged column-factor row stride (entries)
+static_assert(D2 == 8 || D2 == 16, "D2: 8 or 16");
+#ifndef VLMP_FILTER32_WARPS_PER_SM
+#define VLMP_FILTER32_WARPS_PER_SM 20
+#endif
+
+// ---------------------------------------------------------------------------------
+// per-length FP32 factors (after k_bound2 wrote U): p32 = {df, dg, b, w}, cq = {a, b}, where
+// b = s 2^-k (rounded down), a = q(U) b, w = q(max U over rows o .. o+D2-1); +inf factors for
+// invalid windows. magblk[o / 256] = max over the block of mag = max(||x_o||, |df_o|, |dg_o|) 2^-k
+// (rounded up; ||x|| from the prefix sums plus their rounding allowance).
+struct Prep32Args {
+    const Prm* prm; const double* cum; const double* cum2;
+    float4* p32; float2* cq; unsigned* magblk;
+    long long N, A; int m; double sscale; int* forced;
+};
+
+__global__ void __launch_bounds__(256) k_prep32(Prep32Args a) {
+    const long long o = blockIdx.x * 256LL + threadIdx.x;
+    float mag = 0.f;
+    if (o < a.A) {
+        const Prm p = a.prm[o];
+        const float df = (float)(p.df * a.sscale), dg = (float)(p.dg * a.sscale);
+        float b = INFINITY, w = 3.0e38f, ca = INFINITY;
+        if (o < a.N) {
+            float uw = -INFINITY;
+#pragma unroll
+            for (int k = 0; k < D2; ++k)
+                if (o + k < a.N) uw = fmaxf(uw, a.prm[o + k].U);
+            if (uw != -INFINITY) w = __double2float_rd(qfac(uw));
+            if (p.inv == p.inv) {
+                b = qscale(p.inv, a.sscale);
+                ca = __double2float_rd(qfac(p.U) * (double)b);
+                if (a.forced && q_forced(p, a.sscale)) atomicOr(a.forced, 1);
+            }
+            const double L = (double)a.m;
+            const double s = a.cum[o + a.m] - a.cum[o], ss = a.cum2[o + a.m] - a.cum2[o];
+            const double mu = s / L;
+            const double vu = fmax(ss / L - mu * mu, 0.0) + 0x1p-44 * (fabs(ss) / L + mu * mu);
+            const double nrm = sqrt(vu * L) * a.sscale;
+            const double mx = fmax(nrm, fmax(fabs(p.df), fabs(p.dg)) * a.sscale);
+            mag = __double2float_ru(mx * (1.0 + 0x1p-20));
+        }
+        a.p32[o] = make_float4(df, dg, b, w);
+        a.cq[o] = make_float2(ca, b);
+    }
+    // one 256-offset block per CTA: max over the block (non-negative floats order as integers)
+    unsigned v = __reduce_max_sync(FULLMASK, __float_as_uint(mag));
+    __shared__ unsigned wm[8];
+    if ((threadIdx.x & 31) == 0) wm[threadIdx.x >> 5] = v;
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        unsigned r = 0;
+#pragma unroll
+        for (int k = 0; k < 8; ++k) r = max(r, wm[k]);
+        a.magblk[blockIdx.x] = r;
+    }
+}
+
+// ---------------------------------------------------------------------------------
+struct Tile32Args {
+    const float4* p32; const float2* cq; const unsigned* magblk;
+    const double* tn; const double* mu; double* seeds;
+    const int2* tiles;      // FP64 tile list (band, segment)
+    const int2* tiles32;    // FP32 tiles: {FP64 tile of the lower band, of the upper band or -1}
+    Run* runs; unsigned long long* run_count; long long run_cap;
+    unsigned long long* counters;   // [2] flagged lane-rows, [3] runs
+    const int* forced;
+    long long N, dlo; int n_tiles32, S, m, e, update_seeds;
+    double sscale;
+};
+
+struct Smem32 {
+    float4 row[2][GR2];          // {df, dg, b, w} of the group's rows
+    float4 fresh[2][GR2];        // the column entering lane 31's ring at each row of the group
+    float2 cq[2][GR2 * CQS];     // (a, b) of the column entering lane L at row kk: [kk * 33 + L]
+    unsigned short rs[32 * D2];  // run start (row within the tile) per lane and diagonal
+    unsigned short msk[32 * GR2];   // exact FP32 pass masks of a lane's flagged rows in a group
+};
+
+struct Plan32 {
+    const char* src_rf; unsigned dst_rf;   // rows (lanes < GR2) / fresh columns (lanes 16..)
+    const char* src_cq; unsigned dst_cq;   // entering column factors, D2 entries per lane
+};
+constexpr unsigned RF_BUF = sizeof(float4) * GR2;
+constexpr unsigned CQ2_BUF = sizeof(float2) * GR2 * CQS;
+
+template <int OFF_D, int OFF_S, int BYTES>
+__device__ __forceinline__ void cpa(unsigned d, const char* s) {
+    if (BYTES == 16)
+        asm volatile("cp.async.cg.shared.global [%0+%2], [%1+%3], 16;\n" :: "r"(d), "l"(s), "n"(OFF_D), "n"(OFF_S) : "memory");
+    else
+        asm volatile("cp.async.ca.shared.global [%0+%2], [%1+%3], 8;\n" :: "r"(d), "l"(s), "n"(OFF_D), "n"(OFF_S) : "memory");
+}
+
+template <int K>
+__device__ __forceinline__ void stage_cq2(unsigned dc, const char* sc) {
+    if constexpr (K < D2) {
+        // entry f = lane + 32 K -> (kk, L) = (f % D2, f / D2) -> slot kk * 33 + L
+        cpa<K * (32 / D2) * 8, K * 256, 8>(dc, sc);
+        stage_cq2<K + 1>(dc, sc);
+    }
+}
+
+__device__ __forceinline__ void stage32(const Plan32& p, int g, int b, int lane) {
+    const long long gr = (long long)g * (GR2 * sizeof(float4));
+    if ((lane & 15) < GR2) cpa<0, 0, 16>(p.dst_rf + (unsigned)b * RF_BUF, p.src_rf + gr);
+    stage_cq2<0>(p.dst_cq + (unsigned)b * CQ2_BUF, p.src_cq + (long long)g * (GR2 * sizeof(float2)));
+    cp_async_commit();
+}
+
+__global__ void __launch_bounds__(32, VLMP_FILTER32_WARPS_PER_SM) k_tile32(Tile32Args a) {
+    extern __shared__ __align__(128) unsigned char smem_raw[];
+    Smem32& sm = *reinterpret_cast<Smem32*>(smem_raw);
+    const int lane = threadIdx.x;
+    const int wid = blockIdx.x;
+    if (wid >= a.n_tiles32) return;
+    if (*a.forced) return;   // weak bounds: the host re-runs this set of lengths on the FP64 path
+    const int2 pr2 = a.tiles32[wid];
+    const int2 tA = a.tiles[pr2.x];
+    const long long d0 = a.dlo + (long long)tA.x * BAND;
+    const long long i0 = (long long)tA.y * a.S;
+    const long long rows_valid = a.N - d0 - i0;
+    // halves (FP64 tiles): empty or entirely trivial ones stay so at later lengths
+    const bool liveA = rows_valid > 0 && d0 + BAND - 1 >= a.e;
+    const bool liveB = pr2.y >= 0 && rows_valid - BAND > 0 && d0 + 2 * BAND - 1 >= a.e;
+    if (!liveA && !liveB) return;
+    const int half = lane / LPT;
+    const bool live = half == 0 ? liveA : liveB;
+    const int nrows = (int)(rows_valid < a.S ? rows_valid : a.S);
+    const int ngroups = (nrows + GR2 - 1) / GR2;
+    const long long cbase = i0 + d0 + (long long)D2 * lane;   // column of slot 0 at row i0
+
+    // ---- slack: rows [i0, i0 + nrows), columns [i0 + d0, i0 + nrows - 1 + d0 + BAND2 - 1]
+    float eps;
+    {
+        const long long rb0 = i0 >> 8, rb1 = (i0 + nrows - 1) >> 8;
+        const long long cb0 = (i0 + d0) >> 8, cb1 = (i0 + nrows - 1 + d0 + BAND2 - 1) >> 8;
+        unsigned mr = 0, mc = 0;
+        for (long long k = rb0 + lane; k <= rb1; k += 32) mr = max(mr, a.magblk[k]);
+        for (long long k = cb0 + lane; k <= cb1; k += 32) mc = max(mc, a.magblk[k]);
+        mr = __reduce_max_sync(FULLMASK, mr);
+        mc = __reduce_max_sync(FULLMASK, mc);
+        const double bound = (4.0 * a.S + 16.0) * 0x1p-24 * 1.05 *
+                             (double)__uint_as_float(mr) * (double)__uint_as_float(mc);
+        eps = __double2float_ru(bound);
+    }
+
+    // ---- seeds: FP64 cov at row i0 (carried to length m+1 in place, as k_tile does)
+    float cov[D2];
+    {
+        const int w64 = half == 0 ? pr2.x : pr2.y;
+        double* seedp = a.seeds + (long long)(live ? w64 : 0) * BAND + (lane % LPT) * D2;
+        const double s2 = a.sscale * a.sscale;
+        double xi = 0.0;
+        if (live && a.update_seeds) {
+            const double wgt = (double)a.m / (double)(a.m + 1);
+            xi = (a.tn[i0 + a.m] - a.mu[i0]) * wgt;
+        }
+#pragma unroll
+        for (int s = 0; s < D2; ++s) {
+            cov[s] = -INFINITY;
+            if (live) {
+                const double c = seedp[s];
+                if (a.update_seeds) seedp[s] = fma(xi, a.tn[cbase + s + a.m] - a.mu[cbase + s], c);
+                if (d0 + D2 * lane + s >= a.e) cov[s] = __fadd_ru((float)(c * s2), eps);
+            }
+        }
+    }
+
+    // ---- column ring (profile.cu tile_body): phys p < D2-1 = slot p at row i0, phys D2-1 =
+    // the column leaving slot 0 at row i0-1; cA = min(a_c, w_entry b_c) per resident column
+    float cdf[D2], cdg[D2], cA[D2];
+    {
+        const float w0 = a.p32[i0].w;
+#pragma unroll
+        for (int s = 0; s < D2; ++s) {
+            const long long c = s < D2 - 1 ? cbase + s : cbase - 1;
+            const float4 pc = a.p32[c];
+            cdf[s] = pc.x; cdg[s] = pc.y;
+            const float2 q = a.cq[c];
+            cA[s] = fminf(q.x, __fmul_rd(w0, q.y));
+        }
+        // pre-adjust so that the uniform recurrence at row i0 reproduces the seed
+        const float4 pr = a.p32[i0];
+        const float4 pl = a.p32[cbase + D2 - 1];
+#pragma unroll
+        for (int s = 0; s < D2; ++s) {
+            const float df = s < D2 - 1 ? cdf[s] : pl.x, dg = s < D2 - 1 ? cdg[s] : pl.y;
+            cov[s] = fmaf(-df, pr.y, cov[s]);
+            cov[s] = fmaf(-pr.x, dg, cov[s]);
+        }
+    }
+
+    // ---- staging plan
+    Plan32 plan;
+    {
+        const int q = lane & 15;
+        if (lane < 16) {
+            plan.src_rf = reinterpret_cast<const char*>(a.p32 + i0 + q);
+            plan.dst_rf = (unsigned)__cvta_generic_to_shared(&sm.row[0][q < GR2 ? q : 0]);
+        } else {
+            plan.src_rf = reinterpret_cast<const char*>(a.p32 + i0 + q + d0 + BAND2 - 1);
+            plan.dst_rf = (unsigned)__cvta_generic_to_shared(&sm.fresh[0][q < GR2 ? q : 0]);
+        }
+        plan.src_cq = reinterpret_cast<const char*>(a.cq + i0 + d0 + D2 - 1 + lane);
+        plan.dst_cq = (unsigned)__cvta_generic_to_shared(&sm.cq[0][(lane % D2) * CQS + lane / D2]);
+    }
+
+    // ---- runs. A flagged row's exact FP32 mask is recomputed at the next row (before the ring
+    // moves on) and parked in shared memory; once per group the lane folds its flagged rows,
+    // in row order, into runs: open = diagonals that passed at its last flagged row last_r.
+    unsigned open = 0;
+    int last_r = -2;
+    unsigned nslow = 0;
+    unsigned short* rs = sm.rs + lane * D2;
+    unsigned short* msk = sm.msk + lane * GR2;
+    auto emit = [&](int s, int r_start, int r_end) {
+        const unsigned long long at = atomicAdd(a.run_count, 1ull);
+        if ((long long)at < a.run_cap) {
+            Run rr;
+            rr.i = (int)(i0 + r_start); rr.j = rr.i + (int)(d0 + D2 * lane) + s; rr.len = r_end - r_start + 1;
+            rr.pad = 0;
+            a.runs[at] = rr;
+        }
+    };
+    // rows gbase + t for the set bits t of flags (ascending), masks in msk[t]
+    auto fold_rows = [&](unsigned flags, int gbase) {
+        while (flags) {
+            const int t = __ffs(flags) - 1; flags &= flags - 1;
+            const int r = gbase + t;
+            const unsigned mask = msk[t];
+            unsigned ended, started;
+            int endr;
+            if (last_r == r - 1) { ended = open & ~mask; started = mask & ~open; endr = r - 1; }
+            else { ended = open; started = mask; endr = last_r; }
+            while (ended) { const int q = __ffs(ended) - 1; ended &= ended - 1; emit(q, rs[q], endr); }
+            while (started) { const int q = __ffs(started) - 1; started &= started - 1; rs[q] = (unsigned short)r; }
+            open = mask; last_r = r;
+            ++nslow;
+        }
+    };
+
+    stage32(plan, 0, 0, lane);
+    cp_async_wait_all();
+    __syncwarp();
+
+    bool pass_prev = false;
+    float bprev = 0.f;
+    unsigned gflags = 0;      // flagged rows of the current group (bit kk)
+    for (int g = 0; g < ngroups; ++g) {
+        const int b = g & 1;
+        if (g + 1 < ngroups) stage32(plan, g + 1, b ^ 1, lane);
+#pragma unroll
+        for (int kk = 0; kk < GR2; ++kk) {
+            const float4 pr = sm.row[b][kk];
+            // deferred: row kk-1 (previous group's last row at kk = 0) flagged -> its exact mask
+            if (__builtin_expect(pass_prev, 0)) {
+                const int kp = (kk + GR2 - 1) % D2;
+                unsigned mask = 0;
+#pragma unroll
+                for (int s = 0; s < D2; ++s) {
+                    const float z = fmaf(-cA[(s + kp) % D2], bprev, cov[s]);
+                    mask |= (__float_as_uint(z) >> 31 ^ 1u) << s;
+                }
+                msk[(kk + GR2 - 1) % GR2] = (unsigned short)mask;
+                gflags |= 1u << ((kk + GR2 - 1) % GR2);
+            }
+            if (kk == 0 && g > 0 && gflags) {   // the previous group's flagged rows -> runs
+                fold_rows(gflags, (g - 1) * GR2);
+                gflags = 0;
+            }
+            {   // rotation: phys (kk-1) mod D2 receives lane+1's outgoing column
+                const int q = (kk + D2 - 1) % D2;
+                if (lane == 0 && kk == 0) { const float4 f = sm.fresh[b][0]; cdf[q] = f.x; cdg[q] = f.y; }
+                cdf[q] = __shfl_sync(FULLMASK, cdf[q], (lane + 1) & 31);
+                cdg[q] = __shfl_sync(FULLMASK, cdg[q], (lane + 1) & 31);
+                const float2 cq = sm.cq[b][kk * CQS + lane];
+                cA[q] = fminf(cq.x, __fmul_rd(pr.w, cq.y));
+            }
+#pragma unroll
+            for (int s = 0; s < D2; ++s) {
+                const int p = (s + kk) % D2;
+                cov[s] = fmaf(pr.x, cdg[p], cov[s]);
+                cov[s] = fmaf(cdf[p], pr.y, cov[s]);
+            }
+            unsigned z[D2];
+#pragma unroll
+            for (int s = 0; s < D2; ++s) {
+                const int p = (s + kk) % D2;
+                z[s] = __float_as_uint(fmaf(-cA[p], pr.z, cov[s]));
+            }
+#pragma unroll
+            for (int w = 1; w < D2; w *= 2)
+#pragma unroll
+                for (int s = 0; s + w < D2; s += 2 * w) z[s] &= z[s + w];
+            pass_prev = (int)z[0] >= 0;            // some cell's z has its sign bit clear
+            bprev = pr.z;
+            if (kk + 1 < GR2 && lane == 0) {
+                // slot 0's column (phys kk) is dead after this row: fetch the next fresh one now
+                const float4 f = sm.fresh[b][kk + 1];
+                cdf[kk % D2] = f.x; cdg[kk % D2] = f.y;
+            }
+        }
+        cp_async_wait_all();
+        __syncwarp();
+    }
+    if (pass_prev) {   // the last row
+        constexpr int kp = (GR2 - 1) % D2;
+        unsigned mask = 0;
+#pragma unroll
+        for (int s = 0; s < D2; ++s) {
+            const float z = fmaf(-cA[(s + kp) % D2], bprev, cov[s]);
+            mask |= (__float_as_uint(z) >> 31 ^ 1u) << s;
+        }
+        msk[GR2 - 1] = (unsigned short)mask;
+        gflags |= 1u << (GR2 - 1);
+    }
+    if (gflags) fold_rows(gflags, (ngroups - 1) * GR2);
+    while (open) { const int q = __ffs(open) - 1; open &= open - 1; emit(q, rs[q], last_r); }
+    if (nslow) atomicAdd(a.counters + 2, (unsigned long long)nslow);
+}
+
+// ---------------------------------------------------------------------------------
+// Exact evaluation of the logged runs: one warp per run. Centred FP64 dot product at the first
+// cell (lane-strided terms, fixed xor-tree reduction), then the diagonal recurrence along the
+// run as an ordered inclusive warp scan of the per-step terms df_i dg_j + df_j dg_i; keys by
+// the full-fold formula r = 1 - cov inv_i inv_j, exact tests hi(r) <= U (row and column side,
+// as k_log_merge), 128-bit CAS folds. Deterministic (fixed reduction and scan orders).
+__global__ void __launch_bounds__(256) k_runs(const Run* __restrict__ runs, const unsigned long long* run_count,
+                                             long long cap, const Prm* __restrict__ prm,
+                                             const double* __restrict__ tn, const double* __restrict__ mu,
+                                             int m, int e, ulonglong2* acc, unsigned long long* counters) {
+    const unsigned long long cnt = *run_count;
+    const long long nr = (long long)(cnt < (unsigned long long)cap ? cnt : (unsigned long long)cap);
+    const int lane = threadIdx.x & 31;
+    const long long w0 = (blockIdx.x * (long long)blockDim.x + threadIdx.x) >> 5;
+    const long long nw = ((long long)gridDim.x * blockDim.x) >> 5;
+    unsigned long long cells = 0, merged = 0;
+    for (long long q = w0; q < nr; q += nw) {
+        const Run R = runs[q];
+        const long long i = R.i, j = R.j;
+        const double mi = mu[i], mj = mu[j];
+        double dot = 0.0;
+        for (int k = lane; k < m; k += 32) dot = fma(tn[i + k] - mi, tn[j + k] - mj, dot);
+#pragma unroll
+        for (int off = 16; off >= 1; off >>= 1) dot += __shfl_xor_sync(FULLMASK, dot, off);
+        double carry = dot;
+        const bool ok_diag = j - i >= e;
+        for (int c0 = 0; c0 < R.len; c0 += 32) {
+            const int k = c0 + lane;
+            const bool valid = k < R.len;
+            double term = 0.0, ii = 0.0, ij = 0.0;
+            float ui = -INFINITY, uj = -INFINITY;
+            if (valid) {
+                const Prm pi = prm[i + k], pj = prm[j + k];
+                if (k > 0) term = fma(pi.df, pj.dg, pj.df * pi.dg);
+                ii = pi.inv; ij = pj.inv; ui = pi.U; uj = pj.U;
+            }
+#pragma unroll
+            for (int off = 1; off < 32; off <<= 1) {
+                const double t = __shfl_up_sync(FULLMASK, term, off);
+                if (lane >= off) term += t;
+            }
+            const double cv = carry + term;
+            carry = __shfl_sync(FULLMASK, cv, 31);
+            if (valid && ok_diag) {
+                const double r = fma(-(cv * ii), ij, 1.0);
+                const float h = __int_as_float(__double2hiint(r));
+                const unsigned long long key = clamp_key(r) & ~PMASK;
+                if (h <= ui) { acc_merge(acc + i + k, key, j + k); ++merged; }
+                if (h <= uj) { acc_merge(acc + j + k, key, i + k); ++merged; }
+            }
+        }
+        if (lane == 0) cells += (unsigned long long)R.len;
+    }
+#pragma unroll
+    for (int off = 16; off >= 1; off >>= 1) {
+        merged += __shfl_xor_sync(FULLMASK, merged, off);
+        cells += __shfl_xor_sync(FULLMASK, cells, off);
+    }
+    if (lane == 0 && (merged | cells)) { atomicAdd(counters + 0, merged); atomicAdd(counters + 4, cells); }
+}
+
+// ---------------------------------------------------------------------------------
+// host side
+int tile32_width() { return D2; }
+
+size_t tile32_smem() { return sizeof(Smem32); }
+
+// FP32 tiles from the FP64 tile list: D2 = 16 pairs (band b, band b+1) of one row segment,
+// b - band_lo even; D2 = 8 keeps the FP64 tiles. Order follows the (longest-first) FP64 list.
+void build_tiles32(const std::vector<int2>& tiles, long long band_lo, std::vector<int2>& out) {
+    out.clear();
+    if (D2 == 8) {
+        for (size_t k = 0; k < tiles.size(); ++k) out.push_back(make_int2((int)k, -1));
+        return;
+    }
+    std::vector<std::pair<long long, int>> keyed;   // (band, seg) -> index
+    keyed.reserve(tiles.size());
+    auto key = [](long long b, long long g) { return (b << 32) | g; };
+    for (size_t k = 0; k < tiles.size(); ++k) keyed.push_back({key(tiles[k].x, tiles[k].y), (int)k});
+    std::sort(keyed.begin(), keyed.end());
+    auto find = [&](long long kk) {
+        auto it = std::lower_bound(keyed.begin(), keyed.end(), std::make_pair(kk, -1));
+        return (it != keyed.end() && it->first == kk) ? it->second : -1;
+    };
+    for (size_t k = 0; k < tiles.size(); ++k) {
+        if (((long long)tiles[k].x - band_lo) % 2 != 0) continue;
+        out.push_back(make_int2((int)k, find(key((long long)tiles[k].x + 1, tiles[k].y))));
+    }
+}
+
+int launch_filter32(vlmp_session* s, cudaStream_t st, const Prm* prm, const double* mu, long long N, int m, int e,
+                    long long dl, int S, int update_seeds, long long n_t32, const int* forced,
+                    ulonglong2* acc, Run* runs, unsigned long long* run_count, long long run_cap) {
+    const long long A = s->A;
+    Prep32Args pa{prm, s->d_cum, s->d_cum2, s->d_p32, s->d_cq32, s->d_magblk, N, A, m, s->sscale,
+                  const_cast<int*>(forced)};
+    k_prep32<<<blocks(A, 256), 256, 0, st>>>(pa);
+    if (n_t32) {
+        Tile32Args ta{s->d_p32, s->d_cq32, s->d_magblk, s->d_tn, mu, s->d_seeds, s->d_tiles, s->d_tiles32,
+                      runs, run_count, run_cap, s->d_counters, forced, N, dl, (int)n_t32, S, m, e,
+                      update_seeds, s->sscale};
+        k_tile32<<<(unsigned)n_t32, 32, sizeof(Smem32), st>>>(ta);
+        k_runs<<<148 * 8, 256, 0, st>>>(runs, run_count, run_cap, prm, s->d_tn, mu, m, e, acc, s->d_counters);
+    }
+    return 0;
+}
+
+int filter32_setup() {
+    cudaError_t e = cudaFuncSetAttribute(k_tile32, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sizeof(Smem32));
+    if (e != cudaSuccess) return fail(VLMP_E_CUDA, std::string("k_tile32 smem: ") + cudaGetErrorString(e));
+    return 0;
+}
+
+}  // namespace vlmp_impl

@@ -160,35 +160,7 @@ __global__ void k_bound_self(const ulonglong2* __restrict__ acc, Prm* prm, long 
     prm[o].U = u;
 }
 
-// ---------------------------------------------------------------------------------
-// Filter thresholds in the covariance domain. A cell (i, j) must reach the exact tests when
-// its key r = 1 - cov inv_i inv_j satisfies hi(r) <= max(U_i, U_j), i.e. r <= R(U) with
-// R(U) the largest double of that high word. With q(U) = 1 - R(U) - 2^-20 and s = 1/inv:
-//   r <= R(U)  =>  cov >= q(U) s_i s_j            (2^-20 >> the FP64 rounding of r)
-// so the tile kernel tests  hi(cov) >= hi(t),  t = a_j * b_i  (FP32, rounded down), with
-// b = s 2^-k (per-session power-of-two scale) and a_j = q(max(U_j, Uwin_i)) b_j -- no
-// per-cell FP64 work beyond the recurrence. q < 2^-20 (a bound at corr ~ 0) is clamped to
-// 0, which still passes every cell of positive covariance; only offsets whose OWN bound is
-// that weak may need non-positive-covariance cells: they are "forced" (1-best: the length
-// falls back to the exact full-fold kernel; m-best: the offset is recomputed exactly).
-constexpr double QSLACK = 1.0 / (1 << 20);
-
-__device__ inline double qfac(float u) {
-    const double R = __hiloint2double(__float_as_int(u), (int)0xFFFFFFFF);
-    const double q = 1.0 - R - QSLACK;
-    return q >= QSLACK ? q : 0.0;      // also 0 for u = +inf / NaN
-}
-
-__device__ inline float qscale(double inv, double sscale) {
-    return __double2float_rd((1.0 / inv) * sscale);   // NaN for an invalid window
-}
-
-// the offset's own bound is too weak for the covariance-domain filter (see above)
-__device__ inline bool q_forced(const Prm& p, double sscale) {
-    if (!(p.inv == p.inv)) return false;
-    const float b = qscale(p.inv, sscale);
-    return qfac(p.U) == 0.0 || !(b >= 0x1p-40f && b <= 0x1p40f);
-}
+// Filter thresholds in the covariance domain: qfac / qscale / q_forced (vlmp_internal.cuh).
 
 // colq[o] = (a_o = q(U_o) b_o, b_o) for columns; rowq[o] = (b_o, q(Uwin_o)) for rows, where
 // Uwin_o = max U[o .. o+D-1]: a column entering a lane at row o meets rows o .. o+D-1 there
@@ -233,35 +205,12 @@ struct TileArgs {
     const int* seed_map;           // tile list subset: seed slot of each listed tile (or nullptr)
 };
 
-__device__ inline bool key_less(unsigned long long k1, long long i1, unsigned long long k2, long long i2) {
-    return k1 < k2 || (k1 == k2 && i1 < i2);
-}
-
-// exact lexicographic (key, idx) min into a 16-byte accumulator (128-bit CAS)
-__device__ void acc_merge(ulonglong2* slot, unsigned long long key, long long idx) {
-    unsigned __int128* p = reinterpret_cast<unsigned __int128*>(slot);
-    const volatile unsigned long long* vp = reinterpret_cast<volatile unsigned long long*>(slot);
-    unsigned __int128 cur = ((unsigned __int128)vp[1] << 64) | vp[0];
-    const unsigned __int128 want = ((unsigned __int128)(unsigned long long)idx << 64) | key;
-    while (key_less(key, idx, (unsigned long long)cur, (long long)(cur >> 64))) {
-        unsigned __int128 prev = atomicCAS(p, cur, want);
-        if (prev == cur) return;
-        cur = prev;
-    }
-}
-
-__device__ inline unsigned long long clamp_key(double r) {
-    return r < 0.0 ? 0ull : (unsigned long long)__double_as_longlong(r);
-}
-
 __device__ inline double pack_low(double v, unsigned idx) {
     int lo = __double2loint(v), hi = __double2hiint(v);
     lo = (lo & ~(int)PMASK) | (int)idx;
     return __hiloint2double(hi, lo);
 }
 
-__device__ inline void cp_async_commit() { asm volatile("cp.async.commit_group;\n" ::: "memory"); }
-__device__ inline void cp_async_wait_all() { asm volatile("cp.async.wait_group 0;\n" ::: "memory"); }
 
 
 // Staging groups of GR rows. Over a group, lane L's ring receives columns
@@ -1102,7 +1051,7 @@ constexpr uint32_t F_NO_SAMPLED_START = 1u << 30;   // internal: first length by
 
 static int profile_impl(vlmp_session* s, int32_t lmin, int32_t lmax, int64_t band_lo,
                         int64_t band_hi, uint32_t flags, bool* overflow_out, bool* used_sampled,
-                        int li_lo = 0, int li_hi = -1) {
+                        int li_lo = 0, int li_hi = -1, bool* fp32_fallback = nullptr) {
     CU(cudaSetDevice(s->device));
     cudaStream_t st = s->stream;
     const long long n = s->n, A = s->A;
@@ -1154,6 +1103,24 @@ static int profile_impl(vlmp_session* s, int32_t lmin, int32_t lmax, int64_t ban
         CU(cudaMemcpyAsync(s->d_tiles_s, tiles_s.data(), Ts * sizeof(int2), cudaMemcpyHostToDevice, st));
         CU(cudaMemcpyAsync(s->d_smap, smap.data(), Ts * sizeof(int), cudaMemcpyHostToDevice, st));
     }
+    // filtered lengths: FP32 walk + exact FP64 runs (filter32.cu) unless asked for the FP64 filter
+    const bool fp32 = !(flags & VLMP_F_FP64_FILTER) && !getenv("VLMP_FP64_FILTER");
+    std::vector<int2> tiles32;
+    if (fp32) {
+        build_tiles32(tiles, band_lo, tiles32);
+        if ((rc = ensure(s->d_tiles32, s->tiles32_cap, std::max<size_t>(tiles32.size(), 1)))) return rc;
+        if (!s->d_p32) {
+            if ((rc = ensure1(s->d_p32, A))) return rc;
+            if ((rc = ensure1(s->d_cq32, A))) return rc;
+            if ((rc = ensure1(s->d_magblk, A / 256 + 1))) return rc;
+        }
+        if (!tiles32.empty())
+            CU(cudaMemcpyAsync(s->d_tiles32, tiles32.data(), tiles32.size() * sizeof(int2), cudaMemcpyHostToDevice, st));
+        if ((rc = filter32_setup())) return rc;
+    }
+    const long long T32 = (long long)tiles32.size();
+    Run* runs = reinterpret_cast<Run*>(s->d_log);
+    const long long run_cap_full = (long long)(s->log_cap * sizeof(RowRec) / sizeof(Run));
     const size_t smem = WARPS_PER_CTA * sizeof(WarpSmem);
     CU(cudaFuncSetAttribute(k_tile<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
     CU(cudaFuncSetAttribute(k_tile<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
@@ -1167,6 +1134,8 @@ static int profile_impl(vlmp_session* s, int32_t lmin, int32_t lmax, int64_t ban
     // overflow -> exact full-fold re-run path
     long long eff_cap = (long long)s->log_cap;
     if (const char* env = getenv("VLMP_LOG_CAP")) eff_cap = std::max(1LL, std::min(eff_cap, atoll(env)));
+    long long run_cap = run_cap_full;
+    if (const char* env = getenv("VLMP_LOG_CAP")) run_cap = std::max(1LL, std::min(run_cap, atoll(env)));
     if (li_lo < 0) li_lo = 0;
     if (li_hi >= n_len || (li_hi < 0 && li_lo == 0)) li_hi = n_len - 1;   // default: every length
     if (li_hi < li_lo) li_hi = -1;                                        // empty shard: no work
@@ -1202,8 +1171,9 @@ static int profile_impl(vlmp_session* s, int32_t lmin, int32_t lmax, int64_t ban
             Bound2Args ba{s->d_tn, prm, prm_prev, mu_prev, mu, s->d_acc + (long long)(li - 1) * A, prm,
                           N, N + 1, m, e, margin, s->d_fixcnt + li};
             k_bound2<<<blocks(N, 256), 256, 0, st>>>(ba);
-            k_qprep<<<blocks(A, 256), 256, 0, st>>>(prm, s->d_colq, s->d_rowq, N, A, s->sscale,
-                                                    s->d_forced + li);
+            if (!fp32)
+                k_qprep<<<blocks(A, 256), 256, 0, st>>>(prm, s->d_colq, s->d_rowq, N, A, s->sscale,
+                                                        s->d_forced + li);
             klaunch += 2;
         }
         while (s->lev.size() < (size_t)2 * (li + 1)) {
@@ -1222,14 +1192,28 @@ static int profile_impl(vlmp_session* s, int32_t lmin, int32_t lmax, int64_t ban
                 tsa.tiles = s->d_tiles_s; tsa.n_tiles = (int)Ts; tsa.seed_map = s->d_smap; tsa.update_seeds = 0;
                 k_tile<true><<<blocks(Ts, WARPS_PER_CTA), WARPS_PER_CTA * 32, smem, st>>>(tsa);
                 k_bound_self<<<blocks(N, 256), 256, 0, st>>>(s->d_acc + (long long)li * A, prm, N, margin);
-                k_qprep<<<blocks(A, 256), 256, 0, st>>>(prm, s->d_colq, s->d_rowq, N, A, s->sscale,
-                                                        s->d_forced + li);
-                k_tile<false><<<blocks(T, WARPS_PER_CTA), WARPS_PER_CTA * 32, smem, st>>>(ta);
-                k_log_merge<<<148 * 8, 256, 0, st>>>(s->d_log, s->d_logcnt + li, eff_cap,
-                                                     prm, e, s->d_acc + (long long)li * A, s->d_counters);
-                klaunch += 4;
+                if (fp32) {
+                    // the sampled folds only bound this length; its keys come from the exact runs
+                    k_fill_acc<<<blocks(A, 256), 256, 0, st>>>(s->d_acc + (long long)li * A, A);
+                    if ((rc = launch_filter32(s, st, prm, mu, N, m, e, dl, S, ta.update_seeds, T32,
+                                              s->d_forced + li, s->d_acc + (long long)li * A, runs,
+                                              s->d_logcnt + li, run_cap))) return rc;
+                    klaunch += 5;
+                } else {
+                    k_qprep<<<blocks(A, 256), 256, 0, st>>>(prm, s->d_colq, s->d_rowq, N, A, s->sscale,
+                                                            s->d_forced + li);
+                    k_tile<false><<<blocks(T, WARPS_PER_CTA), WARPS_PER_CTA * 32, smem, st>>>(ta);
+                    k_log_merge<<<148 * 8, 256, 0, st>>>(s->d_log, s->d_logcnt + li, eff_cap,
+                                                         prm, e, s->d_acc + (long long)li * A, s->d_counters);
+                    klaunch += 4;
+                }
             } else if (full) k_tile<true><<<blocks(T, WARPS_PER_CTA), WARPS_PER_CTA * 32, smem, st>>>(ta);
-            else {
+            else if (fp32) {
+                if ((rc = launch_filter32(s, st, prm, mu, N, m, e, dl, S, ta.update_seeds, T32, s->d_forced + li,
+                                          s->d_acc + (long long)li * A, runs, s->d_logcnt + li, run_cap)))
+                    return rc;
+                klaunch += 2;
+            } else {
                 k_tile<false><<<blocks(T, WARPS_PER_CTA), WARPS_PER_CTA * 32, smem, st>>>(ta);
                 k_log_merge<<<148 * 8, 256, 0, st>>>(s->d_log, s->d_logcnt + li, eff_cap,
                                                      prm, e, s->d_acc + (long long)li * A, s->d_counters);
@@ -1263,7 +1247,8 @@ static int profile_impl(vlmp_session* s, int32_t lmin, int32_t lmax, int64_t ban
     {   // a candidate log that overflowed lost candidates: the caller redoes the run exactly
         std::vector<unsigned long long> lc(n_len);
         CU(cudaMemcpy(lc.data(), s->d_logcnt, n_len * sizeof(unsigned long long), cudaMemcpyDeviceToHost));
-        for (auto c : lc) { overflow |= (long long)c > eff_cap; max_log = std::max(max_log, (double)c); }
+        const long long cap_used = fp32 ? run_cap : eff_cap;
+        for (auto c : lc) { overflow |= (long long)c > cap_used; max_log = std::max(max_log, (double)c); }
     }
     int n_forced = 0;
     double n_fix = 0;
@@ -1287,7 +1272,11 @@ static int profile_impl(vlmp_session* s, int32_t lmin, int32_t lmax, int64_t ban
     s->stats[5] = launches; s->stats[6] = n_filtered; s->stats[7] = n_full; s->stats[8] = (double)cnt[0];
     s->stats[9] = klaunch; s->stats[10] = first_ms; s->stats[11] = (double)cnt[2];
     s->stats[12] = n_fix; s->stats[14] = n_forced; s->stats[15] = max_log;
+    s->stats[16] = fp32 ? 1.0 : 0.0; s->stats[17] = fp32 ? max_log : 0.0; s->stats[18] = (double)cnt[4];
     *overflow_out = overflow;
+    // the FP32 path cannot take lengths whose own bounds are too weak, nor a lost run log:
+    // the caller re-runs the whole set on the FP64 path (which handles both exactly)
+    if (fp32_fallback) *fp32_fallback = fp32 && (overflow || n_forced > 0);
     return 0;
 }
 
@@ -1295,8 +1284,13 @@ static int profile_impl(vlmp_session* s, int32_t lmin, int32_t lmax, int64_t ban
 // sampled start (its bounds are the loosest), then with full folds at every length.
 static int profile_retrying(vlmp_session* s, int32_t lmin, int32_t lmax, int64_t band_lo, int64_t band_hi,
                             uint32_t flags, int li_lo, int li_hi) {
-    bool overflow = false, sampled = false;
-    int rc = profile_impl(s, lmin, lmax, band_lo, band_hi, flags, &overflow, &sampled, li_lo, li_hi);
+    bool overflow = false, sampled = false, fb = false;
+    int rc = profile_impl(s, lmin, lmax, band_lo, band_hi, flags, &overflow, &sampled, li_lo, li_hi, &fb);
+    if (rc == 0 && fb) {
+        flags |= VLMP_F_FP64_FILTER;
+        rc = profile_impl(s, lmin, lmax, band_lo, band_hi, flags, &overflow, &sampled, li_lo, li_hi);
+        s->stats[13] = 3;
+    }
     if (rc == 0 && overflow && sampled) {
         rc = profile_impl(s, lmin, lmax, band_lo, band_hi, flags | F_NO_SAMPLED_START, &overflow, &sampled,
                           li_lo, li_hi);

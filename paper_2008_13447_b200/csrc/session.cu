@@ -102,7 +102,7 @@ int vlmp_set_series(vlmp_session* s, const double* t, const double* cum, const d
 
 int vlmp_stats(vlmp_session* s, double* out, int32_t n_out) {
     if (!s || !out) return fail(VLMP_E_INVALID_PARAMETERS, "null argument");
-    for (int q = 0; q < n_out && q < 16; ++q) out[q] = s->stats[q];
+    for (int q = 0; q < n_out && q < 20; ++q) out[q] = s->stats[q];
     return 0;
 }
 

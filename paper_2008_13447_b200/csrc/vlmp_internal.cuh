@@ -113,6 +113,62 @@ struct __align__(32) Prm {
 struct __align__(16) RowRec { int i; int j0; int pad0, pad1; double cov[D]; };
 
 
+// ---------------------------------------------------------------------------------
+// shared device helpers (profile.cu, filter32.cu)
+__device__ inline bool key_less(unsigned long long k1, long long i1, unsigned long long k2, long long i2) {
+    return k1 < k2 || (k1 == k2 && i1 < i2);
+}
+
+// exact lexicographic (key, idx) min into a 16-byte accumulator (128-bit CAS)
+__device__ inline void acc_merge(ulonglong2* slot, unsigned long long key, long long idx) {
+    unsigned __int128* p = reinterpret_cast<unsigned __int128*>(slot);
+    const volatile unsigned long long* vp = reinterpret_cast<volatile unsigned long long*>(slot);
+    unsigned __int128 cur = ((unsigned __int128)vp[1] << 64) | vp[0];
+    const unsigned __int128 want = ((unsigned __int128)(unsigned long long)idx << 64) | key;
+    while (key_less(key, idx, (unsigned long long)cur, (long long)(cur >> 64))) {
+        unsigned __int128 prev = atomicCAS(p, cur, want);
+        if (prev == cur) return;
+        cur = prev;
+    }
+}
+
+__device__ inline unsigned long long clamp_key(double r) {
+    return r < 0.0 ? 0ull : (unsigned long long)__double_as_longlong(r);
+}
+
+__device__ inline void cp_async_commit() { asm volatile("cp.async.commit_group;\n" ::: "memory"); }
+__device__ inline void cp_async_wait_all() { asm volatile("cp.async.wait_group 0;\n" ::: "memory"); }
+
+// Filter thresholds in the covariance domain (profile.cu k_qprep, filter32.cu k_prep32). A cell
+// (i, j) must reach the exact tests when its key r = 1 - cov inv_i inv_j satisfies
+// hi(r) <= max(U_i, U_j), i.e. r <= R(U) with R(U) the largest double of that high word. With
+// q(U) = 1 - R(U) - 2^-20 and s = 1/inv:  r <= R(U)  =>  cov >= q(U) s_i s_j  (2^-20 >> the
+// FP64 rounding of r). q < 2^-20 (a bound at corr ~ 0) is clamped to 0, which still passes every
+// cell of positive covariance; only offsets whose OWN bound is that weak may need
+// non-positive-covariance cells: they are "forced" (the length falls back to exact full folds).
+constexpr double QSLACK = 1.0 / (1 << 20);
+
+__device__ inline double qfac(float u) {
+    const double R = __hiloint2double(__float_as_int(u), (int)0xFFFFFFFF);
+    const double q = 1.0 - R - QSLACK;
+    return q >= QSLACK ? q : 0.0;      // also 0 for u = +inf / NaN
+}
+
+__device__ inline float qscale(double inv, double sscale) {
+    return __double2float_rd((1.0 / inv) * sscale);   // NaN for an invalid window
+}
+
+// the offset's own bound is too weak for the covariance-domain filter (see above)
+__device__ inline bool q_forced(const Prm& p, double sscale) {
+    if (!(p.inv == p.inv)) return false;
+    const float b = qscale(p.inv, sscale);
+    return qfac(p.U) == 0.0 || !(b >= 0x1p-40f && b <= 0x1p40f);
+}
+
+// FP32 filter (filter32.cu): a run of consecutive passing cells along one diagonal of a tile,
+// (i, j), (i+1, j+1), ..., len cells; evaluated exactly in FP64 by k_runs
+struct __align__(16) Run { int i; int j; int len; int pad; };
+
 template <class T>
 int ensure(T*& p, size_t& cap, size_t count) {
     if (count <= cap && p) return 0;
@@ -149,6 +205,9 @@ struct vlmp_session {
     long long* d_previdx = nullptr;
     float2* d_colq = nullptr; float2* d_rowq = nullptr;   // filter factors (k_qprep)
     int* d_forced = nullptr; size_t forced_cap = 0;      // per-length: full-fold fallback
+    float4* d_p32 = nullptr; float2* d_cq32 = nullptr;   // FP32 filter: {df, dg, b, w}, {a, b}
+    unsigned* d_magblk = nullptr;                        // FP32 filter: per-256-offset magnitude bound
+    int2* d_tiles32 = nullptr; size_t tiles32_cap = 0;   // FP32 filter tiles (pairs of FP64 tiles)
     unsigned long long* d_fixcnt = nullptr; size_t fixcnt_cap = 0;   // per-length re-bounded offsets
     double sscale = 1.0; int hiC = 896 << 20;            // filter: 2^-k scale, hi-word bias
     // tiles / seeds
@@ -178,6 +237,17 @@ struct vlmp_session {
     long long* d_redo = nullptr; size_t redo_cap = 0;
     // run state
     int lmin = 0, lmax = 0, n_len = 0; bool have_profile = false, have_final = false, have_finals = false;
-    double stats[16] = {};
+    double stats[20] = {};
     std::vector<cudaEvent_t> lev;   // 2 per length: tile-kernel start/stop
 };
+
+namespace vlmp_impl {
+// filter32.cu
+int tile32_width();
+size_t tile32_smem();
+int filter32_setup();
+void build_tiles32(const std::vector<int2>& tiles, long long band_lo, std::vector<int2>& out);
+int launch_filter32(vlmp_session* s, cudaStream_t st, const Prm* prm, const double* mu, long long N, int m, int e,
+                    long long dl, int S, int update_seeds, long long n_t32, const int* forced,
+                    ulonglong2* acc, Run* runs, unsigned long long* run_count, long long run_cap);
+}  // namespace vlmp_impl
