@@ -35,7 +35,7 @@ constexpr int GR2 = D2;                     // rows per staging group (ring retu
 constexpr int CQS = 33;                     // staged column-factor row stride (entries)
 static_assert(D2 == 8 || D2 == 16, "D2: 8 or 16");
 #ifndef VLMP_FILTER32_WARPS_PER_SM
-#define VLMP_FILTER32_WARPS_PER_SM 20
+#define VLMP_FILTER32_WARPS_PER_SM 16   // 128 registers: no spills (20 warps at 96 spill the staging plan)
 #endif
 
 // ---------------------------------------------------------------------------------
@@ -94,7 +94,7 @@ __global__ void __launch_bounds__(256) k_prep32(Prep32Args a) {
 // ---------------------------------------------------------------------------------
 struct Tile32Args {
     const float4* p32; const float2* cq; const unsigned* magblk;
-    const double* tn; const double* mu; double* seeds;
+    const double* __restrict__ tn; const double* __restrict__ mu; double* seeds;
     const int2* tiles;      // FP64 tile list (band, segment)
     const int2* tiles32;    // FP32 tiles: {FP64 tile of the lower band, of the upper band or -1}
     Run* runs; unsigned long long* run_count; long long run_cap;
@@ -143,6 +143,14 @@ __device__ __forceinline__ void stage32(const Plan32& p, int g, int b, int lane)
     cp_async_commit();
 }
 
+// the flagged-row mask is recomputed from cov / cA (live anyway) instead of keeping the row's
+// z values alive across rows: volatile, so the compiler cannot merge it with the fast path's FMAs
+__device__ __forceinline__ float fma_nocse(float a, float b, float c) {
+    float d;
+    asm volatile("fma.rn.f32 %0, %1, %2, %3;" : "=f"(d) : "f"(a), "f"(b), "f"(c));
+    return d;
+}
+
 __global__ void __launch_bounds__(32, VLMP_FILTER32_WARPS_PER_SM) k_tile32(Tile32Args a) {
     extern __shared__ __align__(128) unsigned char smem_raw[];
     Smem32& sm = *reinterpret_cast<Smem32*>(smem_raw);
@@ -180,26 +188,28 @@ __global__ void __launch_bounds__(32, VLMP_FILTER32_WARPS_PER_SM) k_tile32(Tile3
         eps = __double2float_ru(bound);
     }
 
-    // ---- seeds: FP64 cov at row i0 (carried to length m+1 in place, as k_tile does)
+    // ---- seeds: FP64 cov at row i0 (carried to length m+1 in place, as k_tile does). All
+    // loads first (one batch), then the Welford step and the stores.
     float cov[D2];
     {
         const int w64 = half == 0 ? pr2.x : pr2.y;
-        double* seedp = a.seeds + (long long)(live ? w64 : 0) * BAND + (lane % LPT) * D2;
+        double* __restrict__ seedp = a.seeds + (long long)(live ? w64 : 0) * BAND + (lane % LPT) * D2;
         const double s2 = a.sscale * a.sscale;
-        double xi = 0.0;
+        double c64[D2];
+#pragma unroll
+        for (int s = 0; s < D2; ++s) c64[s] = live ? seedp[s] : 0.0;
         if (live && a.update_seeds) {
             const double wgt = (double)a.m / (double)(a.m + 1);
-            xi = (a.tn[i0 + a.m] - a.mu[i0]) * wgt;
+            const double xi = (a.tn[i0 + a.m] - a.mu[i0]) * wgt;
+            double xs[D2];
+#pragma unroll
+            for (int s = 0; s < D2; ++s) xs[s] = a.tn[cbase + s + a.m] - a.mu[cbase + s];
+#pragma unroll
+            for (int s = 0; s < D2; ++s) seedp[s] = fma(xi, xs[s], c64[s]);
         }
 #pragma unroll
-        for (int s = 0; s < D2; ++s) {
-            cov[s] = -INFINITY;
-            if (live) {
-                const double c = seedp[s];
-                if (a.update_seeds) seedp[s] = fma(xi, a.tn[cbase + s + a.m] - a.mu[cbase + s], c);
-                if (d0 + D2 * lane + s >= a.e) cov[s] = __fadd_ru((float)(c * s2), eps);
-            }
-        }
+        for (int s = 0; s < D2; ++s)
+            cov[s] = (live && d0 + D2 * lane + s >= a.e) ? __fadd_ru((float)(c64[s] * s2), eps) : -INFINITY;
     }
 
     // ---- column ring (profile.cu tile_body): phys p < D2-1 = slot p at row i0, phys D2-1 =
@@ -294,7 +304,7 @@ __global__ void __launch_bounds__(32, VLMP_FILTER32_WARPS_PER_SM) k_tile32(Tile3
                 unsigned mask = 0;
 #pragma unroll
                 for (int s = 0; s < D2; ++s) {
-                    const float z = fmaf(-cA[(s + kp) % D2], bprev, cov[s]);
+                    const float z = fma_nocse(-cA[(s + kp) % D2], bprev, cov[s]);
                     mask |= (__float_as_uint(z) >> 31 ^ 1u) << s;
                 }
                 msk[(kk + GR2 - 1) % GR2] = (unsigned short)mask;

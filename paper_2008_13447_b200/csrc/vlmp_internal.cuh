@@ -205,8 +205,9 @@ struct vlmp_session {
     long long* d_previdx = nullptr;
     float2* d_colq = nullptr; float2* d_rowq = nullptr;   // filter factors (k_qprep)
     int* d_forced = nullptr; size_t forced_cap = 0;      // per-length: full-fold fallback
-    float4* d_p32 = nullptr; float2* d_cq32 = nullptr;   // FP32 filter: {df, dg, b, w}, {a, b}
-    unsigned* d_magblk = nullptr;                        // FP32 filter: per-256-offset magnitude bound
+    float4* d_p32 = nullptr; size_t p32_cap = 0;         // FP32 filter: {df, dg, b, w}
+    float2* d_cq32 = nullptr; size_t cq32_cap = 0;       // FP32 filter: {a, b}
+    unsigned* d_magblk = nullptr; size_t magblk_cap = 0; // FP32 filter: per-256-offset magnitude bound
     int2* d_tiles32 = nullptr; size_t tiles32_cap = 0;   // FP32 filter tiles (pairs of FP64 tiles)
     unsigned long long* d_fixcnt = nullptr; size_t fixcnt_cap = 0;   // per-length re-bounded offsets
     double sscale = 1.0; int hiC = 896 << 20;            // filter: 2^-k scale, hi-word bias
