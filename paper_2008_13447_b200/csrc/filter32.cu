@@ -65,7 +65,14 @@ __global__ void __launch_bounds__(256) k_prep32(Prep32Args a) {
             if (p.inv == p.inv) {
                 b = qscale(p.inv, a.sscale);
                 ca = __double2float_rd(qfac(p.U) * (double)b);
-                if (a.forced && q_forced(p, a.sscale)) atomicOr(a.forced, 1);
+                if (q_forced(p, a.sscale)) {
+                    // bound too weak for the covariance-domain test (or b out of range): every
+                    // cell of this offset passes -- as a column cA = -inf (z = +inf), as a row
+                    // b = NaN (z = NaN, sign bit clear); k_runs evaluates them exactly
+                    ca = -INFINITY;
+                    b = __int_as_float(0x7FC00000);
+                    if (a.forced) atomicOr(a.forced, 1);
+                }
             }
             const double L = (double)a.m;
             const double s = a.cum[o + a.m] - a.cum[o], ss = a.cum2[o + a.m] - a.cum2[o];
@@ -76,7 +83,7 @@ __global__ void __launch_bounds__(256) k_prep32(Prep32Args a) {
             mag = __double2float_ru(mx * (1.0 + 0x1p-20));
         }
         a.p32[o] = make_float4(df, dg, b, w);
-        a.cq[o] = make_float2(ca, b);
+        a.cq[o] = make_float2(ca, b == b ? b : 1.0f);
     }
     // one 256-offset block per CTA: max over the block (non-negative floats order as integers)
     unsigned v = __reduce_max_sync(FULLMASK, __float_as_uint(mag));
@@ -157,7 +164,6 @@ __global__ void __launch_bounds__(32, VLMP_FILTER32_WARPS_PER_SM) k_tile32(Tile3
     const int lane = threadIdx.x;
     const int wid = blockIdx.x;
     if (wid >= a.n_tiles32) return;
-    if (*a.forced) return;   // weak bounds: the host re-runs this set of lengths on the FP64 path
     const int2 pr2 = a.tiles32[wid];
     const int2 tA = a.tiles[pr2.x];
     const long long d0 = a.dlo + (long long)tA.x * BAND;
@@ -381,15 +387,25 @@ __global__ void __launch_bounds__(256) k_runs(const Run* __restrict__ runs, cons
     const long long w0 = (blockIdx.x * (long long)blockDim.x + threadIdx.x) >> 5;
     const long long nw = ((long long)gridDim.x * blockDim.x) >> 5;
     unsigned long long cells = 0, merged = 0;
+    // warp-cooperative centred dot product of windows (a, b): lane-strided terms, fixed xor tree
+    auto wdot = [&](long long a_, long long b_) {
+        const double ma = mu[a_], mb = mu[b_];
+        double d = 0.0;
+        for (int k = lane; k < m; k += 32) d = fma(tn[a_ + k] - ma, tn[b_ + k] - mb, d);
+#pragma unroll
+        for (int off = 16; off >= 1; off >>= 1) d += __shfl_xor_sync(FULLMASK, d, off);
+        return d;
+    };
     for (long long q = w0; q < nr; q += nw) {
         const Run R = runs[q];
         const long long i = R.i, j = R.j;
-        const double mi = mu[i], mj = mu[j];
-        double dot = 0.0;
-        for (int k = lane; k < m; k += 32) dot = fma(tn[i + k] - mi, tn[j + k] - mj, dot);
-#pragma unroll
-        for (int off = 16; off >= 1; off >>= 1) dot += __shfl_xor_sync(FULLMASK, dot, off);
+        const double dot = wdot(i, j);
         double carry = dot;
+        // magnitude carried by the recurrence: |cov at the last exact point| + sum |steps| since.
+        // Its rounding error is below 2^-47 of that (<= 160 roundings of 2^-53 each); a cell whose
+        // own scale s_i s_j is below 1/8 of it (error above 2^-44 of the cell's scale, the key
+        // resolution) is recomputed directly -- a run that walks out of a high-variance stretch.
+        double mag = fabs(dot);
         const bool ok_diag = j - i >= e;
         for (int c0 = 0; c0 < R.len; c0 += 32) {
             const int k = c0 + lane;
@@ -401,13 +417,32 @@ __global__ void __launch_bounds__(256) k_runs(const Run* __restrict__ runs, cons
                 if (k > 0) term = fma(pi.df, pj.dg, pj.df * pi.dg);
                 ii = pi.inv; ij = pj.inv; ui = pi.U; uj = pj.U;
             }
+            double at = fabs(term);
 #pragma unroll
             for (int off = 1; off < 32; off <<= 1) {
                 const double t = __shfl_up_sync(FULLMASK, term, off);
-                if (lane >= off) term += t;
+                const double ta = __shfl_up_sync(FULLMASK, at, off);
+                if (lane >= off) { term += t; at += ta; }
             }
-            const double cv = carry + term;
-            carry = __shfl_sync(FULLMASK, cv, 31);
+            double cv = carry + term;
+            const double scale = 1.0 / (ii * ij);   // s_i s_j (NaN / 0 for invalid windows)
+            const bool inexact = valid && ok_diag && !((mag + at) <= 8.0 * scale);
+            unsigned redo = __ballot_sync(FULLMASK, inexact);
+            if (redo) {   // rare: exact direct sums for the flagged cells of this chunk
+                const unsigned tail = __ballot_sync(FULLMASK, valid);
+                const int last = 31 - __clz(tail);
+                redo |= 1u << last;              // the carry restarts from an exact value
+                while (redo) {
+                    const int l = __ffs(redo) - 1; redo &= redo - 1;
+                    const double d = wdot(i + c0 + l, j + c0 + l);
+                    if (lane == l) cv = d;
+                }
+                const double cl = __shfl_sync(FULLMASK, cv, last);
+                carry = cl; mag = fabs(cl);
+            } else {
+                carry = __shfl_sync(FULLMASK, cv, 31);
+                mag += __shfl_sync(FULLMASK, at, 31);
+            }
             if (valid && ok_diag) {
                 const double r = fma(-(cv * ii), ij, 1.0);
                 const float h = __int_as_float(__double2hiint(r));

@@ -73,11 +73,25 @@ __global__ void k_params(ParamArgs a) {
 // key, cov = (1 - r) / (inv_o inv_c) (r kept to 2^-44), plus / minus one step of the
 // diagonal recurrence; the Welford co-moment step carries it to length m. Any valid cell's
 // key bounds the minimum; the reconstruction error (~1e-13) is far below the margin.
+// exact centred co-moment of windows a, b at length m (direct sum, two accumulators): bounds
+// must be keys of real cells, whatever the recurrence's accuracy on the series
+__device__ inline double direct_cov(const double* __restrict__ tn, long long a, double ma, long long b, double mb, int m) {
+    double c0 = 0.0, c1 = 0.0;
+    int k = 0;
+    for (; k + 1 < m; k += 2) {
+        c0 = fma(tn[a + k] - ma, tn[b + k] - mb, c0);
+        c1 = fma(tn[a + k + 1] - ma, tn[b + k + 1] - mb, c1);
+    }
+    if (k < m) c0 = fma(tn[a + k] - ma, tn[b + k] - mb, c0);
+    return c0 + c1;
+}
+
 struct Bound2Args {
     const double* tn; const Prm* prm; const Prm* pprev; const double* mu_prev; const double* mu;
     const ulonglong2* acc_prev; Prm* out;
     long long N, Nprev; int m, e; double margin;
     unsigned long long* fix_cnt;   // offsets re-bounded by a direct dot product
+    int exact;                     // bound = exact key of the chosen candidate (FP32 walk)
 };
 
 __global__ void k_bound2(Bound2Args a) {
@@ -89,13 +103,15 @@ __global__ void k_bound2(Bound2Args a) {
     const double wgt = (double)(m - 1) / (double)m;
     const double xo = a.tn[o + m - 1] - a.mu_prev[o];
     double best = INFINITY;
+    long long best_c = -1;
     auto eval = [&](long long c, double covp) {
         const long long dd = c > o ? c - o : o - c;
         if (c < 0 || c >= a.N || dd < a.e) return;
         const double ic = a.prm[c].inv;
         if (!(ic == ic)) return;
         const double covm = fma(wgt * xo, a.tn[c + m - 1] - a.mu_prev[c], covp);
-        best = fmin(best, fma(-(covm * io), ic, 1.0));
+        const double r = fma(-(covm * io), ic, 1.0);
+        if (r < best) { best = r; best_c = c; }
     };
     auto cov_of = [&](long long i, const ulonglong2& v) {   // winner's covariance at m-1
         const double r = __longlong_as_double((long long)v.x);
@@ -134,9 +150,15 @@ __global__ void k_bound2(Bound2Args a) {
                 double cv = 0.0;
                 for (int k = 0; k < m; ++k) cv = fma(a.tn[o + k] - mo, a.tn[c + k] - mc, cv);
                 best = fma(-(cv * io), ic, 1.0);
+                best_c = -1;   // already exact
                 atomicAdd(a.fix_cnt, 1ull);
             }
         }
+    }
+    if (a.exact && best_c >= 0) {
+        // the candidate was chosen on reconstructed covariances; its bound is its exact key
+        const double cv = direct_cov(a.tn, o, a.mu[o], best_c, a.mu[best_c], m);
+        best = fma(-(cv * io), a.prm[best_c].inv, 1.0);
     }
     float out = INFINITY;   // no bound: every cell of this offset is a candidate
     if (best < INFINITY) out = __int_as_float(__double2hiint(fmax(best, 0.0) + a.margin));
@@ -146,7 +168,8 @@ __global__ void k_bound2(Bound2Args a) {
 
 // Bound of a shard's first length from its own partial minima (a full-fold pass over a
 // sample of the bands): any folded cell is a valid cell of this length.
-__global__ void k_bound_self(const ulonglong2* __restrict__ acc, Prm* prm, long long N, double margin) {
+__global__ void k_bound_self(const ulonglong2* __restrict__ acc, Prm* prm, long long N, double margin,
+                             const double* __restrict__ tn, const double* __restrict__ mu, int m, int exact) {
     const long long o = blockIdx.x * (long long)blockDim.x + threadIdx.x;
     if (o >= N) return;
     const double io = prm[o].inv;
@@ -154,8 +177,14 @@ __global__ void k_bound_self(const ulonglong2* __restrict__ acc, Prm* prm, long 
     if (io == io) {
         const ulonglong2 v = acc[o];
         u = INFINITY;
-        if (v.x != KEY_NONE)
-            u = __int_as_float(__double2hiint(fmax(__longlong_as_double((long long)v.x), 0.0) + margin));
+        if (v.x != KEY_NONE) {
+            double r = __longlong_as_double((long long)v.x);
+            if (exact) {   // the folded winner's exact key (the fold's own key may be inaccurate)
+                const long long c = (long long)v.y;
+                r = fma(-(direct_cov(tn, o, mu[o], c, mu[c], m) * io), prm[c].inv, 1.0);
+            }
+            u = __int_as_float(__double2hiint(fmax(r, 0.0) + margin));
+        }
     }
     prm[o].U = u;
 }
@@ -1075,12 +1104,18 @@ static int profile_impl(vlmp_session* s, int32_t lmin, int32_t lmax, int64_t ban
 #define VLMP_FIRST_SAMPLE 4
 #endif
     constexpr int SAMPLE = VLMP_FIRST_SAMPLE;
+    // filtered lengths: FP32 walk + exact FP64 runs (filter32.cu) unless asked for the FP64 filter
+    const bool fp32 = !(flags & (VLMP_F_FP64_FILTER | VLMP_F_FULL_EVERY_LENGTH)) && !getenv("VLMP_FP64_FILTER");
+    const bool sampled_start = SAMPLE > 1 && (band_hi - band_lo) >= 8 * SAMPLE &&
+                               !(flags & (VLMP_F_FULL_EVERY_LENGTH | F_NO_SAMPLED_START));
+    // FP32 walk: the first length's folds only bound it (exact keys of their winners); its keys
+    // come from the FP32 pass's exact runs like every other length's. Few bands: fold them all.
+    const bool bound_start = sampled_start || fp32;
+    const int sample = sampled_start ? SAMPLE : 1;
     std::vector<int2> tiles_s;
     std::vector<int> smap;
     for (size_t k = 0; k < tiles.size(); ++k)
-        if ((tiles[k].x - band_lo) % SAMPLE == 0) { tiles_s.push_back(tiles[k]); smap.push_back((int)k); }
-    const bool sampled_start = SAMPLE > 1 && (band_hi - band_lo) >= 8 * SAMPLE &&
-                               !(flags & (VLMP_F_FULL_EVERY_LENGTH | F_NO_SAMPLED_START));
+        if ((tiles[k].x - band_lo) % sample == 0) { tiles_s.push_back(tiles[k]); smap.push_back((int)k); }
     *used_sampled = sampled_start;
     const long long T = (long long)tiles.size();
     int rc;
@@ -1097,14 +1132,12 @@ static int profile_impl(vlmp_session* s, int32_t lmin, int32_t lmax, int64_t ban
     CU(cudaMemsetAsync(s->d_forced, 0, n_len * sizeof(int), st));
     if (T) CU(cudaMemcpyAsync(s->d_tiles, tiles.data(), T * sizeof(int2), cudaMemcpyHostToDevice, st));
     const long long Ts = (long long)tiles_s.size();
-    if (sampled_start && Ts) {
+    if (bound_start && Ts) {
         if ((rc = ensure(s->d_tiles_s, s->tiles_s_cap, (size_t)Ts))) return rc;
         if ((rc = ensure(s->d_smap, s->smap_cap, (size_t)Ts))) return rc;
         CU(cudaMemcpyAsync(s->d_tiles_s, tiles_s.data(), Ts * sizeof(int2), cudaMemcpyHostToDevice, st));
         CU(cudaMemcpyAsync(s->d_smap, smap.data(), Ts * sizeof(int), cudaMemcpyHostToDevice, st));
     }
-    // filtered lengths: FP32 walk + exact FP64 runs (filter32.cu) unless asked for the FP64 filter
-    const bool fp32 = !(flags & VLMP_F_FP64_FILTER) && !getenv("VLMP_FP64_FILTER");
     std::vector<int2> tiles32;
     if (fp32) {
         build_tiles32(tiles, band_lo, tiles32);
@@ -1167,7 +1200,7 @@ static int profile_impl(vlmp_session* s, int32_t lmin, int32_t lmax, int64_t ban
         }
         if (!full) {
             Bound2Args ba{s->d_tn, prm, prm_prev, mu_prev, mu, s->d_acc + (long long)(li - 1) * A, prm,
-                          N, N + 1, m, e, margin, s->d_fixcnt + li};
+                          N, N + 1, m, e, margin, s->d_fixcnt + li, fp32 ? 1 : 0};
             k_bound2<<<blocks(N, 256), 256, 0, st>>>(ba);
             if (!fp32)
                 k_qprep<<<blocks(A, 256), 256, 0, st>>>(prm, s->d_colq, s->d_rowq, N, A, s->sscale,
@@ -1184,12 +1217,13 @@ static int profile_impl(vlmp_session* s, int32_t lmin, int32_t lmax, int64_t ban
                         s->d_counters, s->d_log, s->d_logcnt + li, eff_cap,
                         N, dl, (int)T, S, m, e, li + 1 <= li_hi,
                         s->d_colq, s->d_rowq, s->d_forced + li, s->hiC};
-            if (full && li == li_lo && sampled_start && Ts) {
+            if (full && li == li_lo && bound_start && Ts) {
                 // sampled full folds (seeds untouched) -> bounds -> filtered pass over all bands
                 TileArgs tsa = ta;
                 tsa.tiles = s->d_tiles_s; tsa.n_tiles = (int)Ts; tsa.seed_map = s->d_smap; tsa.update_seeds = 0;
                 k_tile<true><<<blocks(Ts, WARPS_PER_CTA), WARPS_PER_CTA * 32, smem, st>>>(tsa);
-                k_bound_self<<<blocks(N, 256), 256, 0, st>>>(s->d_acc + (long long)li * A, prm, N, margin);
+                k_bound_self<<<blocks(N, 256), 256, 0, st>>>(s->d_acc + (long long)li * A, prm, N, margin,
+                                                             s->d_tn, mu, m, fp32 ? 1 : 0);
                 if (fp32) {
                     // the sampled folds only bound this length; its keys come from the exact runs
                     k_fill_acc<<<blocks(A, 256), 256, 0, st>>>(s->d_acc + (long long)li * A, A);
@@ -1211,6 +1245,17 @@ static int profile_impl(vlmp_session* s, int32_t lmin, int32_t lmax, int64_t ban
                                           s->d_acc + (long long)li * A, runs, s->d_logcnt + li, run_cap)))
                     return rc;
                 klaunch += 2;
+                if (const char* dp = getenv("VLMP_DUMP_RUNS")) {   // dev aid: one length's run log
+                    if (li == atoi(getenv("VLMP_DUMP_LI") ? getenv("VLMP_DUMP_LI") : "64")) {
+                        unsigned long long c = 0;
+                        CU(cudaMemcpyAsync(&c, s->d_logcnt + li, 8, cudaMemcpyDeviceToHost, st));
+                        CU(cudaStreamSynchronize(st));
+                        c = std::min<unsigned long long>(c, (unsigned long long)run_cap);
+                        std::vector<Run> h(c);
+                        CU(cudaMemcpy(h.data(), runs, c * sizeof(Run), cudaMemcpyDeviceToHost));
+                        if (FILE* f = fopen(dp, "wb")) { fwrite(h.data(), sizeof(Run), c, f); fclose(f); }
+                    }
+                }
             } else {
                 k_tile<false><<<blocks(T, WARPS_PER_CTA), WARPS_PER_CTA * 32, smem, st>>>(ta);
                 k_log_merge<<<148 * 8, 256, 0, st>>>(s->d_log, s->d_logcnt + li, eff_cap,
@@ -1271,10 +1316,10 @@ static int profile_impl(vlmp_session* s, int32_t lmin, int32_t lmax, int64_t ban
     s->stats[9] = klaunch; s->stats[10] = first_ms; s->stats[11] = (double)cnt[2];
     s->stats[12] = n_fix; s->stats[14] = n_forced; s->stats[15] = max_log;
     s->stats[16] = fp32 ? 1.0 : 0.0; s->stats[17] = fp32 ? max_log : 0.0; s->stats[18] = (double)cnt[4];
+    s->stats[19] = (double)cnt[3];
     *overflow_out = overflow;
-    // the FP32 path cannot take lengths whose own bounds are too weak, nor a lost run log:
-    // the caller re-runs the whole set on the FP64 path (which handles both exactly)
-    if (fp32_fallback) *fp32_fallback = fp32 && (overflow || n_forced > 0);
+    // a lost run log: the caller re-runs the whole set on the FP64 filter path
+    if (fp32_fallback) *fp32_fallback = fp32 && overflow;
     return 0;
 }
 
