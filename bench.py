@@ -272,11 +272,19 @@ def run_ours(args):
         if world > 1:
             torch.distributed.destroy_process_group()
         return
-    # roofline of the dominant kernel (k_tile): 4 FP64 FMA-pipe instructions per update
+    # roofline of the dominant kernels (k_tile32 walk + k_runs exact runs):
+    # the exhaustive algorithm costs 4 FP64 FMA-pipe instructions per update (2 recurrence DFMA,
+    # DMUL, DFMA key) -- achieved = W * 8 flops / tile time against the measured DFMA peak. The
+    # walk executes that work as 3 FP32 FFMA per cell (2 recurrence + 1 bound test), reported
+    # against the FP32 FMA pipe (128 lanes/SM/clk at the sampled SM clock) as executed_fp32_frac.
     peak_dfma = sess.measure_fp64_peak()
     avg_tile_s = tile_ms * 1e-3 / args.steps
     achieved = W * 4 * 2 / avg_tile_s / 1e12          # TFLOP/s (2 flops per FMA-pipe instr)
     peak = peak_dfma * 2 / 1e12 * world            # aggregate over the N GPUs of the job
+    clk_sum = clk.summary()
+    sm_hz = (clk_sum.get("sm_mhz") or 1965.0) * 1e6
+    executed_cells = st.get("executed_updates", W) if world == 1 else W
+    ffma_frac = executed_cells * 3 / avg_tile_s / (148 * 128 * sm_hz * world)
     prof_traffic = None
     tr_path = os.path.join(ROOT, "profiles", "tile_traffic.json")
     if os.path.exists(tr_path):
@@ -301,15 +309,17 @@ def run_ours(args):
                      "frac": achieved / peak, "traffic": prof_traffic,
                      "peak_source": "measured DFMA microbenchmark (vlmp_measure_fp64_peak); "
                                     "MEASURED_PEAKS.json has no FP64 figure",
-                     "kernel": "k_tile", "avg_tile_ms_per_step": avg_tile_s * 1e3,
+                     "kernel": "k_tile32 + k_runs", "avg_tile_ms_per_step": avg_tile_s * 1e3,
                      "flops_per_update": "8 = the exhaustive cell's 4 FP64 FMA-pipe instr (2 recurrence "
-                                         "DFMA + DMUL + DFMA key); the filter kernel executes the 2 "
-                                         "recurrence DFMA and tests in FP32/INT",
-                     "executed_fp64_frac": achieved / peak / 2},
+                                         "DFMA + DMUL + DFMA key); the walk executes 3 FP32 FFMA per cell "
+                                         "(recurrence + bound test under a rigorous error slack) and the "
+                                         "exact FP64 work only on the cells that pass (k_runs)",
+                     "executed_fp32_frac": ffma_frac,
+                     "run_cells_per_step": st.get("run_cells"), "runs_fp32_walk": st.get("fp32_walk")},
         "cpu_baseline": cpu,
         "e2e": e2e_line,
         "gpu_launches": launches,
-        "clocks": clk.summary(),
+        "clocks": clk_sum,
     }
     print(json.dumps(line), flush=True)
     if world > 1:
