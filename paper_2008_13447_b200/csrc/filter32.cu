@@ -417,16 +417,16 @@ __global__ void __launch_bounds__(256) k_runs(const Run* __restrict__ runs, cons
                 if (k > 0) term = fma(pi.df, pj.dg, pj.df * pi.dg);
                 ii = pi.inv; ij = pj.inv; ui = pi.U; uj = pj.U;
             }
-            double at = fabs(term);
+            float at = __double2float_ru(fabs(term));   // a bound: FP32, rounded up, is enough
 #pragma unroll
             for (int off = 1; off < 32; off <<= 1) {
                 const double t = __shfl_up_sync(FULLMASK, term, off);
-                const double ta = __shfl_up_sync(FULLMASK, at, off);
-                if (lane >= off) { term += t; at += ta; }
+                const float ta = __shfl_up_sync(FULLMASK, at, off);
+                if (lane >= off) { term += t; at = __fadd_ru(at, ta); }
             }
             double cv = carry + term;
             const double scale = 1.0 / (ii * ij);   // s_i s_j (NaN / 0 for invalid windows)
-            const bool inexact = valid && ok_diag && !((mag + at) <= 8.0 * scale);
+            const bool inexact = valid && ok_diag && !((mag + (double)at) <= 8.0 * scale);
             unsigned redo = __ballot_sync(FULLMASK, inexact);
             if (redo) {   // rare: exact direct sums for the flagged cells of this chunk
                 const unsigned tail = __ballot_sync(FULLMASK, valid);
@@ -441,7 +441,7 @@ __global__ void __launch_bounds__(256) k_runs(const Run* __restrict__ runs, cons
                 carry = cl; mag = fabs(cl);
             } else {
                 carry = __shfl_sync(FULLMASK, cv, 31);
-                mag += __shfl_sync(FULLMASK, at, 31);
+                mag += (double)__shfl_sync(FULLMASK, at, 31);
             }
             if (valid && ok_diag) {
                 const double r = fma(-(cv * ii), ij, 1.0);

@@ -102,16 +102,19 @@ __global__ void k_bound2(Bound2Args a) {
     const int m = a.m;
     const double wgt = (double)(m - 1) / (double)m;
     const double xo = a.tn[o + m - 1] - a.mu_prev[o];
-    double best = INFINITY;
+    double best = INFINITY, best_mag = 0.0;
     long long best_c = -1;
-    auto eval = [&](long long c, double covp) {
+    // covp: the candidate's covariance at m-1 reconstructed from its stored key, plus at most
+    // one recurrence step; mag bounds the magnitudes it was assembled from
+    auto eval = [&](long long c, double covp, double mag) {
         const long long dd = c > o ? c - o : o - c;
         if (c < 0 || c >= a.N || dd < a.e) return;
         const double ic = a.prm[c].inv;
         if (!(ic == ic)) return;
-        const double covm = fma(wgt * xo, a.tn[c + m - 1] - a.mu_prev[c], covp);
+        const double yc = a.tn[c + m - 1] - a.mu_prev[c];
+        const double covm = fma(wgt * xo, yc, covp);
         const double r = fma(-(covm * io), ic, 1.0);
-        if (r < best) { best = r; best_c = c; }
+        if (r < best) { best = r; best_c = c; best_mag = mag + fabs(wgt * xo * yc) + fabs(covm); }
     };
     auto cov_of = [&](long long i, const ulonglong2& v) {   // winner's covariance at m-1
         const double r = __longlong_as_double((long long)v.x);
@@ -119,14 +122,15 @@ __global__ void k_bound2(Bound2Args a) {
     };
     if (o < a.Nprev) {
         const ulonglong2 v = a.acc_prev[o];
-        if (v.x != KEY_NONE) eval((long long)v.y, cov_of(o, v));
+        if (v.x != KEY_NONE) { const double cv = cov_of(o, v); eval((long long)v.y, cv, fabs(cv)); }
     }
     if (o >= 1 && o - 1 < a.Nprev) {
         const ulonglong2 v = a.acc_prev[o - 1];
         if (v.x != KEY_NONE) {   // (o, c0+1) follows (o-1, c0) on its diagonal
             const long long c = (long long)v.y + 1;
             const Prm po = a.pprev[o], pc = a.pprev[c];
-            eval(c, cov_of(o - 1, v) + po.df * pc.dg + pc.df * po.dg);
+            const double cv = cov_of(o - 1, v), t1 = po.df * pc.dg, t2 = pc.df * po.dg;
+            eval(c, cv + t1 + t2, fabs(cv) + fabs(t1) + fabs(t2));
         }
     }
     if (o + 1 < a.Nprev) {
@@ -134,7 +138,8 @@ __global__ void k_bound2(Bound2Args a) {
         if (v.x != KEY_NONE && v.y >= 1) {   // (o, c0-1) precedes (o+1, c0) on its diagonal
             const long long c0 = (long long)v.y;
             const Prm po = a.pprev[o + 1], pc = a.pprev[c0];
-            eval(c0 - 1, cov_of(o + 1, v) - po.df * pc.dg - pc.df * po.dg);
+            const double cv = cov_of(o + 1, v), t1 = po.df * pc.dg, t2 = pc.df * po.dg;
+            eval(c0 - 1, cv - t1 - t2, fabs(cv) + fabs(t1) + fabs(t2));
         }
     }
     if (!(best < INFINITY) && o < a.Nprev && a.acc_prev[o].x != KEY_NONE) {
@@ -155,10 +160,12 @@ __global__ void k_bound2(Bound2Args a) {
             }
         }
     }
-    if (a.exact && best_c >= 0) {
-        // the candidate was chosen on reconstructed covariances; its bound is its exact key
+    if (a.exact && best_c >= 0 && !(best_mag * io * a.prm[best_c].inv <= 0x1p10)) {
+        // the reconstruction's rounding (~2^-50 of the magnitudes it summed) could exceed the
+        // 2^-26 margin relative to this cell's own scale s_o s_c: bound by its exact key instead
         const double cv = direct_cov(a.tn, o, a.mu[o], best_c, a.mu[best_c], m);
         best = fma(-(cv * io), a.prm[best_c].inv, 1.0);
+        atomicAdd(a.fix_cnt, 1ull);
     }
     float out = INFINITY;   // no bound: every cell of this offset is a candidate
     if (best < INFINITY) out = __int_as_float(__double2hiint(fmax(best, 0.0) + a.margin));
