@@ -1020,13 +1020,18 @@ void order_tiles(std::vector<int2>& tiles, long long N0, long long dl, int S) {
 }
 
 int seg_rows(long long n) {
-    // S = G*D rows per tile (whole GR-row groups); larger for longer series to bound the
-    // number of tiles and the seed store (config 5: S = 16384, ~1.1M tiles, 2.2 GB of seeds)
+    // S = G*D rows per tile (whole GR-row groups). Short segments keep the FP32 walk's error
+    // slack small (it grows with the rows walked from the FP64 seed) and the launch tail fine;
+    // the cost is the seed store, 8 B per (diagonal, segment) ~ 4 n^2 / S bytes. S = 1024
+    // while that fits in a fifth of the device (config 4: 4.3 GB), doubling beyond.
 #ifndef VLMP_SEG_G0
 #define VLMP_SEG_G0 128
 #endif
     long long G = VLMP_SEG_G0;
-    while (G * D * 256 < n && G < 2048) G *= 2;
+    size_t free_b = 0, total_b = 0;
+    double budget = 8e9;
+    if (cudaMemGetInfo(&free_b, &total_b) == cudaSuccess) budget = (double)total_b / 5.0;
+    while (4.0 * (double)n * (double)n / (double)(G * D) > budget && G < 2048) G *= 2;
     return (int)(G * D);
 }
 
