@@ -20,18 +20,24 @@ def _free_port():
     return p
 
 
-def _rank(rank, world, port, t, lmin, lmax, out, mode="bands"):
+def _rank(rank, world, port, t, lmin, lmax, out, mode="bands", backend="gloo"):
     import torch
     import torch.distributed as dist
     os.environ["MASTER_ADDR"] = "127.0.0.1"
     os.environ["MASTER_PORT"] = str(port)
-    dist.init_process_group("gloo", rank=rank, world_size=world)
+    if backend == "nccl":
+        dist.init_process_group("nccl", rank=rank, world_size=world, device_id=torch.device("cuda", 0))
+    else:
+        dist.init_process_group("gloo", rank=rank, world_size=world)
     try:
         from paper_2008_13447_b200 import _lib, distributed, ingest
         s = ingest(t)
         sess = _lib.Session(0)
         if mode == "lengths":
-            distributed.profile_length_sharded(sess, s, lmin, lmax, rank, world)
+            # NCCL: a 1-rank group with the exchange forced on, so the two all-reduces over
+            # the library's device buffers run through NCCL on the B200
+            distributed.profile_length_sharded(sess, s, lmin, lmax, rank, world,
+                                               exchange=True if backend == "nccl" else None)
         else:
             distributed.profile_sharded(sess, s, lmin, lmax, rank, world)
         d, nm, ln, ix, pop = sess.valmp_arrays()
@@ -45,11 +51,11 @@ def _rank(rank, world, port, t, lmin, lmax, out, mode="bands"):
         dist.destroy_process_group()
 
 
-def _sharded_equals_single(tmp_path, world, mode, t, lmin, lmax):
+def _sharded_equals_single(tmp_path, world, mode, t, lmin, lmax, backend="gloo"):
     import torch.multiprocessing as mp
     from paper_2008_13447_b200 import _lib, ingest
-    out = str(tmp_path / f"sharded_{mode}_{world}.npz")
-    mp.start_processes(_rank, args=(world, _free_port(), t, lmin, lmax, out, mode), nprocs=world,
+    out = str(tmp_path / f"sharded_{mode}_{world}_{backend}.npz")
+    mp.start_processes(_rank, args=(world, _free_port(), t, lmin, lmax, out, mode, backend), nprocs=world,
                        join=True, start_method="spawn")
     got = np.load(out)
     sess = _lib.session(0)
@@ -80,3 +86,11 @@ def test_length_shards_equal_single(tmp_path, world):
     filtered lengths): bit-identical to one process."""
     t = np.cumsum(np.random.default_rng(45).standard_normal(6000))
     _sharded_equals_single(tmp_path, world, "lengths", t, 48, 64)
+
+
+def test_nccl_exchange_single_rank(tmp_path):
+    """The NCCL transport of the length-shard exchange (MIN / MAX all-reduce on the library's
+    own device buffers via __cuda_array_interface__) on the pool's one GPU: a 1-rank NCCL
+    group with the exchange forced on must reproduce the single-process run bit for bit."""
+    t = np.cumsum(np.random.default_rng(31).standard_normal(20000))
+    _sharded_equals_single(tmp_path, 1, "lengths", t, 100, 116, backend="nccl")
