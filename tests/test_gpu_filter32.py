@@ -111,3 +111,43 @@ def test_fp32_slack_with_spiky_variance():
         assert np.all(ip >= 0), L
         assert np.all(pair(o, ip) <= d * (1 + 1e-9)), L
         assert np.mean(ip == nn) > 0.999, L
+
+
+def test_fp32_constant_stretches(oracle_mod):
+    """Constant stretches put invalid windows (sigma below the floor: no neighbour, never a
+    neighbour) inside tiles: their FP32 factors are +inf and the walk must neither pass nor
+    poison their cells; valid offsets must still match the oracle exactly."""
+    rng = np.random.default_rng(21)
+    t = np.cumsum(rng.standard_normal(9000))
+    # exact zeros: the prefix sums stay exactly flat, so sigma = 0 < floor (a constant stretch at
+    # another level keeps prefix-sum noise above the floor: noise-decided in every implementation)
+    t[2000:2600] = 0.0
+    t[5000:5100] = 0.0
+    s = vl.ingest(t)
+    run = api.GpuRun(s, 50, 60)
+    assert run.stats["fp32_walk"] == 1
+    ref = oracle_mod.run(s, 50, 60, k_discord=1, keep_profiles=True)
+    for L in range(50, 61):
+        mp, ip = run.profile(L)
+        omp, oip = ref["profiles"][L]
+        assert np.array_equal(ip, oip), L
+        fin = np.isfinite(omp)
+        assert np.array_equal(fin, np.isfinite(mp)), L
+        # reported values: the reference's pair_distance of the chosen pair (series.py:169-194);
+        # the oracle's own STOMP-order values drift next to the flat stretches (ill-conditioned)
+        cv = oracle_mod.canonical_values(s, ip, L)
+        assert np.allclose(mp[fin], cv[fin], rtol=1e-12, atol=1e-12), L
+
+
+def test_fp32_white_noise(oracle_mod):
+    """White noise with short windows: weak correlations everywhere, the least favourable case
+    for the bound filter (many passing cells, short runs). Profiles equal the oracle's."""
+    t = np.random.default_rng(8).standard_normal(4000)
+    s = vl.ingest(t)
+    run = api.GpuRun(s, 10, 16)
+    ref = oracle_mod.run(s, 10, 16, k_discord=1, keep_profiles=True)
+    for L in range(10, 17):
+        mp, ip = run.profile(L)
+        omp, oip = ref["profiles"][L]
+        assert np.array_equal(ip, oip), L
+        assert np.allclose(mp, omp, rtol=1e-7, atol=1e-9)
