@@ -29,11 +29,15 @@ namespace vlmp_impl {
 #define VLMP_D2 16
 #endif
 constexpr int D2 = VLMP_D2;                 // diagonals per lane (FP32 walk)
-constexpr int BAND2 = 32 * D2;              // diagonals per FP32 tile
-constexpr int LPT = BAND / D2;              // lanes per FP64 tile (16 or 32)
+[[maybe_unused]] constexpr int BAND2 = 32 * D2;   // diagonals per FP32 tile (scalar walk)
+[[maybe_unused]] constexpr int LPT = BAND / D2;     // lanes per FP64 tile (scalar walk)
 constexpr int GR2 = D2;                     // rows per staging group (ring returns to phase)
 constexpr int CQS = 33;                     // staged column-factor row stride (entries)
 static_assert(D2 == 8 || D2 == 16, "D2: 8 or 16");
+#ifndef VLMP_PACKED
+#define VLMP_PACKED 1            // two-band packed walk (FFMA2 on band pairs); 0: scalar FFMA, 16 diagonals per lane
+#endif
+constexpr int WIN = VLMP_PACKED ? 8 : D2;   // rows a column meets in one lane (the w window)
 #ifndef VLMP_FILTER32_WARPS_PER_SM
 #define VLMP_FILTER32_WARPS_PER_SM 16   // 128 registers: no spills (20 warps at 96 spill the staging plan)
 #endif
@@ -59,7 +63,7 @@ __global__ void __launch_bounds__(256) k_prep32(Prep32Args a) {
         if (o < a.N) {
             float uw = -INFINITY;
 #pragma unroll
-            for (int k = 0; k < D2; ++k)
+            for (int k = 0; k < WIN; ++k)
                 if (o + k < a.N) uw = fmaxf(uw, a.prm[o + k].U);
             if (uw != -INFINITY) w = __double2float_rd(qfac(uw));
             if (p.inv == p.inv) {
@@ -158,6 +162,7 @@ __device__ __forceinline__ float fma_nocse(float a, float b, float c) {
     return d;
 }
 
+#if !VLMP_PACKED
 __global__ void __launch_bounds__(32, VLMP_FILTER32_WARPS_PER_SM) k_tile32(Tile32Args a) {
     extern __shared__ __align__(128) unsigned char smem_raw[];
     Smem32& sm = *reinterpret_cast<Smem32*>(smem_raw);
@@ -371,6 +376,261 @@ __global__ void __launch_bounds__(32, VLMP_FILTER32_WARPS_PER_SM) k_tile32(Tile3
     if (nslow) atomicAdd(a.counters + 2, (unsigned long long)nslow);
 }
 
+#else   // VLMP_PACKED: two-band packed walk
+// Each lane owns 8 diagonals in band A (d0 + 8L + s) and the same 8 in band B (d0 + 256 + 8L
+// + s): cells (s, A) and (s, B) form one FP32 register pair, and so do the ring slots of their
+// columns (256 apart), which rotate together -- every update is a whole pair, every FFMA2
+// operand is a natural pair or a broadcast (no half moves). Lane 31's new pair is (lane 0's
+// outgoing B column, the fresh column d0 + 511 + i): lane 0 prepares it before the shuffle.
+typedef unsigned long long u64;
+__device__ __forceinline__ u64 pk2(float lo, float hi) {
+    u64 r; asm("mov.b64 %0, {%1, %2};" : "=l"(r) : "f"(lo), "f"(hi)); return r;
+}
+__device__ __forceinline__ float lo2(u64 v) { return __uint_as_float((unsigned)v); }
+__device__ __forceinline__ float hi2(u64 v) { return __uint_as_float((unsigned)(v >> 32)); }
+__device__ __forceinline__ u64 fma2(u64 x, u64 y, u64 z) {
+    u64 d; asm("fma.rn.f32x2 %0, %1, %2, %3;" : "=l"(d) : "l"(x), "l"(y), "l"(z)); return d;
+}
+__device__ __forceinline__ u64 bc2(float x) { return pk2(x, x); }
+
+constexpr int DP = 8;        // diagonals per lane per band
+constexpr int GRP = 8;       // rows per staging group (ring phase)
+struct Smem32p {
+    float4 row[2][GRP];          // {df, dg, b, w}
+    float4 fresh[2][GRP];        // the B-band column entering lane 31 at each row
+    float4 cq[2][GRP * CQS];     // {aA, bA, aB, bB} of the pair entering lane L at row kk: [kk * 33 + L]
+    unsigned short rs[32 * 16];  // run starts per lane and cell (bits 0-7 band A, 8-15 band B)
+    unsigned short msk[32 * GRP];
+};
+
+__global__ void __launch_bounds__(32, VLMP_FILTER32_WARPS_PER_SM) k_tile32(Tile32Args a) {
+    extern __shared__ __align__(128) unsigned char smem_raw[];
+    Smem32p& sm = *reinterpret_cast<Smem32p*>(smem_raw);
+    const int lane = threadIdx.x;
+    const int wid = blockIdx.x;
+    if (wid >= a.n_tiles32) return;
+    const int2 pr2 = a.tiles32[wid];
+    const int2 tA = a.tiles[pr2.x];
+    const long long d0 = a.dlo + (long long)tA.x * BAND;
+    const long long i0 = (long long)tA.y * a.S;
+    const long long rows_valid = a.N - d0 - i0;
+    const bool liveA = rows_valid > 0 && d0 + BAND - 1 >= a.e;
+    const bool liveB = pr2.y >= 0 && rows_valid - BAND > 0 && d0 + 2 * BAND - 1 >= a.e;
+    if (!liveA && !liveB) return;
+    const int nrows = (int)(rows_valid < a.S ? rows_valid : a.S);
+    const int ngroups = (nrows + GRP - 1) / GRP;
+    const long long cbA = i0 + d0 + (long long)DP * lane;   // band A column of slot 0 at row i0
+    const long long cbB = cbA + BAND;
+
+    float eps;
+    {
+        const long long rb0 = i0 >> 8, rb1 = (i0 + nrows - 1) >> 8;
+        const long long cb0 = (i0 + d0) >> 8, cb1 = (i0 + nrows - 1 + d0 + 2 * BAND - 1) >> 8;
+        unsigned mr = 0, mc = 0;
+        for (long long k = rb0 + lane; k <= rb1; k += 32) mr = max(mr, a.magblk[k]);
+        for (long long k = cb0 + lane; k <= cb1; k += 32) mc = max(mc, a.magblk[k]);
+        mr = __reduce_max_sync(FULLMASK, mr);
+        mc = __reduce_max_sync(FULLMASK, mc);
+        const double bound = (4.0 * a.S + 16.0) * 0x1p-24 * 1.05 *
+                             (double)__uint_as_float(mr) * (double)__uint_as_float(mc);
+        eps = __double2float_ru(bound);
+    }
+
+    // ---- seeds of both bands (FP64, carried to m+1 in place as k_tile does)
+    u64 cov[DP];
+    {
+        const double s2 = a.sscale * a.sscale;
+        double* __restrict__ spA = a.seeds + (long long)pr2.x * BAND + DP * lane;
+        double* __restrict__ spB = a.seeds + (long long)(liveB ? pr2.y : pr2.x) * BAND + DP * lane;
+        double cA64[DP], cB64[DP];
+#pragma unroll
+        for (int s = 0; s < DP; ++s) { cA64[s] = liveA ? spA[s] : 0.0; cB64[s] = liveB ? spB[s] : 0.0; }
+        if (a.update_seeds) {
+            const double wgt = (double)a.m / (double)(a.m + 1);
+            const double xi = (a.tn[i0 + a.m] - a.mu[i0]) * wgt;
+            double xa[DP], xb[DP];
+#pragma unroll
+            for (int s = 0; s < DP; ++s) {
+                xa[s] = a.tn[cbA + s + a.m] - a.mu[cbA + s];
+                xb[s] = a.tn[cbB + s + a.m] - a.mu[cbB + s];
+            }
+#pragma unroll
+            for (int s = 0; s < DP; ++s) {
+                if (liveA) spA[s] = fma(xi, xa[s], cA64[s]);
+                if (liveB) spB[s] = fma(xi, xb[s], cB64[s]);
+            }
+        }
+#pragma unroll
+        for (int s = 0; s < DP; ++s) {
+            const float ca = (liveA && d0 + DP * lane + s >= a.e) ? __fadd_ru((float)(cA64[s] * s2), eps) : -INFINITY;
+            const float cb = (liveB && d0 + BAND + DP * lane + s >= a.e) ? __fadd_ru((float)(cB64[s] * s2), eps) : -INFINITY;
+            cov[s] = pk2(ca, cb);
+        }
+    }
+
+    // ---- ring of column pairs; N = -cA
+    u64 F[DP], G[DP], NA[DP];
+    {
+        const float w0 = a.p32[i0].w;
+#pragma unroll
+        for (int s = 0; s < DP; ++s) {
+            const long long ca = s < DP - 1 ? cbA + s : cbA - 1;
+            const float4 pa = a.p32[ca], pb = a.p32[ca + BAND];
+            F[s] = pk2(pa.x, pb.x); G[s] = pk2(pa.y, pb.y);
+            const float2 qa = a.cq[ca], qb = a.cq[ca + BAND];
+            NA[s] = pk2(fmaxf(-qa.x, __fmul_ru(-w0, qa.y)), fmaxf(-qb.x, __fmul_ru(-w0, qb.y)));
+        }
+        const float4 pr = a.p32[i0];
+        const float4 plA = a.p32[cbA + DP - 1], plB = a.p32[cbB + DP - 1];
+#pragma unroll
+        for (int s = 0; s < DP; ++s) {
+            const u64 f = s < DP - 1 ? F[s] : pk2(plA.x, plB.x);
+            const u64 g = s < DP - 1 ? G[s] : pk2(plA.y, plB.y);
+            cov[s] = fma2(bc2(-pr.y), f, cov[s]);
+            cov[s] = fma2(bc2(-pr.x), g, cov[s]);
+        }
+    }
+
+    // ---- staging: rows (lanes 0-7), fresh B columns (lanes 8-15), entering column factors
+    const char* src_rf; unsigned dst_rf;
+    {
+        const int q = lane & 7;
+        if (lane < 8) {
+            src_rf = reinterpret_cast<const char*>(a.p32 + i0 + q);
+            dst_rf = (unsigned)__cvta_generic_to_shared(&sm.row[0][q]);
+        } else {
+            src_rf = reinterpret_cast<const char*>(a.p32 + i0 + q + d0 + 2 * BAND - 1);
+            dst_rf = (unsigned)__cvta_generic_to_shared(&sm.fresh[0][q]);
+        }
+    }
+    // entering A column f = 8L + kk (f = lane + 32k) -> slot kk * 33 + L, low half; B: high half
+    const char* src_cq = reinterpret_cast<const char*>(a.cq + i0 + d0 + DP - 1 + lane);
+    const unsigned dst_cq = (unsigned)__cvta_generic_to_shared(&sm.cq[0][(lane % 8) * CQS + lane / 8]);
+    constexpr unsigned RFP = sizeof(float4) * GRP, CQP = sizeof(float4) * GRP * CQS;
+    auto stage = [&](int g, int b) {
+        const long long gr = (long long)g * (GRP * sizeof(float4));
+        if (lane < 16) cpa<0, 0, 16>(dst_rf + (unsigned)b * RFP, src_rf + gr);
+        const unsigned dc = dst_cq + (unsigned)b * CQP;
+        const char* sc = src_cq + (long long)g * (GRP * sizeof(float2));
+#define STG(K) cpa<(K) * 4 * 16, (K) * 256, 8>(dc, sc); cpa<(K) * 4 * 16 + 8, (K) * 256 + BAND * 8, 8>(dc, sc);
+        STG(0) STG(1) STG(2) STG(3) STG(4) STG(5) STG(6) STG(7)
+#undef STG
+        cp_async_commit();
+    };
+
+    // ---- runs (cells 0-7: band A diagonal d0 + 8L + s; 8-15: band B, + 256)
+    unsigned open = 0;
+    int last_r = -2;
+    unsigned nslow = 0;
+    unsigned short* rs = sm.rs + lane * 16;
+    unsigned short* msk = sm.msk + lane * GRP;
+    auto emit = [&](int c, int r_start, int r_end) {
+        const int dcell = (int)(d0 + DP * lane) + (c & 7) + (c >> 3) * BAND;
+        const unsigned long long at = atomicAdd(a.run_count, 1ull);
+        if ((long long)at < a.run_cap) {
+            Run rr;
+            rr.i = (int)(i0 + r_start); rr.j = rr.i + dcell; rr.len = r_end - r_start + 1; rr.pad = 0;
+            a.runs[at] = rr;
+        }
+    };
+    auto fold_rows = [&](unsigned flags, int gbase) {
+        while (flags) {
+            const int t = __ffs(flags) - 1; flags &= flags - 1;
+            const int r = gbase + t;
+            const unsigned mask = msk[t];
+            unsigned ended, started;
+            int endr;
+            if (last_r == r - 1) { ended = open & ~mask; started = mask & ~open; endr = r - 1; }
+            else { ended = open; started = mask; endr = last_r; }
+            while (ended) { const int q = __ffs(ended) - 1; ended &= ended - 1; emit(q, rs[q], endr); }
+            while (started) { const int q = __ffs(started) - 1; started &= started - 1; rs[q] = (unsigned short)r; }
+            open = mask; last_r = r;
+            ++nslow;
+        }
+    };
+
+    stage(0, 0);
+    cp_async_wait_all();
+    __syncwarp();
+
+    bool pass_prev = false;
+    float bprev = 0.f;
+    unsigned gflags = 0;
+    for (int g = 0; g < ngroups; ++g) {
+        const int b = g & 1;
+        if (g + 1 < ngroups) stage(g + 1, b ^ 1);
+#pragma unroll
+        for (int kk = 0; kk < GRP; ++kk) {
+            const float4 pr = sm.row[b][kk];
+            if (__builtin_expect(pass_prev, 0)) {
+                const int kp = (kk + GRP - 1) % DP;
+                unsigned mask = 0;
+#pragma unroll
+                for (int s = 0; s < DP; ++s) {
+                    const u64 nq = NA[(s + kp) % DP];
+                    const float za = fma_nocse(lo2(nq), bprev, lo2(cov[s]));
+                    const float zb = fma_nocse(hi2(nq), bprev, hi2(cov[s]));
+                    mask |= (__float_as_uint(za) >> 31 ^ 1u) << s;
+                    mask |= (__float_as_uint(zb) >> 31 ^ 1u) << (s + 8);
+                }
+                msk[(kk + GRP - 1) % GRP] = (unsigned short)mask;
+                gflags |= 1u << ((kk + GRP - 1) % GRP);
+            }
+            if (kk == 0 && g > 0 && gflags) { fold_rows(gflags, (g - 1) * GRP); gflags = 0; }
+            {   // rotation: phys (kk-1) mod 8 receives lane+1's outgoing pair
+                const int q = (kk + DP - 1) % DP;
+                if (lane == 0 && kk == 0) {
+                    const float4 f = sm.fresh[b][0];
+                    F[q] = pk2(hi2(F[q]), f.x); G[q] = pk2(hi2(G[q]), f.y);
+                }
+                F[q] = __shfl_sync(FULLMASK, F[q], (lane + 1) & 31);
+                G[q] = __shfl_sync(FULLMASK, G[q], (lane + 1) & 31);
+                const float4 cq = sm.cq[b][kk * CQS + lane];
+                NA[q] = pk2(fmaxf(-cq.x, __fmul_ru(-pr.w, cq.y)), fmaxf(-cq.z, __fmul_ru(-pr.w, cq.w)));
+            }
+            unsigned z[16];
+#pragma unroll
+            for (int s = 0; s < DP; ++s) {
+                const int p = (s + kk) % DP;
+                cov[s] = fma2(bc2(pr.x), G[p], cov[s]);
+                cov[s] = fma2(F[p], bc2(pr.y), cov[s]);
+                const u64 zz = fma2(NA[p], bc2(pr.z), cov[s]);
+                z[s] = (unsigned)zz; z[s + 8] = (unsigned)(zz >> 32);
+            }
+#pragma unroll
+            for (int w = 1; w < 16; w *= 2)
+#pragma unroll
+                for (int s = 0; s + w < 16; s += 2 * w) z[s] &= z[s + w];
+            pass_prev = (int)z[0] >= 0;
+            bprev = pr.z;
+            if (kk + 1 < GRP && lane == 0) {
+                const float4 f = sm.fresh[b][kk + 1];
+                F[kk % DP] = pk2(hi2(F[kk % DP]), f.x); G[kk % DP] = pk2(hi2(G[kk % DP]), f.y);
+            }
+        }
+        cp_async_wait_all();
+        __syncwarp();
+    }
+    if (pass_prev) {
+        constexpr int kp = (GRP - 1) % DP;
+        unsigned mask = 0;
+#pragma unroll
+        for (int s = 0; s < DP; ++s) {
+            const u64 nq = NA[(s + kp) % DP];
+            const float za = fmaf(lo2(nq), bprev, lo2(cov[s]));
+            const float zb = fmaf(hi2(nq), bprev, hi2(cov[s]));
+            mask |= (__float_as_uint(za) >> 31 ^ 1u) << s;
+            mask |= (__float_as_uint(zb) >> 31 ^ 1u) << (s + 8);
+        }
+        msk[GRP - 1] = (unsigned short)mask;
+        gflags |= 1u << (GRP - 1);
+    }
+    if (gflags) fold_rows(gflags, (ngroups - 1) * GRP);
+    while (open) { const int q = __ffs(open) - 1; open &= open - 1; emit(q, rs[q], last_r); }
+    if (nslow) atomicAdd(a.counters + 2, (unsigned long long)nslow);
+}
+#endif  // VLMP_PACKED
+
 // ---------------------------------------------------------------------------------
 // Exact evaluation of the logged runs: one warp per run. Centred FP64 dot product at the first
 // cell (lane-strided terms, fixed xor-tree reduction), then the diagonal recurrence along the
@@ -465,7 +725,12 @@ __global__ void __launch_bounds__(256) k_runs(const Run* __restrict__ runs, cons
 // host side
 int tile32_width() { return D2; }
 
-size_t tile32_smem() { return sizeof(Smem32); }
+#if VLMP_PACKED
+using SmemT = Smem32p;
+#else
+using SmemT = Smem32;
+#endif
+size_t tile32_smem() { return sizeof(SmemT); }
 
 // FP32 tiles from the FP64 tile list: D2 = 16 pairs (band b, band b+1) of one row segment,
 // b - band_lo even; D2 = 8 keeps the FP64 tiles. Order follows the (longest-first) FP64 list.
@@ -501,14 +766,14 @@ int launch_filter32(vlmp_session* s, cudaStream_t st, const Prm* prm, const doub
         Tile32Args ta{s->d_p32, s->d_cq32, s->d_magblk, s->d_tn, mu, s->d_seeds, s->d_tiles, s->d_tiles32,
                       runs, run_count, run_cap, s->d_counters, forced, N, dl, (int)n_t32, S, m, e,
                       update_seeds, s->sscale};
-        k_tile32<<<(unsigned)n_t32, 32, sizeof(Smem32), st>>>(ta);
+        k_tile32<<<(unsigned)n_t32, 32, sizeof(SmemT), st>>>(ta);
         k_runs<<<148 * 8, 256, 0, st>>>(runs, run_count, run_cap, prm, s->d_tn, mu, m, e, acc, s->d_counters);
     }
     return 0;
 }
 
 int filter32_setup() {
-    cudaError_t e = cudaFuncSetAttribute(k_tile32, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sizeof(Smem32));
+    cudaError_t e = cudaFuncSetAttribute(k_tile32, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sizeof(SmemT));
     if (e != cudaSuccess) return fail(VLMP_E_CUDA, std::string("k_tile32 smem: ") + cudaGetErrorString(e));
     return 0;
 }
