@@ -72,16 +72,18 @@ int vlmp_set_series(vlmp_session* s, const double* t, const double* cum, const d
     long long A = ((n + 1024 + 255) / 256) * 256 + 256;
     s->n = n; s->A = A; s->floor_ = sigma_floor;
     int rc;
-    if ((rc = ensure1(s->d_tn, 2 * A + 4096))) return rc;
-    if ((rc = ensure1(s->d_cum, n + 1))) return rc;
-    if ((rc = ensure1(s->d_cum2, n + 1))) return rc;
-    if ((rc = ensure1(s->d_prm, A))) return rc;
-    if ((rc = ensure1(s->d_mu, A))) return rc;
-    if ((rc = ensure1(s->d_prm2, A))) return rc;
-    if ((rc = ensure1(s->d_mu2, A))) return rc;
-    if ((rc = ensure1(s->d_previdx, A))) return rc;
-    if ((rc = ensure1(s->d_colq, A))) return rc;
-    if ((rc = ensure1(s->d_rowq, A))) return rc;
+    // grow-only: cudaFree / cudaMalloc synchronise the device and cost up to ~1 s on a
+    // loaded allocator -- a repeat call with the same (or a shorter) series allocates nothing
+    if ((rc = ensure(s->d_tn, s->tn_cap, (size_t)(2 * A + 4096)))) return rc;
+    if ((rc = ensure(s->d_cum, s->cum_cap, (size_t)(n + 1)))) return rc;
+    if ((rc = ensure(s->d_cum2, s->cum2_cap, (size_t)(n + 1)))) return rc;
+    if ((rc = ensure(s->d_prm, s->prm_cap, (size_t)A))) return rc;
+    if ((rc = ensure(s->d_mu, s->mu_cap, (size_t)A))) return rc;
+    if ((rc = ensure(s->d_prm2, s->prm2_cap, (size_t)A))) return rc;
+    if ((rc = ensure(s->d_mu2, s->mu2_cap, (size_t)A))) return rc;
+    if ((rc = ensure(s->d_previdx, s->previdx_cap, (size_t)A))) return rc;
+    if ((rc = ensure(s->d_colq, s->colq_cap, (size_t)A))) return rc;
+    if ((rc = ensure(s->d_rowq, s->rowq_cap, (size_t)A))) return rc;
     {   // filter scale: b = sigma sqrt(m) 2^-k stays O(1) whatever the series' units
         double ss = 0.0;
         for (long long i = 0; i < n; ++i) ss += t[i] * t[i];

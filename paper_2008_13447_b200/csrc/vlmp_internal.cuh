@@ -199,6 +199,8 @@ struct vlmp_session {
     long long n = 0, A = 0;
     double floor_ = 0.0;
     double* d_tn = nullptr; double* d_cum = nullptr; double* d_cum2 = nullptr;
+    size_t tn_cap = 0, cum_cap = 0, cum2_cap = 0, prm_cap = 0, mu_cap = 0, prm2_cap = 0, mu2_cap = 0,
+           previdx_cap = 0, colq_cap = 0, rowq_cap = 0;
     // per-length scratch
     Prm* d_prm = nullptr; double* d_mu = nullptr;
     Prm* d_prm2 = nullptr; double* d_mu2 = nullptr;     // previous length's (1-best bound)
