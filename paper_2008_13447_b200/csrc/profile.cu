@@ -1090,6 +1090,31 @@ int vlmp_band_split(vlmp_session* s, int32_t lmin, int32_t lmax, int32_t parts, 
 // to the single-run chain); accumulators of other lengths stay empty.
 constexpr uint32_t F_NO_SAMPLED_START = 1u << 30;   // internal: first length by full folds
 
+// dev aid (scripts/diag_bounds.py, run-log analysis): VLMP_DUMP_PRM / VLMP_DUMP_RUNS = file,
+// VLMP_DUMP_LI = length index (default 64) -- one length's bounds or FP32-walk run log
+static int debug_dump(cudaStream_t st, int li, const Prm* prm, long long N, const Run* runs,
+                      const unsigned long long* run_count, long long run_cap) {
+    const char* dp = getenv("VLMP_DUMP_PRM");
+    const char* dr = getenv("VLMP_DUMP_RUNS");
+    if (!dp && !dr) return 0;
+    if (li != atoi(getenv("VLMP_DUMP_LI") ? getenv("VLMP_DUMP_LI") : "64")) return 0;
+    CU(cudaStreamSynchronize(st));
+    if (dp) {
+        std::vector<Prm> h(N);
+        CU(cudaMemcpy(h.data(), prm, N * sizeof(Prm), cudaMemcpyDeviceToHost));
+        if (FILE* f = fopen(dp, "wb")) { fwrite(h.data(), sizeof(Prm), N, f); fclose(f); }
+    }
+    if (dr) {
+        unsigned long long c = 0;
+        CU(cudaMemcpy(&c, run_count, 8, cudaMemcpyDeviceToHost));
+        c = std::min<unsigned long long>(c, (unsigned long long)run_cap);
+        std::vector<Run> h(c);
+        CU(cudaMemcpy(h.data(), runs, c * sizeof(Run), cudaMemcpyDeviceToHost));
+        if (FILE* f = fopen(dr, "wb")) { fwrite(h.data(), sizeof(Run), c, f); fclose(f); }
+    }
+    return 0;
+}
+
 static int profile_impl(vlmp_session* s, int32_t lmin, int32_t lmax, int64_t band_lo,
                         int64_t band_hi, uint32_t flags, bool* overflow_out, bool* used_sampled,
                         int li_lo = 0, int li_hi = -1, bool* fp32_fallback = nullptr) {
@@ -1257,17 +1282,7 @@ static int profile_impl(vlmp_session* s, int32_t lmin, int32_t lmax, int64_t ban
                                           s->d_acc + (long long)li * A, runs, s->d_logcnt + li, run_cap)))
                     return rc;
                 klaunch += 2;
-                if (const char* dp = getenv("VLMP_DUMP_RUNS")) {   // dev aid: one length's run log
-                    if (li == atoi(getenv("VLMP_DUMP_LI") ? getenv("VLMP_DUMP_LI") : "64")) {
-                        unsigned long long c = 0;
-                        CU(cudaMemcpyAsync(&c, s->d_logcnt + li, 8, cudaMemcpyDeviceToHost, st));
-                        CU(cudaStreamSynchronize(st));
-                        c = std::min<unsigned long long>(c, (unsigned long long)run_cap);
-                        std::vector<Run> h(c);
-                        CU(cudaMemcpy(h.data(), runs, c * sizeof(Run), cudaMemcpyDeviceToHost));
-                        if (FILE* f = fopen(dp, "wb")) { fwrite(h.data(), sizeof(Run), c, f); fclose(f); }
-                    }
-                }
+                if ((rc = debug_dump(st, li, prm, N, runs, s->d_logcnt + li, run_cap))) return rc;
             } else {
                 k_tile<false><<<blocks(T, WARPS_PER_CTA), WARPS_PER_CTA * 32, smem, st>>>(ta);
                 k_log_merge<<<148 * 8, 256, 0, st>>>(s->d_log, s->d_logcnt + li, eff_cap,

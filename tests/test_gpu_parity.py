@@ -177,6 +177,28 @@ def test_cfg2_sampled_rows_against_oracle(oracle_mod):
     assert sorted((int(off[300 - 256, 0]), int(nbr[300 - 256, 0]))) == [5234, 10194]
 
 
+def test_cfg3_sampled_rows_against_oracle(oracle_mod):
+    """Size-independent check at BASELINE config 3 (n = 262,144, lengths 400..600, a noisy
+    sinusoid mixture with a planted discord): sampled (row, length) profiles recomputed by the
+    oracle's exhaustive row scan, plus the planted discord among the top discords."""
+    s = vl.ingest(gen.series_for(3))
+    run = api.GpuRun(s, 400, 600)
+    assert run.stats["fp32_walk"] == 1 and run.stats["exact_redo"] == 0
+    rng = np.random.default_rng(3)
+    for L in (400, 517, 600):
+        mp, ip = run.profile(L)
+        for r in rng.integers(0, mp.shape[0], 8):
+            omp, oip = oracle_mod.profile(s, L, nthreads=8, row_lo=int(r), row_hi=int(r) + 1)
+            if ip[r] != oip[r]:   # only an exact-arithmetic tie may pick another neighbour
+                a = oracle_mod.pair_distance(s, r, ip[r], L); b = oracle_mod.pair_distance(s, r, oip[r], L)
+                assert abs(a - b) <= 1e-9 * max(a, b), (L, r)
+            assert mp[r] == pytest.approx(omp[r], rel=1e-6, abs=1e-9)
+    _, d0 = gen.config3()
+    dist, off = run.discords(1)
+    o = int(off[500 - 400, 0])
+    assert d0 - 500 < o < d0 + 500, (o, d0)   # the planted noise segment is the top discord
+
+
 @pytest.mark.parametrize("case", ["constant_stretch", "dc_offset", "short", "spikes", "lmin4"])
 def test_edge_cases_against_oracle(case, oracle_mod):
     rng = np.random.default_rng(7)
