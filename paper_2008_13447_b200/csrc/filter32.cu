@@ -7,9 +7,10 @@
 // so it runs the diagonal recurrence (SCAMP form)
 //     cov(i,j) = cov(i-1,j-1) + df_i dg_j + df_j dg_i
 // in FP32 from each tile's FP64 seed, with a rigorous error slack eps folded into the seed:
-//   |cov32 - cov| <= (4 S + 16) 2^-24 * 1.05 * max_rows(mag) * max_cols(mag)  (mag >= ||x||, |df|, |dg|)
-// (two roundings per FFMA, the FP32 inputs, the seed conversion; |cov| <= s_i s_j by
-// Cauchy-Schwarz). A cell passes when cov32 + eps >= cA_j b_i, where cA_j b_i <= q(max(U_i,U_j))
+//   |cov32 - cov| <= u [(2K + 1) Sr Sc + 3.02 K (DFr DGc + DFc DGr)] (1 + 1%),  u = 2^-24,
+// K = S + 1 walked rows, Sr/Sc/DF/DG the maxima of the window norms s = ||x|| and of |df|, |dg|
+// over the tile's rows / columns (per row: two FFMA roundings and the FP32-rounded inputs;
+// |cov| <= s_i s_j by Cauchy-Schwarz). A cell passes when cov32 + eps >= cA_j b_i, where cA_j b_i <= q(max(U_i,U_j))
 // s_i s_j (profile.cu's covariance-domain threshold, in FP32 rounded down): one FFMA per cell,
 // its sign bit ANDed over the lane's cells. Passing cells are grouped into runs along their
 // diagonals (the lane tracks which of its diagonals passed at its previous flagged row) and
@@ -45,17 +46,18 @@ constexpr int WIN = VLMP_PACKED ? 8 : D2;   // rows a column meets in one lane (
 // ---------------------------------------------------------------------------------
 // per-length FP32 factors (after k_bound2 wrote U): p32 = {df, dg, b, w}, cq = {a, b}, where
 // b = s 2^-k (rounded down), a = q(U) b, w = q(max U over rows o .. o+D2-1); +inf factors for
-// invalid windows. magblk[o / 256] = max over the block of mag = max(||x_o||, |df_o|, |dg_o|) 2^-k
-// (rounded up; ||x|| from the prefix sums plus their rounding allowance).
+// invalid windows. Block maxima over 256 offsets for the walk's error slack, in
+// magblk[3 * nb]: [0, nb) the window norm ||x_o|| 2^-k (from the prefix sums plus their
+// rounding allowance), [nb, 2 nb) |df_o| 2^-k, [2 nb, 3 nb) |dg_o| 2^-k (all rounded up).
 struct Prep32Args {
     const Prm* prm; const double* cum; const double* cum2;
-    float4* p32; float2* cq; unsigned* magblk;
+    float4* p32; float2* cq; unsigned* magblk; long long nb;
     long long N, A; int m; double sscale; int* forced;
 };
 
 __global__ void __launch_bounds__(256) k_prep32(Prep32Args a) {
     const long long o = blockIdx.x * 256LL + threadIdx.x;
-    float mag = 0.f;
+    float msv = 0.f, mdf = 0.f, mdg = 0.f;
     if (o < a.A) {
         const Prm p = a.prm[o];
         const float df = (float)(p.df * a.sscale), dg = (float)(p.dg * a.sscale);
@@ -82,29 +84,31 @@ __global__ void __launch_bounds__(256) k_prep32(Prep32Args a) {
             const double s = a.cum[o + a.m] - a.cum[o], ss = a.cum2[o + a.m] - a.cum2[o];
             const double mu = s / L;
             const double vu = fmax(ss / L - mu * mu, 0.0) + 0x1p-44 * (fabs(ss) / L + mu * mu);
-            const double nrm = sqrt(vu * L) * a.sscale;
-            const double mx = fmax(nrm, fmax(fabs(p.df), fabs(p.dg)) * a.sscale);
-            mag = __double2float_ru(mx * (1.0 + 0x1p-20));
+            msv = __double2float_ru(sqrt(vu * L) * a.sscale * (1.0 + 0x1p-20));
+            mdf = __double2float_ru(fabs(p.df) * a.sscale * (1.0 + 0x1p-20));
+            mdg = __double2float_ru(fabs(p.dg) * a.sscale * (1.0 + 0x1p-20));
         }
         a.p32[o] = make_float4(df, dg, b, w);
         a.cq[o] = make_float2(ca, b == b ? b : 1.0f);
     }
-    // one 256-offset block per CTA: max over the block (non-negative floats order as integers)
-    unsigned v = __reduce_max_sync(FULLMASK, __float_as_uint(mag));
-    __shared__ unsigned wm[8];
-    if ((threadIdx.x & 31) == 0) wm[threadIdx.x >> 5] = v;
+    // one 256-offset block per CTA: maxima over the block (non-negative floats order as integers)
+    const unsigned v0 = __reduce_max_sync(FULLMASK, __float_as_uint(msv));
+    const unsigned v1 = __reduce_max_sync(FULLMASK, __float_as_uint(mdf));
+    const unsigned v2 = __reduce_max_sync(FULLMASK, __float_as_uint(mdg));
+    __shared__ unsigned wm[3][8];
+    if ((threadIdx.x & 31) == 0) { wm[0][threadIdx.x >> 5] = v0; wm[1][threadIdx.x >> 5] = v1; wm[2][threadIdx.x >> 5] = v2; }
     __syncthreads();
-    if (threadIdx.x == 0) {
+    if (threadIdx.x < 3) {
         unsigned r = 0;
 #pragma unroll
-        for (int k = 0; k < 8; ++k) r = max(r, wm[k]);
-        a.magblk[blockIdx.x] = r;
+        for (int k = 0; k < 8; ++k) r = max(r, wm[threadIdx.x][k]);
+        a.magblk[threadIdx.x * a.nb + blockIdx.x] = r;
     }
 }
 
 // ---------------------------------------------------------------------------------
 struct Tile32Args {
-    const float4* p32; const float2* cq; const unsigned* magblk;
+    const float4* p32; const float2* cq; const unsigned* magblk; long long nb;
     const double* __restrict__ tn; const double* __restrict__ mu; double* seeds;
     const int2* tiles;      // FP64 tile list (band, segment)
     const int2* tiles32;    // FP32 tiles: {FP64 tile of the lower band, of the upper band or -1}
@@ -184,18 +188,26 @@ __global__ void __launch_bounds__(32, VLMP_FILTER32_WARPS_PER_SM) k_tile32(Tile3
     const int ngroups = (nrows + GR2 - 1) / GR2;
     const long long cbase = i0 + d0 + (long long)D2 * lane;   // column of slot 0 at row i0
 
-    // ---- slack: rows [i0, i0 + nrows), columns [i0 + d0, i0 + nrows - 1 + d0 + BAND2 - 1]
+    // ---- FP32 error slack. Per walked row (two FFMA over FP32-rounded df, dg) the covariance
+    // error grows by at most 2u|cov| + 3.02u(|df_i dg_j| + |df_j dg_i|), u = 2^-24, with
+    // |cov| <= s_i s_j (Cauchy-Schwarz); S + 1 rows (with the seed pre-adjust) plus the seed's
+    // conversion, over the maxima of s, |df|, |dg| on the tile's rows and columns.
     float eps;
     {
         const long long rb0 = i0 >> 8, rb1 = (i0 + nrows - 1) >> 8;
         const long long cb0 = (i0 + d0) >> 8, cb1 = (i0 + nrows - 1 + d0 + BAND2 - 1) >> 8;
-        unsigned mr = 0, mc = 0;
-        for (long long k = rb0 + lane; k <= rb1; k += 32) mr = max(mr, a.magblk[k]);
-        for (long long k = cb0 + lane; k <= cb1; k += 32) mc = max(mc, a.magblk[k]);
-        mr = __reduce_max_sync(FULLMASK, mr);
-        mc = __reduce_max_sync(FULLMASK, mc);
-        const double bound = (4.0 * a.S + 16.0) * 0x1p-24 * 1.05 *
-                             (double)__uint_as_float(mr) * (double)__uint_as_float(mc);
+        unsigned r[3] = {0, 0, 0}, c[3] = {0, 0, 0};
+#pragma unroll
+        for (int q = 0; q < 3; ++q) {
+            for (long long k = rb0 + lane; k <= rb1; k += 32) r[q] = max(r[q], a.magblk[q * a.nb + k]);
+            for (long long k = cb0 + lane; k <= cb1; k += 32) c[q] = max(c[q], a.magblk[q * a.nb + k]);
+            r[q] = __reduce_max_sync(FULLMASK, r[q]);
+            c[q] = __reduce_max_sync(FULLMASK, c[q]);
+        }
+        const double Sr = __uint_as_float(r[0]), DFr = __uint_as_float(r[1]), DGr = __uint_as_float(r[2]);
+        const double Sc = __uint_as_float(c[0]), DFc = __uint_as_float(c[1]), DGc = __uint_as_float(c[2]);
+        const double K = (double)a.S + 1.0;
+        const double bound = 0x1p-24 * 1.01 * ((2.0 * K + 1.0) * 1.001 * Sr * Sc + 3.02 * K * (DFr * DGc + DFc * DGr));
         eps = __double2float_ru(bound);
     }
 
@@ -422,17 +434,26 @@ __global__ void __launch_bounds__(32, VLMP_FILTER32_WARPS_PER_SM) k_tile32(Tile3
     const long long cbA = i0 + d0 + (long long)DP * lane;   // band A column of slot 0 at row i0
     const long long cbB = cbA + BAND;
 
+    // ---- FP32 error slack. Per walked row (two FFMA over FP32-rounded df, dg) the covariance
+    // error grows by at most 2u|cov| + 3.02u(|df_i dg_j| + |df_j dg_i|), u = 2^-24, with
+    // |cov| <= s_i s_j (Cauchy-Schwarz); S + 1 rows (with the seed pre-adjust) plus the seed's
+    // conversion, over the maxima of s, |df|, |dg| on the tile's rows and columns.
     float eps;
     {
         const long long rb0 = i0 >> 8, rb1 = (i0 + nrows - 1) >> 8;
         const long long cb0 = (i0 + d0) >> 8, cb1 = (i0 + nrows - 1 + d0 + 2 * BAND - 1) >> 8;
-        unsigned mr = 0, mc = 0;
-        for (long long k = rb0 + lane; k <= rb1; k += 32) mr = max(mr, a.magblk[k]);
-        for (long long k = cb0 + lane; k <= cb1; k += 32) mc = max(mc, a.magblk[k]);
-        mr = __reduce_max_sync(FULLMASK, mr);
-        mc = __reduce_max_sync(FULLMASK, mc);
-        const double bound = (4.0 * a.S + 16.0) * 0x1p-24 * 1.05 *
-                             (double)__uint_as_float(mr) * (double)__uint_as_float(mc);
+        unsigned r[3] = {0, 0, 0}, c[3] = {0, 0, 0};
+#pragma unroll
+        for (int q = 0; q < 3; ++q) {
+            for (long long k = rb0 + lane; k <= rb1; k += 32) r[q] = max(r[q], a.magblk[q * a.nb + k]);
+            for (long long k = cb0 + lane; k <= cb1; k += 32) c[q] = max(c[q], a.magblk[q * a.nb + k]);
+            r[q] = __reduce_max_sync(FULLMASK, r[q]);
+            c[q] = __reduce_max_sync(FULLMASK, c[q]);
+        }
+        const double Sr = __uint_as_float(r[0]), DFr = __uint_as_float(r[1]), DGr = __uint_as_float(r[2]);
+        const double Sc = __uint_as_float(c[0]), DFc = __uint_as_float(c[1]), DGc = __uint_as_float(c[2]);
+        const double K = (double)a.S + 1.0;
+        const double bound = 0x1p-24 * 1.01 * ((2.0 * K + 1.0) * 1.001 * Sr * Sc + 3.02 * K * (DFr * DGc + DFc * DGr));
         eps = __double2float_ru(bound);
     }
 
@@ -759,11 +780,12 @@ int launch_filter32(vlmp_session* s, cudaStream_t st, const Prm* prm, const doub
                     long long dl, int S, int update_seeds, long long n_t32, const int* forced,
                     ulonglong2* acc, Run* runs, unsigned long long* run_count, long long run_cap) {
     const long long A = s->A;
-    Prep32Args pa{prm, s->d_cum, s->d_cum2, s->d_p32, s->d_cq32, s->d_magblk, N, A, m, s->sscale,
+    const long long nb = A / 256 + 1;
+    Prep32Args pa{prm, s->d_cum, s->d_cum2, s->d_p32, s->d_cq32, s->d_magblk, nb, N, A, m, s->sscale,
                   const_cast<int*>(forced)};
     k_prep32<<<blocks(A, 256), 256, 0, st>>>(pa);
     if (n_t32) {
-        Tile32Args ta{s->d_p32, s->d_cq32, s->d_magblk, s->d_tn, mu, s->d_seeds, s->d_tiles, s->d_tiles32,
+        Tile32Args ta{s->d_p32, s->d_cq32, s->d_magblk, nb, s->d_tn, mu, s->d_seeds, s->d_tiles, s->d_tiles32,
                       runs, run_count, run_cap, s->d_counters, forced, N, dl, (int)n_t32, S, m, e,
                       update_seeds, s->sscale};
         k_tile32<<<(unsigned)n_t32, 32, sizeof(SmemT), st>>>(ta);
