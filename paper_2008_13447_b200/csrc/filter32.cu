@@ -53,6 +53,7 @@ struct Prep32Args {
     const Prm* prm; const double* cum; const double* cum2;
     float4* p32; float2* cq; unsigned* magblk; long long nb;
     long long N, A; int m; double sscale; int* forced;
+    float4* cq4;   // packed walk: {a_o, b_o, a_{o+256}, b_{o+256}} (nullptr: not built)
 };
 
 __global__ void __launch_bounds__(256) k_prep32(Prep32Args a) {
@@ -106,6 +107,15 @@ __global__ void __launch_bounds__(256) k_prep32(Prep32Args a) {
     }
 }
 
+// packed walk: the column factors of a band pair (o, o + 256) in one 16-byte entry, so the walk
+// stages each entering pair with one cp.async
+__global__ void k_pair_cq(const float2* __restrict__ cq, float4* cq4, long long A) {
+    const long long o = blockIdx.x * (long long)blockDim.x + threadIdx.x;
+    if (o + BAND >= A) return;
+    const float2 x = cq[o], y = cq[o + BAND];
+    cq4[o] = make_float4(x.x, x.y, y.x, y.y);
+}
+
 // ---------------------------------------------------------------------------------
 struct Tile32Args {
     const float4* p32; const float2* cq; const unsigned* magblk; long long nb;
@@ -117,6 +127,7 @@ struct Tile32Args {
     const int* forced;
     long long N, dlo; int n_tiles32, S, m, e, update_seeds;
     double sscale;
+    const float4* cq4;      // packed walk: band-pair column factors
 };
 
 struct Smem32 {
@@ -140,6 +151,11 @@ __device__ __forceinline__ void cpa(unsigned d, const char* s) {
         asm volatile("cp.async.cg.shared.global [%0+%2], [%1+%3], 16;\n" :: "r"(d), "l"(s), "n"(OFF_D), "n"(OFF_S) : "memory");
     else
         asm volatile("cp.async.ca.shared.global [%0+%2], [%1+%3], 8;\n" :: "r"(d), "l"(s), "n"(OFF_D), "n"(OFF_S) : "memory");
+}
+// 16 bytes through L1: column factors are re-read by the neighbouring tiles on the SM
+template <int OFF_D, int OFF_S>
+__device__ __forceinline__ void cpa_l1(unsigned d, const char* s) {
+    asm volatile("cp.async.ca.shared.global [%0+%2], [%1+%3], 16;\n" :: "r"(d), "l"(s), "n"(OFF_D), "n"(OFF_S) : "memory");
 }
 
 template <int K>
@@ -524,16 +540,16 @@ __global__ void __launch_bounds__(32, VLMP_FILTER32_WARPS_PER_SM) k_tile32(Tile3
             dst_rf = (unsigned)__cvta_generic_to_shared(&sm.fresh[0][q]);
         }
     }
-    // entering A column f = 8L + kk (f = lane + 32k) -> slot kk * 33 + L, low half; B: high half
-    const char* src_cq = reinterpret_cast<const char*>(a.cq + i0 + d0 + DP - 1 + lane);
+    // entering pair f = 8L + kk (f = lane + 32k): one 16-byte {aA, bA, aB, bB} -> slot kk * 33 + L
+    const char* src_cq = reinterpret_cast<const char*>(a.cq4 + i0 + d0 + DP - 1 + lane);
     const unsigned dst_cq = (unsigned)__cvta_generic_to_shared(&sm.cq[0][(lane % 8) * CQS + lane / 8]);
     constexpr unsigned RFP = sizeof(float4) * GRP, CQP = sizeof(float4) * GRP * CQS;
     auto stage = [&](int g, int b) {
         const long long gr = (long long)g * (GRP * sizeof(float4));
         if (lane < 16) cpa<0, 0, 16>(dst_rf + (unsigned)b * RFP, src_rf + gr);
         const unsigned dc = dst_cq + (unsigned)b * CQP;
-        const char* sc = src_cq + (long long)g * (GRP * sizeof(float2));
-#define STG(K) cpa<(K) * 4 * 16, (K) * 256, 8>(dc, sc); cpa<(K) * 4 * 16 + 8, (K) * 256 + BAND * 8, 8>(dc, sc);
+        const char* sc = src_cq + (long long)g * (GRP * sizeof(float4));
+#define STG(K) cpa_l1<(K) * 4 * 16, (K) * 512>(dc, sc);
         STG(0) STG(1) STG(2) STG(3) STG(4) STG(5) STG(6) STG(7)
 #undef STG
         cp_async_commit();
@@ -782,12 +798,15 @@ int launch_filter32(vlmp_session* s, cudaStream_t st, const Prm* prm, const doub
     const long long A = s->A;
     const long long nb = A / 256 + 1;
     Prep32Args pa{prm, s->d_cum, s->d_cum2, s->d_p32, s->d_cq32, s->d_magblk, nb, N, A, m, s->sscale,
-                  const_cast<int*>(forced)};
+                  const_cast<int*>(forced), nullptr};
     k_prep32<<<blocks(A, 256), 256, 0, st>>>(pa);
     if (n_t32) {
+#if VLMP_PACKED
+        k_pair_cq<<<blocks(A, 256), 256, 0, st>>>(s->d_cq32, s->d_cq4, A);
+#endif
         Tile32Args ta{s->d_p32, s->d_cq32, s->d_magblk, nb, s->d_tn, mu, s->d_seeds, s->d_tiles, s->d_tiles32,
                       runs, run_count, run_cap, s->d_counters, forced, N, dl, (int)n_t32, S, m, e,
-                      update_seeds, s->sscale};
+                      update_seeds, s->sscale, s->d_cq4};
         k_tile32<<<(unsigned)n_t32, 32, sizeof(SmemT), st>>>(ta);
         k_runs<<<148 * 8, 256, 0, st>>>(runs, run_count, run_cap, prm, s->d_tn, mu, m, e, acc, s->d_counters);
     }

@@ -1181,6 +1181,7 @@ static int profile_impl(vlmp_session* s, int32_t lmin, int32_t lmax, int64_t ban
         if ((rc = ensure(s->d_tiles32, s->tiles32_cap, std::max<size_t>(tiles32.size(), 1)))) return rc;
         if ((rc = ensure(s->d_p32, s->p32_cap, (size_t)A))) return rc;
         if ((rc = ensure(s->d_cq32, s->cq32_cap, (size_t)A))) return rc;
+        if ((rc = ensure(s->d_cq4, s->cq4_cap, (size_t)A))) return rc;
         if ((rc = ensure(s->d_magblk, s->magblk_cap, (size_t)(3 * (A / 256 + 1))))) return rc;
         if (!tiles32.empty())
             CU(cudaMemcpyAsync(s->d_tiles32, tiles32.data(), tiles32.size() * sizeof(int2), cudaMemcpyHostToDevice, st));
