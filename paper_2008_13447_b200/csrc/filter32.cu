@@ -674,10 +674,14 @@ __global__ void __launch_bounds__(32, VLMP_FILTER32_WARPS_PER_SM) k_tile32(Tile3
 // run as an ordered inclusive warp scan of the per-step terms df_i dg_j + df_j dg_i; keys by
 // the full-fold formula r = 1 - cov inv_i inv_j, exact tests hi(r) <= U (row and column side,
 // as k_log_merge), 128-bit CAS folds. Deterministic (fixed reduction and scan orders).
+// slots == nullptr: fold into the 1-best accumulators; else (m-best mode, m > 1 discords) append
+// every cell that passes an exact test to its offset's candidate slots (SLOT_CAP per offset;
+// k_select_m keeps the m smallest and recomputes offsets whose slots overflowed)
 __global__ void __launch_bounds__(256) k_runs(const Run* __restrict__ runs, const unsigned long long* run_count,
                                              long long cap, const Prm* __restrict__ prm,
                                              const double* __restrict__ tn, const double* __restrict__ mu,
-                                             int m, int e, ulonglong2* acc, unsigned long long* counters) {
+                                             int m, int e, ulonglong2* acc, unsigned long long* counters,
+                                             ulonglong2* slots, int* slot_cnt) {
     const unsigned long long cnt = *run_count;
     const long long nr = (long long)(cnt < (unsigned long long)cap ? cnt : (unsigned long long)cap);
     const int lane = threadIdx.x & 31;
@@ -744,8 +748,21 @@ __global__ void __launch_bounds__(256) k_runs(const Run* __restrict__ runs, cons
                 const double r = fma(-(cv * ii), ij, 1.0);
                 const float h = __int_as_float(__double2hiint(r));
                 const unsigned long long key = clamp_key(r) & ~PMASK;
-                if (h <= ui) { acc_merge(acc + i + k, key, j + k); ++merged; }
-                if (h <= uj) { acc_merge(acc + j + k, key, i + k); ++merged; }
+                if (slots) {
+                    if (h <= ui) {
+                        const int at = atomicAdd(slot_cnt + i + k, 1);
+                        if (at < SLOT_CAP) slots[(i + k) * SLOT_CAP + at] = make_ulonglong2(key, (unsigned long long)(j + k));
+                        ++merged;
+                    }
+                    if (h <= uj) {
+                        const int at = atomicAdd(slot_cnt + j + k, 1);
+                        if (at < SLOT_CAP) slots[(j + k) * SLOT_CAP + at] = make_ulonglong2(key, (unsigned long long)(i + k));
+                        ++merged;
+                    }
+                } else {
+                    if (h <= ui) { acc_merge(acc + i + k, key, j + k); ++merged; }
+                    if (h <= uj) { acc_merge(acc + j + k, key, i + k); ++merged; }
+                }
             }
         }
         if (lane == 0) cells += (unsigned long long)R.len;
@@ -794,7 +811,8 @@ void build_tiles32(const std::vector<int2>& tiles, long long band_lo, std::vecto
 
 int launch_filter32(vlmp_session* s, cudaStream_t st, const Prm* prm, const double* mu, long long N, int m, int e,
                     long long dl, int S, int update_seeds, long long n_t32, const int* forced,
-                    ulonglong2* acc, Run* runs, unsigned long long* run_count, long long run_cap) {
+                    ulonglong2* acc, Run* runs, unsigned long long* run_count, long long run_cap,
+                    ulonglong2* slots, int* slot_cnt) {
     const long long A = s->A;
     const long long nb = A / 256 + 1;
     Prep32Args pa{prm, s->d_cum, s->d_cum2, s->d_p32, s->d_cq32, s->d_magblk, nb, N, A, m, s->sscale,
@@ -808,7 +826,8 @@ int launch_filter32(vlmp_session* s, cudaStream_t st, const Prm* prm, const doub
                       runs, run_count, run_cap, s->d_counters, forced, N, dl, (int)n_t32, S, m, e,
                       update_seeds, s->sscale, s->d_cq4};
         k_tile32<<<(unsigned)n_t32, 32, sizeof(SmemT), st>>>(ta);
-        k_runs<<<148 * 8, 256, 0, st>>>(runs, run_count, run_cap, prm, s->d_tn, mu, m, e, acc, s->d_counters);
+        k_runs<<<148 * 8, 256, 0, st>>>(runs, run_count, run_cap, prm, s->d_tn, mu, m, e, acc, s->d_counters,
+                                        slots, slot_cnt);
     }
     return 0;
 }

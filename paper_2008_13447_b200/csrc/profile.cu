@@ -734,8 +734,6 @@ __global__ void k_import(ulonglong2* acc, const unsigned long long* keys, const 
 // The filter tile kernel runs with U = a bound on each offset's m-th best key; passing
 // cells go to per-offset slots; k_select_m keeps the m smallest (key, index); offsets
 // whose slots overflow are recomputed exactly from direct dot products.
-constexpr int MB_MAX = 8;                 // largest supported m
-constexpr int SLOT_CAP = 24;              // candidate slots per offset per length
 
 struct BoundMArgs {
     const double* tn; const double* mu; Prm* prm;
@@ -1484,6 +1482,26 @@ int vlmp_profile_mbest(vlmp_session* s, int32_t lmin, int32_t lmax, int32_t mb) 
     const size_t smem = WARPS_PER_CTA * sizeof(WarpSmem);
     CU(cudaFuncSetAttribute(k_tile<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
     CU(cudaFuncSetAttribute(k_tile<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    // the filtered pass: FP32 walk + exact runs into the candidate slots (filter32.cu) unless the
+    // FP64 walk + covariance log is asked for (VLMP_FP64_FILTER, A/B checks)
+    const bool fp32 = !getenv("VLMP_FP64_FILTER");
+    std::vector<int2> tiles32;
+    Run* runs = reinterpret_cast<Run*>(s->d_log);
+    const long long run_cap = (long long)(s->log_cap * sizeof(RowRec) / sizeof(Run));
+    if (fp32) {
+        build_tiles32(tiles, 0, tiles32);
+        if ((rc = ensure(s->d_tiles32, s->tiles32_cap, std::max<size_t>(tiles32.size(), 1)))) return rc;
+        if ((rc = ensure(s->d_p32, s->p32_cap, (size_t)A))) return rc;
+        if ((rc = ensure(s->d_cq32, s->cq32_cap, (size_t)A))) return rc;
+        if ((rc = ensure(s->d_cq4, s->cq4_cap, (size_t)A))) return rc;
+        if ((rc = ensure(s->d_magblk, s->magblk_cap, (size_t)(3 * (A / 256 + 1))))) return rc;
+        if ((rc = ensure(s->d_forced, s->forced_cap, (size_t)n_len))) return rc;
+        CU(cudaMemsetAsync(s->d_forced, 0, n_len * sizeof(int), st));
+        if (!tiles32.empty())
+            CU(cudaMemcpyAsync(s->d_tiles32, tiles32.data(), tiles32.size() * sizeof(int2), cudaMemcpyHostToDevice, st));
+        if ((rc = filter32_setup())) return rc;
+    }
+    const long long T32 = (long long)tiles32.size();
     CU(cudaEventRecord(s->ev[0], st));
     const double margin = 1.0 / (1 << 26);
     long long redo_total = 0;
@@ -1511,13 +1529,21 @@ int vlmp_profile_mbest(vlmp_session* s, int32_t lmin, int32_t lmax, int32_t mb) 
             bm.prevm = s->d_ipm + (long long)(li - 1) * A * mb;
         }
         k_bound_m<<<blocks(N * 32, 256), 256, 0, st>>>(bm);
-        // no full-fold fallback here (it folds the 1-best only): forced offsets are recomputed
-        k_qprep<<<blocks(A, 256), 256, 0, st>>>(s->d_prm, s->d_colq, s->d_rowq, N, A, s->sscale, nullptr);
-        if (T) {
-            ta.update_seeds = li + 1 < n_len;
-            k_tile<false><<<blocks(T, WARPS_PER_CTA), WARPS_PER_CTA * 32, smem, st>>>(ta);
-            k_log_slots<<<296, 128, 0, st>>>(s->d_log, s->d_logcnt + li, (long long)s->log_cap, s->d_prm, e,
-                                             s->d_slots, s->d_slotcnt, s->d_counters);
+        if (fp32) {
+            // forced offsets (weak bounds) pass every cell of the walk: their slots overflow and
+            // k_recompute_m takes them exactly
+            if ((rc = launch_filter32(s, st, s->d_prm, s->d_mu, N, m, e, dl, S, li + 1 < n_len, T32,
+                                      s->d_forced + li, s->d_acc, runs, s->d_logcnt + li, run_cap,
+                                      s->d_slots, s->d_slotcnt))) return rc;
+        } else {
+            // no full-fold fallback here (it folds the 1-best only): forced offsets are recomputed
+            k_qprep<<<blocks(A, 256), 256, 0, st>>>(s->d_prm, s->d_colq, s->d_rowq, N, A, s->sscale, nullptr);
+            if (T) {
+                ta.update_seeds = li + 1 < n_len;
+                k_tile<false><<<blocks(T, WARPS_PER_CTA), WARPS_PER_CTA * 32, smem, st>>>(ta);
+                k_log_slots<<<296, 128, 0, st>>>(s->d_log, s->d_logcnt + li, (long long)s->log_cap, s->d_prm, e,
+                                                 s->d_slots, s->d_slotcnt, s->d_counters);
+            }
         }
         CU(cudaMemsetAsync(s->d_ro_cnt, 0, 8, st));
         int* out = s->d_ipm + (long long)li * A * mb;
@@ -1536,7 +1562,8 @@ int vlmp_profile_mbest(vlmp_session* s, int32_t lmin, int32_t lmax, int32_t mb) 
     std::vector<unsigned long long> lc(n_len);
     CU(cudaMemcpy(lc.data(), s->d_logcnt, n_len * sizeof(unsigned long long), cudaMemcpyDeviceToHost));
     for (auto c : lc)
-        if (c > s->log_cap) return fail(VLMP_E_CUDA, "m-best candidate log overflow (bounds too weak for this series)");
+        if ((long long)c > (fp32 ? run_cap : (long long)s->log_cap))
+            return fail(VLMP_E_CUDA, "m-best candidate log overflow (bounds too weak for this series)");
     // finalize: canonical sorted distances of the m best; MP/IP (first neighbour) for VALMP
     if ((rc = ensure(s->d_mpm, s->mpm_cap, (size_t)n_len * A * mb))) return rc;
     dim3 grid(blocks(N0, 128), n_len);

@@ -165,6 +165,9 @@ __device__ inline bool q_forced(const Prm& p, double sscale) {
     return qfac(p.U) == 0.0 || !(b >= 0x1p-40f && b <= 0x1p40f);
 }
 
+constexpr int MB_MAX = 8;                 // m-best mode: largest supported m
+constexpr int SLOT_CAP = 24;              // m-best mode: candidate slots per offset per length
+
 // FP32 filter (filter32.cu): a run of consecutive passing cells along one diagonal of a tile,
 // (i, j), (i+1, j+1), ..., len cells; evaluated exactly in FP64 by k_runs
 struct __align__(16) Run { int i; int j; int len; int pad; };
@@ -253,5 +256,6 @@ int filter32_setup();
 void build_tiles32(const std::vector<int2>& tiles, long long band_lo, std::vector<int2>& out);
 int launch_filter32(vlmp_session* s, cudaStream_t st, const Prm* prm, const double* mu, long long N, int m, int e,
                     long long dl, int S, int update_seeds, long long n_t32, const int* forced,
-                    ulonglong2* acc, Run* runs, unsigned long long* run_count, long long run_cap);
+                    ulonglong2* acc, Run* runs, unsigned long long* run_count, long long run_cap,
+                    ulonglong2* slots = nullptr, int* slot_cnt = nullptr);
 }  // namespace vlmp_impl

@@ -151,3 +151,32 @@ def test_fp32_white_noise(oracle_mod):
         omp, oip = ref["profiles"][L]
         assert np.array_equal(ip, oip), L
         assert np.allclose(mp, omp, rtol=1e-7, atol=1e-9)
+
+
+def test_m_best_on_fp32_walk_spiky():
+    """m-best mode (m-th discords) on the FP32 walk over the high dynamic-range series: each
+    offset's m = 3 nearest neighbours equal the exact ones under the reference's statistics."""
+    rng = np.random.default_rng(12)
+    t = rng.standard_normal(6000) * 1e-3
+    t[1000:1400] += rng.standard_normal(400) * 50.0
+    t[4000:4600] += np.cumsum(rng.standard_normal(600)) * 20.0
+    s = vl.ingest(t)
+    sess = _lib.session(0)
+    with sess.lock:
+        sess.set_series(s.values, s._cum, s._cum2, s.sigma_floor)
+        sess.profile_mbest(40, 44, 3)
+        got = {L: sess.profile_m_arrays(L) for L in range(40, 45)}
+    for L in range(40, 45):
+        d, nbr = got[L]
+        W = np.lib.stride_tricks.sliding_window_view(t, L)
+        mu = (s._cum[L:] - s._cum[:-L]) / L
+        var = np.maximum((s._cum2[L:] - s._cum2[:-L]) / L - mu * mu, 0.0)
+        X = (W - mu[:, None]) / np.sqrt(var * L)[:, None]
+        N, e = W.shape[0], (L + 1) // 2
+        idx = np.arange(N)
+        for b0 in range(0, N, 1024):
+            r2 = np.maximum(2 * L * (1 - X[b0:b0 + 1024] @ X.T), 0)
+            r2[np.abs(idx[b0:b0 + 1024, None] - idx[None, :]) < e] = np.inf
+            best = np.sort(r2, 1)[:, :3]
+            mine = np.take_along_axis(r2, nbr[b0:b0 + 1024, :3], 1)
+            assert np.allclose(np.sort(mine, 1), best, rtol=1e-9, atol=1e-12), (L, b0)
