@@ -19,12 +19,16 @@ struct FinArgs {
 // product is a sequential left-to-right sum over k < m, so when an offset keeps the same
 // canonical pair (a, b) from length m-1 to m its sum at m is the sum at m-1 plus one term
 // -- bit-identical to recomputing it. Only neighbour changes pay the O(m) sum.
+// gridDim.y chunks of lengths per offset (more threads in flight); a chunk's first pair sums
+// from scratch, which is the same sequential sum the incremental path extends
 __global__ void k_finalize_walk(FinArgs a) {
     const long long o = blockIdx.x * (long long)blockDim.x + threadIdx.x;
     if (o >= a.n - a.lmin + 1) return;
     long long pa = -1, pb = -1; int pm = -1;
     double qt = 0.0;
-    for (int li = 0; li < a.n_len; ++li) {
+    const int l0 = (int)((long long)a.n_len * blockIdx.y / gridDim.y);
+    const int l1 = (int)((long long)a.n_len * (blockIdx.y + 1) / gridDim.y);
+    for (int li = l0; li < l1; ++li) {
         const int m = a.lmin + li;
         if (o > a.n - m) break;
         if (li < a.li_lo || li > a.li_hi) {   // another shard's length: neutral for MIN / MAX
@@ -311,7 +315,8 @@ static int finalize_impl(vlmp_session* s, int li_lo, int li_hi, bool readoffs) {
     if (li_lo <= li_hi) {
         FinArgs fa{s->d_tn, s->d_cum, s->d_cum2, s->d_acc, s->d_mp, s->d_ip, n, A, s->lmin, s->n_len, s->floor_,
                    li_lo, li_hi};
-        k_finalize_walk<<<blocks(n0, 64), 64, 0, st>>>(fa);
+        const unsigned chunks = (unsigned)std::min(8, std::max(1, s->n_len / 8));
+        k_finalize_walk<<<dim3(blocks(n0, 64), chunks), 64, 0, st>>>(fa);
         s->stats[9] += 1;
     }
     if (readoffs) {
