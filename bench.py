@@ -304,7 +304,7 @@ def run_ours(args):
                    "lmax": c.lmax, "k_motif": c.k_motif, "k_discord": c.k_discord,
                    "W_updates": W, "parallelism": f"length shards x{world}",
                    "l2": "working set (series + per-length params, 2.6 MB) is L2-resident by design; "
-                         "no flush: the kernel is FP64-bound, not memory-bound"},
+                         "no flush: the walk is latency/FMA-pipe bound (FP32), not memory-bound"},
         "roofline": {"bound": "fp64_fma", "achieved": achieved, "peak": peak, "unit": "TFLOP/s",
                      "frac": achieved / peak, "traffic": prof_traffic,
                      "peak_source": "measured DFMA microbenchmark (vlmp_measure_fp64_peak); "
