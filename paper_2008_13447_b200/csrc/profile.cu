@@ -1208,13 +1208,26 @@ static int profile_impl(vlmp_session* s, int32_t lmin, int32_t lmax, int64_t ban
     if (li_hi < li_lo) li_hi = -1;                                        // empty shard: no work
     std::vector<int> timed;   // lengths whose tile pass ran (event pairs)
     if (li_lo > 0 && li_lo <= li_hi && T) {
-        // a later length shard: seeds at lmin (direct sums), carried to its first length
-        ParamArgs pa{s->d_tn, s->d_cum, s->d_cum2, s->d_prm, s->d_mu, n, n - lmin + 1, A, lmin, s->floor_};
-        k_params<<<blocks(A, 256), 256, 0, st>>>(pa);
-        SeedArgs sa{s->d_tn, s->d_mu, s->d_tiles, s->d_seeds, dl, (int)T, S, lmin};
-        k_seed_init<<<blocks(T * 32, WARPS_PER_CTA * 32), WARPS_PER_CTA * 32, 0, st>>>(sa);
-        k_seed_forward<<<blocks(T * 32, 128), 128, 0, st>>>(sa, s->d_cum, lmin + li_lo);
-        klaunch += 3;
+        if (fp32) {
+            // a later length shard on the FP32 walk: the seeds only start the walk (its slack
+            // covers their rounding; keys come from the exact runs), so they are direct sums at
+            // the shard's first length -- no carry through the lengths before it
+            const int m0 = lmin + li_lo;
+            ParamArgs pa{s->d_tn, s->d_cum, s->d_cum2, s->d_prm, s->d_mu, n, n - m0 + 1, A, m0, s->floor_};
+            k_params<<<blocks(A, 256), 256, 0, st>>>(pa);
+            SeedArgs sa{s->d_tn, s->d_mu, s->d_tiles, s->d_seeds, dl, (int)T, S, m0};
+            k_seed_init<<<blocks(T * 32, WARPS_PER_CTA * 32), WARPS_PER_CTA * 32, 0, st>>>(sa);
+            klaunch += 2;
+        } else {
+            // FP64 walk: seeds at lmin (direct sums), carried to the shard's first length with
+            // the tile kernel's own Welford step (bit-identical to the single-GPU chain)
+            ParamArgs pa{s->d_tn, s->d_cum, s->d_cum2, s->d_prm, s->d_mu, n, n - lmin + 1, A, lmin, s->floor_};
+            k_params<<<blocks(A, 256), 256, 0, st>>>(pa);
+            SeedArgs sa{s->d_tn, s->d_mu, s->d_tiles, s->d_seeds, dl, (int)T, S, lmin};
+            k_seed_init<<<blocks(T * 32, WARPS_PER_CTA * 32), WARPS_PER_CTA * 32, 0, st>>>(sa);
+            k_seed_forward<<<blocks(T * 32, 128), 128, 0, st>>>(sa, s->d_cum, lmin + li_lo);
+            klaunch += 3;
+        }
     }
     for (int li = (li_lo <= li_hi ? li_lo : 0); li <= li_hi; ++li) {
         const int m = lmin + li;

@@ -1,0 +1,37 @@
+"""Per-shard cost of length-sharded runs, measured on one GPU (dev aid): each rank's work
+(seed carry-forward, first-length pass, filtered walks, finalize of its lengths, read-offs) is
+run alone; the slowest shard against the single-GPU step gives the strong-scaling efficiency
+the exchange-free part allows (the NVLink all-reduces are not included)."""
+import os, sys, time
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+import numpy as np
+import torch
+from paper_2008_13447_b200 import _lib, distributed, gen, ingest
+lmin, lmax = 256, 384
+s = ingest(gen.series_for(2))
+sess = _lib.session(0)
+
+def timed(fn, reps=3):
+    best = 1e30
+    for _ in range(reps):
+        torch.cuda.synchronize(); t0 = time.perf_counter(); fn(); torch.cuda.synchronize()
+        best = min(best, time.perf_counter() - t0)
+    return best * 1e3
+
+with sess.lock:
+    sess.set_series(s.values, s._cum, s._cum2, s.sigma_floor)
+    def single():
+        sess.profile(lmin, lmax, 0, -1, 0); sess.finalize(); sess.smallest_rows(6); sess.discords(3)
+    t1 = timed(single)
+    print("single GPU step %.1f ms" % t1)
+    for world in (2, 4, 8):
+        cuts = distributed.length_split(s.n, lmin, lmax, world)
+        ts = []
+        for r in range(world):
+            lo, hi = int(cuts[r]), int(cuts[r + 1]) - 1
+            def shard():
+                sess.profile_lengths(lmin, lmax, lo, hi); sess.finalize_lengths(lo, hi)
+                sess.finalize_readoffs(); sess.smallest_rows(6); sess.discords(3)
+            ts.append(timed(shard))
+        print("world %d: shard ms %s  max %.1f  efficiency (no exchange) %.2f" % (
+            world, " ".join("%.1f" % t for t in ts), max(ts), t1 / (world * max(ts))), flush=True)
