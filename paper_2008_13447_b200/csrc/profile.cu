@@ -1123,16 +1123,23 @@ static int profile_impl(vlmp_session* s, int32_t lmin, int32_t lmax, int64_t ban
     const long long nb = n_bands_for(n, lmin);
     if (band_hi < 0 || band_hi > nb) band_hi = nb;
     if (band_lo < 0) band_lo = 0;
-    const int S = seg_rows(n);
+    if (s->tc_n != n) { s->tc_n = n; s->tc_S = seg_rows(n); s->tc_key[0] = -1; }
+    const int S = s->tc_S;
     const long long N0 = n - lmin + 1, dl = dlo_for(lmin);
     // tile list using N at lmin (a superset of every later length's tiles), launched
-    // longest-first (order_tiles)
+    // longest-first (order_tiles); built and uploaded once per (series length, lmin, bands)
+    const bool fp32_key = !(flags & (VLMP_F_FP64_FILTER | VLMP_F_FULL_EVERY_LENGTH)) && !getenv("VLMP_FP64_FILTER");
+    const long long mode_key = (long long)flags | (fp32_key ? (1LL << 40) : 0);   // the sample list depends on both
+    const bool tiles_cached = s->tc_key[0] == n && s->tc_key[1] == lmin && s->tc_key[2] == band_lo &&
+                              s->tc_key[3] == band_hi && s->tc_key[4] == mode_key;
     std::vector<int2> tiles;
-    for (long long b = band_lo; b < band_hi; ++b) {
-        long long rows = N0 - (dl + b * BAND);
-        for (long long sg = 0; sg * S < rows; ++sg) tiles.push_back(make_int2((int)b, (int)sg));
+    if (!tiles_cached) {
+        for (long long b = band_lo; b < band_hi; ++b) {
+            long long rows = N0 - (dl + b * BAND);
+            for (long long sg = 0; sg * S < rows; ++sg) tiles.push_back(make_int2((int)b, (int)sg));
+        }
+        order_tiles(tiles, N0, dl, S);
     }
-    order_tiles(tiles, N0, dl, S);
     // a shard's first length: full folds over every SAMPLE-th band first (cheap), whose minima
     // bound the filtered pass over all bands -- instead of full folds everywhere
 #ifndef VLMP_FIRST_SAMPLE
@@ -1152,7 +1159,7 @@ static int profile_impl(vlmp_session* s, int32_t lmin, int32_t lmax, int64_t ban
     for (size_t k = 0; k < tiles.size(); ++k)
         if ((tiles[k].x - band_lo) % sample == 0) { tiles_s.push_back(tiles[k]); smap.push_back((int)k); }
     *used_sampled = sampled_start;
-    const long long T = (long long)tiles.size();
+    const long long T = tiles_cached ? s->tc_T : (long long)tiles.size();
     int rc;
     if ((rc = ensure(s->d_tiles, s->tiles_cap, (size_t)std::max<long long>(T, 1)))) return rc;
     if ((rc = ensure(s->d_seeds, s->seeds_cap, (size_t)std::max<long long>(T, 1) * BAND))) return rc;
@@ -1165,9 +1172,9 @@ static int profile_impl(vlmp_session* s, int32_t lmin, int32_t lmax, int64_t ban
     CU(cudaMemsetAsync(s->d_fixcnt, 0, n_len * sizeof(unsigned long long), st));
     CU(cudaMemsetAsync(s->d_logcnt, 0, n_len * sizeof(unsigned long long), st));
     CU(cudaMemsetAsync(s->d_forced, 0, n_len * sizeof(int), st));
-    if (T) CU(cudaMemcpyAsync(s->d_tiles, tiles.data(), T * sizeof(int2), cudaMemcpyHostToDevice, st));
-    const long long Ts = (long long)tiles_s.size();
-    if (bound_start && Ts) {
+    if (T && !tiles_cached) CU(cudaMemcpyAsync(s->d_tiles, tiles.data(), T * sizeof(int2), cudaMemcpyHostToDevice, st));
+    const long long Ts = tiles_cached ? s->tc_Ts : (long long)tiles_s.size();
+    if (bound_start && Ts && !tiles_cached) {
         if ((rc = ensure(s->d_tiles_s, s->tiles_s_cap, (size_t)Ts))) return rc;
         if ((rc = ensure(s->d_smap, s->smap_cap, (size_t)Ts))) return rc;
         CU(cudaMemcpyAsync(s->d_tiles_s, tiles_s.data(), Ts * sizeof(int2), cudaMemcpyHostToDevice, st));
@@ -1175,7 +1182,7 @@ static int profile_impl(vlmp_session* s, int32_t lmin, int32_t lmax, int64_t ban
     }
     std::vector<int2> tiles32;
     if (fp32) {
-        build_tiles32(tiles, band_lo, tiles32);
+        if (!tiles_cached) build_tiles32(tiles, band_lo, tiles32);
         if ((rc = ensure(s->d_tiles32, s->tiles32_cap, std::max<size_t>(tiles32.size(), 1)))) return rc;
         if ((rc = ensure(s->d_p32, s->p32_cap, (size_t)A))) return rc;
         if ((rc = ensure(s->d_cq32, s->cq32_cap, (size_t)A))) return rc;
@@ -1185,7 +1192,12 @@ static int profile_impl(vlmp_session* s, int32_t lmin, int32_t lmax, int64_t ban
             CU(cudaMemcpyAsync(s->d_tiles32, tiles32.data(), tiles32.size() * sizeof(int2), cudaMemcpyHostToDevice, st));
         if ((rc = filter32_setup())) return rc;
     }
-    const long long T32 = (long long)tiles32.size();
+    const long long T32 = (fp32 && tiles_cached) ? s->tc_T32 : (long long)tiles32.size();
+    if (!tiles_cached) {
+        s->tc_key[0] = n; s->tc_key[1] = lmin; s->tc_key[2] = band_lo; s->tc_key[3] = band_hi;
+        s->tc_key[4] = mode_key;
+        s->tc_T = T; s->tc_Ts = Ts; s->tc_T32 = T32;
+    }
     Run* runs = reinterpret_cast<Run*>(s->d_log);
     const long long run_cap_full = (long long)(s->log_cap * sizeof(RowRec) / sizeof(Run));
     const size_t smem = WARPS_PER_CTA * sizeof(WarpSmem);

@@ -71,6 +71,7 @@ int vlmp_set_series(vlmp_session* s, const double* t, const double* cum, const d
     CU(cudaSetDevice(s->device));
     long long A = ((n + 1024 + 255) / 256) * 256 + 256;
     s->n = n; s->A = A; s->floor_ = sigma_floor;
+    if (s->tc_n != n) { s->tc_n = -1; s->tc_key[0] = -1; }   // tile lists depend on n only
     int rc;
     // grow-only: cudaFree / cudaMalloc synchronise the device and cost up to ~1 s on a
     // loaded allocator -- a repeat call with the same (or a shorter) series allocates nothing

@@ -217,7 +217,9 @@ struct vlmp_session {
     int2* d_tiles32 = nullptr; size_t tiles32_cap = 0;   // FP32 filter tiles (pairs of FP64 tiles)
     unsigned long long* d_fixcnt = nullptr; size_t fixcnt_cap = 0;   // per-length re-bounded offsets
     double sscale = 1.0; int hiC = 896 << 20;            // filter: 2^-k scale, hi-word bias
-    // tiles / seeds
+    // tiles / seeds (host tile lists cached per (n, lmin, bands, flags): tc_*)
+    long long tc_n = -1, tc_key[5] = {-1, -1, -1, -1, -1}, tc_T = 0, tc_Ts = 0, tc_T32 = 0;
+    int tc_S = 0;
     int2* d_tiles = nullptr; size_t tiles_cap = 0;
     int2* d_tiles_s = nullptr; size_t tiles_s_cap = 0;   // sampled bands of a shard's first length
     int* d_smap = nullptr; size_t smap_cap = 0;          // their seed slots
