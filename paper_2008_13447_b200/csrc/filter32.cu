@@ -56,31 +56,43 @@ struct Prep32Args {
     float4* cq4;   // packed walk: {a_o, b_o, a_{o+256}, b_{o+256}} (nullptr: not built)
 };
 
+// the column factors (cA, b) of offset o: +inf for windows past N or undefined; a forced offset
+// (bound too weak for the covariance-domain test, or b out of range) passes every cell -- as a
+// column cA = -inf (z = +inf), as a row b = NaN (z = NaN, sign bit clear); k_runs evaluates
+// them exactly
+__device__ __forceinline__ void col_factors(const Prm& p, long long o, long long N, double sscale,
+                                            float& ca, float& b, bool& forced) {
+    ca = INFINITY; b = INFINITY; forced = false;
+    if (o < N && p.inv == p.inv) {
+        b = qscale(p.inv, sscale);
+        ca = __double2float_rd(qfac(p.U) * (double)b);
+        if (q_forced(p, sscale)) { ca = -INFINITY; b = __int_as_float(0x7FC00000); forced = true; }
+    }
+}
+
 __global__ void __launch_bounds__(256) k_prep32(Prep32Args a) {
     const long long o = blockIdx.x * 256LL + threadIdx.x;
     float msv = 0.f, mdf = 0.f, mdg = 0.f;
     if (o < a.A) {
         const Prm p = a.prm[o];
         const float df = (float)(p.df * a.sscale), dg = (float)(p.dg * a.sscale);
-        float b = INFINITY, w = 3.0e38f, ca = INFINITY;
+        float b, w = 3.0e38f, ca;
+        bool forced;
+        col_factors(p, o, a.N, a.sscale, ca, b, forced);
+        if (forced && a.forced) atomicOr(a.forced, 1);
+        if (a.cq4 && o + BAND < a.A) {
+            // packed walk: the band pair (o, o + 256) in one 16-byte entry, so the walk stages
+            // each entering pair with one cp.async
+            float ca2, b2; bool f2;
+            col_factors(a.prm[o + BAND], o + BAND, a.N, a.sscale, ca2, b2, f2);
+            a.cq4[o] = make_float4(ca, b == b ? b : 1.0f, ca2, b2 == b2 ? b2 : 1.0f);
+        }
         if (o < a.N) {
             float uw = -INFINITY;
 #pragma unroll
             for (int k = 0; k < WIN; ++k)
                 if (o + k < a.N) uw = fmaxf(uw, a.prm[o + k].U);
             if (uw != -INFINITY) w = __double2float_rd(qfac(uw));
-            if (p.inv == p.inv) {
-                b = qscale(p.inv, a.sscale);
-                ca = __double2float_rd(qfac(p.U) * (double)b);
-                if (q_forced(p, a.sscale)) {
-                    // bound too weak for the covariance-domain test (or b out of range): every
-                    // cell of this offset passes -- as a column cA = -inf (z = +inf), as a row
-                    // b = NaN (z = NaN, sign bit clear); k_runs evaluates them exactly
-                    ca = -INFINITY;
-                    b = __int_as_float(0x7FC00000);
-                    if (a.forced) atomicOr(a.forced, 1);
-                }
-            }
             const double L = (double)a.m;
             const double s = a.cum[o + a.m] - a.cum[o], ss = a.cum2[o + a.m] - a.cum2[o];
             const double mu = s / L;
@@ -105,15 +117,6 @@ __global__ void __launch_bounds__(256) k_prep32(Prep32Args a) {
         for (int k = 0; k < 8; ++k) r = max(r, wm[threadIdx.x][k]);
         a.magblk[threadIdx.x * a.nb + blockIdx.x] = r;
     }
-}
-
-// packed walk: the column factors of a band pair (o, o + 256) in one 16-byte entry, so the walk
-// stages each entering pair with one cp.async
-__global__ void k_pair_cq(const float2* __restrict__ cq, float4* cq4, long long A) {
-    const long long o = blockIdx.x * (long long)blockDim.x + threadIdx.x;
-    if (o + BAND >= A) return;
-    const float2 x = cq[o], y = cq[o + BAND];
-    cq4[o] = make_float4(x.x, x.y, y.x, y.y);
 }
 
 // ---------------------------------------------------------------------------------
@@ -816,12 +819,9 @@ int launch_filter32(vlmp_session* s, cudaStream_t st, const Prm* prm, const doub
     const long long A = s->A;
     const long long nb = A / 256 + 1;
     Prep32Args pa{prm, s->d_cum, s->d_cum2, s->d_p32, s->d_cq32, s->d_magblk, nb, N, A, m, s->sscale,
-                  const_cast<int*>(forced), nullptr};
+                  const_cast<int*>(forced), (VLMP_PACKED && n_t32) ? s->d_cq4 : nullptr};
     k_prep32<<<blocks(A, 256), 256, 0, st>>>(pa);
     if (n_t32) {
-#if VLMP_PACKED
-        k_pair_cq<<<blocks(A, 256), 256, 0, st>>>(s->d_cq32, s->d_cq4, A);
-#endif
         Tile32Args ta{s->d_p32, s->d_cq32, s->d_magblk, nb, s->d_tn, mu, s->d_seeds, s->d_tiles, s->d_tiles32,
                       runs, run_count, run_cap, s->d_counters, forced, N, dl, (int)n_t32, S, m, e,
                       update_seeds, s->sscale, s->d_cq4};

@@ -6,7 +6,10 @@ import os, sys, time
 sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 import numpy as np
 import torch
-from paper_2008_13447_b200 import _lib, distributed, gen, ingest
+from paper_2008_13447_b200 import _lib
+if os.environ.get("VLMP_LIB"):
+    _lib.LIB_PATH = os.environ["VLMP_LIB"]
+from paper_2008_13447_b200 import distributed, gen, ingest
 lmin, lmax = 256, 384
 s = ingest(gen.series_for(2))
 sess = _lib.session(0)
