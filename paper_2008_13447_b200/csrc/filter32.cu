@@ -424,6 +424,10 @@ __device__ __forceinline__ u64 fma2(u64 x, u64 y, u64 z) {
 }
 __device__ __forceinline__ u64 bc2(float x) { return pk2(x, x); }
 
+__device__ __forceinline__ unsigned and3(unsigned x, unsigned y, unsigned z) {
+    unsigned d; asm("lop3.b32 %0, %1, %2, %3, 0x80;" : "=r"(d) : "r"(x), "r"(y), "r"(z)); return d;
+}
+
 constexpr int DP = 8;        // diagonals per lane per band
 constexpr int GRP = 8;       // rows per staging group (ring phase)
 struct Smem32p {
@@ -637,10 +641,13 @@ __global__ void __launch_bounds__(32, VLMP_FILTER32_WARPS_PER_SM) k_tile32(Tile3
                 const u64 zz = fma2(NA[p], bc2(pr.z), cov[s]);
                 z[s] = (unsigned)zz; z[s + 8] = (unsigned)(zz >> 32);
             }
-#pragma unroll
-            for (int w = 1; w < 16; w *= 2)
-#pragma unroll
-                for (int s = 0; s + w < 16; s += 2 * w) z[s] &= z[s + w];
+            {   // sign bits ANDed by a depth-3 tree of 3-input LOP3s (left to itself the compiler
+                // chains 8 dependent LOP3s: ~32 cycles between the row's last FFMA2 and its branch)
+                const unsigned t0 = and3(z[0], z[8], z[1]), t1 = and3(z[9], z[2], z[10]);
+                const unsigned t2 = and3(z[3], z[11], z[4]), t3 = and3(z[12], z[5], z[13]);
+                const unsigned t4 = and3(z[6], z[14], z[7]);
+                z[0] = and3(and3(t0, t1, t2), t3, and3(t4, z[15], ~0u));
+            }
             pass_prev = (int)z[0] >= 0;
             bprev = pr.z;
             if (kk + 1 < GRP && lane == 0) {
