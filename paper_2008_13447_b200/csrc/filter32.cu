@@ -39,6 +39,9 @@ static_assert(D2 == 8 || D2 == 16, "D2: 8 or 16");
 #define VLMP_PACKED 1            // two-band packed walk (FFMA2 on band pairs); 0: scalar FFMA, 16 diagonals per lane
 #endif
 constexpr int WIN = VLMP_PACKED ? 8 : D2;   // rows a column meets in one lane (the w window)
+#ifndef VLMP_PAIR_SEP
+#define VLMP_PAIR_SEP 2          // packed walk: band B = band A + VLMP_PAIR_SEP bands (1: adjacent)
+#endif
 #ifndef VLMP_FILTER32_WARPS_PER_SM
 #define VLMP_FILTER32_WARPS_PER_SM 16   // 128 registers: no spills (20 warps at 96 spill the staging plan)
 #endif
@@ -53,7 +56,8 @@ struct Prep32Args {
     const Prm* prm; const double* cum; const double* cum2;
     float4* p32; float2* cq; unsigned* magblk; long long nb;
     long long N, A; int m; double sscale; int* forced;
-    float4* cq4;   // packed walk: {a_o, b_o, a_{o+256}, b_{o+256}} (nullptr: not built)
+    float4* cq4;   // packed walk: {a_o, b_o, a_o', b_o'}, o' = o + PSEP (nullptr: not built)
+    float4* pf4;   // packed walk, PSEP > 256: {df_o, df_o', dg_o, dg_o'} (lane 31's fresh pair)
 };
 
 // the column factors (cA, b) of offset o: +inf for windows past N or undefined; a forced offset
@@ -70,6 +74,8 @@ __device__ __forceinline__ void col_factors(const Prm& p, long long o, long long
     }
 }
 
+constexpr int PSEP = VLMP_PAIR_SEP * BAND;   // diagonal offset of a packed tile's band B
+
 __global__ void __launch_bounds__(256) k_prep32(Prep32Args a) {
     const long long o = blockIdx.x * 256LL + threadIdx.x;
     float msv = 0.f, mdf = 0.f, mdg = 0.f;
@@ -80,12 +86,14 @@ __global__ void __launch_bounds__(256) k_prep32(Prep32Args a) {
         bool forced;
         col_factors(p, o, a.N, a.sscale, ca, b, forced);
         if (forced && a.forced) atomicOr(a.forced, 1);
-        if (a.cq4 && o + BAND < a.A) {
-            // packed walk: the band pair (o, o + 256) in one 16-byte entry, so the walk stages
+        if (a.cq4 && o + PSEP < a.A) {
+            // packed walk: the band pair (o, o + PSEP) in one 16-byte entry, so the walk stages
             // each entering pair with one cp.async
+            const Prm p2 = a.prm[o + PSEP];
             float ca2, b2; bool f2;
-            col_factors(a.prm[o + BAND], o + BAND, a.N, a.sscale, ca2, b2, f2);
+            col_factors(p2, o + PSEP, a.N, a.sscale, ca2, b2, f2);
             a.cq4[o] = make_float4(ca, b == b ? b : 1.0f, ca2, b2 == b2 ? b2 : 1.0f);
+            if (a.pf4) a.pf4[o] = make_float4(df, (float)(p2.df * a.sscale), dg, (float)(p2.dg * a.sscale));
         }
         if (o < a.N) {
             float uw = -INFINITY;
@@ -131,6 +139,7 @@ struct Tile32Args {
     long long N, dlo; int n_tiles32, S, m, e, update_seeds;
     double sscale;
     const float4* cq4;      // packed walk: band-pair column factors
+    const float4* pf4;      // packed walk, PSEP > 256: band-pair {df, df', dg, dg'}
 };
 
 struct Smem32 {
@@ -432,11 +441,20 @@ constexpr int DP = 8;        // diagonals per lane per band
 constexpr int GRP = 8;       // rows per staging group (ring phase)
 struct Smem32p {
     float4 row[2][GRP];          // {df, dg, b, w}
-    float4 fresh[2][GRP];        // the B-band column entering lane 31 at each row
+    float4 fresh[2][GRP];        // lane 31's entering column(s) at each row: PSEP = 256: the
+                                 // B-band p32 entry; else the pf4 entry of the A-band column
     float4 cq[2][GRP * CQS];     // {aA, bA, aB, bB} of the pair entering lane L at row kk: [kk * 33 + L]
     unsigned short rs[32 * 16];  // run starts per lane and cell (bits 0-7 band A, 8-15 band B)
     unsigned short msk[32 * GRP];
 };
+
+// lane 0's outgoing pair becomes lane 31's incoming one. Adjacent bands (PSEP = 256): (lane 0's
+// band-B column, the fresh column) -- a half move; PSEP > 256: two fresh columns, loaded whole
+// ({df, df'} and {dg, dg'} are the two 8-byte halves of the staged pf4 entry)
+__device__ __forceinline__ void fresh_pair(u64& F, u64& G, const float4& f) {
+    if (PSEP == BAND) { F = pk2(hi2(F), f.x); G = pk2(hi2(G), f.y); }
+    else { F = reinterpret_cast<const u64*>(&f)[0]; G = reinterpret_cast<const u64*>(&f)[1]; }
+}
 
 __global__ void __launch_bounds__(32, VLMP_FILTER32_WARPS_PER_SM) k_tile32(Tile32Args a) {
     extern __shared__ __align__(128) unsigned char smem_raw[];
@@ -450,12 +468,12 @@ __global__ void __launch_bounds__(32, VLMP_FILTER32_WARPS_PER_SM) k_tile32(Tile3
     const long long i0 = (long long)tA.y * a.S;
     const long long rows_valid = a.N - d0 - i0;
     const bool liveA = rows_valid > 0 && d0 + BAND - 1 >= a.e;
-    const bool liveB = pr2.y >= 0 && rows_valid - BAND > 0 && d0 + 2 * BAND - 1 >= a.e;
+    const bool liveB = pr2.y >= 0 && rows_valid - PSEP > 0 && d0 + PSEP + BAND - 1 >= a.e;
     if (!liveA && !liveB) return;
     const int nrows = (int)(rows_valid < a.S ? rows_valid : a.S);
     const int ngroups = (nrows + GRP - 1) / GRP;
     const long long cbA = i0 + d0 + (long long)DP * lane;   // band A column of slot 0 at row i0
-    const long long cbB = cbA + BAND;
+    const long long cbB = cbA + PSEP;
 
     // ---- FP32 error slack. Per walked row (two FFMA over FP32-rounded df, dg) the covariance
     // error grows by at most 2u|cov| + 3.02u(|df_i dg_j| + |df_j dg_i|), u = 2^-24, with
@@ -464,7 +482,7 @@ __global__ void __launch_bounds__(32, VLMP_FILTER32_WARPS_PER_SM) k_tile32(Tile3
     float eps;
     {
         const long long rb0 = i0 >> 8, rb1 = (i0 + nrows - 1) >> 8;
-        const long long cb0 = (i0 + d0) >> 8, cb1 = (i0 + nrows - 1 + d0 + 2 * BAND - 1) >> 8;
+        const long long cb0 = (i0 + d0) >> 8, cb1 = (i0 + nrows - 1 + d0 + PSEP + BAND - 1) >> 8;
         unsigned r[3] = {0, 0, 0}, c[3] = {0, 0, 0};
 #pragma unroll
         for (int q = 0; q < 3; ++q) {
@@ -507,7 +525,7 @@ __global__ void __launch_bounds__(32, VLMP_FILTER32_WARPS_PER_SM) k_tile32(Tile3
 #pragma unroll
         for (int s = 0; s < DP; ++s) {
             const float ca = (liveA && d0 + DP * lane + s >= a.e) ? __fadd_ru((float)(cA64[s] * s2), eps) : -INFINITY;
-            const float cb = (liveB && d0 + BAND + DP * lane + s >= a.e) ? __fadd_ru((float)(cB64[s] * s2), eps) : -INFINITY;
+            const float cb = (liveB && d0 + PSEP + DP * lane + s >= a.e) ? __fadd_ru((float)(cB64[s] * s2), eps) : -INFINITY;
             cov[s] = pk2(ca, cb);
         }
     }
@@ -519,9 +537,9 @@ __global__ void __launch_bounds__(32, VLMP_FILTER32_WARPS_PER_SM) k_tile32(Tile3
 #pragma unroll
         for (int s = 0; s < DP; ++s) {
             const long long ca = s < DP - 1 ? cbA + s : cbA - 1;
-            const float4 pa = a.p32[ca], pb = a.p32[ca + BAND];
+            const float4 pa = a.p32[ca], pb = a.p32[ca + PSEP];
             F[s] = pk2(pa.x, pb.x); G[s] = pk2(pa.y, pb.y);
-            const float2 qa = a.cq[ca], qb = a.cq[ca + BAND];
+            const float2 qa = a.cq[ca], qb = a.cq[ca + PSEP];
             NA[s] = pk2(fmaxf(-qa.x, __fmul_ru(-w0, qa.y)), fmaxf(-qb.x, __fmul_ru(-w0, qb.y)));
         }
         const float4 pr = a.p32[i0];
@@ -543,7 +561,8 @@ __global__ void __launch_bounds__(32, VLMP_FILTER32_WARPS_PER_SM) k_tile32(Tile3
             src_rf = reinterpret_cast<const char*>(a.p32 + i0 + q);
             dst_rf = (unsigned)__cvta_generic_to_shared(&sm.row[0][q]);
         } else {
-            src_rf = reinterpret_cast<const char*>(a.p32 + i0 + q + d0 + 2 * BAND - 1);
+            src_rf = PSEP == BAND ? reinterpret_cast<const char*>(a.p32 + i0 + q + d0 + 2 * BAND - 1)
+                                  : reinterpret_cast<const char*>(a.pf4 + i0 + q + d0 + BAND - 1);
             dst_rf = (unsigned)__cvta_generic_to_shared(&sm.fresh[0][q]);
         }
     }
@@ -569,7 +588,7 @@ __global__ void __launch_bounds__(32, VLMP_FILTER32_WARPS_PER_SM) k_tile32(Tile3
     unsigned short* rs = sm.rs + lane * 16;
     unsigned short* msk = sm.msk + lane * GRP;
     auto emit = [&](int c, int r_start, int r_end) {
-        const int dcell = (int)(d0 + DP * lane) + (c & 7) + (c >> 3) * BAND;
+        const int dcell = (int)(d0 + DP * lane) + (c & 7) + (c >> 3) * PSEP;
         const unsigned long long at = atomicAdd(a.run_count, 1ull);
         if ((long long)at < a.run_cap) {
             Run rr;
@@ -623,10 +642,7 @@ __global__ void __launch_bounds__(32, VLMP_FILTER32_WARPS_PER_SM) k_tile32(Tile3
             if (kk == 0 && g > 0 && gflags) { fold_rows(gflags, (g - 1) * GRP); gflags = 0; }
             {   // rotation: phys (kk-1) mod 8 receives lane+1's outgoing pair
                 const int q = (kk + DP - 1) % DP;
-                if (lane == 0 && kk == 0) {
-                    const float4 f = sm.fresh[b][0];
-                    F[q] = pk2(hi2(F[q]), f.x); G[q] = pk2(hi2(G[q]), f.y);
-                }
+                if (lane == 0 && kk == 0) fresh_pair(F[q], G[q], sm.fresh[b][0]);
                 F[q] = __shfl_sync(FULLMASK, F[q], (lane + 1) & 31);
                 G[q] = __shfl_sync(FULLMASK, G[q], (lane + 1) & 31);
                 const float4 cq = sm.cq[b][kk * CQS + lane];
@@ -650,10 +666,7 @@ __global__ void __launch_bounds__(32, VLMP_FILTER32_WARPS_PER_SM) k_tile32(Tile3
             }
             pass_prev = (int)z[0] >= 0;
             bprev = pr.z;
-            if (kk + 1 < GRP && lane == 0) {
-                const float4 f = sm.fresh[b][kk + 1];
-                F[kk % DP] = pk2(hi2(F[kk % DP]), f.x); G[kk % DP] = pk2(hi2(G[kk % DP]), f.y);
-            }
+            if (kk + 1 < GRP && lane == 0) fresh_pair(F[kk % DP], G[kk % DP], sm.fresh[b][kk + 1]);
         }
         cp_async_wait_all();
         __syncwarp();
@@ -813,9 +826,11 @@ void build_tiles32(const std::vector<int2>& tiles, long long band_lo, std::vecto
         auto it = std::lower_bound(keyed.begin(), keyed.end(), std::make_pair(kk, -1));
         return (it != keyed.end() && it->first == kk) ? it->second : -1;
     };
+    // packed walk: band b pairs with b + VLMP_PAIR_SEP (bands b mod 2 SEP < SEP lead); scalar: b, b + 1
+    const long long sep = VLMP_PACKED ? VLMP_PAIR_SEP : 1;
     for (size_t k = 0; k < tiles.size(); ++k) {
-        if (((long long)tiles[k].x - band_lo) % 2 != 0) continue;
-        out.push_back(make_int2((int)k, find(key((long long)tiles[k].x + 1, tiles[k].y))));
+        if (((long long)tiles[k].x - band_lo) % (2 * sep) >= sep) continue;
+        out.push_back(make_int2((int)k, find(key((long long)tiles[k].x + sep, tiles[k].y))));
     }
 }
 
@@ -826,12 +841,13 @@ int launch_filter32(vlmp_session* s, cudaStream_t st, const Prm* prm, const doub
     const long long A = s->A;
     const long long nb = A / 256 + 1;
     Prep32Args pa{prm, s->d_cum, s->d_cum2, s->d_p32, s->d_cq32, s->d_magblk, nb, N, A, m, s->sscale,
-                  const_cast<int*>(forced), (VLMP_PACKED && n_t32) ? s->d_cq4 : nullptr};
+                  const_cast<int*>(forced), (VLMP_PACKED && n_t32) ? s->d_cq4 : nullptr,
+                  (VLMP_PACKED && n_t32 && VLMP_PAIR_SEP > 1) ? s->d_pf4 : nullptr};
     k_prep32<<<blocks(A, 256), 256, 0, st>>>(pa);
     if (n_t32) {
         Tile32Args ta{s->d_p32, s->d_cq32, s->d_magblk, nb, s->d_tn, mu, s->d_seeds, s->d_tiles, s->d_tiles32,
                       runs, run_count, run_cap, s->d_counters, forced, N, dl, (int)n_t32, S, m, e,
-                      update_seeds, s->sscale, s->d_cq4};
+                      update_seeds, s->sscale, s->d_cq4, s->d_pf4};
         k_tile32<<<(unsigned)n_t32, 32, sizeof(SmemT), st>>>(ta);
         k_runs<<<148 * 8, 256, 0, st>>>(runs, run_count, run_cap, prm, s->d_tn, mu, m, e, acc, s->d_counters,
                                         slots, slot_cnt);

@@ -1187,6 +1187,7 @@ static int profile_impl(vlmp_session* s, int32_t lmin, int32_t lmax, int64_t ban
         if ((rc = ensure(s->d_p32, s->p32_cap, (size_t)A))) return rc;
         if ((rc = ensure(s->d_cq32, s->cq32_cap, (size_t)A))) return rc;
         if ((rc = ensure(s->d_cq4, s->cq4_cap, (size_t)A))) return rc;
+        if ((rc = ensure(s->d_pf4, s->pf4_cap, (size_t)A))) return rc;
         if ((rc = ensure(s->d_magblk, s->magblk_cap, (size_t)(3 * (A / 256 + 1))))) return rc;
         if (!tiles32.empty())
             CU(cudaMemcpyAsync(s->d_tiles32, tiles32.data(), tiles32.size() * sizeof(int2), cudaMemcpyHostToDevice, st));
@@ -1519,6 +1520,7 @@ int vlmp_profile_mbest(vlmp_session* s, int32_t lmin, int32_t lmax, int32_t mb) 
         if ((rc = ensure(s->d_p32, s->p32_cap, (size_t)A))) return rc;
         if ((rc = ensure(s->d_cq32, s->cq32_cap, (size_t)A))) return rc;
         if ((rc = ensure(s->d_cq4, s->cq4_cap, (size_t)A))) return rc;
+        if ((rc = ensure(s->d_pf4, s->pf4_cap, (size_t)A))) return rc;
         if ((rc = ensure(s->d_magblk, s->magblk_cap, (size_t)(3 * (A / 256 + 1))))) return rc;
         if ((rc = ensure(s->d_forced, s->forced_cap, (size_t)n_len))) return rc;
         CU(cudaMemsetAsync(s->d_forced, 0, n_len * sizeof(int), st));

@@ -54,7 +54,7 @@ void vlmp_destroy(vlmp_session* s) {
     cudaStreamSynchronize(s->stream);
     void* ptrs[] = {s->d_tn, s->d_cum, s->d_cum2, s->d_prm, s->d_mu, s->d_prm2, s->d_mu2,
                     s->d_previdx, s->d_colq, s->d_rowq, s->d_forced, s->d_fixcnt, s->d_tiles, s->d_tiles_s, s->d_smap, s->d_seeds, s->d_acc, s->d_mp, s->d_ip, s->d_counters,
-                    s->d_log, s->d_logcnt, s->d_p32, s->d_cq32, s->d_cq4, s->d_magblk, s->d_tiles32, s->d_ro_i64, s->d_ro_f64, s->d_ro_cnt,
+                    s->d_log, s->d_logcnt, s->d_p32, s->d_cq32, s->d_cq4, s->d_pf4, s->d_magblk, s->d_tiles32, s->d_ro_i64, s->d_ro_f64, s->d_ro_cnt,
                     s->d_slots, s->d_slotcnt, s->d_ipm, s->d_mpm, s->d_redo, s->d_vdist, s->d_vnorm, s->d_vlen, s->d_vidx, s->d_vpop};
     for (void* p : ptrs) if (p) cudaFree(p);
     for (auto& ev : s->ev) if (ev) cudaEventDestroy(ev);

@@ -213,6 +213,7 @@ struct vlmp_session {
     float4* d_p32 = nullptr; size_t p32_cap = 0;         // FP32 filter: {df, dg, b, w}
     float2* d_cq32 = nullptr; size_t cq32_cap = 0;       // FP32 filter: {a, b}
     float4* d_cq4 = nullptr; size_t cq4_cap = 0;         // packed walk: band-pair {a, b, a', b'}
+    float4* d_pf4 = nullptr; size_t pf4_cap = 0;         // packed walk: band-pair {df, df', dg, dg'}
     unsigned* d_magblk = nullptr; size_t magblk_cap = 0; // FP32 filter: per-256-offset magnitude bound
     int2* d_tiles32 = nullptr; size_t tiles32_cap = 0;   // FP32 filter tiles (pairs of FP64 tiles)
     unsigned long long* d_fixcnt = nullptr; size_t fixcnt_cap = 0;   // per-length re-bounded offsets
