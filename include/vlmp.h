@@ -174,7 +174,8 @@ int vlmp_range_query(vlmp_session* s, int64_t n_q, const int64_t* owners, const 
  * with full folds at every length; m-best: offsets recomputed), out[14] lengths that fell back to full folds (an offset's own bound
  * too weak for the covariance-domain filter), out[15] largest per-length log fill,
  * out[16] 1 if the filtered lengths ran the FP32 walk (filter32.cu), out[17] largest
- * per-length run count of that walk, out[18] cells evaluated exactly in its runs (n_out <= 20).
+ * per-length run count of that walk, out[18] cells evaluated exactly in its runs, out[19] the
+ * row-segment length S of the tile walks (n_out <= 20).
  */
 int vlmp_stats(vlmp_session* s, double* out, int32_t n_out);
 

@@ -241,7 +241,7 @@ class Session:
         keys = ["profile_ms", "finalize_ms", "executed_updates", "W", "tile_ms", "tile_launches",
                 "filtered_lengths", "full_lengths", "slow_merges", "kernel_launches", "first_tile_ms",
                 "slow_rowsteps", "bound_fixes", "exact_redo", "fallback_lengths", "max_log_records",
-                "fp32_walk", "max_runs", "run_cells", "reserved"]
+                "fp32_walk", "max_runs", "run_cells", "seg_rows"]
         return {k: float(out[i]) for i, k in enumerate(keys)}
 
     def event_record(self, slot):

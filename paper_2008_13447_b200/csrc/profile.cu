@@ -1368,7 +1368,7 @@ static int profile_impl(vlmp_session* s, int32_t lmin, int32_t lmax, int64_t ban
     s->stats[9] = klaunch; s->stats[10] = first_ms; s->stats[11] = (double)cnt[2];
     s->stats[12] = n_fix; s->stats[14] = n_forced; s->stats[15] = max_log;
     s->stats[16] = fp32 ? 1.0 : 0.0; s->stats[17] = fp32 ? max_log : 0.0; s->stats[18] = (double)cnt[4];
-    s->stats[19] = (double)cnt[3];
+    s->stats[19] = (double)S;
     *overflow_out = overflow;
     // a lost run log: the caller re-runs the whole set on the FP64 filter path
     if (fp32_fallback) *fp32_fallback = fp32 && overflow;

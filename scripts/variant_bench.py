@@ -18,5 +18,5 @@ for rep in range(3):
     run = api.GpuRun(s2, 256, 384)
     st = run.stats
     best = st if best is None or st["tile_ms"] < best["tile_ms"] else best
-print(os.environ.get("VLMP_LIB", "default"), "cfg1 mismatches", bad, "fp32", best.get("fp32_walk"), "redo", best.get("exact_redo"), "run_cells %.3e max_runs %d" % (best.get("run_cells", 0), best.get("max_runs", 0)), "cfg2 tile_ms %.2f first %.2f profile_ms %.2f slow merges %d lane-rows %d bound fixes %d fallback lengths %d" % (
+print(os.environ.get("VLMP_LIB", "default"), "cfg1 mismatches", bad, "fp32", best.get("fp32_walk"), "redo", best.get("exact_redo"), "run_cells %.3e max_runs %d S %d" % (best.get("run_cells", 0), best.get("max_runs", 0), best.get("seg_rows", 0)), "cfg2 tile_ms %.2f first %.2f profile_ms %.2f slow merges %d lane-rows %d bound fixes %d fallback lengths %d" % (
     best["tile_ms"], best["first_tile_ms"], best["profile_ms"], best["slow_merges"], best.get("slow_rowsteps", -1), best.get("bound_fixes", -1), best.get("fallback_lengths", -1)), flush=True)

@@ -12,5 +12,5 @@ s = vl.ingest(gen.series_for(cfg))
 run = api.GpuRun(s, c.lmin, c.lmin + 2)
 run = api.GpuRun(s, c.lmin, c.lmax)
 st = run.stats
-print(os.environ.get("VLMP_LIB"), "cfg", cfg, "tile_ms %.1f profile_ms %.1f lane-rows %.3e run_cells %.3e redo %d" % (
+print(os.environ.get("VLMP_LIB"), "cfg", cfg, "S", st.get("seg_rows"), "tile_ms %.1f profile_ms %.1f lane-rows %.3e run_cells %.3e redo %d" % (
     st["tile_ms"], st["profile_ms"], st["slow_rowsteps"], st["run_cells"], st["exact_redo"]), flush=True)
