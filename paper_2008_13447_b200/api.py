@@ -23,7 +23,8 @@ import numpy as np
 from . import _lib, policy
 from . import exceptions as E
 from .results import (VALMP, DiscordMatrix, DiscordScan, MatrixProfile, ProfileResult,
-                      VariableLengthDiscordMatrix, update_variable_length_discords)
+                      VariableLengthDiscordMatrix, merge_variable_length_discords,
+                      update_variable_length_discords)
 from .series import as_series
 
 
@@ -282,16 +283,15 @@ def mine(series, lmin: int, lmax: int, k_motif: int = 1, k_discord: int = 1, *,
         trace.add_length(length, n_profiles=n_dp, n_valid=n_dp, n_nonvalid=0, n_recomputed=0,
                          full_recompute=False, motif=top[0] if top else None)
     dist, off = run.discords(k_discord)
-    merged = VariableLengthDiscordMatrix.empty(k_discord, 1)
-    per_length = {}
-    for li in range(lmax - lmin + 1):
-        length = lmin + li
-        dkm = DiscordMatrix.empty(k_discord, 1, length)
-        dkm.dist[:, 0] = dist[li]
-        dkm.offset[:, 0] = off[li]
-        dkm._occupied = {int(o) for o in off[li] if o >= 0}
-        per_length[length] = dkm
-        update_variable_length_discords(dkm, merged, k_discord, 1)
+    # per-length matrices are (k, 1) views of one batch array; the cross-length merge is
+    # update_variable_length_discords over ascending lengths, vectorised
+    dist3 = np.array(dist, dtype=np.float64).reshape(-1, k_discord, 1)
+    off3 = np.array(off, dtype=np.int64).reshape(-1, k_discord, 1)
+    offs = off3[:, :, 0].tolist()
+    per_length = {lmin + li: DiscordMatrix(dist3[li], off3[li], lmin + li, {o for o in offs[li] if o >= 0})
+                  for li in range(lmax - lmin + 1)}
+    merged = merge_variable_length_discords(dist3, off3, np.arange(lmin, lmax + 1),
+                                            VariableLengthDiscordMatrix.empty(k_discord, 1))
     if ranking is not None:
         _feed_ranking(run, v, ranking)
     return MiningResult(v, motifs, DiscordScan(merged, per_length), trace, run.stats)
@@ -317,7 +317,8 @@ def _topk_from_rows(run: GpuRun, k: int):
     li, a, b, dv = li[o], a[o], b[o], dv[o]
     starts = np.searchsorted(li, np.arange(nl + 1))
     out = {}
+    al, bl, dl = a.tolist(), b.tolist(), dv.tolist()
     for q in range(nl):
-        lo, hi = starts[q], min(starts[q + 1], starts[q] + k)
-        out[run.lmin + q] = [(int(x), int(y), float(z)) for x, y, z in zip(a[lo:hi], b[lo:hi], dv[lo:hi])]
+        lo, hi = int(starts[q]), int(min(starts[q + 1], starts[q] + k))
+        out[run.lmin + q] = list(zip(al[lo:hi], bl[lo:hi], dl[lo:hi]))
     return out

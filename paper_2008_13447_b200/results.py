@@ -187,6 +187,27 @@ def update_fixed_length_discords(dkm, best_dists, off: int, k: int, m: int) -> b
     return False
 
 
+def merge_variable_length_discords(dist, offset, lengths, merged):
+    """update_variable_length_discords applied to every length at once (lengths ascending):
+    dist, offset [n_len, k, m]. A cell replaces the merged one whenever its score d / sqrt(length)
+    is >= (NaN never), so it ends at the LAST length whose score equals the largest non-NaN
+    score, or keeps its initial value when no score is a number."""
+    score = dist / np.sqrt(np.asarray(lengths, dtype=np.int64))[:, None, None]
+    ok = ~np.isnan(score)
+    if not ok.any():
+        return merged
+    top = np.max(np.where(ok, score, -np.inf), axis=0)
+    top = np.maximum(top, np.where(np.isnan(merged.dist), -np.inf, merged.dist))
+    hit = ok & (score == top[None])
+    won = hit.any(axis=0)
+    last = score.shape[0] - 1 - np.argmax(hit[::-1], axis=0)
+    kk, mm = np.indices(last.shape)
+    merged.dist[won] = top[won]
+    merged.offset[won] = offset[last, kk, mm][won]
+    merged.length[won] = np.asarray(lengths, dtype=np.int64)[last][won]
+    return merged
+
+
 def update_variable_length_discords(dkm, merged, k: int, m: int):
     """Cell-wise merge on d / sqrt(length); ties go to the later length."""
     score = dkm.dist / np.sqrt(dkm.length)

@@ -175,3 +175,30 @@ def test_length_split_balances_and_covers():
                 assert max(w) / min(w) < 1.1
     c = D.length_split(100, 10, 12, 8)          # more ranks than lengths: empty tail shards
     assert c.tolist() == [0, 1, 2, 3, 3, 3, 3, 3, 3]
+
+
+@pytest.mark.parametrize("seed", range(6))
+def test_batch_discord_merge_equals_sequential(seed):
+    """mine()'s vectorised cross-length merge == update_variable_length_discords applied length
+    by length (results.py; the reference's merge, discords.py), on ties across lengths, -inf
+    (absent discords) and NaN cells."""
+    from paper_2008_13447_b200.results import (DiscordMatrix, VariableLengthDiscordMatrix,
+                                               merge_variable_length_discords,
+                                               update_variable_length_discords)
+    rng = np.random.default_rng(seed)
+    nl, k, m = 9, 4, 2
+    lengths = np.arange(30, 30 + nl)
+    dist = rng.integers(0, 4, (nl, k, m)).astype(np.float64) * np.sqrt(lengths)[:, None, None]
+    dist[rng.random((nl, k, m)) < 0.2] = -np.inf
+    if seed % 2:
+        dist[rng.random((nl, k, m)) < 0.15] = np.nan
+    if seed == 5:
+        dist[:, 0, 0] = np.nan
+    off = rng.integers(-1, 500, (nl, k, m))
+    seq = VariableLengthDiscordMatrix.empty(k, m)
+    for li in range(nl):
+        update_variable_length_discords(DiscordMatrix(dist[li].copy(), off[li].copy(), int(lengths[li])), seq, k, m)
+    bat = merge_variable_length_discords(dist, off, lengths, VariableLengthDiscordMatrix.empty(k, m))
+    assert np.array_equal(seq.dist, bat.dist)
+    assert np.array_equal(seq.offset, bat.offset)
+    assert np.array_equal(seq.length, bat.length)
