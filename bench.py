@@ -19,7 +19,6 @@ import json
 import os
 import subprocess
 import sys
-import threading
 import time
 
 import numpy as np
@@ -59,29 +58,39 @@ class ClockSampler:
     def __init__(self, device):
         self.device = device
         self.samples = []
-        self._stop = threading.Event()
-        self._t = None
-
-    def _run(self):
-        while not self._stop.is_set():
-            try:
-                out = subprocess.run(["nvidia-smi", "-i", str(self.device), f"--query-gpu={self.Q}",
-                                      "--format=csv,noheader,nounits"], capture_output=True,
-                                     text=True, timeout=5).stdout.strip()
-                if out:
-                    self.samples.append([x.strip() for x in out.split(",")])
-            except Exception:
-                pass
-            self._stop.wait(0.2)
+        self._p = None
+        self._f = None
 
     def __enter__(self):
-        self._t = threading.Thread(target=self._run, daemon=True)
-        self._t.start()
+        # one nvidia-smi process looping every 200 ms (B200_PROFILING.md's clocks line), started
+        # before the timed region -- its NVML start-up is over before the first timed step
+        import tempfile
+        try:
+            self._f = tempfile.TemporaryFile(mode="w+")
+            self._p = subprocess.Popen(["nvidia-smi", "-i", str(self.device), f"--query-gpu={self.Q}",
+                                        "--format=csv,noheader,nounits", "-lms", "200"],
+                                       stdout=self._f, stderr=subprocess.DEVNULL, text=True)
+            t0 = time.time()
+            while time.time() - t0 < 3.0 and os.fstat(self._f.fileno()).st_size == 0 and self._p.poll() is None:
+                time.sleep(0.02)
+        except Exception:
+            self._p = None
         return self
 
     def __exit__(self, *exc):
-        self._stop.set()
-        self._t.join(timeout=10)
+        if self._p is None:
+            return
+        time.sleep(0.05)
+        self._p.terminate()
+        try:
+            self._p.wait(timeout=5)
+        except Exception:
+            self._p.kill()
+        self._f.seek(0)
+        for line in self._f.read().splitlines():
+            if line.strip():
+                self.samples.append([x.strip() for x in line.split(",")])
+        self._f.close()
 
     def summary(self):
         if not self.samples:
@@ -205,15 +214,17 @@ def run_ours(args):
         torch.distributed.barrier()
     torch.cuda.synchronize()
     tile_ms, launches = 0.0, 0
-    with ClockSampler(local) as clk:
-        sess.event_record(0)
-        for _ in range(args.steps):
-            step()
-            st = sess.stats()
-            tile_ms += st["tile_ms"]
-            launches += int(st["kernel_launches"]) + 2
-        sess.event_record(1)
-        ms = sess.event_elapsed_ms()
+    # one clock sampler spans both timed regions (device-resident steps, then e2e): its start-up
+    # and teardown stay outside them
+    clk = ClockSampler(local).__enter__()
+    sess.event_record(0)
+    for _ in range(args.steps):
+        step()
+        st = sess.stats()
+        tile_ms += st["tile_ms"]
+        launches += int(st["kernel_launches"]) + 2
+    sess.event_record(1)
+    ms = sess.event_elapsed_ms()
     torch.cuda.synchronize()
     if world > 1:
         import torch.distributed as dist
@@ -244,7 +255,7 @@ def run_ours(args):
             e2e_step()
         dist.barrier()
         t0 = time.perf_counter()
-        reps = max(2, min(args.steps, 5))
+        reps = max(2, min(2 * args.steps, 10))
         for _ in range(reps):
             e2e_step()
         tt = torch.tensor([(time.perf_counter() - t0) / reps], device="cuda")
@@ -259,7 +270,7 @@ def run_ours(args):
         for _ in range(2):
             mine(s, c.lmin, c.lmax, k_motif=c.k_motif, k_discord=c.k_discord)
         t0 = time.perf_counter()
-        reps = max(2, min(args.steps, 5))
+        reps = max(2, min(2 * args.steps, 10))
         for _ in range(reps):
             res = mine(s, c.lmin, c.lmax, k_motif=c.k_motif, k_discord=c.k_discord)
         e2e_s = (time.perf_counter() - t0) / reps
@@ -267,6 +278,7 @@ def run_ours(args):
                     "h2d_bytes_per_step": int(8 * (s.n + 2 * (s.n + 1))),
                     "d2h_bytes_per_step": int(n0 * (8 * 4 + 1) + nl * (2 * c.k_motif * 24 + kd * 16)),
                     "ms_per_step": e2e_s * 1e3}
+    clk.__exit__(None, None, None)
 
     if rank != 0:
         if world > 1:
