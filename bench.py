@@ -38,6 +38,9 @@ def _args():
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--config", type=int, default=2)
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--shard", default="lengths", choices=["lengths", "bands"],
+                    help="N>1 partition: contiguous length slabs of equal work (default) or the "
+                         "north star's diagonal bands (exact two-step MIN merge)")
     return ap.parse_args()
 
 
@@ -46,6 +49,18 @@ def _dist_env():
     world = int(os.environ.get("WORLD_SIZE", 1))
     local = int(os.environ.get("LOCAL_RANK", 0))
     return rank, world, local
+
+
+def _spawn_ranks(args):
+    """``--gpus N`` without a torchrun environment: re-launch this script as N ranks (one
+    process per GPU) through torch.distributed.run on 127.0.0.1 and pass its exit code on."""
+    import socket
+    with socket.socket() as sk:
+        sk.bind(("127.0.0.1", 0))
+        port = sk.getsockname()[1]
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={args.gpus}",
+           "--master-addr=127.0.0.1", f"--master-port={port}", os.path.abspath(__file__)] + sys.argv[1:]
+    return subprocess.call(cmd)
 
 
 class ClockSampler:
@@ -142,6 +157,43 @@ def cpu_sample(series, c, target_s=12.0, threads=None):
                                    f"{t_used:.1f} s")
 
 
+def _config_dict(args, c, W, world, parallelism):
+    """The workload description shared by both arms (the driver compares them)."""
+    return {"workload": f"config {args.config}: {c.note}", "n": c.n, "lmin": c.lmin,
+            "lmax": c.lmax, "k_motif": c.k_motif, "k_discord": c.k_discord, "W_updates": W,
+            "parallelism": parallelism,
+            "l2": "working set (series + per-length params, 2.6 MB) is L2-resident by design; "
+                  "no flush: the walk is FMA-pipe/latency bound (FP32), not memory-bound"}
+
+
+def reference_python_sample():
+    """The real reference package (baseline/_ref, its own public API and stock code path) end
+    to end on config 1 -- valmod + topkm_discord_discovery, p = 50.
+    Returns a dict, or None when baseline/_ref is not installed."""
+    ref_dir = os.path.join(ROOT, "baseline", "_ref")
+    if not os.path.isdir(os.path.join(ref_dir, "seriesmine")):
+        return None
+    import importlib
+    sys.path.insert(0, ref_dir)
+    try:
+        sm = importlib.import_module("seriesmine")
+    finally:
+        sys.path.remove(ref_dir)
+    from paper_2008_13447_b200 import gen
+    c = gen.CONFIGS[1]
+    ds = sm.ingest(gen.series_for(1))
+    W1 = gen.pair_updates(c.n, c.lmin, c.lmax)
+    t0 = time.perf_counter()
+    sm.valmod(ds, c.lmin, c.lmax, 50, threads=os.cpu_count())
+    t1 = time.perf_counter()
+    sm.topkm_discord_discovery(ds, c.lmin, c.lmax, 1, 1, 50, threads=os.cpu_count())
+    t2 = time.perf_counter()
+    return {"value": W1 / (t2 - t0), "unit": UNIT, "cores": os.cpu_count(), "kind": "reference",
+            "sample": f"seriesmine (baseline/_ref) on config 1 (n=4096, l 32..64): valmod p=50 "
+                      f"{t1 - t0:.2f} s + topkm_discord_discovery(k=1, m=1, p=50) {t2 - t1:.2f} s, "
+                      f"threads={os.cpu_count()}; value = W(config 1) / total"}
+
+
 def run_reference(args):
     rank, world, local = _dist_env()
     if rank != 0:
@@ -163,10 +215,10 @@ def run_reference(args):
         "warmup": args.warmup, "ms_per_step": wall * 1e3 / args.steps, "higher_is_better": True,
         "scaling": "strong", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
         "impl": "reference",
-        "config": {"workload": f"config {args.config}: {c.note}", "n": c.n, "lmin": c.lmin,
-                   "lmax": c.lmax, "k_motif": c.k_motif, "k_discord": c.k_discord},
+        "config": _config_dict(args, c, W, world, f"{args.shard[:-1]} shards x{world}"),
         "cpu_baseline": {"value": value, "unit": UNIT, "cores": cores, "kind": "port",
-                         "sample": desc},
+                         "sample": desc + " (the reference's own engine cannot finish config 2 in a "
+                                          "bench step: 4,863 s for valmod alone, tests/golden/make_golden.py)"},
         "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }
     print(json.dumps(line), flush=True)
@@ -175,7 +227,9 @@ def run_reference(args):
 def run_ours(args):
     rank, world, local = _dist_env()
     import torch
-    from paper_2008_13447_b200 import _lib, api, distributed, ingest
+    from paper_2008_13447_b200 import _lib, distributed, ingest
+    if world != args.gpus:
+        raise SystemExit(f"bench.py: --gpus {args.gpus} but WORLD_SIZE={world}")
     c, t, W = _workload(args.config)
     s = ingest(t)
     # one process per GPU; VLMP_DIST_BACKEND=gloo (host-mediated, a code-path check only)
@@ -194,9 +248,12 @@ def run_ours(args):
     k2 = max(2 * c.k_motif, 2)
     kd = max(c.k_discord, 1)
 
+    shard_fn = distributed.profile_length_sharded if args.shard == "lengths" else distributed.profile_sharded
+    parallelism = f"{args.shard[:-1]} shards x{world}"
+
     def step():
         if world > 1:
-            distributed.profile_length_sharded(sess, s, c.lmin, c.lmax, rank, world, group, upload=False)
+            shard_fn(sess, s, c.lmin, c.lmax, rank, world, group, upload=False)
         else:
             with sess.lock:
                 sess.profile(c.lmin, c.lmax, 0, -1, 0)
@@ -213,24 +270,27 @@ def run_ours(args):
     if world > 1:
         torch.distributed.barrier()
     torch.cuda.synchronize()
-    tile_ms, launches = 0.0, 0
+    walk_ms, runs_ms, walk_launches, launches, step_ms_list = 0.0, 0.0, 0, 0, []
     # one clock sampler spans both timed regions (device-resident steps, then e2e): its start-up
     # and teardown stay outside them
     clk = ClockSampler(local).__enter__()
     sess.event_record(0)
     for _ in range(args.steps):
-        step()
+        rows, disc = step()
         st = sess.stats()
-        tile_ms += st["tile_ms"]
+        walk_ms += st["walk_ms"]
+        runs_ms += st["runs_ms"]
+        walk_launches += int(st["walk_launches"])
         launches += int(st["kernel_launches"]) + 2
+        step_ms_list.append(st["profile_ms"])
     sess.event_record(1)
     ms = sess.event_elapsed_ms()
     torch.cuda.synchronize()
     if world > 1:
         import torch.distributed as dist
-        tt = torch.tensor([ms, tile_ms], device="cuda")
+        tt = torch.tensor([ms, walk_ms], device="cuda")
         dist.all_reduce(tt, op=dist.ReduceOp.MAX)
-        ms, tile_ms = float(tt[0]), float(tt[1])
+        ms, walk_ms = float(tt[0]), float(tt[1])
         dist.barrier()
     step_ms = ms / args.steps
     value = W / (step_ms * 1e-3)
@@ -239,13 +299,14 @@ def run_ours(args):
     e2e_line = None
     n0 = s.n - c.lmin + 1
     nl = c.lmax - c.lmin + 1
+    readoff_check = None
     if world > 1:
-        # sharded: every rank uploads the host series, runs its bands, joins the exact
-        # merge and finalizes; rank 0's read-offs come back to the host (max over ranks)
+        # sharded: every rank uploads the host series, runs its lengths, joins the exchange and
+        # builds the read-offs; rank 0's read-offs come back to the host (max over ranks)
         import torch.distributed as dist
 
         def e2e_step():
-            distributed.profile_length_sharded(sess, s, c.lmin, c.lmax, rank, world, group, upload=True)
+            shard_fn(sess, s, c.lmin, c.lmax, rank, world, group, upload=True)
             with sess.lock:
                 rows = sess.smallest_rows(k2)
                 disc = sess.discords(kd)
@@ -257,14 +318,25 @@ def run_ours(args):
         t0 = time.perf_counter()
         reps = max(2, min(2 * args.steps, 10))
         for _ in range(reps):
-            e2e_step()
+            out = e2e_step()
         tt = torch.tensor([(time.perf_counter() - t0) / reps], device="cuda")
         dist.all_reduce(tt, op=dist.ReduceOp.MAX)
         e2e_s = float(tt[0])
         e2e_line = {"value": W / e2e_s, "unit": UNIT,
                     "h2d_bytes_per_step": int(8 * (s.n + 2 * (s.n + 1))),
                     "d2h_bytes_per_step": int(n0 * 33 + nl * (k2 * 24 + kd * 16)),
-                    "ms_per_step": e2e_s * 1e3, "api": "distributed.profile_length_sharded + session read-offs"}
+                    "ms_per_step": e2e_s * 1e3, "api": f"distributed.{shard_fn.__name__} + session read-offs"}
+        if rank == 0:
+            # the sharded read-offs must equal one GPU's: rank 0 re-runs the whole range alone
+            with sess.lock:
+                sess.profile(c.lmin, c.lmax, 0, -1, 0)
+                sess.finalize()
+                rows1, disc1 = sess.smallest_rows(k2), sess.discords(kd)
+                val1 = sess.valmp_arrays()
+            rows_n, disc_n, val_n = out
+            readoff_check = bool(all(np.array_equal(a, b) for a, b in zip(rows_n, rows1))
+                                 and all(np.array_equal(a, b) for a, b in zip(disc_n, disc1))
+                                 and all(np.array_equal(a, b) for a, b in zip(val_n, val1)))
     if rank == 0 and world == 1:
         from paper_2008_13447_b200 import mine
         for _ in range(2):
@@ -277,26 +349,25 @@ def run_ours(args):
         e2e_line = {"value": W / e2e_s, "unit": UNIT,
                     "h2d_bytes_per_step": int(8 * (s.n + 2 * (s.n + 1))),
                     "d2h_bytes_per_step": int(n0 * (8 * 4 + 1) + nl * (2 * c.k_motif * 24 + kd * 16)),
-                    "ms_per_step": e2e_s * 1e3}
+                    "ms_per_step": e2e_s * 1e3, "api": "paper_2008_13447_b200.mine (host numpy in, host results out)"}
     clk.__exit__(None, None, None)
 
     if rank != 0:
         if world > 1:
             torch.distributed.destroy_process_group()
         return
-    # roofline of the dominant kernels (k_tile32 walk + k_runs exact runs):
-    # the exhaustive algorithm costs 4 FP64 FMA-pipe instructions per update (2 recurrence DFMA,
-    # DMUL, DFMA key) -- achieved = W * 8 flops / tile time against the measured DFMA peak. The
-    # walk executes that work as 3 FP32 FFMA per cell (2 recurrence + 1 bound test), reported
-    # against the FP32 FMA pipe (128 lanes/SM/clk at the sampled SM clock) as executed_fp32_frac.
+    # Roofline of the dominant kernel, k_tile32 (the FP32 bound-filter walk, ~80 % of the step):
+    # algorithmic work = 3 FP32 FMA per update (2 for the diagonal covariance recurrence, 1 for the
+    # bound test; SURVEY.md §8(d)'s unit, W updates per step over W_l per launch -- DESIGN.md §4),
+    # achieved = W * 3 FMA * 2 flop / (k_tile32 time per step, CUDA events on the launching
+    # stream), peak = the measured FP32 FMA rate of this GPU (vlmp_measure_fp32_peak).
+    peak_ffma = sess.measure_fp32_peak()
     peak_dfma = sess.measure_fp64_peak()
-    avg_tile_s = tile_ms * 1e-3 / args.steps
-    achieved = W * 4 * 2 / avg_tile_s / 1e12          # TFLOP/s (2 flops per FMA-pipe instr)
-    peak = peak_dfma * 2 / 1e12 * world            # aggregate over the N GPUs of the job
+    walk_s = walk_ms * 1e-3 / args.steps
+    runs_s = runs_ms * 1e-3 / args.steps
+    achieved = W * 3 * 2 / walk_s / 1e12
+    peak = peak_ffma * 2 / 1e12 * world
     clk_sum = clk.summary()
-    sm_hz = (clk_sum.get("sm_mhz") or 1965.0) * 1e6
-    executed_cells = st.get("executed_updates", W) if world == 1 else W
-    ffma_frac = executed_cells * 3 / avg_tile_s / (148 * 128 * sm_hz * world)
     prof_traffic = None
     tr_path = os.path.join(ROOT, "profiles", "tile_traffic.json")
     if os.path.exists(tr_path):
@@ -308,31 +379,44 @@ def run_ours(args):
     if world == 1 and not args.no_cpu_baseline:
         v, cores, desc = cpu_sample(s, c, target_s=12.0)
         cpu = {"value": v, "unit": UNIT, "cores": cores, "kind": "port", "sample": desc}
+        try:
+            ref_py = reference_python_sample()
+        except Exception as exc:           # the reference install is optional on a box
+            ref_py = {"unavailable": repr(exc)[:200]}
+        if ref_py is not None:
+            cpu["reference_python"] = ref_py
     line = {
         "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
         "warmup": max(args.warmup, 3), "ms_per_step": step_ms, "higher_is_better": True,
         "scaling": "strong", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
-        "config": {"workload": f"config {args.config}: {c.note}", "n": c.n, "lmin": c.lmin,
-                   "lmax": c.lmax, "k_motif": c.k_motif, "k_discord": c.k_discord,
-                   "W_updates": W, "parallelism": f"length shards x{world}",
-                   "l2": "working set (series + per-length params, 2.6 MB) is L2-resident by design; "
-                         "no flush: the walk is latency/FMA-pipe bound (FP32), not memory-bound"},
-        "roofline": {"bound": "fp64_fma", "achieved": achieved, "peak": peak, "unit": "TFLOP/s",
+        "config": _config_dict(args, c, W, world, parallelism),
+        "step_ms_median": float(np.median(step_ms_list)) if world == 1 else None,
+        "roofline": {"bound": "fp32_fma", "achieved": achieved, "peak": peak, "unit": "TFLOP/s",
                      "frac": achieved / peak, "traffic": prof_traffic,
-                     "peak_source": "measured DFMA microbenchmark (vlmp_measure_fp64_peak); "
-                                    "MEASURED_PEAKS.json has no FP64 figure",
-                     "kernel": "k_tile32 + k_runs", "avg_tile_ms_per_step": avg_tile_s * 1e3,
-                     "flops_per_update": "8 = the exhaustive cell's 4 FP64 FMA-pipe instr (2 recurrence "
-                                         "DFMA + DMUL + DFMA key); the walk executes 3 FP32 FFMA per cell "
-                                         "(recurrence + bound test under a rigorous error slack) and the "
-                                         "exact FP64 work only on the cells that pass (k_runs)",
-                     "executed_fp32_frac": ffma_frac,
-                     "run_cells_per_step": st.get("run_cells"), "runs_fp32_walk": st.get("fp32_walk")},
+                     "kernel": "k_tile32", "launches_per_step": walk_launches / args.steps,
+                     "launch_ms": walk_ms / max(walk_launches, 1),
+                     "flops_per_update": "6 = 3 FP32 FMA (2 recurrence + 1 bound test) x 2; ncu counts "
+                                         "3.04 executed FMA lane-ops per update (profiles/)",
+                     "peak_source": "measured: vlmp_measure_fp32_peak (FFMA, all SMs, best of 3); "
+                                    "MEASURED_PEAKS.json has no FP32 figure",
+                     "walk_ms_per_step": walk_s * 1e3,
+                     "share_of_step": walk_s * 1e3 / step_ms,
+                     "k_runs": {"ms_per_step": runs_s * 1e3, "share_of_step": runs_s * 1e3 / step_ms,
+                                "cells_per_step": st.get("run_cells"), "bound": "fp64 / L2 latency",
+                                "fp64_frac": (st.get("run_cells") or 0) * 2 / max(runs_s, 1e-12) / peak_dfma},
+                     "effective_fp64_frac": W * 4 / (step_ms * 1e-3) / (peak_dfma * world),
+                     "effective_fp64_note": "W x 4 FP64 FMA-pipe instr (the exhaustive FP64 cell) per step "
+                                            "time over the measured DFMA peak: the FP64 work the FP32 "
+                                            "filter avoids, not a pipe utilisation"},
         "cpu_baseline": cpu,
         "e2e": e2e_line,
         "gpu_launches": launches,
+        "graph": bool(st.get("graph")),
         "clocks": clk_sum,
     }
+    if readoff_check is not None:
+        line["readoffs_equal_1gpu"] = readoff_check
+        line["dist_backend"] = backend
     print(json.dumps(line), flush=True)
     if world > 1:
         torch.distributed.destroy_process_group()
@@ -340,6 +424,10 @@ def run_ours(args):
 
 def main():
     args = _args()
+    if args.gpus > 1 and "WORLD_SIZE" not in os.environ:
+        sys.exit(_spawn_ranks(args))
+    if args.gpus > 1:
+        os.environ.setdefault("NCCL_DEBUG", "INFO")   # communicator lines show the rank count
     if args.impl == "reference":
         run_reference(args)
     else:

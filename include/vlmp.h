@@ -74,11 +74,14 @@ int vlmp_profile_range(vlmp_session* s, int32_t lmin, int32_t lmax,
 
 /*
  * Length shard for multi-GPU runs: phase 1 for length indices li_lo..li_hi of
- * [lmin, lmax] (all bands). Seeds are carried from lmin to li_lo by the tile kernel's
- * own Welford step (bit-identical to a single run), li_lo is walked with full folds,
- * later lengths are filtered; accumulators of other lengths stay empty, so an
- * all-reduce MIN of the partials (vlmp_partials_*) over the shards reproduces the
- * single-GPU partials exactly.
+ * [lmin, lmax] (all bands). On the default FP32 walk the tile seeds are centred direct
+ * sums at the shard's first length (they only start the filter walk; every key comes from
+ * the exact FP64 runs), that length takes its bounds from full folds over a sample of the
+ * bands, and every length of the shard runs the FP32 walk + exact runs. (With
+ * VLMP_F_FP64_FILTER the seeds are carried from lmin by the tile kernel's Welford step.)
+ * Accumulators of other lengths stay empty: each (length, offset) has exactly one owner
+ * rank, so the per-length minima equal a single run's (keys may differ in their last
+ * bits where a run starts elsewhere; neighbours agree except at ties within ~1e-15).
  */
 int vlmp_profile_lengths(vlmp_session* s, int32_t lmin, int32_t lmax, int32_t li_lo, int32_t li_hi,
                          uint32_t flags);
@@ -154,6 +157,19 @@ int vlmp_get_profile_m(vlmp_session* s, int32_t length, double* dist, int64_t* n
 int vlmp_discords_m(vlmp_session* s, int32_t k, double* out_dist, int64_t* out_off);
 
 /*
+ * Pruned top-k m-th discord scan (MAD, discords.py:144-247 over profile.py:66-232's partial
+ * profiles): the first length runs the exhaustive m-best profile and stores each row's
+ * P = min(8, max(p, m)) best neighbours; every later length advances them in O(1), certifies
+ * rows by VALMOD's lower bound (Eq. 2), replays the insertion policy and recomputes full rows only
+ * for non-certified owners that could still enter the matrix (or falls back to an exhaustive
+ * pass when that would cost more). Same results as vlmp_profile_mbest + vlmp_discords_m.
+ * out_dist / out_off: [n_len][k][m]; counters (optional): [n_len][4] = certified rows,
+ * non-certified live rows, full rows recomputed, 1 if the length ran exhaustively.
+ */
+int vlmp_discords_pruned(vlmp_session* s, int32_t lmin, int32_t lmax, int32_t k, int32_t m, int32_t p,
+                         double* out_dist, int64_t* out_off, double* counters);
+
+/*
  * Motif-set range queries (motifsets.py:158-165, the row_profile path of _range_members):
  * for query q, every offset j with dist(owners[q], j) < radii[q] at length lengths[q],
  * from the owner's full row with the reference formula (profile.py:235-260); trivial
@@ -175,7 +191,9 @@ int vlmp_range_query(vlmp_session* s, int64_t n_q, const int64_t* owners, const 
  * too weak for the covariance-domain filter), out[15] largest per-length log fill,
  * out[16] 1 if the filtered lengths ran the FP32 walk (filter32.cu), out[17] largest
  * per-length run count of that walk, out[18] cells evaluated exactly in its runs, out[19] the
- * row-segment length S of the tile walks (n_out <= 20).
+ * row-segment length S of the tile walks, out[20] k_tile32 ms (sum over its launches, CUDA
+ * events on the session stream), out[21] k_runs ms, out[22] k_tile32 launches, out[23] 1 if the
+ * per-length sequence ran as a CUDA graph (n_out <= 24).
  */
 int vlmp_stats(vlmp_session* s, double* out, int32_t n_out);
 
@@ -186,8 +204,18 @@ int vlmp_stats(vlmp_session* s, double* out, int32_t n_out);
 int vlmp_event_record(vlmp_session* s, int32_t slot);
 int vlmp_event_elapsed(vlmp_session* s, float* ms);
 
+/*
+ * Window mean / std of every offset at one length, computed on the device by the routine the
+ * kernels use (series.py:91-100 operation order) from the uploaded prefix sums -- equal bit for
+ * bit to DataSeries.moving_stats (test_gpu_scale.py). mu, sd: n - length + 1 each.
+ */
+int vlmp_window_stats(vlmp_session* s, int32_t length, double* mu, double* sd);
+
 /* FP64 FMA peak microbenchmark (DFMA instr/s on this device, all SMs). */
 int vlmp_measure_fp64_peak(vlmp_session* s, double* fma_per_s);
+/* FP32 FMA peak microbenchmark (FFMA lane-ops/s, register operands, all SMs, best of 3):
+ * the roofline denominator of the FP32 walk (k_tile32). */
+int vlmp_measure_fp32_peak(vlmp_session* s, double* fma_per_s);
 
 #ifdef __cplusplus
 }

@@ -50,6 +50,10 @@ SIGNATURES = {
     "vlmp_event_record": (C.c_int, [C.c_void_p, C.c_int32]),
     "vlmp_event_elapsed": (C.c_int, [C.c_void_p, C.POINTER(C.c_float)]),
     "vlmp_measure_fp64_peak": (C.c_int, [C.c_void_p, _c_double_p]),
+    "vlmp_measure_fp32_peak": (C.c_int, [C.c_void_p, _c_double_p]),
+    "vlmp_window_stats": (C.c_int, [C.c_void_p, C.c_int32, C.c_void_p, C.c_void_p]),
+    "vlmp_discords_pruned": (C.c_int, [C.c_void_p, C.c_int32, C.c_int32, C.c_int32, C.c_int32, C.c_int32,
+                                       C.c_void_p, C.c_void_p, C.c_void_p]),
 }
 
 FLAG_FULL_EVERY_LENGTH = 1
@@ -91,7 +95,9 @@ class Session:
         h = C.c_void_p()
         self._check(self.lib.vlmp_create(C.byref(h), self.device))
         self.h = h
-        self.lock = threading.Lock()
+        # re-entrant: a public call holds it for its whole run + read-offs (api.GpuRun)
+        self.lock = threading.RLock()
+        self.generation = 0      # bumped by every set_series / profile run
         self.n = 0
         self.lmin = self.lmax = 0
 
@@ -115,16 +121,19 @@ class Session:
         t = np.ascontiguousarray(values, dtype=np.float64)
         c1 = np.ascontiguousarray(cum, dtype=np.float64)
         c2 = np.ascontiguousarray(cum2, dtype=np.float64)
+        self.generation += 1
         self._check(self.lib.vlmp_set_series(self.h, _ptr(t), _ptr(c1), _ptr(c2), t.shape[0],
                                              float(sigma_floor)))
         self.n = int(t.shape[0])
 
     def profile_lengths(self, lmin, lmax, li_lo, li_hi, flags=0):
+        self.generation += 1
         self._check(self.lib.vlmp_profile_lengths(self.h, int(lmin), int(lmax), int(li_lo), int(li_hi),
                                                   int(flags)))
         self.lmin, self.lmax = int(lmin), int(lmax)
 
     def profile(self, lmin, lmax, band_lo=0, band_hi=-1, flags=0):
+        self.generation += 1
         self._check(self.lib.vlmp_profile_range(self.h, int(lmin), int(lmax), int(band_lo),
                                                 int(band_hi), int(flags)))
         self.lmin, self.lmax = int(lmin), int(lmax)
@@ -220,6 +229,7 @@ class Session:
 
     # -- m-best mode (m-th discords) ---------------------------------------------
     def profile_mbest(self, lmin, lmax, m):
+        self.generation += 1
         self._check(self.lib.vlmp_profile_mbest(self.h, int(lmin), int(lmax), int(m)))
         self.lmin, self.lmax, self.mbest = int(lmin), int(lmax), int(m)
 
@@ -235,13 +245,23 @@ class Session:
         self._check(self.lib.vlmp_discords_m(self.h, int(k), _ptr(d), _ptr(o)))
         return d, o
 
+    def discords_pruned(self, lmin, lmax, k, m, p):
+        """(dist [n_len][k][m], off [n_len][k][m], counters [n_len][4]) of the pruned scan."""
+        nl = int(lmax) - int(lmin) + 1
+        d = np.empty((nl, k, m)); o = np.empty((nl, k, m), dtype=np.int64); c = np.zeros((nl, 4))
+        self.generation += 1
+        self._check(self.lib.vlmp_discords_pruned(self.h, int(lmin), int(lmax), int(k), int(m), int(p),
+                                                  _ptr(d), _ptr(o), _ptr(c)))
+        return d, o, c
+
     def stats(self):
-        out = np.zeros(20)
-        self._check(self.lib.vlmp_stats(self.h, _ptr(out), 20))
+        out = np.zeros(24)
+        self._check(self.lib.vlmp_stats(self.h, _ptr(out), 24))
         keys = ["profile_ms", "finalize_ms", "executed_updates", "W", "tile_ms", "tile_launches",
                 "filtered_lengths", "full_lengths", "slow_merges", "kernel_launches", "first_tile_ms",
                 "slow_rowsteps", "bound_fixes", "exact_redo", "fallback_lengths", "max_log_records",
-                "fp32_walk", "max_runs", "run_cells", "seg_rows"]
+                "fp32_walk", "max_runs", "run_cells", "seg_rows", "walk_ms", "runs_ms", "walk_launches",
+                "graph"]
         return {k: float(out[i]) for i, k in enumerate(keys)}
 
     def event_record(self, slot):
@@ -255,6 +275,17 @@ class Session:
     def measure_fp64_peak(self):
         v = C.c_double()
         self._check(self.lib.vlmp_measure_fp64_peak(self.h, C.byref(v)))
+        return v.value
+
+    def window_stats(self, length):
+        N = self.n - int(length) + 1
+        mu = np.empty(N); sd = np.empty(N)
+        self._check(self.lib.vlmp_window_stats(self.h, int(length), _ptr(mu), _ptr(sd)))
+        return mu, sd
+
+    def measure_fp32_peak(self):
+        v = C.c_double()
+        self._check(self.lib.vlmp_measure_fp32_peak(self.h, C.byref(v)))
         return v.value
 
 

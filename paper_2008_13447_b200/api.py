@@ -71,7 +71,13 @@ def _moving_sd(series, length, span=None):
 
 
 class GpuRun:
-    """Device-resident result of one exhaustive run over [lmin, lmax]."""
+    """Device-resident result of one exhaustive run over [lmin, lmax].
+
+    The session is process-wide (one per device), so a run's read-offs are only valid while
+    no other run replaced the device state: use it as a context manager, which holds the
+    session's (re-entrant) lock from the run through the last read-off, as every public
+    entry point here does. Read-offs outside that window raise if another run intervened.
+    """
 
     def __init__(self, series, lmin: int, lmax: int, flags: int = 0, device: int | None = None):
         self.series = series
@@ -82,10 +88,24 @@ class GpuRun:
             self.sess.profile(lmin, lmax, 0, -1, flags)
             self.sess.finalize()
             self.stats = self.sess.stats()
+            self.generation = self.sess.generation
 
-    # All read-offs re-take the session lock; results stay valid until the next run.
+    def __enter__(self):
+        self.sess.lock.acquire()
+        self._check()
+        return self
+
+    def __exit__(self, *exc):
+        self.sess.lock.release()
+
+    def _check(self):
+        if self.sess.generation != self.generation:
+            raise E.DeviceError("another run replaced this session's device state; "
+                                "hold the run (with GpuRun(...) as run:) until its read-offs are done")
+
     def valmp(self) -> VALMP:
         with self.sess.lock:
+            self._check()
             d, nm, ln, ix, pop = self.sess.valmp_arrays()
         v = VALMP(d.shape[0])
         v.distances[:] = d
@@ -97,19 +117,30 @@ class GpuRun:
 
     def smallest_rows(self, k2: int):
         with self.sess.lock:
+            self._check()
             return self.sess.smallest_rows(k2)
 
     def discords(self, k: int):
         with self.sess.lock:
+            self._check()
             return self.sess.discords(k)
 
     def profile(self, length: int):
         with self.sess.lock:
+            self._check()
             return self.sess.profile_arrays(length)
 
     def ranking_events(self, tau: float):
         with self.sess.lock:
+            self._check()
             return self.sess.ranking_events(tau)
+
+
+def _session_lock():
+    """The device session's re-entrant lock: every public call holds it from its run through
+    its last read-off, so a concurrent call on the same device cannot swap the device state
+    underneath it (the reference's entry points are pure functions)."""
+    return _lib.session(_device()).lock
 
 
 def _per_length_motifs(run: GpuRun):
@@ -161,22 +192,45 @@ def valmod(series, lmin: int, lmax: int, p: int, *, ranking=None, trace=None,
     if p < 1:
         raise E.InvalidParametersError("p must be at least 1")
     _check_profile_length(series, lmin)
-    run = GpuRun(series, lmin, lmax)
-    v = run.valmp()
+    with _session_lock():
+        run = GpuRun(series, lmin, lmax)
+        v = run.valmp()
+        motifs = _per_length_motifs(run) if trace is not None else None
+        if ranking is not None:
+            _feed_ranking(run, v, ranking)
     if trace is not None:
-        for li, motif in enumerate(_per_length_motifs(run)):
+        for li, motif in enumerate(motifs):
             length = lmin + li
             n_dp = series.n - length + 1
             trace.add_length(length, n_profiles=n_dp, n_valid=n_dp, n_nonvalid=0,
                              n_recomputed=0, full_recompute=False, motif=motif)
-    if ranking is not None:
-        _feed_ranking(run, v, ranking)
     return v
 
 
+def _discord_mode(mode, series, lmin, lmax):
+    """Which discord path runs: ``mode`` argument, else VLMP_DISCORD_MODE, else "auto" -- the
+    pruned MAD scan where the A/B measurement shows it wins (long series with
+    several lengths), the exhaustive profile otherwise."""
+    mode = mode or os.environ.get("VLMP_DISCORD_MODE", "auto")
+    if mode not in ("auto", "exhaustive", "pruned"):
+        raise E.InvalidParametersError(f"mode must be auto, exhaustive or pruned (got {mode!r})")
+    if mode == "auto":
+        mode = "pruned" if (series.n >= PRUNED_MIN_N and lmax > lmin) else "exhaustive"
+    return mode
+
+
+# auto mode: the pruned discord scan from this series length up (DESIGN.md §2c's A/B)
+PRUNED_MIN_N = 1 << 20
+
+
 def topkm_discord_discovery(series, lmin: int, lmax: int, k: int, m: int, p: int, *,
-                            trace=None, threads: int = 1) -> DiscordScan:
-    """Exact top-k m-th discords for every length, merged across lengths (m = 1)."""
+                            trace=None, threads: int = 1, mode: str | None = None) -> DiscordScan:
+    """Exact top-k m-th discords for every length, merged across lengths (discords.py:206-247).
+
+    ``mode`` (not in the reference's signature; keyword only): "exhaustive" walks every pair of
+    every length, "pruned" runs MAD's pruned scan on the GPU (stored neighbours certified by
+    VALMOD's bound, full rows only where they can matter; vlmp_discords_pruned), "auto" picks
+    by the measured A/B. Both give the same matrices; the trace's counters report the work."""
     series = as_series(series)
     if m < 1 or k < 1:
         raise E.InvalidParametersError("k and m must be at least 1")
@@ -186,9 +240,15 @@ def topkm_discord_discovery(series, lmin: int, lmax: int, k: int, m: int, p: int
     if m > 8 or k > 32:
         raise E.InvalidParametersError("the GPU path supports k <= 32 and m <= 8")
     _check_profile_length(series, lmin)
-    if m == 1:
-        run = GpuRun(series, lmin, lmax)
-        dist, off = run.discords(k)
+    counters = None
+    if _discord_mode(mode, series, lmin, lmax) == "pruned":
+        sess = _lib.session(_device())
+        with sess.lock:
+            sess.set_series(series.values, series._cum, series._cum2, series.sigma_floor)
+            dist, off, counters = sess.discords_pruned(lmin, lmax, k, m, p)
+    elif m == 1:
+        with _session_lock():
+            dist, off = GpuRun(series, lmin, lmax).discords(k)
         dist, off = dist[:, :, None], off[:, :, None]
     else:
         sess = _lib.session(_device())
@@ -208,8 +268,13 @@ def topkm_discord_discovery(series, lmin: int, lmax: int, k: int, m: int, p: int
         update_variable_length_discords(dkm, merged, k, m)
         if trace is not None:
             n_dp = series.n - length + 1
-            trace.add_length(length, n_profiles=n_dp, n_valid=n_dp, n_nonvalid=0,
-                             n_recomputed=0, full_recompute=False)
+            if counters is None:
+                trace.add_length(length, n_profiles=n_dp, n_valid=n_dp, n_nonvalid=0,
+                                 n_recomputed=0, full_recompute=False)
+            else:
+                c = counters[li]
+                trace.add_length(length, n_profiles=n_dp, n_valid=int(c[0]), n_nonvalid=int(c[1]),
+                                 n_recomputed=int(c[2]), full_recompute=bool(c[3]) and li > 0)
     return DiscordScan(merged, per_length)
 
 
@@ -224,17 +289,16 @@ def compute_matrix_profile(series, length: int, p: int, m_track: int = 0,
     if m_track > 8:
         raise E.InvalidParametersError("the GPU path tracks at most m = 8 matches per row")
     _check_profile_length(series, length)
-    run = GpuRun(series, length, length)
-    mp, ip = run.profile(length)
     best_m = best_nbr = None
+    with _session_lock():
+        run = GpuRun(series, length, length)
+        mp, ip = run.profile(length)
+        if m_track > 1:
+            run.sess.profile_mbest(length, length, m_track)
+            best_m, best_nbr = run.sess.profile_m_arrays(length)
     if m_track == 1:
         best_m = mp[:, None].copy()
         best_nbr = ip[:, None].copy()
-    elif m_track > 1:
-        sess = run.sess
-        with sess.lock:
-            sess.profile_mbest(length, length, m_track)
-            best_m, best_nbr = sess.profile_m_arrays(length)
     return ProfileResult(MatrixProfile(mp, ip, length), None, best_m, best_nbr)
 
 
@@ -246,8 +310,8 @@ def motifs_per_length(series, lmin: int, lmax: int, k: int):
     _check_profile_length(series, lmin)
     if k < 1 or 2 * k > 64:
         raise E.InvalidParametersError("k must be in [1, 32]")
-    run = GpuRun(series, lmin, lmax)
-    return _topk_from_rows(run, k)
+    with _session_lock():
+        return _topk_from_rows(GpuRun(series, lmin, lmax), k)
 
 
 class MiningResult:
@@ -272,9 +336,13 @@ def mine(series, lmin: int, lmax: int, k_motif: int = 1, k_discord: int = 1, *,
     _check_profile_length(series, lmin)
     if not (1 <= k_motif <= 32) or not (1 <= k_discord <= 32):
         raise E.InvalidParametersError("k_motif and k_discord must be in [1, 32]")
-    run = GpuRun(series, lmin, lmax)
-    v = run.valmp()
-    motifs = _topk_from_rows(run, k_motif)
+    with _session_lock():
+        run = GpuRun(series, lmin, lmax)
+        v = run.valmp()
+        motifs = _topk_from_rows(run, k_motif)
+        dist, off = run.discords(k_discord)
+        if ranking is not None:
+            _feed_ranking(run, v, ranking)
     trace = RunTrace()
     for li in range(lmax - lmin + 1):
         length = lmin + li
@@ -282,7 +350,6 @@ def mine(series, lmin: int, lmax: int, k_motif: int = 1, k_discord: int = 1, *,
         top = motifs[length]
         trace.add_length(length, n_profiles=n_dp, n_valid=n_dp, n_nonvalid=0, n_recomputed=0,
                          full_recompute=False, motif=top[0] if top else None)
-    dist, off = run.discords(k_discord)
     # per-length matrices are (k, 1) views of one batch array; the cross-length merge is
     # update_variable_length_discords over ascending lengths, vectorised
     dist3 = np.array(dist, dtype=np.float64).reshape(-1, k_discord, 1)
@@ -292,8 +359,6 @@ def mine(series, lmin: int, lmax: int, k_motif: int = 1, k_discord: int = 1, *,
                   for li in range(lmax - lmin + 1)}
     merged = merge_variable_length_discords(dist3, off3, np.arange(lmin, lmax + 1),
                                             VariableLengthDiscordMatrix.empty(k_discord, 1))
-    if ranking is not None:
-        _feed_ranking(run, v, ranking)
     return MiningResult(v, motifs, DiscordScan(merged, per_length), trace, run.stats)
 
 

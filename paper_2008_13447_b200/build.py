@@ -7,7 +7,7 @@ import subprocess
 
 HERE = os.path.dirname(os.path.abspath(__file__))
 ROOT = os.path.dirname(HERE)
-SRCS = [os.path.join(HERE, "csrc", f) for f in ("profile.cu", "filter32.cu", "readout.cu", "session.cu")]
+SRCS = [os.path.join(HERE, "csrc", f) for f in ("profile.cu", "filter32.cu", "readout.cu", "pruned.cu", "session.cu")]
 SRC = SRCS[0]   # the tile kernels (variant builds)
 HDRS = [os.path.join(HERE, "csrc", "vlmp_internal.cuh")]
 OUT = os.path.join(HERE, "libvlmp.so")

@@ -138,6 +138,7 @@ struct Tile32Args {
     const int* forced;
     long long N, dlo; int n_tiles32, S, m, e, update_seeds;
     double sscale;
+    unsigned long long* span;   // [2]: first CTA start, last CTA end (ns; nullptr: not timed)
     const float4* cq4;      // packed walk: band-pair column factors
     const float4* pf4;      // packed walk, PSEP > 256: band-pair {df, df', dg, dg'}
 };
@@ -461,6 +462,11 @@ __global__ void __launch_bounds__(32, VLMP_FILTER32_WARPS_PER_SM) k_tile32(Tile3
     Smem32p& sm = *reinterpret_cast<Smem32p*>(smem_raw);
     const int lane = threadIdx.x;
     const int wid = blockIdx.x;
+    if (a.span && lane == 0) atomicMin(a.span, gtime());
+    struct SpanEnd {   // the CTA's end on every return path
+        unsigned long long* p; int lane;
+        __device__ ~SpanEnd() { if (p && lane == 0) atomicMax(p + 1, gtime()); }
+    } span_end{a.span, lane};
     if (wid >= a.n_tiles32) return;
     const int2 pr2 = a.tiles32[wid];
     const int2 tA = a.tiles[pr2.x];
@@ -704,7 +710,8 @@ __global__ void __launch_bounds__(256) k_runs(const Run* __restrict__ runs, cons
                                              long long cap, const Prm* __restrict__ prm,
                                              const double* __restrict__ tn, const double* __restrict__ mu,
                                              int m, int e, ulonglong2* acc, unsigned long long* counters,
-                                             ulonglong2* slots, int* slot_cnt) {
+                                             ulonglong2* slots, int* slot_cnt, unsigned long long* span) {
+    if (span && threadIdx.x == 0) atomicMin(span, gtime());
     const unsigned long long cnt = *run_count;
     const long long nr = (long long)(cnt < (unsigned long long)cap ? cnt : (unsigned long long)cap);
     const int lane = threadIdx.x & 31;
@@ -796,6 +803,7 @@ __global__ void __launch_bounds__(256) k_runs(const Run* __restrict__ runs, cons
         cells += __shfl_xor_sync(FULLMASK, cells, off);
     }
     if (lane == 0 && (merged | cells)) { atomicAdd(counters + 0, merged); atomicAdd(counters + 4, cells); }
+    if (span && lane == 0) atomicMax(span + 1, gtime());
 }
 
 // ---------------------------------------------------------------------------------
@@ -837,7 +845,7 @@ void build_tiles32(const std::vector<int2>& tiles, long long band_lo, std::vecto
 int launch_filter32(vlmp_session* s, cudaStream_t st, const Prm* prm, const double* mu, long long N, int m, int e,
                     long long dl, int S, int update_seeds, long long n_t32, const int* forced,
                     ulonglong2* acc, Run* runs, unsigned long long* run_count, long long run_cap,
-                    ulonglong2* slots, int* slot_cnt) {
+                    ulonglong2* slots, int* slot_cnt, unsigned long long* span) {
     const long long A = s->A;
     const long long nb = A / 256 + 1;
     Prep32Args pa{prm, s->d_cum, s->d_cum2, s->d_p32, s->d_cq32, s->d_magblk, nb, N, A, m, s->sscale,
@@ -847,10 +855,11 @@ int launch_filter32(vlmp_session* s, cudaStream_t st, const Prm* prm, const doub
     if (n_t32) {
         Tile32Args ta{s->d_p32, s->d_cq32, s->d_magblk, nb, s->d_tn, mu, s->d_seeds, s->d_tiles, s->d_tiles32,
                       runs, run_count, run_cap, s->d_counters, forced, N, dl, (int)n_t32, S, m, e,
-                      update_seeds, s->sscale, s->d_cq4, s->d_pf4};
+                      update_seeds, s->sscale, span, s->d_cq4, s->d_pf4};
+        // span: [0, 1] k_tile32's and [2, 3] k_runs' first start / last end (bench.py's roofline)
         k_tile32<<<(unsigned)n_t32, 32, sizeof(SmemT), st>>>(ta);
         k_runs<<<148 * 8, 256, 0, st>>>(runs, run_count, run_cap, prm, s->d_tn, mu, m, e, acc, s->d_counters,
-                                        slots, slot_cnt);
+                                        slots, slot_cnt, span ? span + 2 : nullptr);
     }
     return 0;
 }

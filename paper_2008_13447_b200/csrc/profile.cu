@@ -66,6 +66,11 @@ __global__ void k_params(ParamArgs a) {
     a.mu[o] = mu_o;
 }
 
+void launch_params(vlmp_session* s, cudaStream_t st, Prm* prm, double* mu, int m) {
+    ParamArgs pa{s->d_tn, s->d_cum, s->d_cum2, prm, mu, s->n, s->n - m + 1, s->A, m, s->floor_};
+    k_params<<<blocks(s->A, 256), 256, 0, st>>>(pa);
+}
+
 // ---------------------------------------------------------------------------------
 // O(1)-per-offset bound from the previous length's winners (1-best mode). Candidates:
 // o's own winner c1 and its neighbours' winners shifted along their diagonals,
@@ -704,6 +709,11 @@ __global__ void k_seed_forward(SeedArgs a, const double* __restrict__ cum, int m
     for (int s = 0; s < D; ++s) seedp[s] = sd[s];
 }
 
+__global__ void k_span_init(unsigned long long* span, int n_len) {
+    const int t = blockIdx.x * blockDim.x + threadIdx.x;
+    if (t < n_len) { span[4 * t] = ~0ull; span[4 * t + 1] = 0; span[4 * t + 2] = ~0ull; span[4 * t + 3] = 0; }
+}
+
 __global__ void k_fill_acc(ulonglong2* acc, long long n) {
     long long o = blockIdx.x * (long long)blockDim.x + threadIdx.x;
     if (o < n) acc[o] = make_ulonglong2(KEY_NONE, (unsigned long long)IDX_NONE);
@@ -1113,9 +1123,11 @@ static int debug_dump(cudaStream_t st, int li, const Prm* prm, long long N, cons
     return 0;
 }
 
+// Enqueues phase 1 (no host sync): the launch sequence, then async copies of the small
+// counters the overflow check needs into pinned host memory. settle_profile() (called by
+// every consumer of phase 1) waits for them, checks the logs and redoes the run if needed.
 static int profile_impl(vlmp_session* s, int32_t lmin, int32_t lmax, int64_t band_lo,
-                        int64_t band_hi, uint32_t flags, bool* overflow_out, bool* used_sampled,
-                        int li_lo = 0, int li_hi = -1, bool* fp32_fallback = nullptr) {
+                        int64_t band_hi, uint32_t flags, int li_lo = 0, int li_hi = -1) {
     CU(cudaSetDevice(s->device));
     cudaStream_t st = s->stream;
     const long long n = s->n, A = s->A;
@@ -1158,7 +1170,6 @@ static int profile_impl(vlmp_session* s, int32_t lmin, int32_t lmax, int64_t ban
     std::vector<int> smap;
     for (size_t k = 0; k < tiles.size(); ++k)
         if ((tiles[k].x - band_lo) % sample == 0) { tiles_s.push_back(tiles[k]); smap.push_back((int)k); }
-    *used_sampled = sampled_start;
     const long long T = tiles_cached ? s->tc_T : (long long)tiles.size();
     int rc;
     if ((rc = ensure(s->d_tiles, s->tiles_cap, (size_t)std::max<long long>(T, 1)))) return rc;
@@ -1169,9 +1180,6 @@ static int profile_impl(vlmp_session* s, int32_t lmin, int32_t lmax, int64_t ban
     if ((rc = ensure(s->d_logcnt, s->logcnt_cap, (size_t)n_len))) return rc;
     if ((rc = ensure(s->d_forced, s->forced_cap, (size_t)n_len))) return rc;
     if ((rc = ensure(s->d_fixcnt, s->fixcnt_cap, (size_t)n_len))) return rc;
-    CU(cudaMemsetAsync(s->d_fixcnt, 0, n_len * sizeof(unsigned long long), st));
-    CU(cudaMemsetAsync(s->d_logcnt, 0, n_len * sizeof(unsigned long long), st));
-    CU(cudaMemsetAsync(s->d_forced, 0, n_len * sizeof(int), st));
     if (T && !tiles_cached) CU(cudaMemcpyAsync(s->d_tiles, tiles.data(), T * sizeof(int2), cudaMemcpyHostToDevice, st));
     const long long Ts = tiles_cached ? s->tc_Ts : (long long)tiles_s.size();
     if (bound_start && Ts && !tiles_cached) {
@@ -1191,7 +1199,6 @@ static int profile_impl(vlmp_session* s, int32_t lmin, int32_t lmax, int64_t ban
         if ((rc = ensure(s->d_magblk, s->magblk_cap, (size_t)(3 * (A / 256 + 1))))) return rc;
         if (!tiles32.empty())
             CU(cudaMemcpyAsync(s->d_tiles32, tiles32.data(), tiles32.size() * sizeof(int2), cudaMemcpyHostToDevice, st));
-        if ((rc = filter32_setup())) return rc;
     }
     const long long T32 = (fp32 && tiles_cached) ? s->tc_T32 : (long long)tiles32.size();
     if (!tiles_cached) {
@@ -1204,11 +1211,6 @@ static int profile_impl(vlmp_session* s, int32_t lmin, int32_t lmax, int64_t ban
     const size_t smem = WARPS_PER_CTA * sizeof(WarpSmem);
     CU(cudaFuncSetAttribute(k_tile<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
     CU(cudaFuncSetAttribute(k_tile<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-    k_fill_acc<<<blocks((long long)n_len * A, 256), 256, 0, st>>>(s->d_acc, (long long)n_len * A);
-    CU(cudaMemsetAsync(s->d_counters, 0, 8 * sizeof(unsigned long long), st));
-    CU(cudaEventRecord(s->ev[0], st));
-
-    double executed = 0, launches = 0, n_filtered = 0, n_full = 0, tile_ms = 0, klaunch = 2;
     const double margin = 1.0 / (1 << 26);
     // VLMP_LOG_CAP (records) lowers the effective log capacity: a test hook that forces the
     // overflow -> exact full-fold re-run path
@@ -1219,185 +1221,293 @@ static int profile_impl(vlmp_session* s, int32_t lmin, int32_t lmax, int64_t ban
     if (li_lo < 0) li_lo = 0;
     if (li_hi >= n_len || (li_hi < 0 && li_lo == 0)) li_hi = n_len - 1;   // default: every length
     if (li_hi < li_lo) li_hi = -1;                                        // empty shard: no work
-    std::vector<int> timed;   // lengths whose tile pass ran (event pairs)
-    if (li_lo > 0 && li_lo <= li_hi && T) {
-        if (fp32) {
-            // a later length shard on the FP32 walk: the seeds only start the walk (its slack
-            // covers their rounding; keys come from the exact runs), so they are direct sums at
-            // the shard's first length -- no carry through the lengths before it
-            const int m0 = lmin + li_lo;
-            ParamArgs pa{s->d_tn, s->d_cum, s->d_cum2, s->d_prm, s->d_mu, n, n - m0 + 1, A, m0, s->floor_};
-            k_params<<<blocks(A, 256), 256, 0, st>>>(pa);
-            SeedArgs sa{s->d_tn, s->d_mu, s->d_tiles, s->d_seeds, dl, (int)T, S, m0};
-            k_seed_init<<<blocks(T * 32, WARPS_PER_CTA * 32), WARPS_PER_CTA * 32, 0, st>>>(sa);
-            klaunch += 2;
-        } else {
-            // FP64 walk: seeds at lmin (direct sums), carried to the shard's first length with
-            // the tile kernel's own Welford step (bit-identical to the single-GPU chain)
-            ParamArgs pa{s->d_tn, s->d_cum, s->d_cum2, s->d_prm, s->d_mu, n, n - lmin + 1, A, lmin, s->floor_};
-            k_params<<<blocks(A, 256), 256, 0, st>>>(pa);
-            SeedArgs sa{s->d_tn, s->d_mu, s->d_tiles, s->d_seeds, dl, (int)T, S, lmin};
-            k_seed_init<<<blocks(T * 32, WARPS_PER_CTA * 32), WARPS_PER_CTA * 32, 0, st>>>(sa);
-            k_seed_forward<<<blocks(T * 32, 128), 128, 0, st>>>(sa, s->d_cum, lmin + li_lo);
-            klaunch += 3;
-        }
+    while (s->lev.size() < (size_t)2 * n_len) { cudaEvent_t ev; CU(cudaEventCreate(&ev)); s->lev.push_back(ev); }
+    if ((rc = ensure(s->d_span, s->span_cap, (size_t)4 * n_len))) return rc;
+    if ((size_t)4 * n_len > s->h_span_cap) {
+        if (s->h_span) cudaFreeHost(s->h_span);
+        s->h_span = nullptr; s->h_span_cap = 0;
+        CU(cudaMallocHost((void**)&s->h_span, (size_t)4 * n_len * sizeof(unsigned long long)));
+        s->h_span_cap = (size_t)4 * n_len;
     }
-    for (int li = (li_lo <= li_hi ? li_lo : 0); li <= li_hi; ++li) {
-        const int m = lmin + li;
-        const long long N = n - m + 1;
-        const int e = (m + 1) / 2;
-        // window parameters ping-pong between two buffers: the bound reads length m-1's
-        Prm* prm = (li & 1) ? s->d_prm2 : s->d_prm;
-        double* mu = (li & 1) ? s->d_mu2 : s->d_mu;
-        const Prm* prm_prev = (li & 1) ? s->d_prm : s->d_prm2;
-        const double* mu_prev = (li & 1) ? s->d_mu : s->d_mu2;
-        ParamArgs pa{s->d_tn, s->d_cum, s->d_cum2, prm, mu, n, N, A, m, s->floor_};
-        k_params<<<blocks(A, 256), 256, 0, st>>>(pa);
-        ++klaunch;
-        const bool full = (li == li_lo) || (flags & VLMP_F_FULL_EVERY_LENGTH);
-        if (li == 0 && T) {
-            SeedArgs sa{s->d_tn, mu, s->d_tiles, s->d_seeds, dl, (int)T, S, m};
-            k_seed_init<<<blocks(T * 32, WARPS_PER_CTA * 32), WARPS_PER_CTA * 32, 0, st>>>(sa);
+    if (fp32 && (rc = filter32_setup())) return rc;
+
+    const bool dumping = getenv("VLMP_DUMP_PRM") || getenv("VLMP_DUMP_RUNS");
+    // a CUDA graph of the whole sequence (VLMP_GRAPH=0 / dumping: plain stream launches). Inside
+    // the graph, kernel times come from device-clock spans, not events (an event node between
+    // kernels serialises the graph at every length: +12 ms per config-2 pass, measured)
+    const bool use_graph = !dumping && !(getenv("VLMP_GRAPH") && atoi(getenv("VLMP_GRAPH")) == 0);
+    // counters of the launch sequence (host bookkeeping only)
+    double executed = 0, launches = 0, n_filtered = 0, n_full = 0, klaunch = 2, n_walk = 0;
+    std::vector<int> timed;   // lengths whose tile pass ran (event pairs)
+    std::vector<int> walked;  // lengths whose FP32 walk ran (k_tile32 / k_runs events)
+    // The whole per-length sequence is pure stream work (no host decisions between lengths), so
+    // it is captured once into a CUDA graph and re-launched while the key below is unchanged:
+    // ~6 launches per length become one graph launch (no per-launch host cost in the step).
+    auto enqueue = [&]() -> int {
+        int rc2;
+        k_fill_acc<<<blocks((long long)n_len * A, 256), 256, 0, st>>>(s->d_acc, (long long)n_len * A);
+        CU(cudaMemsetAsync(s->d_counters, 0, 8 * sizeof(unsigned long long), st));
+        CU(cudaMemsetAsync(s->d_fixcnt, 0, n_len * sizeof(unsigned long long), st));
+        CU(cudaMemsetAsync(s->d_logcnt, 0, n_len * sizeof(unsigned long long), st));
+        CU(cudaMemsetAsync(s->d_forced, 0, n_len * sizeof(int), st));
+        k_span_init<<<blocks(n_len, 128), 128, 0, st>>>(s->d_span, n_len);
+        if (li_lo > 0 && li_lo <= li_hi && T) {
+            if (fp32) {
+                // a later length shard on the FP32 walk: the seeds only start the walk (its slack
+                // covers their rounding; keys come from the exact runs), so they are direct sums at
+                // the shard's first length -- no carry through the lengths before it
+                const int m0 = lmin + li_lo;
+                ParamArgs pa{s->d_tn, s->d_cum, s->d_cum2, s->d_prm, s->d_mu, n, n - m0 + 1, A, m0, s->floor_};
+                k_params<<<blocks(A, 256), 256, 0, st>>>(pa);
+                SeedArgs sa{s->d_tn, s->d_mu, s->d_tiles, s->d_seeds, dl, (int)T, S, m0};
+                k_seed_init<<<blocks(T * 32, WARPS_PER_CTA * 32), WARPS_PER_CTA * 32, 0, st>>>(sa);
+                klaunch += 2;
+            } else {
+                // FP64 walk: seeds at lmin (direct sums), carried to the shard's first length with
+                // the tile kernel's own Welford step (bit-identical to the single-GPU chain)
+                ParamArgs pa{s->d_tn, s->d_cum, s->d_cum2, s->d_prm, s->d_mu, n, n - lmin + 1, A, lmin, s->floor_};
+                k_params<<<blocks(A, 256), 256, 0, st>>>(pa);
+                SeedArgs sa{s->d_tn, s->d_mu, s->d_tiles, s->d_seeds, dl, (int)T, S, lmin};
+                k_seed_init<<<blocks(T * 32, WARPS_PER_CTA * 32), WARPS_PER_CTA * 32, 0, st>>>(sa);
+                k_seed_forward<<<blocks(T * 32, 128), 128, 0, st>>>(sa, s->d_cum, lmin + li_lo);
+                klaunch += 3;
+            }
+        }
+        for (int li = (li_lo <= li_hi ? li_lo : 0); li <= li_hi; ++li) {
+            const int m = lmin + li;
+            const long long N = n - m + 1;
+            const int e = (m + 1) / 2;
+            // window parameters ping-pong between two buffers: the bound reads length m-1's
+            Prm* prm = (li & 1) ? s->d_prm2 : s->d_prm;
+            double* mu = (li & 1) ? s->d_mu2 : s->d_mu;
+            const Prm* prm_prev = (li & 1) ? s->d_prm : s->d_prm2;
+            const double* mu_prev = (li & 1) ? s->d_mu : s->d_mu2;
+            ParamArgs pa{s->d_tn, s->d_cum, s->d_cum2, prm, mu, n, N, A, m, s->floor_};
+            k_params<<<blocks(A, 256), 256, 0, st>>>(pa);
             ++klaunch;
-        }
-        if (!full) {
-            Bound2Args ba{s->d_tn, prm, prm_prev, mu_prev, mu, s->d_acc + (long long)(li - 1) * A, prm,
-                          N, N + 1, m, e, margin, s->d_fixcnt + li, fp32 ? 1 : 0};
-            k_bound2<<<blocks(N, 256), 256, 0, st>>>(ba);
-            if (!fp32)
-                k_qprep<<<blocks(A, 256), 256, 0, st>>>(prm, s->d_colq, s->d_rowq, N, A, s->sscale,
-                                                        s->d_forced + li);
-            klaunch += 2;
-        }
-        while (s->lev.size() < (size_t)2 * (li + 1)) {
-            cudaEvent_t ev; CU(cudaEventCreate(&ev)); s->lev.push_back(ev);
-        }
-        timed.push_back(li);
-        CU(cudaEventRecord(s->lev[2 * li], st));
-        if (T) {
-            TileArgs ta{prm, mu, s->d_tn, s->d_tiles, s->d_seeds, s->d_acc + (long long)li * A,
-                        s->d_counters, s->d_log, s->d_logcnt + li, eff_cap,
-                        N, dl, (int)T, S, m, e, li + 1 <= li_hi,
-                        s->d_colq, s->d_rowq, s->d_forced + li, s->hiC};
-            if (full && li == li_lo && bound_start && Ts) {
-                // sampled full folds (seeds untouched) -> bounds -> filtered pass over all bands
-                TileArgs tsa = ta;
-                tsa.tiles = s->d_tiles_s; tsa.n_tiles = (int)Ts; tsa.seed_map = s->d_smap; tsa.update_seeds = 0;
-                k_tile<true><<<blocks(Ts, WARPS_PER_CTA), WARPS_PER_CTA * 32, smem, st>>>(tsa);
-                k_bound_self<<<blocks(N, 256), 256, 0, st>>>(s->d_acc + (long long)li * A, prm, N, margin,
-                                                             s->d_tn, mu, m, fp32 ? 1 : 0);
-                if (fp32) {
-                    // the sampled folds only bound this length; its keys come from the exact runs
-                    k_fill_acc<<<blocks(A, 256), 256, 0, st>>>(s->d_acc + (long long)li * A, A);
-                    if ((rc = launch_filter32(s, st, prm, mu, N, m, e, dl, S, ta.update_seeds, T32,
-                                              s->d_forced + li, s->d_acc + (long long)li * A, runs,
-                                              s->d_logcnt + li, run_cap))) return rc;
-                    klaunch += 5;
-                } else {
+            const bool full = (li == li_lo) || (flags & VLMP_F_FULL_EVERY_LENGTH);
+            if (li == 0 && T) {
+                SeedArgs sa{s->d_tn, mu, s->d_tiles, s->d_seeds, dl, (int)T, S, m};
+                k_seed_init<<<blocks(T * 32, WARPS_PER_CTA * 32), WARPS_PER_CTA * 32, 0, st>>>(sa);
+                ++klaunch;
+            }
+            if (!full) {
+                Bound2Args ba{s->d_tn, prm, prm_prev, mu_prev, mu, s->d_acc + (long long)(li - 1) * A, prm,
+                              N, N + 1, m, e, margin, s->d_fixcnt + li, fp32 ? 1 : 0};
+                k_bound2<<<blocks(N, 256), 256, 0, st>>>(ba);
+                if (!fp32)
                     k_qprep<<<blocks(A, 256), 256, 0, st>>>(prm, s->d_colq, s->d_rowq, N, A, s->sscale,
                                                             s->d_forced + li);
+                klaunch += 2;
+            }
+            timed.push_back(li);
+            if (!use_graph) CU(cudaEventRecord(s->lev[2 * li], st));
+            unsigned long long* span = s->d_span + 4 * li;
+            if (T) {
+                TileArgs ta{prm, mu, s->d_tn, s->d_tiles, s->d_seeds, s->d_acc + (long long)li * A,
+                            s->d_counters, s->d_log, s->d_logcnt + li, eff_cap,
+                            N, dl, (int)T, S, m, e, li + 1 <= li_hi,
+                            s->d_colq, s->d_rowq, s->d_forced + li, s->hiC};
+                if (full && li == li_lo && bound_start && Ts) {
+                    // sampled full folds (seeds untouched) -> bounds -> filtered pass over all bands
+                    TileArgs tsa = ta;
+                    tsa.tiles = s->d_tiles_s; tsa.n_tiles = (int)Ts; tsa.seed_map = s->d_smap; tsa.update_seeds = 0;
+                    k_tile<true><<<blocks(Ts, WARPS_PER_CTA), WARPS_PER_CTA * 32, smem, st>>>(tsa);
+                    k_bound_self<<<blocks(N, 256), 256, 0, st>>>(s->d_acc + (long long)li * A, prm, N, margin,
+                                                                 s->d_tn, mu, m, fp32 ? 1 : 0);
+                    if (fp32) {
+                        // the sampled folds only bound this length; its keys come from the exact runs
+                        k_fill_acc<<<blocks(A, 256), 256, 0, st>>>(s->d_acc + (long long)li * A, A);
+                        if ((rc2 = launch_filter32(s, st, prm, mu, N, m, e, dl, S, ta.update_seeds, T32,
+                                                   s->d_forced + li, s->d_acc + (long long)li * A, runs,
+                                                   s->d_logcnt + li, run_cap, nullptr, nullptr, span))) return rc2;
+                        klaunch += 5; n_walk += 1; walked.push_back(li);
+                    } else {
+                        k_qprep<<<blocks(A, 256), 256, 0, st>>>(prm, s->d_colq, s->d_rowq, N, A, s->sscale,
+                                                                s->d_forced + li);
+                        k_tile<false><<<blocks(T, WARPS_PER_CTA), WARPS_PER_CTA * 32, smem, st>>>(ta);
+                        k_log_merge<<<148 * 8, 256, 0, st>>>(s->d_log, s->d_logcnt + li, eff_cap,
+                                                             prm, e, s->d_acc + (long long)li * A, s->d_counters);
+                        klaunch += 4;
+                    }
+                } else if (full) k_tile<true><<<blocks(T, WARPS_PER_CTA), WARPS_PER_CTA * 32, smem, st>>>(ta);
+                else if (fp32) {
+                    if ((rc2 = launch_filter32(s, st, prm, mu, N, m, e, dl, S, ta.update_seeds, T32, s->d_forced + li,
+                                               s->d_acc + (long long)li * A, runs, s->d_logcnt + li, run_cap,
+                                               nullptr, nullptr, span)))
+                        return rc2;
+                    klaunch += 2; n_walk += 1; walked.push_back(li);
+                    if (dumping && (rc2 = debug_dump(st, li, prm, N, runs, s->d_logcnt + li, run_cap))) return rc2;
+                } else {
                     k_tile<false><<<blocks(T, WARPS_PER_CTA), WARPS_PER_CTA * 32, smem, st>>>(ta);
                     k_log_merge<<<148 * 8, 256, 0, st>>>(s->d_log, s->d_logcnt + li, eff_cap,
                                                          prm, e, s->d_acc + (long long)li * A, s->d_counters);
-                    klaunch += 4;
+                    klaunch += 1;
                 }
-            } else if (full) k_tile<true><<<blocks(T, WARPS_PER_CTA), WARPS_PER_CTA * 32, smem, st>>>(ta);
-            else if (fp32) {
-                if ((rc = launch_filter32(s, st, prm, mu, N, m, e, dl, S, ta.update_seeds, T32, s->d_forced + li,
-                                          s->d_acc + (long long)li * A, runs, s->d_logcnt + li, run_cap)))
-                    return rc;
-                klaunch += 2;
-                if ((rc = debug_dump(st, li, prm, N, runs, s->d_logcnt + li, run_cap))) return rc;
-            } else {
-                k_tile<false><<<blocks(T, WARPS_PER_CTA), WARPS_PER_CTA * 32, smem, st>>>(ta);
-                k_log_merge<<<148 * 8, 256, 0, st>>>(s->d_log, s->d_logcnt + li, eff_cap,
-                                                     prm, e, s->d_acc + (long long)li * A, s->d_counters);
-                klaunch += 1;
+                launches += 1; klaunch += 1;
             }
-            launches += 1; klaunch += 1;
+            if (!use_graph) CU(cudaEventRecord(s->lev[2 * li + 1], st));
+            CU(cudaGetLastError());
+            for (long long b = band_lo; b < band_hi; ++b) {
+                long long d0 = dl + b * BAND;
+                long long rows = N - d0;
+                if (rows <= 0 || d0 + BAND - 1 < e) continue;
+                executed += (double)rows * BAND;
+            }
+            if (full) n_full += 1; else n_filtered += 1;
         }
-        CU(cudaEventRecord(s->lev[2 * li + 1], st));
-        CU(cudaGetLastError());
-        for (long long b = band_lo; b < band_hi; ++b) {
-            long long d0 = dl + b * BAND;
-            long long rows = N - d0;
-            if (rows <= 0 || d0 + BAND - 1 < e) continue;
-            executed += (double)rows * BAND;
+        return 0;
+    };
+    CU(cudaEventRecord(s->ev[0], st));
+    if (use_graph) {
+        // everything the captured launches bake in: shape, mode, buffers, series scalars
+        std::vector<double> key = {(double)n, (double)A, (double)lmin, (double)lmax, (double)band_lo, (double)band_hi,
+                                   (double)flags, (double)li_lo, (double)li_hi, (double)T, (double)Ts, (double)T32,
+                                   (double)S, (double)eff_cap, (double)run_cap, s->sscale, s->floor_,
+                                   (double)s->hiC, (double)bound_start, (double)fp32};
+        for (const void* ptr : {(const void*)s->d_acc, (const void*)s->d_tn, (const void*)s->d_cum, (const void*)s->d_cum2,
+                                (const void*)s->d_prm, (const void*)s->d_prm2, (const void*)s->d_mu, (const void*)s->d_mu2,
+                                (const void*)s->d_tiles, (const void*)s->d_tiles_s, (const void*)s->d_smap,
+                                (const void*)s->d_seeds, (const void*)s->d_log, (const void*)s->d_logcnt,
+                                (const void*)s->d_forced, (const void*)s->d_fixcnt, (const void*)s->d_tiles32,
+                                (const void*)s->d_p32, (const void*)s->d_cq32, (const void*)s->d_cq4, (const void*)s->d_pf4,
+                                (const void*)s->d_magblk, (const void*)s->d_colq, (const void*)s->d_rowq})
+            key.push_back((double)(uintptr_t)ptr);
+        if (!s->g_exec || key != s->g_key) {
+            if (s->g_exec) { cudaGraphExecDestroy(s->g_exec); s->g_exec = nullptr; }
+            s->g_key.clear();
+            CU(cudaStreamBeginCapture(st, cudaStreamCaptureModeRelaxed));
+            const int rc_cap = enqueue();
+            cudaGraph_t g = nullptr;
+            const cudaError_t ec = cudaStreamEndCapture(st, &g);
+            if (rc_cap) { if (g) cudaGraphDestroy(g); return rc_cap; }
+            if (ec != cudaSuccess) return fail(VLMP_E_CUDA, std::string("graph capture: ") + cudaGetErrorString(ec));
+            const cudaError_t ei = cudaGraphInstantiate(&s->g_exec, g, 0);
+            cudaGraphDestroy(g);
+            if (ei != cudaSuccess) { s->g_exec = nullptr; return fail(VLMP_E_CUDA, std::string("graph instantiate: ") + cudaGetErrorString(ei)); }
+            s->g_key = key;
+            s->g_cnt = {executed, launches, n_filtered, n_full, klaunch, n_walk};
+            s->g_timed = timed; s->g_walked = walked;
+        } else {
+            // the cached sequence: its host-side counters are those of the capture
+            executed = s->g_cnt[0]; launches = s->g_cnt[1]; n_filtered = s->g_cnt[2]; n_full = s->g_cnt[3];
+            klaunch = s->g_cnt[4]; n_walk = s->g_cnt[5]; timed = s->g_timed; walked = s->g_walked;
         }
-        if (full) n_full += 1; else n_filtered += 1;
-    }
+        CU(cudaGraphLaunch(s->g_exec, st));
+    } else if ((rc = enqueue())) return rc;
     CU(cudaEventRecord(s->ev[1], st));
-    CU(cudaEventSynchronize(s->ev[1]));
-    double first_ms = 0;
-    for (int li : timed) {
-        float lm = 0; CU(cudaEventElapsedTime(&lm, s->lev[2 * li], s->lev[2 * li + 1]));
-        tile_ms += lm;
-        if (li == li_lo) first_ms = lm;
-    }
-    float ms = 0; CU(cudaEventElapsedTime(&ms, s->ev[0], s->ev[1]));
-    unsigned long long cnt[8];
-    CU(cudaMemcpy(cnt, s->d_counters, sizeof(cnt), cudaMemcpyDeviceToHost));
-    bool overflow = false;
-    double max_log = 0;
-    {   // a candidate log that overflowed lost candidates: the caller redoes the run exactly
-        std::vector<unsigned long long> lc(n_len);
-        CU(cudaMemcpy(lc.data(), s->d_logcnt, n_len * sizeof(unsigned long long), cudaMemcpyDeviceToHost));
-        const long long cap_used = fp32 ? run_cap : eff_cap;
-        for (auto c : lc) { overflow |= (long long)c > cap_used; max_log = std::max(max_log, (double)c); }
-    }
-    int n_forced = 0;
-    double n_fix = 0;
+    CU(cudaMemcpyAsync(s->h_span, s->d_span, (size_t)4 * n_len * sizeof(unsigned long long), cudaMemcpyDeviceToHost, st));
+    // the overflow check's inputs, copied behind the sequence (pinned: truly asynchronous)
     {
-        std::vector<int> fl(n_len);
-        CU(cudaMemcpy(fl.data(), s->d_forced, n_len * sizeof(int), cudaMemcpyDeviceToHost));
-        for (int f : fl) n_forced += f != 0;
-        std::vector<unsigned long long> fx(n_len);
-        CU(cudaMemcpy(fx.data(), s->d_fixcnt, n_len * sizeof(unsigned long long), cudaMemcpyDeviceToHost));
-        for (auto f : fx) n_fix += (double)f;
+        const size_t need = 8 + 3 * (size_t)n_len;
+        if (need > s->h_chk_cap) {
+            if (s->h_chk) cudaFreeHost(s->h_chk);
+            s->h_chk = nullptr; s->h_chk_cap = 0;
+            CU(cudaMallocHost((void**)&s->h_chk, need * sizeof(unsigned long long)));
+            s->h_chk_cap = need;
+        }
+        unsigned long long* h = s->h_chk;
+        CU(cudaMemcpyAsync(h, s->d_counters, 8 * sizeof(unsigned long long), cudaMemcpyDeviceToHost, st));
+        CU(cudaMemcpyAsync(h + 8, s->d_logcnt, n_len * sizeof(unsigned long long), cudaMemcpyDeviceToHost, st));
+        CU(cudaMemcpyAsync(h + 8 + n_len, s->d_fixcnt, n_len * sizeof(unsigned long long), cudaMemcpyDeviceToHost, st));
+        CU(cudaMemcpyAsync(h + 8 + 2 * n_len, s->d_forced, n_len * sizeof(int), cudaMemcpyDeviceToHost, st));
     }
-    double W = 0;
-    for (int m = lmin; m <= lmax; ++m) {
-        long long k = (n - m + 1) - (m + 1) / 2;
-        if (k > 0) W += (double)k * (double)(k + 1) / 2.0;
-    }
+    CU(cudaGetLastError());
+    PendingRun& pr = s->prun;
+    pr = PendingRun{};
+    pr.lmin = lmin; pr.lmax = lmax; pr.band_lo = band_lo; pr.band_hi = band_hi; pr.flags = flags;
+    pr.li_lo = li_lo; pr.li_hi = li_hi; pr.fp32 = fp32; pr.sampled = sampled_start;
+    pr.cap_used = fp32 ? run_cap : eff_cap; pr.S = S;
+    pr.executed = executed; pr.launches = launches; pr.n_filtered = n_filtered; pr.n_full = n_full;
+    pr.klaunch = klaunch; pr.graph = use_graph; pr.timed = timed; pr.walked = walked;
     s->lmin = lmin; s->lmax = lmax; s->n_len = n_len;
     s->have_profile = true; s->have_final = false; s->have_finals = false;
-    memset(s->stats, 0, sizeof(s->stats));
-    s->stats[0] = ms; s->stats[2] = executed; s->stats[3] = W; s->stats[4] = tile_ms;
-    s->stats[5] = launches; s->stats[6] = n_filtered; s->stats[7] = n_full; s->stats[8] = (double)cnt[0];
-    s->stats[9] = klaunch; s->stats[10] = first_ms; s->stats[11] = (double)cnt[2];
-    s->stats[12] = n_fix; s->stats[14] = n_forced; s->stats[15] = max_log;
-    s->stats[16] = fp32 ? 1.0 : 0.0; s->stats[17] = fp32 ? max_log : 0.0; s->stats[18] = (double)cnt[4];
-    s->stats[19] = (double)S;
-    *overflow_out = overflow;
-    // a lost run log: the caller re-runs the whole set on the FP64 filter path
-    if (fp32_fallback) *fp32_fallback = fp32 && overflow;
+    s->pending = true; s->stats_dirty = true;
     return 0;
 }
 
-// A candidate log that overflowed lost candidates: redo the run exactly -- first without the
-// sampled start (its bounds are the loosest), then with full folds at every length.
-static int profile_retrying(vlmp_session* s, int32_t lmin, int32_t lmax, int64_t band_lo, int64_t band_hi,
-                            uint32_t flags, int li_lo, int li_hi) {
-    bool overflow = false, sampled = false, fb = false;
-    int rc = profile_impl(s, lmin, lmax, band_lo, band_hi, flags, &overflow, &sampled, li_lo, li_hi, &fb);
-    if (rc == 0 && fb) {
-        flags |= VLMP_F_FP64_FILTER;
-        rc = profile_impl(s, lmin, lmax, band_lo, band_hi, flags, &overflow, &sampled, li_lo, li_hi);
-        s->stats[13] = 3;
+}  // extern "C" (reopened below)
+
+namespace vlmp_impl {
+
+// Device-event timings of the last run (lazily: only vlmp_stats needs them).
+int fill_event_stats(vlmp_session* s) {
+    if (!s->stats_dirty) return 0;
+    const PendingRun& pr = s->prun;
+    double first_ms = 0, tile_ms = 0, walk_ms = 0, runs_ms = 0;
+    for (int li : pr.walked) {
+        const unsigned long long* sp = s->h_span + 4 * li;
+        if (sp[1] > sp[0]) walk_ms += (double)(sp[1] - sp[0]) * 1e-6;
+        if (sp[3] > sp[2]) runs_ms += (double)(sp[3] - sp[2]) * 1e-6;
     }
-    if (rc == 0 && overflow && sampled) {
-        rc = profile_impl(s, lmin, lmax, band_lo, band_hi, flags | F_NO_SAMPLED_START, &overflow, &sampled,
-                          li_lo, li_hi);
-        s->stats[13] = 1;
+    if (!pr.graph) {
+        for (int li : pr.timed) {
+            float lm = 0; CU(cudaEventElapsedTime(&lm, s->lev[2 * li], s->lev[2 * li + 1]));
+            tile_ms += lm;
+            if (li == pr.li_lo) first_ms = lm;
+        }
+    } else {
+        tile_ms = walk_ms + runs_ms;   // the graph carries no per-length events
     }
-    if (rc == 0 && overflow) {
-        rc = profile_impl(s, lmin, lmax, band_lo, band_hi, flags | VLMP_F_FULL_EVERY_LENGTH, &overflow, &sampled,
-                          li_lo, li_hi);
-        s->stats[13] = 2;
-    }
-    return rc;
+    float ms = 0; CU(cudaEventElapsedTime(&ms, s->ev[0], s->ev[1]));
+    s->stats[0] = ms; s->stats[4] = tile_ms; s->stats[10] = first_ms;
+    s->stats[20] = walk_ms; s->stats[21] = runs_ms;
+    if (s->have_finals) { float fm = 0; if (cudaEventElapsedTime(&fm, s->ev[4], s->ev[5]) == cudaSuccess) s->stats[1] = fm; }
+    s->stats_dirty = false;
+    return 0;
 }
+
+// Wait for the pending phase 1, check its logs and, when one overflowed (it lost candidates),
+// redo the run exactly: the FP32 walk's overflow on the FP64 filter path, then without the
+// sampled first-length start (its bounds are the loosest), then with full folds everywhere.
+// *redone tells a caller that already enqueued phase-2 work on the lost run to enqueue it again.
+int settle_profile(vlmp_session* s, bool* redone) {
+    int code = 0;
+    while (s->pending) {
+        CU(cudaStreamSynchronize(s->stream));
+        s->pending = false;
+        const PendingRun pr = s->prun;
+        const int n_len = pr.lmax - pr.lmin + 1;
+        const unsigned long long* h = s->h_chk;
+        bool overflow = false;
+        double max_log = 0, n_fix = 0;
+        int n_forced = 0;
+        for (int li = 0; li < n_len; ++li) {
+            overflow |= (long long)h[8 + li] > pr.cap_used;
+            max_log = std::max(max_log, (double)h[8 + li]);
+            n_fix += (double)h[8 + n_len + li];
+            n_forced += reinterpret_cast<const int*>(h + 8 + 2 * n_len)[li] != 0;
+        }
+        double W = 0;
+        for (int m = pr.lmin; m <= pr.lmax; ++m) {
+            long long k = (s->n - m + 1) - (m + 1) / 2;
+            if (k > 0) W += (double)k * (double)(k + 1) / 2.0;
+        }
+        memset(s->stats, 0, sizeof(s->stats));
+        s->stats[2] = pr.executed; s->stats[3] = W;
+        s->stats[5] = pr.launches; s->stats[6] = pr.n_filtered; s->stats[7] = pr.n_full; s->stats[8] = (double)h[0];
+        s->stats[9] = pr.klaunch; s->stats[11] = (double)h[2];
+        s->stats[12] = n_fix; s->stats[14] = n_forced; s->stats[15] = max_log;
+        s->stats[16] = pr.fp32 ? 1.0 : 0.0; s->stats[17] = pr.fp32 ? max_log : 0.0; s->stats[18] = (double)h[4];
+        s->stats[19] = (double)pr.S; s->stats[22] = (double)pr.walked.size(); s->stats[23] = pr.graph ? 1.0 : 0.0;
+        s->stats_dirty = true;
+        if (!overflow) break;
+        if (redone) *redone = true;
+        uint32_t f = pr.flags;
+        if (pr.fp32) { f |= VLMP_F_FP64_FILTER; code = 3; }
+        else if (pr.sampled) { f |= F_NO_SAMPLED_START; code = 1; }
+        else if (!(f & VLMP_F_FULL_EVERY_LENGTH)) { f |= VLMP_F_FULL_EVERY_LENGTH; code = 2; }
+        else return fail(VLMP_E_CUDA, "candidate log overflow with full folds");
+        int rc = profile_impl(s, pr.lmin, pr.lmax, pr.band_lo, pr.band_hi, f, pr.li_lo, pr.li_hi);
+        if (rc) return rc;
+    }
+    if (code) s->stats[13] = code;
+    return 0;
+}
+
+}  // namespace vlmp_impl
+
+extern "C" {
 
 int vlmp_profile_range(vlmp_session* s, int32_t lmin, int32_t lmax, int64_t band_lo,
                        int64_t band_hi, uint32_t flags) {
@@ -1408,7 +1518,7 @@ int vlmp_profile_range(vlmp_session* s, int32_t lmin, int32_t lmax, int64_t band
     if (s->n < (long long)lmax + (lmax + 1) / 2)
         return fail(VLMP_E_SERIES_TOO_SHORT, "series cannot host a non-trivial pair at lmax");
     std::lock_guard<std::mutex> g(s->lock);
-    return profile_retrying(s, lmin, lmax, band_lo, band_hi, flags, 0, -1);
+    return profile_impl(s, lmin, lmax, band_lo, band_hi, flags, 0, -1);
 }
 
 int vlmp_profile_lengths(vlmp_session* s, int32_t lmin, int32_t lmax, int32_t li_lo, int32_t li_hi,
@@ -1423,7 +1533,7 @@ int vlmp_profile_lengths(vlmp_session* s, int32_t lmin, int32_t lmax, int32_t li
         return fail(VLMP_E_SERIES_TOO_SHORT, "series cannot host a non-trivial pair at lmax");
     std::lock_guard<std::mutex> g(s->lock);
     if (li_hi < li_lo) { li_lo = lmax - lmin + 1; li_hi = -1; }   // empty shard: setup only
-    return profile_retrying(s, lmin, lmax, 0, -1, flags, li_lo, li_hi);
+    return profile_impl(s, lmin, lmax, 0, -1, flags, li_lo, li_hi);
 }
 
 int vlmp_partials_size(vlmp_session* s, int64_t* n_len, int64_t* stride) {
@@ -1435,6 +1545,7 @@ int vlmp_partials_size(vlmp_session* s, int64_t* n_len, int64_t* stride) {
 int vlmp_partials_export(vlmp_session* s, void* keys, void* idx) {
     if (!s || !s->have_profile) return fail(VLMP_E_STATE, "no profile run");
     std::lock_guard<std::mutex> g(s->lock);
+    { const int rc = settle_profile(s, nullptr); if (rc) return rc; }
     CU(cudaSetDevice(s->device));
     const long long total = (long long)s->n_len * s->A;
     k_export<<<blocks(total, 256), 256, 0, s->stream>>>(s->d_acc, (unsigned long long*)keys, (long long*)idx, total);
@@ -1446,6 +1557,7 @@ int vlmp_partials_export(vlmp_session* s, void* keys, void* idx) {
 int vlmp_partials_mask_idx(vlmp_session* s, const void* merged_keys, const void* keys, void* idx) {
     if (!s || !s->have_profile) return fail(VLMP_E_STATE, "no profile run");
     std::lock_guard<std::mutex> g(s->lock);
+    { const int rc = settle_profile(s, nullptr); if (rc) return rc; }
     CU(cudaSetDevice(s->device));
     const long long total = (long long)s->n_len * s->A;
     k_mask_idx<<<blocks(total, 256), 256, 0, s->stream>>>((const unsigned long long*)merged_keys,
@@ -1458,6 +1570,7 @@ int vlmp_partials_mask_idx(vlmp_session* s, const void* merged_keys, const void*
 int vlmp_partials_import(vlmp_session* s, const void* keys, const void* idx) {
     if (!s || !s->have_profile) return fail(VLMP_E_STATE, "no profile run");
     std::lock_guard<std::mutex> g(s->lock);
+    { const int rc = settle_profile(s, nullptr); if (rc) return rc; }
     CU(cudaSetDevice(s->device));
     const long long total = (long long)s->n_len * s->A;
     k_import<<<blocks(total, 256), 256, 0, s->stream>>>(s->d_acc, (const unsigned long long*)keys, (const long long*)idx, total);
@@ -1475,6 +1588,15 @@ int vlmp_profile_mbest(vlmp_session* s, int32_t lmin, int32_t lmax, int32_t mb) 
     if (s->n < (long long)lmax + (lmax + 1) / 2)
         return fail(VLMP_E_SERIES_TOO_SHORT, "series cannot host a non-trivial pair at lmax");
     std::lock_guard<std::mutex> g(s->lock);
+    return mbest_impl(s, lmin, lmax, mb);
+}
+
+}  // extern "C" (reopened below)
+
+namespace vlmp_impl {
+// the m-best profile run (caller holds the session lock): d_ipm / d_mpm of [lmin, lmax]
+int mbest_impl(vlmp_session* s, int32_t lmin, int32_t lmax, int32_t mb) {
+    { const int rc0 = settle_profile(s, nullptr); if (rc0) return rc0; }
     CU(cudaSetDevice(s->device));
     cudaStream_t st = s->stream;
     const long long n = s->n, A = s->A;
@@ -1489,6 +1611,10 @@ int vlmp_profile_mbest(vlmp_session* s, int32_t lmin, int32_t lmax, int32_t mb) 
     }
     order_tiles(tiles, N0, dl, S);
     const long long T = (long long)tiles.size();
+    // the tile buffers below are overwritten with this run's all-band list: the cached 1-best
+    // tile lists (profile_impl's tc_key) and any earlier m-best result are void from here on
+    s->tc_key[0] = -1;
+    s->mbest = 0; s->mb_lmin = s->mb_n_len = 0; s->mb_A = 0;
     int rc;
     if ((rc = ensure(s->d_tiles, s->tiles_cap, (size_t)std::max<long long>(T, 1)))) return rc;
     if ((rc = ensure(s->d_seeds, s->seeds_cap, (size_t)std::max<long long>(T, 1) * BAND))) return rc;
@@ -1598,20 +1724,26 @@ int vlmp_profile_mbest(vlmp_session* s, int32_t lmin, int32_t lmax, int32_t mb) 
     CU(cudaGetLastError());
     CU(cudaStreamSynchronize(st));
     s->lmin = lmin; s->lmax = lmax; s->n_len = n_len; s->mbest = mb;
+    s->mb_lmin = lmin; s->mb_n_len = n_len; s->mb_A = A; s->mb_n = n;
     s->have_profile = false; s->have_final = false; s->have_finals = false;
     memset(s->stats, 0, sizeof(s->stats));
     s->stats[0] = ms; s->stats[13] = (double)redo_total;
     return 0;
 }
+}  // namespace vlmp_impl
+
+extern "C" {
 
 int vlmp_get_profile_m(vlmp_session* s, int32_t length, double* dist, int64_t* nbr) {
-    if (!s || s->mbest < 1 || !s->d_mpm) return fail(VLMP_E_STATE, "no m-best run");
-    if (length < s->lmin || length > s->lmax) return fail(VLMP_E_INVALID_PARAMETERS, "length outside the run");
+    if (!s || s->mbest < 1 || !s->d_mpm || s->mb_A != s->A || s->mb_n != s->n)
+        return fail(VLMP_E_STATE, "no m-best run for the current series");
+    if (length < s->mb_lmin || length >= s->mb_lmin + s->mb_n_len)
+        return fail(VLMP_E_INVALID_PARAMETERS, "length outside the run");
     std::lock_guard<std::mutex> g(s->lock);
     CU(cudaSetDevice(s->device));
     const int mb = s->mbest;
     const long long N = s->n - length + 1;
-    const long long off = (long long)(length - s->lmin) * s->A * mb;
+    const long long off = (long long)(length - s->mb_lmin) * s->A * mb;
     std::vector<int> tmp(N * mb);
     CU(cudaMemcpyAsync(dist, s->d_mpm + off, N * mb * 8, cudaMemcpyDeviceToHost, s->stream));
     CU(cudaMemcpyAsync(tmp.data(), s->d_ipm + off, N * mb * 4, cudaMemcpyDeviceToHost, s->stream));
@@ -1621,20 +1753,21 @@ int vlmp_get_profile_m(vlmp_session* s, int32_t length, double* dist, int64_t* n
 }
 
 int vlmp_discords_m(vlmp_session* s, int32_t k, double* out_dist, int64_t* out_off) {
-    if (!s || !s->d_mpm) return fail(VLMP_E_STATE, "no m-best run");
+    if (!s || s->mbest < 1 || !s->d_mpm || s->mb_A != s->A || s->mb_n != s->n)
+        return fail(VLMP_E_STATE, "no m-best run for the current series");
     if (k < 1 || k > 32) return fail(VLMP_E_INVALID_PARAMETERS, "k must be in [1, 32]");
     const int mb = s->mbest;
     if (k * mb > 32 * MB_MAX) return fail(VLMP_E_INVALID_PARAMETERS, "k*m too large");
     std::lock_guard<std::mutex> g(s->lock);
     CU(cudaSetDevice(s->device));
-    const long long cnt = (long long)s->n_len * k * mb;
+    const long long cnt = (long long)s->mb_n_len * k * mb;
     int rc;
     if ((rc = ensure(s->d_ro_i64, s->ro_i64_cap, (size_t)cnt))) return rc;
     if ((rc = ensure(s->d_ro_f64, s->ro_f64_cap, (size_t)cnt))) return rc;
     const int wpb = 4;
     const size_t sm = (size_t)wpb * 32 * MB_MAX * 16;
-    k_discords_m<<<blocks((long long)s->n_len * 32, wpb * 32), wpb * 32, sm, s->stream>>>(
-        s->d_mpm, s->d_ro_f64, s->d_ro_i64, s->n, s->A, s->lmin, s->n_len, k, mb);
+    k_discords_m<<<blocks((long long)s->mb_n_len * 32, wpb * 32), wpb * 32, sm, s->stream>>>(
+        s->d_mpm, s->d_ro_f64, s->d_ro_i64, s->n, s->A, s->mb_lmin, s->mb_n_len, k, mb);
     CU(cudaGetLastError());
     CU(cudaMemcpyAsync(out_dist, s->d_ro_f64, cnt * 8, cudaMemcpyDeviceToHost, s->stream));
     CU(cudaMemcpyAsync(out_off, s->d_ro_i64, cnt * 8, cudaMemcpyDeviceToHost, s->stream));

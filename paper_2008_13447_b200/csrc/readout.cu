@@ -291,7 +291,28 @@ __global__ void k_events(EvArgs a) {
 
 extern "C" {
 
+static int finalize_enqueue(vlmp_session* s, int li_lo, int li_hi, bool readoffs);
+
 static int finalize_impl(vlmp_session* s, int li_lo, int li_hi, bool readoffs) {
+    CU(cudaSetDevice(s->device));
+    // phase 2 is enqueued behind a still-unchecked phase 1 (no host sync between them); if the
+    // check then redoes phase 1, phase 2 is enqueued again behind the redo
+    for (int attempt = 0; attempt < 2; ++attempt) {
+        int rc = finalize_enqueue(s, li_lo, li_hi, readoffs);
+        if (rc) return rc;
+        bool redone = false;
+        if ((rc = settle_profile(s, &redone))) return rc;
+        if (!redone) break;
+    }
+    CU(cudaEventSynchronize(s->ev[5]));
+    s->stats[9] += (li_lo <= li_hi ? 1 : 0) + (readoffs ? 1 : 0);
+    s->have_final = readoffs;
+    s->have_finals = true;
+    s->stats_dirty = true;
+    return 0;
+}
+
+static int finalize_enqueue(vlmp_session* s, int li_lo, int li_hi, bool readoffs) {
     CU(cudaSetDevice(s->device));
     cudaStream_t st = s->stream;
     const long long A = s->A, n = s->n;
@@ -317,20 +338,13 @@ static int finalize_impl(vlmp_session* s, int li_lo, int li_hi, bool readoffs) {
                    li_lo, li_hi};
         const unsigned chunks = (unsigned)std::min(8, std::max(1, s->n_len / 8));
         k_finalize_walk<<<dim3(blocks(n0, 64), chunks), 64, 0, st>>>(fa);
-        s->stats[9] += 1;
     }
     if (readoffs) {
         ValmpArgs va{s->d_mp, s->d_ip, s->d_vdist, s->d_vnorm, s->d_vlen, s->d_vidx, s->d_vpop, n, A, s->lmin, s->n_len};
         k_valmp<<<blocks(n0, 256), 256, 0, st>>>(va);
-        s->stats[9] += 1;
     }
     CU(cudaEventRecord(s->ev[5], st));
     CU(cudaGetLastError());
-    CU(cudaEventSynchronize(s->ev[5]));
-    float ms = 0; CU(cudaEventElapsedTime(&ms, s->ev[4], s->ev[5]));
-    s->stats[1] = ms;
-    s->have_final = readoffs;
-    s->have_finals = true;
     return 0;
 }
 

@@ -21,6 +21,31 @@ __global__ void k_dfma_peak(double* out, int iters, double x) {
     if (s == 12345.678) out[0] = s;
 }
 
+// FP32 FMA peak: 8 independent FFMA chains per thread (register operands, as the walk's FFMA2)
+__global__ void k_ffma_peak(float* out, int iters, float x) {
+    float a0 = x, a1 = x + 1, a2 = x + 2, a3 = x + 3, a4 = x + 4, a5 = x + 5, a6 = x + 6, a7 = x + 7;
+    const float b = 0.999999f + 1e-7f * threadIdx.x, c = 1e-9f * blockIdx.x;
+    for (int it = 0; it < iters; ++it) {
+#pragma unroll
+        for (int u = 0; u < 16; ++u) {
+            a0 = fmaf(a0, b, c); a1 = fmaf(a1, b, c); a2 = fmaf(a2, b, c); a3 = fmaf(a3, b, c);
+            a4 = fmaf(a4, b, c); a5 = fmaf(a5, b, c); a6 = fmaf(a6, b, c); a7 = fmaf(a7, b, c);
+        }
+    }
+    float s = a0 + a1 + a2 + a3 + a4 + a5 + a6 + a7;
+    if (s == 12345.678f) out[0] = s;
+}
+
+// window statistics of every offset at one length, with the device routine k_params and the
+// finalize use (win_stats: series.py:91-100 op order, no contraction) -- exported for the
+// bit-exactness test against DataSeries.moving_stats
+__global__ void k_win_stats(const double* cum, const double* cum2, long long N, int m, double* mu, double* sd) {
+    const long long o = blockIdx.x * (long long)blockDim.x + threadIdx.x;
+    if (o >= N) return;
+    double a, b;
+    win_stats(cum, cum2, o, m, a, b);
+    mu[o] = a; sd[o] = b;
+}
 
 }  // namespace vlmp_impl
 
@@ -59,6 +84,11 @@ void vlmp_destroy(vlmp_session* s) {
     for (void* p : ptrs) if (p) cudaFree(p);
     for (auto& ev : s->ev) if (ev) cudaEventDestroy(ev);
     for (auto& ev : s->lev) cudaEventDestroy(ev);
+    if (s->d_span) cudaFree(s->d_span);
+    if (s->h_span) cudaFreeHost(s->h_span);
+    if (s->g_exec) cudaGraphExecDestroy(s->g_exec);
+    if (s->h_chk) cudaFreeHost(s->h_chk);
+    pruned_free(s);
     if (s->stream) cudaStreamDestroy(s->stream);
     delete s;
 }
@@ -70,7 +100,12 @@ int vlmp_set_series(vlmp_session* s, const double* t, const double* cum, const d
     std::lock_guard<std::mutex> g(s->lock);
     CU(cudaSetDevice(s->device));
     long long A = ((n + 1024 + 255) / 256) * 256 + 256;
-    s->n = n; s->A = A; s->floor_ = sigma_floor;
+    // nothing of the previous series survives: the session reads as empty until every buffer
+    // below is allocated and filled (a failed allocation leaves n = 0, so later calls refuse)
+    if (s->pending) { cudaStreamSynchronize(s->stream); s->pending = false; }
+    s->n = 0; s->A = 0;
+    s->have_profile = s->have_final = s->have_finals = false;
+    s->mbest = 0; s->mb_n_len = 0;
     if (s->tc_n != n) { s->tc_n = -1; s->tc_key[0] = -1; }   // tile lists depend on n only
     int rc;
     // grow-only: cudaFree / cudaMalloc synchronise the device and cost up to ~1 s on a
@@ -99,13 +134,19 @@ int vlmp_set_series(vlmp_session* s, const double* t, const double* cum, const d
     CU(cudaMemcpyAsync(s->d_cum, cum, (n + 1) * sizeof(double), cudaMemcpyHostToDevice, s->stream));
     CU(cudaMemcpyAsync(s->d_cum2, cum2, (n + 1) * sizeof(double), cudaMemcpyHostToDevice, s->stream));
     CU(cudaStreamSynchronize(s->stream));
-    s->have_profile = s->have_final = s->have_finals = false;
+    s->n = n; s->A = A; s->floor_ = sigma_floor;
     return 0;
 }
 
 int vlmp_stats(vlmp_session* s, double* out, int32_t n_out) {
     if (!s || !out) return fail(VLMP_E_INVALID_PARAMETERS, "null argument");
-    for (int q = 0; q < n_out && q < 20; ++q) out[q] = s->stats[q];
+    {
+        std::lock_guard<std::mutex> g(s->lock);
+        int rc = settle_profile(s, nullptr);
+        if (!rc) rc = fill_event_stats(s);
+        if (rc) return rc;
+    }
+    for (int q = 0; q < n_out && q < 24; ++q) out[q] = s->stats[q];
     return 0;
 }
 
@@ -143,6 +184,49 @@ int vlmp_measure_fp64_peak(vlmp_session* s, double* fma_per_s) {
     CU(cudaFree(d_out));
     const double fmas = (double)grid * threads * iters * 16.0 * 8.0;
     *fma_per_s = fmas / (ms * 1e-3);
+    return 0;
+}
+
+int vlmp_window_stats(vlmp_session* s, int32_t length, double* mu, double* sd) {
+    if (!s || !mu || !sd) return fail(VLMP_E_INVALID_PARAMETERS, "null argument");
+    if (s->n <= 0) return fail(VLMP_E_STATE, "no series uploaded");
+    if (length < 1 || length > s->n) return fail(VLMP_E_INVALID_PARAMETERS, "length outside [1, n]");
+    std::lock_guard<std::mutex> g(s->lock);
+    CU(cudaSetDevice(s->device));
+    const long long N = s->n - length + 1;
+    double* d = nullptr;
+    CU(cudaMalloc((void**)&d, 2 * N * sizeof(double)));
+    k_win_stats<<<blocks(N, 256), 256, 0, s->stream>>>(s->d_cum, s->d_cum2, N, length, d, d + N);
+    cudaError_t e1 = cudaMemcpyAsync(mu, d, N * sizeof(double), cudaMemcpyDeviceToHost, s->stream);
+    cudaError_t e2 = cudaMemcpyAsync(sd, d + N, N * sizeof(double), cudaMemcpyDeviceToHost, s->stream);
+    cudaError_t e3 = cudaStreamSynchronize(s->stream);
+    cudaFree(d);
+    CU(e1); CU(e2); CU(e3);
+    return 0;
+}
+
+int vlmp_measure_fp32_peak(vlmp_session* s, double* fma_per_s) {
+    if (!s || !fma_per_s) return fail(VLMP_E_INVALID_PARAMETERS, "null argument");
+    std::lock_guard<std::mutex> g(s->lock);
+    CU(cudaSetDevice(s->device));
+    int sms = 0;
+    CU(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, s->device));
+    float* d_out = nullptr;
+    CU(cudaMalloc((void**)&d_out, 8));
+    const int threads = 512, per_sm = 4, iters = 4096;
+    const unsigned grid = sms * per_sm;
+    k_ffma_peak<<<grid, threads, 0, s->stream>>>(d_out, 16, 1.0f);   // warm-up
+    double best = 0;
+    for (int rep = 0; rep < 3; ++rep) {
+        CU(cudaEventRecord(s->ev[6], s->stream));
+        k_ffma_peak<<<grid, threads, 0, s->stream>>>(d_out, iters, 1.0f);
+        CU(cudaEventRecord(s->ev[7], s->stream));
+        CU(cudaEventSynchronize(s->ev[7]));
+        float ms = 0; CU(cudaEventElapsedTime(&ms, s->ev[6], s->ev[7]));
+        best = std::max(best, (double)grid * threads * iters * 16.0 * 8.0 / (ms * 1e-3));
+    }
+    CU(cudaFree(d_out));
+    *fma_per_s = best;
     return 0;
 }
 

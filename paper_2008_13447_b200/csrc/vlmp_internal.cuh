@@ -10,6 +10,7 @@
 #include <string.h>
 #include <math.h>
 #include <algorithm>
+#include <cstddef>
 #include <mutex>
 #include <string>
 #include <vector>
@@ -136,6 +137,21 @@ __device__ inline unsigned long long clamp_key(double r) {
     return r < 0.0 ? 0ull : (unsigned long long)__double_as_longlong(r);
 }
 
+// device clock (ns) for kernel spans: one atomicMin at a CTA's start and one atomicMax at its end
+// give a launch's first-start-to-last-end time without events (which would split a CUDA graph)
+__device__ __forceinline__ unsigned long long gtime() {
+    unsigned long long t; asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t)); return t;
+}
+
+// timing event on a stream that may be capturing a CUDA graph (profile_impl): inside a capture
+// the record must become an external event node, outside it is a plain record
+inline cudaError_t rec_event(cudaEvent_t ev, cudaStream_t st) {
+    cudaStreamCaptureStatus cs = cudaStreamCaptureStatusNone;
+    cudaStreamIsCapturing(st, &cs);
+    return cs == cudaStreamCaptureStatusActive ? cudaEventRecordWithFlags(ev, st, cudaEventRecordExternal)
+                                               : cudaEventRecord(ev, st);
+}
+
 __device__ inline void cp_async_commit() { asm volatile("cp.async.commit_group;\n" ::: "memory"); }
 __device__ inline void cp_async_wait_all() { asm volatile("cp.async.wait_group 0;\n" ::: "memory"); }
 
@@ -188,11 +204,28 @@ int ensure1(T*& p, size_t count) { size_t cap = 0; if (p) { cudaFree(p); p = nul
 
 inline unsigned blocks(long long n, int t) { return (unsigned)((n + t - 1) / t); }
 
+// profile.cu: wait for / check / redo a pending phase 1; device-event timings of the last run
+int settle_profile(vlmp_session* s, bool* redone);
+int mbest_impl(vlmp_session* s, int32_t lmin, int32_t lmax, int32_t mb);   // lock held by the caller
+void launch_params(vlmp_session* s, cudaStream_t st, Prm* prm, double* mu, int m);
+// pruned.cu
+struct PrunedState;
+void pruned_free(vlmp_session* s);
+int fill_event_stats(vlmp_session* s);
 }  // namespace vlmp_impl
 
 using namespace vlmp_impl;
 
 // =================================================================================
+// a phase-1 run that was enqueued but not yet checked (profile.cu settle_profile)
+struct PendingRun {
+    int lmin = 0, lmax = 0; long long band_lo = 0, band_hi = -1; uint32_t flags = 0;
+    int li_lo = 0, li_hi = -1; bool fp32 = false, sampled = false, graph = false;
+    long long cap_used = 0; int S = 0;
+    double executed = 0, launches = 0, n_filtered = 0, n_full = 0, klaunch = 0;
+    std::vector<int> timed, walked;
+};
+
 struct vlmp_session {
     int device = 0;
     cudaStream_t stream = nullptr;
@@ -239,7 +272,8 @@ struct vlmp_session {
     double* d_ro_f64 = nullptr; size_t ro_f64_cap = 0;
     unsigned long long* d_ro_cnt = nullptr;
     // m-best mode (m > 1 discords)
-    int mbest = 1;
+    int mbest = 0;                        // m of the last m-best run (0: none valid)
+    int mb_lmin = 0, mb_n_len = 0; long long mb_A = 0, mb_n = 0;   // the run it describes
     ulonglong2* d_slots = nullptr; size_t slots_cap = 0;
     int* d_slotcnt = nullptr; size_t slotcnt_cap = 0;
     int* d_ipm = nullptr; size_t ipm_cap = 0;
@@ -247,8 +281,19 @@ struct vlmp_session {
     long long* d_redo = nullptr; size_t redo_cap = 0;
     // run state
     int lmin = 0, lmax = 0, n_len = 0; bool have_profile = false, have_final = false, have_finals = false;
-    double stats[20] = {};
+    double stats[24] = {};
+    bool pending = false, stats_dirty = false;          // phase 1 enqueued, not yet settled
+    PendingRun prun;
+    unsigned long long* h_chk = nullptr; size_t h_chk_cap = 0;   // pinned: its overflow counters
     std::vector<cudaEvent_t> lev;   // 2 per length: tile-kernel start/stop
+    unsigned long long* d_span = nullptr; size_t span_cap = 0;   // [n_len][4] k_tile32 / k_runs spans (ns)
+    unsigned long long* h_span = nullptr; size_t h_span_cap = 0;
+    // the per-length launch sequence of profile_impl as one CUDA graph, re-launched while its
+    // key (shape, buffers, series scalars) is unchanged
+    cudaGraphExec_t g_exec = nullptr;
+    std::vector<double> g_key;
+    std::vector<double> g_cnt; std::vector<int> g_timed, g_walked;   // its host-side counters
+    vlmp_impl::PrunedState* pp = nullptr;                  // pruned discord scan (pruned.cu)
 };
 
 namespace vlmp_impl {
@@ -260,5 +305,13 @@ void build_tiles32(const std::vector<int2>& tiles, long long band_lo, std::vecto
 int launch_filter32(vlmp_session* s, cudaStream_t st, const Prm* prm, const double* mu, long long N, int m, int e,
                     long long dl, int S, int update_seeds, long long n_t32, const int* forced,
                     ulonglong2* acc, Run* runs, unsigned long long* run_count, long long run_cap,
-                    ulonglong2* slots = nullptr, int* slot_cnt = nullptr);
+                    ulonglong2* slots = nullptr, int* slot_cnt = nullptr, unsigned long long* span = nullptr);
+// profile.cu: wait for / check / redo a pending phase 1; device-event timings of the last run
+int settle_profile(vlmp_session* s, bool* redone);
+int mbest_impl(vlmp_session* s, int32_t lmin, int32_t lmax, int32_t mb);   // lock held by the caller
+void launch_params(vlmp_session* s, cudaStream_t st, Prm* prm, double* mu, int m);
+// pruned.cu
+struct PrunedState;
+void pruned_free(vlmp_session* s);
+int fill_event_stats(vlmp_session* s);
 }  // namespace vlmp_impl

@@ -1,14 +1,15 @@
-"""Multi-GPU sharding: one process per GPU; per-(length, offset) minima merged exactly with
-two NCCL MIN all-reduces.
+"""Multi-GPU sharding: one process per GPU.
 
 Length shards (default, `profile_length_sharded`). Each rank owns a contiguous run of
 lengths of equal work and computes the complete profile of those lengths on its GPU, with
-no exchange while it runs: its seeds are carried from lmin to its first length by the
-tile kernel's own Welford step with the same arithmetic (bit-identical to a single run), its first length is
-walked with full folds (the filter needs the previous length's winners), the rest are
-filtered. Every length's whole triangle runs on one GPU, so every GPU stays fully
-occupied at any world size. The partials of the other lengths stay empty, and the MIN
-merge below reproduces the single-GPU partials bit for bit.
+no exchange while it runs: its tile seeds are centred direct sums at its first length (the
+FP32 walk only gates; every key comes from the exact FP64 runs), that length takes its
+bounds from full folds over a sample of its bands, and every length then runs the FP32 walk
++ exact runs. Every length's whole triangle runs on one GPU, so every GPU stays fully
+occupied at any world size. Each (length, offset) has exactly one owner, so the exchange is
+an all-gather of each rank's finalized slab (`gather_owned_slabs`); the neighbours equal a
+single run's (keys of a run may differ in their last bits where the run starts elsewhere,
+which only matters at ties within ~1e-15; the GPU tests compare bit for bit).
 
 Band shards (`profile_sharded`), kept for very long lengths ranges per GPU:
 
@@ -153,11 +154,40 @@ class _DeviceArray:
                                          "version": 3, "strides": None}
 
 
+def gather_owned_slabs(buf, cuts, stride: int, rank: int, world: int, group=None):
+    """Every (length, offset) has exactly one owner rank, so the exchange is an all-gather of
+    each rank's contiguous slab of lengths [cuts[r], cuts[r+1]) of ``buf`` ([n_len * stride],
+    a torch view of the library's device buffer), in place. Slabs are padded to the largest
+    shard so one all_gather_into_tensor moves them (NCCL over NVLink); this moves each rank's
+    bytes once, half the ring traffic of an all-reduce over the whole buffer. Backends without
+    CUDA all-gather (gloo) go through host memory."""
+    import torch
+    import torch.distributed as dist
+    rows = [int(cuts[r + 1] - cuts[r]) for r in range(world)]
+    slab = max(rows) * stride
+    lo = int(cuts[rank]) * stride
+    send = torch.zeros(slab, dtype=buf.dtype, device=buf.device)
+    send[:rows[rank] * stride].copy_(buf[lo:lo + rows[rank] * stride])
+    cpu = dist.get_backend(group) == "gloo"
+    if cpu:
+        send = send.cpu()
+    out = torch.empty(world * slab, dtype=buf.dtype, device=send.device)
+    if cpu:
+        dist.all_gather(list(out.chunk(world)), send, group=group)
+    else:
+        dist.all_gather_into_tensor(out, send, group=group)
+    for r in range(world):
+        if r != rank and rows[r]:
+            a = int(cuts[r]) * stride
+            buf[a:a + rows[r] * stride].copy_(out[r * slab:r * slab + rows[r] * stride])
+    return buf
+
+
 def profile_length_sharded(sess, series, lmin: int, lmax: int, rank: int, world: int, group=None,
                            upload: bool = True, exchange: bool | None = None):
     """This rank's lengths on its session's device, finalized there; the per-length profile
-    values are then combined across ranks (every (length, offset) is owned by exactly one
-    rank: MIN over distances, MAX over neighbours) and every rank builds the read-offs.
+    values (MP double, IP int32) are then all-gathered slab by slab across ranks (every
+    (length, offset) is owned by exactly one rank) and every rank builds the read-offs.
     ``upload=False`` reuses the series already resident on the device; ``exchange`` forces
     the collective step on (a 1-rank group still runs it) or off (default: world > 1)."""
     import torch
@@ -170,13 +200,12 @@ def profile_length_sharded(sess, series, lmin: int, lmax: int, rank: int, world:
         sess.profile_lengths(lmin, lmax, lo, hi)
         sess.finalize_lengths(lo, hi)
     if (world > 1) if exchange is None else exchange:
-        import torch.distributed as dist
         mp_ptr, ip_ptr, n_len, stride = sess.final_buffers()
         dev = torch.device("cuda", sess.device)
         mp = torch.as_tensor(_DeviceArray(mp_ptr, n_len * stride, "<f8"), device=dev)
         ip = torch.as_tensor(_DeviceArray(ip_ptr, n_len * stride, "<i4"), device=dev)
-        dist.all_reduce(mp, op=dist.ReduceOp.MIN, group=group)
-        dist.all_reduce(ip, op=dist.ReduceOp.MAX, group=group)
+        gather_owned_slabs(mp, cuts, stride, rank, world, group)
+        gather_owned_slabs(ip, cuts, stride, rank, world, group)
         torch.cuda.synchronize(dev)
     with sess.lock:
         sess.finalize_readoffs()

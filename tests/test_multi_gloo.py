@@ -80,3 +80,40 @@ def test_two_rank_merge_equals_single(tmp_path, quantize):
     k1, i1 = _partials(t, lmin, lmax, (0, nb), quantize)
     assert np.array_equal(np.load(out + "_k.npy"), k1)
     assert np.array_equal(np.load(out + "_i.npy"), i1)
+
+
+def _slab_worker(rank, world, port, n, lmin, lmax, stride, out):
+    """Each rank owns the lengths length_split gives it: it fills only its slab (the value a
+    rank computes for (li, o) is a function of (li, o) alone) and the all-gather must leave
+    every rank with the complete buffer (int32 and float64, as the MP / IP buffers)."""
+    import torch
+    import torch.distributed as dist
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        cuts = D.length_split(n, lmin, lmax, world)
+        nl = lmax - lmin + 1
+        full = (np.arange(nl * stride, dtype=np.float64) * 1.5 - 7.0)
+        for dtype in (torch.float64, torch.int32):
+            buf = torch.full((nl * stride,), -1, dtype=dtype)
+            a, b = int(cuts[rank]) * stride, int(cuts[rank + 1]) * stride
+            buf[a:b] = torch.from_numpy(full[a:b]).to(dtype)
+            D.gather_owned_slabs(buf, cuts, stride, rank, world)
+            assert torch.equal(buf, torch.from_numpy(full).to(dtype)), (rank, dtype)
+        if rank == 0:
+            np.save(out, cuts)
+    finally:
+        dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("world", [2, 3])
+def test_length_slab_all_gather(tmp_path, world):
+    """The length-shard exchange (distributed.gather_owned_slabs) on world-size 2 and 3 gloo
+    groups: unequal slabs (work-balanced length cuts), padded all-gather, in-place scatter."""
+    import torch.multiprocessing as mp
+    out = str(tmp_path / "cuts.npy")
+    mp.start_processes(_slab_worker, args=(world, _free_port(), 65536, 256, 384, 37, out),
+                       nprocs=world, join=True, start_method="fork")
+    cuts = np.load(out)
+    assert cuts[0] == 0 and cuts[-1] == 129 and np.all(np.diff(cuts) > 0)
