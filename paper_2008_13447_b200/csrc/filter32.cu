@@ -42,6 +42,9 @@ constexpr int WIN = VLMP_PACKED ? 8 : D2;   // rows a column meets in one lane (
 #ifndef VLMP_PAIR_SEP
 #define VLMP_PAIR_SEP 2          // packed walk: band B = band A + VLMP_PAIR_SEP bands (1: adjacent)
 #endif
+#ifndef VLMP_ROWPAIR
+#define VLMP_ROWPAIR 0           // packed walk: one pass test and branch per pair of rows
+#endif
 #ifndef VLMP_FILTER32_WARPS_PER_SM
 #define VLMP_FILTER32_WARPS_PER_SM 16   // 128 registers: no spills (20 warps at 96 spill the staging plan)
 #endif
@@ -486,6 +489,9 @@ __global__ void __launch_bounds__(32, VLMP_FILTER32_WARPS_PER_SM) k_tile32(Tile3
     // |cov| <= s_i s_j (Cauchy-Schwarz); S + 1 rows (with the seed pre-adjust) plus the seed's
     // conversion, over the maxima of s, |df|, |dg| on the tile's rows and columns.
     float eps;
+#if VLMP_ROWPAIR
+    float eps_rev;   // slack of a covariance recovered one row back (the row pair's first row)
+#endif
     {
         const long long rb0 = i0 >> 8, rb1 = (i0 + nrows - 1) >> 8;
         const long long cb0 = (i0 + d0) >> 8, cb1 = (i0 + nrows - 1 + d0 + PSEP + BAND - 1) >> 8;
@@ -502,6 +508,11 @@ __global__ void __launch_bounds__(32, VLMP_FILTER32_WARPS_PER_SM) k_tile32(Tile3
         const double K = (double)a.S + 1.0;
         const double bound = 0x1p-24 * 1.01 * ((2.0 * K + 1.0) * 1.001 * Sr * Sc + 3.02 * K * (DFr * DGc + DFc * DGr));
         eps = __double2float_ru(bound);
+#if VLMP_ROWPAIR
+        // one row step undone in FP32 (two FFMA forward, two back): at most four roundings of
+        // magnitudes <= |cov32| + |df_i dg_j| + |df_j dg_i| <= Sr Sc + 2 eps + DFr DGc + DFc DGr
+        eps_rev = __double2float_ru(0x1p-24 * 5.0 * (1.01 * Sr * Sc + 2.0 * (double)eps + DFr * DGc + DFc * DGr));
+#endif
     }
 
     // ---- seeds of both bands (FP64, carried to m+1 in place as k_tile does)
@@ -622,6 +633,92 @@ __global__ void __launch_bounds__(32, VLMP_FILTER32_WARPS_PER_SM) k_tile32(Tile3
     cp_async_wait_all();
     __syncwarp();
 
+#if VLMP_ROWPAIR
+    // Row pairs: rows kk and kk + 1 are walked in one block and their 32 sign bits ANDed into
+    // one pass test and one branch (half the ISETP -> BRA latency chains and reconvergences,
+    // and a block twice as long for the scheduler). A flagged pair recomputes row kk + 1's exact
+    // mask from cov and row kk's from cov with row kk + 1's step undone (slack eps_rev; cell 0's
+    // threshold at row kk is the one row kk + 1's rotation replaced, kept in nold).
+    unsigned gflags = 0;
+    for (int g = 0; g < ngroups; ++g) {
+        const int b = g & 1;
+        if (g + 1 < ngroups) stage(g + 1, b ^ 1);
+#pragma unroll
+        for (int kk = 0; kk < GRP; kk += 2) {
+            const float4 p0 = sm.row[b][kk], p1 = sm.row[b][kk + 1];
+            unsigned t0, t1;
+            u64 nold;
+            {   // row kk: phys (kk-1) mod 8 receives lane+1's outgoing pair
+                const int q = (kk + DP - 1) % DP;
+                if (lane == 0 && kk == 0) fresh_pair(F[q], G[q], sm.fresh[b][0]);
+                F[q] = __shfl_sync(FULLMASK, F[q], (lane + 1) & 31);
+                G[q] = __shfl_sync(FULLMASK, G[q], (lane + 1) & 31);
+                const float4 cq = sm.cq[b][kk * CQS + lane];
+                NA[q] = pk2(fmaxf(-cq.x, __fmul_ru(-p0.w, cq.y)), fmaxf(-cq.z, __fmul_ru(-p0.w, cq.w)));
+                unsigned z[16];
+#pragma unroll
+                for (int s = 0; s < DP; ++s) {
+                    const int p = (s + kk) % DP;
+                    cov[s] = fma2(bc2(p0.x), G[p], cov[s]);
+                    cov[s] = fma2(F[p], bc2(p0.y), cov[s]);
+                    const u64 zz = fma2(NA[p], bc2(p0.z), cov[s]);
+                    z[s] = (unsigned)zz; z[s + 8] = (unsigned)(zz >> 32);
+                }
+                const unsigned a0 = and3(z[0], z[8], z[1]), a1 = and3(z[9], z[2], z[10]);
+                const unsigned a2 = and3(z[3], z[11], z[4]), a3 = and3(z[12], z[5], z[13]);
+                const unsigned a4 = and3(z[6], z[14], z[7]);
+                t0 = and3(and3(a0, a1, a2), a3, and3(a4, z[15], ~0u));
+                if (lane == 0) fresh_pair(F[kk % DP], G[kk % DP], sm.fresh[b][kk + 1]);
+            }
+            {   // row kk + 1: phys kk mod 8
+                const int q = kk % DP;
+                F[q] = __shfl_sync(FULLMASK, F[q], (lane + 1) & 31);
+                G[q] = __shfl_sync(FULLMASK, G[q], (lane + 1) & 31);
+                nold = NA[q];
+                const float4 cq = sm.cq[b][(kk + 1) * CQS + lane];
+                NA[q] = pk2(fmaxf(-cq.x, __fmul_ru(-p1.w, cq.y)), fmaxf(-cq.z, __fmul_ru(-p1.w, cq.w)));
+                unsigned z[16];
+#pragma unroll
+                for (int s = 0; s < DP; ++s) {
+                    const int p = (s + kk + 1) % DP;
+                    cov[s] = fma2(bc2(p1.x), G[p], cov[s]);
+                    cov[s] = fma2(F[p], bc2(p1.y), cov[s]);
+                    const u64 zz = fma2(NA[p], bc2(p1.z), cov[s]);
+                    z[s] = (unsigned)zz; z[s + 8] = (unsigned)(zz >> 32);
+                }
+                const unsigned a0 = and3(z[0], z[8], z[1]), a1 = and3(z[9], z[2], z[10]);
+                const unsigned a2 = and3(z[3], z[11], z[4]), a3 = and3(z[12], z[5], z[13]);
+                const unsigned a4 = and3(z[6], z[14], z[7]);
+                t1 = and3(and3(a0, a1, a2), a3, and3(a4, z[15], ~0u));
+            }
+            if (__builtin_expect((int)(t0 & t1) >= 0, 0)) {   // some cell of the pair passed
+                unsigned m0 = 0, m1 = 0;
+#pragma unroll
+                for (int s = 0; s < DP; ++s) {
+                    const int p = (s + kk + 1) % DP;
+                    const u64 n1 = NA[p];
+                    const float za = fma_nocse(lo2(n1), p1.z, lo2(cov[s]));
+                    const float zb = fma_nocse(hi2(n1), p1.z, hi2(cov[s]));
+                    m1 |= (__float_as_uint(za) >> 31 ^ 1u) << s;
+                    m1 |= (__float_as_uint(zb) >> 31 ^ 1u) << (s + 8);
+                    u64 cr = fma2(F[p], bc2(-p1.y), cov[s]);
+                    cr = fma2(bc2(-p1.x), G[p], cr);
+                    const u64 n0 = s == 0 ? nold : NA[(s + kk) % DP];
+                    const float ya = fma_nocse(lo2(n0), p0.z, lo2(cr) + eps_rev);
+                    const float yb = fma_nocse(hi2(n0), p0.z, hi2(cr) + eps_rev);
+                    m0 |= (__float_as_uint(ya) >> 31 ^ 1u) << s;
+                    m0 |= (__float_as_uint(yb) >> 31 ^ 1u) << (s + 8);
+                }
+                if (m0) { msk[kk] = (unsigned short)m0; gflags |= 1u << kk; }
+                if (m1) { msk[kk + 1] = (unsigned short)m1; gflags |= 1u << (kk + 1); }
+            }
+            if (kk + 2 < GRP && lane == 0) fresh_pair(F[(kk + 1) % DP], G[(kk + 1) % DP], sm.fresh[b][kk + 2]);
+        }
+        if (gflags) { fold_rows(gflags, g * GRP); gflags = 0; }
+        cp_async_wait_all();
+        __syncwarp();
+    }
+#else
     bool pass_prev = false;
     float bprev = 0.f;
     unsigned gflags = 0;
@@ -691,6 +788,7 @@ __global__ void __launch_bounds__(32, VLMP_FILTER32_WARPS_PER_SM) k_tile32(Tile3
         msk[GRP - 1] = (unsigned short)mask;
         gflags |= 1u << (GRP - 1);
     }
+#endif
     if (gflags) fold_rows(gflags, (ngroups - 1) * GRP);
     while (open) { const int q = __ffs(open) - 1; open &= open - 1; emit(q, rs[q], last_r); }
     if (nslow) atomicAdd(a.counters + 2, (unsigned long long)nslow);
