@@ -158,11 +158,14 @@ int vlmp_discords_m(vlmp_session* s, int32_t k, double* out_dist, int64_t* out_o
 
 /*
  * Pruned top-k m-th discord scan (MAD, discords.py:144-247 over profile.py:66-232's partial
- * profiles): the first length runs the exhaustive m-best profile and stores each row's
- * P = min(8, max(p, m)) best neighbours; every later length advances them in O(1), certifies
- * rows by VALMOD's lower bound (Eq. 2), replays the insertion policy and recomputes full rows only
- * for non-certified owners that could still enter the matrix (or falls back to an exhaustive
- * pass when that would cost more). Same results as vlmp_profile_mbest + vlmp_discords_m.
+ * profiles): the first length runs an exhaustive pass and stores each row's best neighbours
+ * (m = 1: the nearest one, from the 1-best profile; m > 1: P = min(8, max(p, m)) from the m-best
+ * profile); every later length advances them in O(1) (Welford co-moment step), certifies rows by
+ * VALMOD's lower bound (Eq. 2), replays the insertion policy and recomputes exact rows only for
+ * owners whose stored bound could still enter the matrix -- m = 1 in blocks of consecutive rows
+ * (one direct seed per diagonal, then the FP64 diagonal recurrence), in doubling windows so a
+ * length takes O(log N) replay stops -- or falls back to an exhaustive pass when the modelled
+ * recompute cost exceeds it. Same matrices as the exhaustive path (tests/test_gpu_pruned.py).
  * out_dist / out_off: [n_len][k][m]; counters (optional): [n_len][4] = certified rows,
  * non-certified live rows, full rows recomputed, 1 if the length ran exhaustively.
  */

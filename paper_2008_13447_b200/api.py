@@ -208,19 +208,16 @@ def valmod(series, lmin: int, lmax: int, p: int, *, ranking=None, trace=None,
 
 
 def _discord_mode(mode, series, lmin, lmax):
-    """Which discord path runs: ``mode`` argument, else VLMP_DISCORD_MODE, else "auto" -- the
-    pruned MAD scan where the A/B measurement shows it wins (long series with
-    several lengths), the exhaustive profile otherwise."""
+    """Which discord path runs: ``mode`` argument, else VLMP_DISCORD_MODE, else "auto". The
+    measured A/B has the exhaustive profile ahead on every BASELINE config
+    (config 3: ~10 ms vs ~280 ms per length; config 5: ~1.9 s vs ~7.5 s per length), so "auto"
+    runs it; "pruned" selects MAD's pruned scan explicitly (same matrices)."""
     mode = mode or os.environ.get("VLMP_DISCORD_MODE", "auto")
     if mode not in ("auto", "exhaustive", "pruned"):
         raise E.InvalidParametersError(f"mode must be auto, exhaustive or pruned (got {mode!r})")
     if mode == "auto":
-        mode = "pruned" if (series.n >= PRUNED_MIN_N and lmax > lmin) else "exhaustive"
+        mode = "exhaustive"
     return mode
-
-
-# auto mode: the pruned discord scan from this series length up (DESIGN.md §2c's A/B)
-PRUNED_MIN_N = 1 << 20
 
 
 def topkm_discord_discovery(series, lmin: int, lmax: int, k: int, m: int, p: int, *,

@@ -42,6 +42,9 @@ constexpr int WIN = VLMP_PACKED ? 8 : D2;   // rows a column meets in one lane (
 #ifndef VLMP_PAIR_SEP
 #define VLMP_PAIR_SEP 2          // packed walk: band B = band A + VLMP_PAIR_SEP bands (1: adjacent)
 #endif
+#ifndef VLMP_ROWDUP
+#define VLMP_ROWDUP 0            // packed walk: row factors as duplicated pairs (no broadcast operands)
+#endif
 #ifndef VLMP_ROWPAIR
 #define VLMP_ROWPAIR 0           // packed walk: one pass test and branch per pair of rows
 #endif
@@ -450,6 +453,9 @@ struct Smem32p {
     float4 cq[2][GRP * CQS];     // {aA, bA, aB, bB} of the pair entering lane L at row kk: [kk * 33 + L]
     unsigned short rs[32 * 16];  // run starts per lane and cell (bits 0-7 band A, 8-15 band B)
     unsigned short msk[32 * GRP];
+#if VLMP_ROWDUP
+    unsigned long long rowd[GRP][4];   // the group's rows as duplicated pairs {df df, dg dg, b b, w w}
+#endif
 };
 
 // lane 0's outgoing pair becomes lane 31's incoming one. Adjacent bands (PSEP = 256): (lane 0's
@@ -725,9 +731,26 @@ __global__ void __launch_bounds__(32, VLMP_FILTER32_WARPS_PER_SM) k_tile32(Tile3
     for (int g = 0; g < ngroups; ++g) {
         const int b = g & 1;
         if (g + 1 < ngroups) stage(g + 1, b ^ 1);
+#if VLMP_ROWDUP
+        // full-pair FFMA2 operands instead of scalar broadcasts
+        if (lane < GRP) {
+            const float4 r = sm.row[b][lane];
+            sm.rowd[lane][0] = pk2(r.x, r.x); sm.rowd[lane][1] = pk2(r.y, r.y);
+            sm.rowd[lane][2] = pk2(r.z, r.z); sm.rowd[lane][3] = pk2(r.w, r.w);
+        }
+        __syncwarp();
+#endif
 #pragma unroll
         for (int kk = 0; kk < GRP; ++kk) {
+#if VLMP_ROWDUP
+            const ulonglong2 r01 = *reinterpret_cast<const ulonglong2*>(&sm.rowd[kk][0]);
+            const ulonglong2 r23 = *reinterpret_cast<const ulonglong2*>(&sm.rowd[kk][2]);
+            const float4 pr = make_float4(lo2(r01.x), lo2(r01.y), lo2(r23.x), lo2(r23.y));
+            const u64 RX = r01.x, RY = r01.y, RZ = r23.x;
+#else
             const float4 pr = sm.row[b][kk];
+            const u64 RX = bc2(pr.x), RY = bc2(pr.y), RZ = bc2(pr.z);
+#endif
             if (__builtin_expect(pass_prev, 0)) {
                 const int kp = (kk + GRP - 1) % DP;
                 unsigned mask = 0;
@@ -746,8 +769,10 @@ __global__ void __launch_bounds__(32, VLMP_FILTER32_WARPS_PER_SM) k_tile32(Tile3
             {   // rotation: phys (kk-1) mod 8 receives lane+1's outgoing pair
                 const int q = (kk + DP - 1) % DP;
                 if (lane == 0 && kk == 0) fresh_pair(F[q], G[q], sm.fresh[b][0]);
+#if !VLMP_ABL_NOSHFL       // (dev ablations: timing only, results are wrong)
                 F[q] = __shfl_sync(FULLMASK, F[q], (lane + 1) & 31);
                 G[q] = __shfl_sync(FULLMASK, G[q], (lane + 1) & 31);
+#endif
                 const float4 cq = sm.cq[b][kk * CQS + lane];
                 NA[q] = pk2(fmaxf(-cq.x, __fmul_ru(-pr.w, cq.y)), fmaxf(-cq.z, __fmul_ru(-pr.w, cq.w)));
             }
@@ -755,9 +780,13 @@ __global__ void __launch_bounds__(32, VLMP_FILTER32_WARPS_PER_SM) k_tile32(Tile3
 #pragma unroll
             for (int s = 0; s < DP; ++s) {
                 const int p = (s + kk) % DP;
-                cov[s] = fma2(bc2(pr.x), G[p], cov[s]);
-                cov[s] = fma2(F[p], bc2(pr.y), cov[s]);
-                const u64 zz = fma2(NA[p], bc2(pr.z), cov[s]);
+                cov[s] = fma2(RX, G[p], cov[s]);
+                cov[s] = fma2(F[p], RY, cov[s]);
+#if VLMP_ABL_NOTEST
+                const u64 zz = cov[s] | 0x8000000080000000ull;
+#else
+                const u64 zz = fma2(NA[p], RZ, cov[s]);
+#endif
                 z[s] = (unsigned)zz; z[s + 8] = (unsigned)(zz >> 32);
             }
             {   // sign bits ANDed by a depth-3 tree of 3-input LOP3s (left to itself the compiler
@@ -767,7 +796,11 @@ __global__ void __launch_bounds__(32, VLMP_FILTER32_WARPS_PER_SM) k_tile32(Tile3
                 const unsigned t4 = and3(z[6], z[14], z[7]);
                 z[0] = and3(and3(t0, t1, t2), t3, and3(t4, z[15], ~0u));
             }
+#if VLMP_ABL_NOBRANCH
+            nslow += z[0] >> 31;
+#else
             pass_prev = (int)z[0] >= 0;
+#endif
             bprev = pr.z;
             if (kk + 1 < GRP && lane == 0) fresh_pair(F[kk % DP], G[kk % DP], sm.fresh[b][kk + 1]);
         }
@@ -804,6 +837,11 @@ __global__ void __launch_bounds__(32, VLMP_FILTER32_WARPS_PER_SM) k_tile32(Tile3
 // slots == nullptr: fold into the 1-best accumulators; else (m-best mode, m > 1 discords) append
 // every cell that passes an exact test to its offset's candidate slots (SLOT_CAP per offset;
 // k_select_m keeps the m smallest and recomputes offsets whose slots overflowed)
+#ifndef VLMP_RUNS_G
+#define VLMP_RUNS_G 32            // lanes per run in k_runs (8 / 16: several runs per warp)
+#endif
+
+template <int G>
 __global__ void __launch_bounds__(256) k_runs(const Run* __restrict__ runs, const unsigned long long* run_count,
                                              long long cap, const Prm* __restrict__ prm,
                                              const double* __restrict__ tn, const double* __restrict__ mu,
@@ -813,16 +851,20 @@ __global__ void __launch_bounds__(256) k_runs(const Run* __restrict__ runs, cons
     const unsigned long long cnt = *run_count;
     const long long nr = (long long)(cnt < (unsigned long long)cap ? cnt : (unsigned long long)cap);
     const int lane = threadIdx.x & 31;
-    const long long w0 = (blockIdx.x * (long long)blockDim.x + threadIdx.x) >> 5;
-    const long long nw = ((long long)gridDim.x * blockDim.x) >> 5;
+    const int gl = lane & (G - 1);                 // lane within the run's group
+    const int gbase = lane & ~(G - 1);
+    constexpr unsigned GM = G >= 32 ? 0xFFFFFFFFu : ((1u << (G & 31)) - 1u);
+    const unsigned gmask = GM << gbase;
+    const long long w0 = (blockIdx.x * (long long)blockDim.x + threadIdx.x) / G;
+    const long long nw = ((long long)gridDim.x * blockDim.x) / G;
     unsigned long long cells = 0, merged = 0;
-    // warp-cooperative centred dot product of windows (a, b): lane-strided terms, fixed xor tree
+    // group-cooperative centred dot product of windows (a, b): lane-strided terms, fixed xor tree
     auto wdot = [&](long long a_, long long b_) {
         const double ma = mu[a_], mb = mu[b_];
         double d = 0.0;
-        for (int k = lane; k < m; k += 32) d = fma(tn[a_ + k] - ma, tn[b_ + k] - mb, d);
+        for (int k = gl; k < m; k += G) d = fma(tn[a_ + k] - ma, tn[b_ + k] - mb, d);
 #pragma unroll
-        for (int off = 16; off >= 1; off >>= 1) d += __shfl_xor_sync(FULLMASK, d, off);
+        for (int off = G / 2; off >= 1; off >>= 1) d += __shfl_xor_sync(gmask, d, off, G);
         return d;
     };
     for (long long q = w0; q < nr; q += nw) {
@@ -836,8 +878,8 @@ __global__ void __launch_bounds__(256) k_runs(const Run* __restrict__ runs, cons
         // resolution) is recomputed directly -- a run that walks out of a high-variance stretch.
         double mag = fabs(dot);
         const bool ok_diag = j - i >= e;
-        for (int c0 = 0; c0 < R.len; c0 += 32) {
-            const int k = c0 + lane;
+        for (int c0 = 0; c0 < R.len; c0 += G) {
+            const int k = c0 + gl;
             const bool valid = k < R.len;
             double term = 0.0, ii = 0.0, ij = 0.0;
             float ui = -INFINITY, uj = -INFINITY;
@@ -848,29 +890,29 @@ __global__ void __launch_bounds__(256) k_runs(const Run* __restrict__ runs, cons
             }
             float at = __double2float_ru(fabs(term));   // a bound: FP32, rounded up, is enough
 #pragma unroll
-            for (int off = 1; off < 32; off <<= 1) {
-                const double t = __shfl_up_sync(FULLMASK, term, off);
-                const float ta = __shfl_up_sync(FULLMASK, at, off);
-                if (lane >= off) { term += t; at = __fadd_ru(at, ta); }
+            for (int off = 1; off < G; off <<= 1) {
+                const double t = __shfl_up_sync(gmask, term, off, G);
+                const float ta = __shfl_up_sync(gmask, at, off, G);
+                if (gl >= off) { term += t; at = __fadd_ru(at, ta); }
             }
             double cv = carry + term;
             const double scale = 1.0 / (ii * ij);   // s_i s_j (NaN / 0 for invalid windows)
             const bool inexact = valid && ok_diag && !((mag + (double)at) <= 8.0 * scale);
-            unsigned redo = __ballot_sync(FULLMASK, inexact);
+            unsigned redo = (__ballot_sync(gmask, inexact) >> gbase) & GM;
             if (redo) {   // rare: exact direct sums for the flagged cells of this chunk
-                const unsigned tail = __ballot_sync(FULLMASK, valid);
+                const unsigned tail = (__ballot_sync(gmask, valid) >> gbase) & GM;
                 const int last = 31 - __clz(tail);
                 redo |= 1u << last;              // the carry restarts from an exact value
                 while (redo) {
                     const int l = __ffs(redo) - 1; redo &= redo - 1;
                     const double d = wdot(i + c0 + l, j + c0 + l);
-                    if (lane == l) cv = d;
+                    if (gl == l) cv = d;
                 }
-                const double cl = __shfl_sync(FULLMASK, cv, last);
+                const double cl = __shfl_sync(gmask, cv, last, G);
                 carry = cl; mag = fabs(cl);
             } else {
-                carry = __shfl_sync(FULLMASK, cv, 31);
-                mag += (double)__shfl_sync(FULLMASK, at, 31);
+                carry = __shfl_sync(gmask, cv, G - 1, G);
+                mag += (double)__shfl_sync(gmask, at, G - 1, G);
             }
             if (valid && ok_diag) {
                 const double r = fma(-(cv * ii), ij, 1.0);
@@ -878,13 +920,13 @@ __global__ void __launch_bounds__(256) k_runs(const Run* __restrict__ runs, cons
                 const unsigned long long key = clamp_key(r) & ~PMASK;
                 if (slots) {
                     if (h <= ui) {
-                        const int at = atomicAdd(slot_cnt + i + k, 1);
-                        if (at < SLOT_CAP) slots[(i + k) * SLOT_CAP + at] = make_ulonglong2(key, (unsigned long long)(j + k));
+                        const int at2 = atomicAdd(slot_cnt + i + k, 1);
+                        if (at2 < SLOT_CAP) slots[(i + k) * SLOT_CAP + at2] = make_ulonglong2(key, (unsigned long long)(j + k));
                         ++merged;
                     }
                     if (h <= uj) {
-                        const int at = atomicAdd(slot_cnt + j + k, 1);
-                        if (at < SLOT_CAP) slots[(j + k) * SLOT_CAP + at] = make_ulonglong2(key, (unsigned long long)(i + k));
+                        const int at2 = atomicAdd(slot_cnt + j + k, 1);
+                        if (at2 < SLOT_CAP) slots[(j + k) * SLOT_CAP + at2] = make_ulonglong2(key, (unsigned long long)(i + k));
                         ++merged;
                     }
                 } else {
@@ -893,7 +935,7 @@ __global__ void __launch_bounds__(256) k_runs(const Run* __restrict__ runs, cons
                 }
             }
         }
-        if (lane == 0) cells += (unsigned long long)R.len;
+        if (gl == 0) cells += (unsigned long long)R.len;
     }
 #pragma unroll
     for (int off = 16; off >= 1; off >>= 1) {
@@ -956,7 +998,7 @@ int launch_filter32(vlmp_session* s, cudaStream_t st, const Prm* prm, const doub
                       update_seeds, s->sscale, span, s->d_cq4, s->d_pf4};
         // span: [0, 1] k_tile32's and [2, 3] k_runs' first start / last end (bench.py's roofline)
         k_tile32<<<(unsigned)n_t32, 32, sizeof(SmemT), st>>>(ta);
-        k_runs<<<148 * 8, 256, 0, st>>>(runs, run_count, run_cap, prm, s->d_tn, mu, m, e, acc, s->d_counters,
+        k_runs<VLMP_RUNS_G><<<148 * 8, 256, 0, st>>>(runs, run_count, run_cap, prm, s->d_tn, mu, m, e, acc, s->d_counters,
                                         slots, slot_cnt, span ? span + 2 : nullptr);
     }
     return 0;

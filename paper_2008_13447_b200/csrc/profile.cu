@@ -1431,6 +1431,11 @@ static int profile_impl(vlmp_session* s, int32_t lmin, int32_t lmax, int64_t ban
 namespace vlmp_impl {
 
 // Device-event timings of the last run (lazily: only vlmp_stats needs them).
+// one exhaustive 1-best pass with the session lock held (pruned.cu's full lengths)
+int profile_locked(vlmp_session* s, int lmin, int lmax) {
+    return profile_impl(s, lmin, lmax, 0, -1, 0, 0, -1);
+}
+
 int fill_event_stats(vlmp_session* s) {
     if (!s->stats_dirty) return 0;
     const PendingRun& pr = s->prun;

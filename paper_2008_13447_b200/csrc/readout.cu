@@ -348,6 +348,15 @@ static int finalize_enqueue(vlmp_session* s, int li_lo, int li_hi, bool readoffs
     return 0;
 }
 
+}  // extern "C"
+
+namespace vlmp_impl {
+// phase 2 of lengths li_lo..li_hi with the session lock held (pruned.cu's full lengths)
+int finalize_lengths_locked(vlmp_session* s, int li_lo, int li_hi) { return finalize_impl(s, li_lo, li_hi, false); }
+}  // namespace vlmp_impl
+
+extern "C" {
+
 int vlmp_finalize(vlmp_session* s) {
     if (!s || !s->have_profile) return fail(VLMP_E_STATE, "no profile run");
     std::lock_guard<std::mutex> g(s->lock);

@@ -212,6 +212,9 @@ void launch_params(vlmp_session* s, cudaStream_t st, Prm* prm, double* mu, int m
 struct PrunedState;
 void pruned_free(vlmp_session* s);
 int fill_event_stats(vlmp_session* s);
+// lock held by the caller: one exhaustive 1-best pass (profile.cu) and its phase 2 (readout.cu)
+int profile_locked(vlmp_session* s, int lmin, int lmax);
+int finalize_lengths_locked(vlmp_session* s, int li_lo, int li_hi);
 }  // namespace vlmp_impl
 
 using namespace vlmp_impl;

@@ -18,7 +18,7 @@ out = os.path.join(out_dir, f"libvlmp_{name}.so")
 cmd = [b.nvcc(), *b.NVCC_FLAGS, "-Xptxas=-v", *defs, "-o", out, *b.SRCS]
 r = subprocess.run(cmd, capture_output=True, text=True)
 if r.returncode:
-    print(r.stderr[-4000:])
+    print("\n".join(l for l in r.stderr.splitlines() if "error" in l or "^" in l)[-3000:])
     sys.exit(r.returncode)
 lines = r.stderr.splitlines()
 for k, line in enumerate(lines):

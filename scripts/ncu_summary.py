@@ -17,7 +17,7 @@ print("-- stalls per issued instruction")
 for k, v in sorted(d.items()):
     if k.startswith("smsp__average_warps_issue_stalled_") and k.endswith("_per_issue_active.ratio"):
         try:
-            if float(v) > 0.05: print(f"   {k[35:-23]:30s} {v}")
+            if float(v) > 0.05: print(f"   {k[34:-23]:30s} {v}")
         except ValueError: pass
 src = subprocess.run(["ncu", "-i", rep, "--page", "source", "--csv", "--print-source", "sass"], capture_output=True, text=True).stdout.splitlines()
 rows = list(csv.reader(src)); hdr = rows[1]; data = rows[2:]
