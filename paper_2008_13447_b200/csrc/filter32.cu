@@ -840,9 +840,12 @@ __global__ void __launch_bounds__(32, VLMP_FILTER32_WARPS_PER_SM) k_tile32(Tile3
 #ifndef VLMP_RUNS_G
 #define VLMP_RUNS_G 32            // lanes per run in k_runs (8 / 16: several runs per warp)
 #endif
+#ifndef VLMP_RUNS_MINB
+#define VLMP_RUNS_MINB 1          // k_runs: minimum resident 256-thread blocks per SM (register cap)
+#endif
 
 template <int G>
-__global__ void __launch_bounds__(256) k_runs(const Run* __restrict__ runs, const unsigned long long* run_count,
+__global__ void __launch_bounds__(256, VLMP_RUNS_MINB) k_runs(const Run* __restrict__ runs, const unsigned long long* run_count,
                                              long long cap, const Prm* __restrict__ prm,
                                              const double* __restrict__ tn, const double* __restrict__ mu,
                                              int m, int e, ulonglong2* acc, unsigned long long* counters,
