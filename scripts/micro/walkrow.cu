@@ -31,7 +31,7 @@ __global__ void __launch_bounds__(32, 16) k_walk(const float4* rows, const float
         NA[s] = pk2(-1e30f, -1e30f);
     }
     float4 rr = rows[lane & 7];
-    unsigned acc = 0, nslow = 0;
+    unsigned acc = 0, nslow = 0, tacc = ~0u;
     for (int it = 0; it < iters; ++it) {
 #pragma unroll
         for (int kk = 0; kk < GRP; ++kk) {
@@ -61,8 +61,17 @@ __global__ void __launch_bounds__(32, 16) k_walk(const float4* rows, const float
                 const unsigned t2 = and3(z[3], z[11], z[4]), t3 = and3(z[12], z[5], z[13]);
                 const unsigned t4 = and3(z[6], z[14], z[7]);
                 const unsigned t = and3(and3(t0, t1, t2), t3, and3(t4, z[15], ~0u));
+                tacc &= t;
+                // F_BR: 1 per-row divergent branch, 2 per-row uniform branch (vote), 3 divergent every
+                // 2 rows, 4 uniform every 2 rows, 5 divergent every 4 rows, 6 divergent every 8 rows
+                const int every = F_BR == 3 || F_BR == 4 ? 2 : F_BR == 5 ? 4 : F_BR == 6 ? 8 : 1;
+                const bool uni = F_BR == 2 || F_BR == 4;
+                const bool at = (kk % every) == every - 1;
+                bool take = false;
+                if (F_BR && at) take = uni ? __any_sync(0xffffffffu, (int)tacc >= 0) : (int)tacc >= 0;
+                if (F_BR && at) tacc = ~0u;
                 if (F_BR) {
-                    if (__builtin_expect((int)t >= 0, 0)) {     // never taken with these data
+                    if (__builtin_expect(take, 0)) {     // never taken with these data
                         unsigned m = 0;
 #pragma unroll
                         for (int s = 0; s < DP; ++s) m |= ((unsigned)cov[s] >> 31) << s;
@@ -114,6 +123,11 @@ int main() {
         run<1, 1, 1, 1, 0>("+tree+branch+shfl", w, rows, cqs, out);
         run<1, 1, 1, 1, 1>("+tree+branch+shfl+lds", w, rows, cqs, out);
         run<1, 1, 0, 1, 1>("+tree+shfl+lds (no br)", w, rows, cqs, out);
+        run<1, 1, 2, 1, 1>("full, uniform br/row", w, rows, cqs, out);
+        run<1, 1, 3, 1, 1>("full, br per 2 rows", w, rows, cqs, out);
+        run<1, 1, 4, 1, 1>("full, uniform br/2 rows", w, rows, cqs, out);
+        run<1, 1, 5, 1, 1>("full, br per 4 rows", w, rows, cqs, out);
+        run<1, 1, 6, 1, 1>("full, br per 8 rows", w, rows, cqs, out);
     }
     return 0;
 }
