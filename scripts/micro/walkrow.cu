@@ -31,17 +31,22 @@ __global__ void __launch_bounds__(32, 16) k_walk(const float4* rows, const float
         NA[s] = pk2(-1e30f, -1e30f);
     }
     float4 rr = rows[lane & 7];
+    float4 prn = srow[0];
     unsigned acc = 0, nslow = 0, tacc = ~0u;
     for (int it = 0; it < iters; ++it) {
 #pragma unroll
         for (int kk = 0; kk < GRP; ++kk) {
-            const float4 pr = F_LD ? srow[kk] : rr;
+            // F_LD: 1 row + column factors from smem, 2 column factors only, 3 row factors only,
+            // 4 as 1 with the row factors prefetched one row ahead
+            float4 pr;
+            if (F_LD == 4) { pr = prn; prn = srow[(kk + 1) % GRP]; }
+            else pr = (F_LD == 1 || F_LD == 3) ? srow[kk] : rr;
             const int q = (kk + DP - 1) % DP;
             if (F_SH) {
                 F[q] = __shfl_sync(0xffffffffu, F[q], (lane + 1) & 31);
                 G[q] = __shfl_sync(0xffffffffu, G[q], (lane + 1) & 31);
             }
-            if (F_LD) {
+            if (F_LD == 1 || F_LD == 2 || F_LD == 4) {
                 const float4 cq = scq[kk * CQS + lane];
                 NA[q] = pk2(fmaxf(-cq.x, __fmul_ru(-pr.w, cq.y)), fmaxf(-cq.z, __fmul_ru(-pr.w, cq.w)));
             }
@@ -123,6 +128,10 @@ int main() {
         run<1, 1, 1, 1, 0>("+tree+branch+shfl", w, rows, cqs, out);
         run<1, 1, 1, 1, 1>("+tree+branch+shfl+lds", w, rows, cqs, out);
         run<1, 1, 0, 1, 1>("+tree+shfl+lds (no br)", w, rows, cqs, out);
+        run<1, 1, 1, 1, 2>("full, cq from smem only", w, rows, cqs, out);
+        run<1, 1, 1, 1, 3>("full, rows from smem only", w, rows, cqs, out);
+        run<1, 1, 1, 1, 4>("full, rows prefetched", w, rows, cqs, out);
+        run<1, 1, 6, 1, 4>("full, rows pf, br/8 rows", w, rows, cqs, out);
         run<1, 1, 2, 1, 1>("full, uniform br/row", w, rows, cqs, out);
         run<1, 1, 3, 1, 1>("full, br per 2 rows", w, rows, cqs, out);
         run<1, 1, 4, 1, 1>("full, uniform br/2 rows", w, rows, cqs, out);
