@@ -162,8 +162,7 @@ def _config_dict(args, c, W, world, parallelism):
     return {"workload": f"config {args.config}: {c.note}", "n": c.n, "lmin": c.lmin,
             "lmax": c.lmax, "k_motif": c.k_motif, "k_discord": c.k_discord, "W_updates": W,
             "parallelism": parallelism,
-            "l2": "working set (series + per-length params, 2.6 MB) is L2-resident by design; "
-                  "no flush: the walk is FMA-pipe/latency bound (FP32), not memory-bound"}
+            "l2": "flushed before every timed step (512 MB overwrite outside the step's event span)"}
 
 
 def reference_python_sample():
@@ -265,26 +264,38 @@ def run_ours(args):
 
     with sess.lock:
         sess.set_series(s.values, s._cum, s._cum2, s.sigma_floor)   # inputs resident in HBM
+    # L2 (126 MB) is flushed before every timed step by overwriting a 512 MB buffer, outside the
+    # step's own CUDA-event span: each step starts cold, like the first pass over a new series
+    flush = torch.empty(512 << 20, dtype=torch.uint8, device="cuda")
+
+    def flush_l2():
+        flush.zero_()
+        torch.cuda.synchronize()
+
     for _ in range(max(args.warmup, 3)):
+        flush_l2()
         step()
     if world > 1:
         torch.distributed.barrier()
     torch.cuda.synchronize()
     walk_ms, runs_ms, walk_launches, launches, step_ms_list = 0.0, 0.0, 0, 0, []
+    ms = 0.0
     # one clock sampler spans both timed regions (device-resident steps, then e2e): its start-up
     # and teardown stay outside them
     clk = ClockSampler(local).__enter__()
-    sess.event_record(0)
     for _ in range(args.steps):
+        flush_l2()
+        sess.event_record(0)          # CUDA events on the session's stream, around the step
         rows, disc = step()
+        sess.event_record(1)
+        one = sess.event_elapsed_ms()
+        ms += one
         st = sess.stats()
         walk_ms += st["walk_ms"]
         runs_ms += st["runs_ms"]
         walk_launches += int(st["walk_launches"])
         launches += int(st["kernel_launches"]) + 2
-        step_ms_list.append(st["profile_ms"])
-    sess.event_record(1)
-    ms = sess.event_elapsed_ms()
+        step_ms_list.append(one)
     torch.cuda.synchronize()
     if world > 1:
         import torch.distributed as dist
@@ -314,12 +325,15 @@ def run_ours(args):
             return rows, disc, val
         for _ in range(2):
             e2e_step()
-        dist.barrier()
-        t0 = time.perf_counter()
         reps = max(2, min(2 * args.steps, 10))
+        e2e_t = 0.0
         for _ in range(reps):
+            flush_l2()
+            dist.barrier()
+            t0 = time.perf_counter()
             out = e2e_step()
-        tt = torch.tensor([(time.perf_counter() - t0) / reps], device="cuda")
+            e2e_t += time.perf_counter() - t0
+        tt = torch.tensor([e2e_t / reps], device="cuda")
         dist.all_reduce(tt, op=dist.ReduceOp.MAX)
         e2e_s = float(tt[0])
         e2e_line = {"value": W / e2e_s, "unit": UNIT,
@@ -341,11 +355,14 @@ def run_ours(args):
         from paper_2008_13447_b200 import mine
         for _ in range(2):
             mine(s, c.lmin, c.lmax, k_motif=c.k_motif, k_discord=c.k_discord)
-        t0 = time.perf_counter()
         reps = max(2, min(2 * args.steps, 10))
+        e2e_s = 0.0
         for _ in range(reps):
+            flush_l2()
+            t0 = time.perf_counter()
             res = mine(s, c.lmin, c.lmax, k_motif=c.k_motif, k_discord=c.k_discord)
-        e2e_s = (time.perf_counter() - t0) / reps
+            e2e_s += time.perf_counter() - t0
+        e2e_s /= reps
         e2e_line = {"value": W / e2e_s, "unit": UNIT,
                     "h2d_bytes_per_step": int(8 * (s.n + 2 * (s.n + 1))),
                     "d2h_bytes_per_step": int(n0 * (8 * 4 + 1) + nl * (2 * c.k_motif * 24 + kd * 16)),
@@ -390,7 +407,7 @@ def run_ours(args):
         "warmup": max(args.warmup, 3), "ms_per_step": step_ms, "higher_is_better": True,
         "scaling": "strong", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
         "config": _config_dict(args, c, W, world, parallelism),
-        "step_ms_median": float(np.median(step_ms_list)) if world == 1 else None,
+        "step_ms_median": float(np.median(step_ms_list)),
         "roofline": {"bound": "fp32_fma", "achieved": achieved, "peak": peak, "unit": "TFLOP/s",
                      "frac": achieved / peak, "traffic": prof_traffic,
                      "kernel": "k_tile32", "launches_per_step": walk_launches / args.steps,

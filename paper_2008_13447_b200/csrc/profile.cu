@@ -99,6 +99,9 @@ struct Bound2Args {
     int exact;                     // bound = exact key of the chosen candidate (FP32 walk)
 };
 
+#ifndef VLMP_BOUND_ADJ
+#define VLMP_BOUND_ADJ 0   // FP32 path: also bound by the own winner's neighbouring diagonals
+#endif
 __global__ void k_bound2(Bound2Args a) {
     const long long o = blockIdx.x * (long long)blockDim.x + threadIdx.x;
     if (o >= a.N) return;
@@ -165,6 +168,23 @@ __global__ void k_bound2(Bound2Args a) {
             }
         }
     }
+#if VLMP_BOUND_ADJ
+    // the own winner's neighbouring diagonals (o, c1 -+ 1..ADJ) by direct centred sums (2m ADJ FMA
+    // per offset): on smooth series a winner that moves between lengths mostly moves by one column,
+    // and a tighter bound lets fewer cells through the walk into the exact runs
+    if (a.exact && o < a.Nprev && a.acc_prev[o].x != KEY_NONE) {
+        const long long c1 = (long long)a.acc_prev[o].y;
+        for (int q = 0; q < 2 * VLMP_BOUND_ADJ; ++q) {
+            const long long c = c1 + ((q & 1) ? -(q / 2 + 1) : (q / 2 + 1));
+            const long long dd = c > o ? c - o : o - c;
+            if (c < 0 || c >= a.N || dd < a.e) continue;
+            const double ic = a.prm[c].inv;
+            if (!(ic == ic)) continue;
+            const double r = fma(-(direct_cov(a.tn, o, a.mu[o], c, a.mu[c], m) * io), ic, 1.0);
+            if (r < best) { best = r; best_c = -1; }   // exact already
+        }
+    }
+#endif
     if (a.exact && best_c >= 0 && !(best_mag * io * a.prm[best_c].inv <= 0x1p10)) {
         // the reconstruction's rounding (~2^-50 of the magnitudes it summed) could exceed the
         // 2^-26 margin relative to this cell's own scale s_o s_c: bound by its exact key instead
