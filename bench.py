@@ -408,6 +408,7 @@ def run_ours(args):
         "scaling": "strong", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
         "config": _config_dict(args, c, W, world, parallelism),
         "step_ms_median": float(np.median(step_ms_list)),
+        "step_ms": [round(x, 3) for x in step_ms_list],
         "roofline": {"bound": "fp32_fma", "achieved": achieved, "peak": peak, "unit": "TFLOP/s",
                      "frac": achieved / peak, "traffic": prof_traffic,
                      "kernel": "k_tile32", "launches_per_step": walk_launches / args.steps,
