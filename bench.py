@@ -82,8 +82,11 @@ class ClockSampler:
         import tempfile
         try:
             self._f = tempfile.TemporaryFile(mode="w+")
+            if os.environ.get("BENCH_NO_CLOCKS"):      # dev knob: no sampler
+                raise RuntimeError("clock sampling disabled")
             self._p = subprocess.Popen(["nvidia-smi", "-i", str(self.device), f"--query-gpu={self.Q}",
-                                        "--format=csv,noheader,nounits", "-lms", "200"],
+                                        "--format=csv,noheader,nounits", "-lms",
+                                        os.environ.get("BENCH_CLOCK_MS", "200")],
                                        stdout=self._f, stderr=subprocess.DEVNULL, text=True)
             t0 = time.time()
             while time.time() - t0 < 3.0 and os.fstat(self._f.fileno()).st_size == 0 and self._p.poll() is None:
@@ -266,10 +269,12 @@ def run_ours(args):
         sess.set_series(s.values, s._cum, s._cum2, s.sigma_floor)   # inputs resident in HBM
     # L2 (126 MB) is flushed before every timed step by overwriting a 512 MB buffer, outside the
     # step's own CUDA-event span: each step starts cold, like the first pass over a new series
-    flush = torch.empty(512 << 20, dtype=torch.uint8, device="cuda")
+    flush_mb = int(os.environ.get("BENCH_FLUSH_MB", "512"))   # dev knob: 0 disables the flush
+    flush = torch.empty(max(flush_mb, 1) << 20, dtype=torch.uint8, device="cuda")
 
     def flush_l2():
-        flush.zero_()
+        if flush_mb:
+            flush.zero_()
         torch.cuda.synchronize()
 
     for _ in range(max(args.warmup, 3)):

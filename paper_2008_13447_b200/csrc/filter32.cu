@@ -840,21 +840,13 @@ __global__ void __launch_bounds__(32, VLMP_FILTER32_WARPS_PER_SM) k_tile32(Tile3
 #ifndef VLMP_RUNS_G
 #define VLMP_RUNS_G 32            // lanes per run in k_runs (8 / 16: several runs per warp)
 #endif
-#ifndef VLMP_RUNS_MINB
-#define VLMP_RUNS_MINB 1          // k_runs: minimum resident 256-thread blocks per SM (register cap)
-#endif
-
-constexpr unsigned long long CC_EMPTY = ~0ull;
-constexpr int CC_PROBES = 8;
-__device__ __forceinline__ unsigned long long cc_hash(unsigned long long key) { return key * 0x9E3779B97F4A7C15ull; }
 
 template <int G>
-__global__ void __launch_bounds__(256, VLMP_RUNS_MINB) k_runs(const Run* __restrict__ runs, const unsigned long long* run_count,
+__global__ void __launch_bounds__(256) k_runs(const Run* __restrict__ runs, const unsigned long long* run_count,
                                              long long cap, const Prm* __restrict__ prm,
                                              const double* __restrict__ tn, const double* __restrict__ mu,
                                              int m, int e, ulonglong2* acc, unsigned long long* counters,
-                                             ulonglong2* slots, int* slot_cnt, unsigned long long* span,
-                                             CovCache cc) {
+                                             ulonglong2* slots, int* slot_cnt, unsigned long long* span) {
     if (span && threadIdx.x == 0) atomicMin(span, gtime());
     const unsigned long long cnt = *run_count;
     const long long nr = (long long)(cnt < (unsigned long long)cap ? cnt : (unsigned long long)cap);
@@ -875,32 +867,10 @@ __global__ void __launch_bounds__(256, VLMP_RUNS_MINB) k_runs(const Run* __restr
         for (int off = G / 2; off >= 1; off >>= 1) d += __shfl_xor_sync(gmask, d, off, G);
         return d;
     };
-    unsigned long long hits = 0;
     for (long long q = w0; q < nr; q += nw) {
         const Run R = runs[q];
         const long long i = R.i, j = R.j;
-        // the run's first cell from the previous length's cache (exact co-moment there + one
-        // Welford step, C_m = C_{m-1} + (m-1)/m (x - mu_x)(y - mu_y)), else a direct dot product
-        int found = 0; double cprev = 0.0;
-        if (cc.key_in && gl == 0) {
-            const unsigned long long key = ((unsigned long long)i << 32) | (unsigned long long)j;
-            unsigned long long h = cc_hash(key);
-            for (int pr = 0; pr < CC_PROBES; ++pr, ++h) {
-                const unsigned long long k2 = cc.key_in[h & cc.mask];
-                if (k2 == key) { found = 1; cprev = cc.val_in[h & cc.mask]; break; }
-                if (k2 == CC_EMPTY) break;
-            }
-        }
-        found = __shfl_sync(gmask, found, 0, G);
-        double dot;
-        if (found) {
-            cprev = __shfl_sync(gmask, cprev, 0, G);
-            const double wgt = (double)(m - 1) / (double)m;
-            dot = fma(wgt * (tn[i + m - 1] - cc.mu_prev[i]), tn[j + m - 1] - cc.mu_prev[j], cprev);
-            if (gl == 0) ++hits;
-        } else {
-            dot = wdot(i, j);
-        }
+        const double dot = wdot(i, j);
         double carry = dot;
         // magnitude carried by the recurrence: |cov at the last exact point| + sum |steps| since.
         // Its rounding error is below 2^-47 of that (<= 160 roundings of 2^-53 each); a cell whose
@@ -944,14 +914,6 @@ __global__ void __launch_bounds__(256, VLMP_RUNS_MINB) k_runs(const Run* __restr
                 carry = __shfl_sync(gmask, cv, G - 1, G);
                 mag += (double)__shfl_sync(gmask, at, G - 1, G);
             }
-            if (valid && ok_diag && cc.key_out) {   // this cell's exact co-moment for the next length
-                const unsigned long long key = ((unsigned long long)(i + k) << 32) | (unsigned long long)(j + k);
-                unsigned long long h = cc_hash(key);
-                for (int pr = 0; pr < CC_PROBES; ++pr, ++h) {
-                    const unsigned long long prev = atomicCAS(cc.key_out + (h & cc.mask), CC_EMPTY, key);
-                    if (prev == CC_EMPTY || prev == key) { cc.val_out[h & cc.mask] = cv; break; }
-                }
-            }
             if (valid && ok_diag) {
                 const double r = fma(-(cv * ii), ij, 1.0);
                 const float h = __int_as_float(__double2hiint(r));
@@ -979,10 +941,8 @@ __global__ void __launch_bounds__(256, VLMP_RUNS_MINB) k_runs(const Run* __restr
     for (int off = 16; off >= 1; off >>= 1) {
         merged += __shfl_xor_sync(FULLMASK, merged, off);
         cells += __shfl_xor_sync(FULLMASK, cells, off);
-        hits += __shfl_xor_sync(FULLMASK, hits, off);
     }
     if (lane == 0 && (merged | cells)) { atomicAdd(counters + 0, merged); atomicAdd(counters + 4, cells); }
-    if (lane == 0 && hits) atomicAdd(counters + 5, hits);
     if (span && lane == 0) atomicMax(span + 1, gtime());
 }
 
@@ -1025,7 +985,7 @@ void build_tiles32(const std::vector<int2>& tiles, long long band_lo, std::vecto
 int launch_filter32(vlmp_session* s, cudaStream_t st, const Prm* prm, const double* mu, long long N, int m, int e,
                     long long dl, int S, int update_seeds, long long n_t32, const int* forced,
                     ulonglong2* acc, Run* runs, unsigned long long* run_count, long long run_cap,
-                    ulonglong2* slots, int* slot_cnt, unsigned long long* span, const CovCache* cc) {
+                    ulonglong2* slots, int* slot_cnt, unsigned long long* span) {
     const long long A = s->A;
     const long long nb = A / 256 + 1;
     Prep32Args pa{prm, s->d_cum, s->d_cum2, s->d_p32, s->d_cq32, s->d_magblk, nb, N, A, m, s->sscale,
@@ -1038,9 +998,8 @@ int launch_filter32(vlmp_session* s, cudaStream_t st, const Prm* prm, const doub
                       update_seeds, s->sscale, span, s->d_cq4, s->d_pf4};
         // span: [0, 1] k_tile32's and [2, 3] k_runs' first start / last end (bench.py's roofline)
         k_tile32<<<(unsigned)n_t32, 32, sizeof(SmemT), st>>>(ta);
-        const CovCache none{nullptr, nullptr, nullptr, nullptr, 0, nullptr};
         k_runs<VLMP_RUNS_G><<<148 * 8, 256, 0, st>>>(runs, run_count, run_cap, prm, s->d_tn, mu, m, e, acc, s->d_counters,
-                                        slots, slot_cnt, span ? span + 2 : nullptr, cc ? *cc : none);
+                                        slots, slot_cnt, span ? span + 2 : nullptr);
     }
     return 0;
 }

@@ -99,9 +99,6 @@ struct Bound2Args {
     int exact;                     // bound = exact key of the chosen candidate (FP32 walk)
 };
 
-#ifndef VLMP_COVCACHE
-#define VLMP_COVCACHE 0    // k_runs: cross-length cache of exact co-moments (VLMP_COVCACHE=0 env: off)
-#endif
 #ifndef VLMP_BOUND_ADJ
 #define VLMP_BOUND_ADJ 0   // FP32 path: also bound by the own winner's neighbouring diagonals
 #endif
@@ -1253,27 +1250,6 @@ static int profile_impl(vlmp_session* s, int32_t lmin, int32_t lmax, int64_t ban
         s->h_span_cap = (size_t)4 * n_len;
     }
     if (fp32 && (rc = filter32_setup())) return rc;
-    // k_runs' cross-length co-moment cache: two tables (ping-pong by length parity) of 32 slots
-    // per offset (power of two); allocation failure only disables it
-    bool use_cc = fp32 && VLMP_COVCACHE && !(getenv("VLMP_COVCACHE") && atoi(getenv("VLMP_COVCACHE")) == 0);
-    if (use_cc) {
-        size_t want = 1;
-        while (want < (size_t)32 * (size_t)N0) want <<= 1;
-        if (want > s->cc_cap) {
-            for (int b = 0; b < 2; ++b) {
-                if (s->d_cc_key[b]) cudaFree(s->d_cc_key[b]);
-                if (s->d_cc_val[b]) cudaFree(s->d_cc_val[b]);
-                s->d_cc_key[b] = nullptr; s->d_cc_val[b] = nullptr;
-            }
-            s->cc_cap = 0;
-            bool ok = true;
-            for (int b = 0; b < 2 && ok; ++b)
-                ok = cudaMalloc((void**)&s->d_cc_key[b], want * sizeof(unsigned long long)) == cudaSuccess &&
-                     cudaMalloc((void**)&s->d_cc_val[b], want * sizeof(double)) == cudaSuccess;
-            if (ok) s->cc_cap = want;
-            else { cudaGetLastError(); use_cc = false; }
-        }
-    }
 
     const bool dumping = getenv("VLMP_DUMP_PRM") || getenv("VLMP_DUMP_RUNS");
     // a CUDA graph of the whole sequence (VLMP_GRAPH=0 / dumping: plain stream launches). Inside
@@ -1317,7 +1293,6 @@ static int profile_impl(vlmp_session* s, int32_t lmin, int32_t lmax, int64_t ban
                 klaunch += 3;
             }
         }
-        bool prev_cached = false;   // the previous length filled its co-moment cache table
         for (int li = (li_lo <= li_hi ? li_lo : 0); li <= li_hi; ++li) {
             const int m = lmin + li;
             const long long N = n - m + 1;
@@ -1348,15 +1323,6 @@ static int profile_impl(vlmp_session* s, int32_t lmin, int32_t lmax, int64_t ban
             timed.push_back(li);
             if (!use_graph) CU(cudaEventRecord(s->lev[2 * li], st));
             unsigned long long* span = s->d_span + 4 * li;
-            CovCache cc{nullptr, nullptr, nullptr, nullptr, 0, nullptr};
-            if (use_cc && T) {
-                const int b = li & 1;
-                CU(cudaMemsetAsync(s->d_cc_key[b], 0xFF, s->cc_cap * sizeof(unsigned long long), st));
-                cc.key_out = s->d_cc_key[b]; cc.val_out = s->d_cc_val[b];
-                cc.mask = (unsigned long long)s->cc_cap - 1;
-                if (prev_cached) { cc.key_in = s->d_cc_key[b ^ 1]; cc.val_in = s->d_cc_val[b ^ 1]; cc.mu_prev = mu_prev; }
-            }
-            bool cached_now = false;
             if (T) {
                 TileArgs ta{prm, mu, s->d_tn, s->d_tiles, s->d_seeds, s->d_acc + (long long)li * A,
                             s->d_counters, s->d_log, s->d_logcnt + li, eff_cap,
@@ -1374,9 +1340,7 @@ static int profile_impl(vlmp_session* s, int32_t lmin, int32_t lmax, int64_t ban
                         k_fill_acc<<<blocks(A, 256), 256, 0, st>>>(s->d_acc + (long long)li * A, A);
                         if ((rc2 = launch_filter32(s, st, prm, mu, N, m, e, dl, S, ta.update_seeds, T32,
                                                    s->d_forced + li, s->d_acc + (long long)li * A, runs,
-                                                   s->d_logcnt + li, run_cap, nullptr, nullptr, span,
-                                                   use_cc ? &cc : nullptr))) return rc2;
-                        cached_now = use_cc;
+                                                   s->d_logcnt + li, run_cap, nullptr, nullptr, span))) return rc2;
                         klaunch += 5; n_walk += 1; walked.push_back(li);
                     } else {
                         k_qprep<<<blocks(A, 256), 256, 0, st>>>(prm, s->d_colq, s->d_rowq, N, A, s->sscale,
@@ -1390,9 +1354,8 @@ static int profile_impl(vlmp_session* s, int32_t lmin, int32_t lmax, int64_t ban
                 else if (fp32) {
                     if ((rc2 = launch_filter32(s, st, prm, mu, N, m, e, dl, S, ta.update_seeds, T32, s->d_forced + li,
                                                s->d_acc + (long long)li * A, runs, s->d_logcnt + li, run_cap,
-                                               nullptr, nullptr, span, use_cc ? &cc : nullptr)))
+                                               nullptr, nullptr, span)))
                         return rc2;
-                    cached_now = use_cc;
                     klaunch += 2; n_walk += 1; walked.push_back(li);
                     if (dumping && (rc2 = debug_dump(st, li, prm, N, runs, s->d_logcnt + li, run_cap))) return rc2;
                 } else {
@@ -1403,7 +1366,6 @@ static int profile_impl(vlmp_session* s, int32_t lmin, int32_t lmax, int64_t ban
                 }
                 launches += 1; klaunch += 1;
             }
-            prev_cached = cached_now;
             if (!use_graph) CU(cudaEventRecord(s->lev[2 * li + 1], st));
             CU(cudaGetLastError());
             for (long long b = band_lo; b < band_hi; ++b) {
@@ -1550,8 +1512,6 @@ int settle_profile(vlmp_session* s, bool* redone) {
         s->stats[2] = pr.executed; s->stats[3] = W;
         s->stats[5] = pr.launches; s->stats[6] = pr.n_filtered; s->stats[7] = pr.n_full; s->stats[8] = (double)h[0];
         s->stats[9] = pr.klaunch; s->stats[11] = (double)h[2];
-        if (getenv("VLMP_CC_DEBUG"))
-            fprintf(stderr, "k_runs: %llu run cells, %llu runs started from the co-moment cache\n", h[4], h[5]);
         s->stats[12] = n_fix; s->stats[14] = n_forced; s->stats[15] = max_log;
         s->stats[16] = pr.fp32 ? 1.0 : 0.0; s->stats[17] = pr.fp32 ? max_log : 0.0; s->stats[18] = (double)h[4];
         s->stats[19] = (double)pr.S; s->stats[22] = (double)pr.walked.size(); s->stats[23] = pr.graph ? 1.0 : 0.0;

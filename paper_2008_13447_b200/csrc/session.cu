@@ -89,10 +89,6 @@ void vlmp_destroy(vlmp_session* s) {
     if (s->g_exec) cudaGraphExecDestroy(s->g_exec);
     if (s->h_chk) cudaFreeHost(s->h_chk);
     pruned_free(s);
-    for (int b = 0; b < 2; ++b) {
-        if (s->d_cc_key[b]) cudaFree(s->d_cc_key[b]);
-        if (s->d_cc_val[b]) cudaFree(s->d_cc_val[b]);
-    }
     if (s->stream) cudaStreamDestroy(s->stream);
     delete s;
 }

@@ -297,9 +297,6 @@ struct vlmp_session {
     std::vector<double> g_key;
     std::vector<double> g_cnt; std::vector<int> g_timed, g_walked;   // its host-side counters
     vlmp_impl::PrunedState* pp = nullptr;                  // pruned discord scan (pruned.cu)
-    unsigned long long* d_cc_key[2] = {nullptr, nullptr};  // k_runs' cross-length co-moment cache
-    double* d_cc_val[2] = {nullptr, nullptr};              // (ping-pong by length parity)
-    size_t cc_cap = 0;
 };
 
 namespace vlmp_impl {
@@ -308,20 +305,10 @@ int tile32_width();
 size_t tile32_smem();
 int filter32_setup();
 void build_tiles32(const std::vector<int2>& tiles, long long band_lo, std::vector<int2>& out);
-// cross-length cache of the exact co-moments k_runs evaluated (filter32.cu): k_runs reads the
-// previous length's table (a run's first cell found there costs one Welford step instead of an
-// m-term dot product) and fills this length's
-struct CovCache {
-    const unsigned long long* key_in; const double* val_in;   // previous length's (nullptr: none)
-    unsigned long long* key_out; double* val_out;             // this length's (nullptr: off)
-    unsigned long long mask;                                  // capacity - 1 (power of two)
-    const double* mu_prev;                                    // the previous length's window means
-};
 int launch_filter32(vlmp_session* s, cudaStream_t st, const Prm* prm, const double* mu, long long N, int m, int e,
                     long long dl, int S, int update_seeds, long long n_t32, const int* forced,
                     ulonglong2* acc, Run* runs, unsigned long long* run_count, long long run_cap,
-                    ulonglong2* slots = nullptr, int* slot_cnt = nullptr, unsigned long long* span = nullptr,
-                    const CovCache* cc = nullptr);
+                    ulonglong2* slots = nullptr, int* slot_cnt = nullptr, unsigned long long* span = nullptr);
 // profile.cu: wait for / check / redo a pending phase 1; device-event timings of the last run
 int settle_profile(vlmp_session* s, bool* redone);
 int mbest_impl(vlmp_session* s, int32_t lmin, int32_t lmax, int32_t mb);   // lock held by the caller
