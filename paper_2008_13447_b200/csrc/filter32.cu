@@ -42,9 +42,6 @@ constexpr int WIN = VLMP_PACKED ? 8 : D2;   // rows a column meets in one lane (
 #ifndef VLMP_PAIR_SEP
 #define VLMP_PAIR_SEP 2          // packed walk: band B = band A + VLMP_PAIR_SEP bands (1: adjacent)
 #endif
-#ifndef VLMP_ROWDUP
-#define VLMP_ROWDUP 0            // packed walk: row factors as duplicated pairs (no broadcast operands)
-#endif
 #ifndef VLMP_ROWPAIR
 #define VLMP_ROWPAIR 0           // packed walk: one pass test and branch per pair of rows
 #endif
@@ -453,9 +450,6 @@ struct Smem32p {
     float4 cq[2][GRP * CQS];     // {aA, bA, aB, bB} of the pair entering lane L at row kk: [kk * 33 + L]
     unsigned short rs[32 * 16];  // run starts per lane and cell (bits 0-7 band A, 8-15 band B)
     unsigned short msk[32 * GRP];
-#if VLMP_ROWDUP
-    unsigned long long rowd[GRP][4];   // the group's rows as duplicated pairs {df df, dg dg, b b, w w}
-#endif
 };
 
 // lane 0's outgoing pair becomes lane 31's incoming one. Adjacent bands (PSEP = 256): (lane 0's
@@ -731,26 +725,9 @@ __global__ void __launch_bounds__(32, VLMP_FILTER32_WARPS_PER_SM) k_tile32(Tile3
     for (int g = 0; g < ngroups; ++g) {
         const int b = g & 1;
         if (g + 1 < ngroups) stage(g + 1, b ^ 1);
-#if VLMP_ROWDUP
-        // full-pair FFMA2 operands instead of scalar broadcasts
-        if (lane < GRP) {
-            const float4 r = sm.row[b][lane];
-            sm.rowd[lane][0] = pk2(r.x, r.x); sm.rowd[lane][1] = pk2(r.y, r.y);
-            sm.rowd[lane][2] = pk2(r.z, r.z); sm.rowd[lane][3] = pk2(r.w, r.w);
-        }
-        __syncwarp();
-#endif
 #pragma unroll
         for (int kk = 0; kk < GRP; ++kk) {
-#if VLMP_ROWDUP
-            const ulonglong2 r01 = *reinterpret_cast<const ulonglong2*>(&sm.rowd[kk][0]);
-            const ulonglong2 r23 = *reinterpret_cast<const ulonglong2*>(&sm.rowd[kk][2]);
-            const float4 pr = make_float4(lo2(r01.x), lo2(r01.y), lo2(r23.x), lo2(r23.y));
-            const u64 RX = r01.x, RY = r01.y, RZ = r23.x;
-#else
             const float4 pr = sm.row[b][kk];
-            const u64 RX = bc2(pr.x), RY = bc2(pr.y), RZ = bc2(pr.z);
-#endif
             if (__builtin_expect(pass_prev, 0)) {
                 const int kp = (kk + GRP - 1) % DP;
                 unsigned mask = 0;
@@ -780,12 +757,12 @@ __global__ void __launch_bounds__(32, VLMP_FILTER32_WARPS_PER_SM) k_tile32(Tile3
 #pragma unroll
             for (int s = 0; s < DP; ++s) {
                 const int p = (s + kk) % DP;
-                cov[s] = fma2(RX, G[p], cov[s]);
-                cov[s] = fma2(F[p], RY, cov[s]);
+                cov[s] = fma2(bc2(pr.x), G[p], cov[s]);
+                cov[s] = fma2(F[p], bc2(pr.y), cov[s]);
 #if VLMP_ABL_NOTEST
                 const u64 zz = cov[s] | 0x8000000080000000ull;
 #else
-                const u64 zz = fma2(NA[p], RZ, cov[s]);
+                const u64 zz = fma2(NA[p], bc2(pr.z), cov[s]);
 #endif
                 z[s] = (unsigned)zz; z[s + 8] = (unsigned)(zz >> 32);
             }
@@ -837,6 +814,9 @@ __global__ void __launch_bounds__(32, VLMP_FILTER32_WARPS_PER_SM) k_tile32(Tile3
 // slots == nullptr: fold into the 1-best accumulators; else (m-best mode, m > 1 discords) append
 // every cell that passes an exact test to its offset's candidate slots (SLOT_CAP per offset;
 // k_select_m keeps the m smallest and recomputes offsets whose slots overflowed)
+#ifndef VLMP_WDOT_ACC2
+#define VLMP_WDOT_ACC2 0          // k_runs: two partial sums per lane in the direct dot product
+#endif
 #ifndef VLMP_RUNS_G
 #define VLMP_RUNS_G 32            // lanes per run in k_runs (8 / 16: several runs per warp)
 #endif
@@ -861,8 +841,20 @@ __global__ void __launch_bounds__(256) k_runs(const Run* __restrict__ runs, cons
     // group-cooperative centred dot product of windows (a, b): lane-strided terms, fixed xor tree
     auto wdot = [&](long long a_, long long b_) {
         const double ma = mu[a_], mb = mu[b_];
+#if VLMP_WDOT_ACC2
+        // two interleaved partial sums per lane (a shorter dependent FMA chain), fixed order
+        double d = 0.0, d2 = 0.0;
+        int k = gl;
+        for (; k + G < m; k += 2 * G) {
+            d = fma(tn[a_ + k] - ma, tn[b_ + k] - mb, d);
+            d2 = fma(tn[a_ + k + G] - ma, tn[b_ + k + G] - mb, d2);
+        }
+        if (k < m) d = fma(tn[a_ + k] - ma, tn[b_ + k] - mb, d);
+        d += d2;
+#else
         double d = 0.0;
         for (int k = gl; k < m; k += G) d = fma(tn[a_ + k] - ma, tn[b_ + k] - mb, d);
+#endif
 #pragma unroll
         for (int off = G / 2; off >= 1; off >>= 1) d += __shfl_xor_sync(gmask, d, off, G);
         return d;
@@ -889,15 +881,19 @@ __global__ void __launch_bounds__(256) k_runs(const Run* __restrict__ runs, cons
                 ii = pi.inv; ij = pj.inv; ui = pi.U; uj = pj.U;
             }
             float at = __double2float_ru(fabs(term));   // a bound: FP32, rounded up, is enough
+            // inclusive scan over the chunk's nv cells only (runs are ~4 cells long on average):
+            // the steps past nv would leave lanes < nv unchanged, so the sums are the same
+            const int nv = R.len - c0 < G ? R.len - c0 : G;
 #pragma unroll
             for (int off = 1; off < G; off <<= 1) {
+                if (off >= nv) break;
                 const double t = __shfl_up_sync(gmask, term, off, G);
                 const float ta = __shfl_up_sync(gmask, at, off, G);
                 if (gl >= off) { term += t; at = __fadd_ru(at, ta); }
             }
             double cv = carry + term;
-            const double scale = 1.0 / (ii * ij);   // s_i s_j (NaN / 0 for invalid windows)
-            const bool inexact = valid && ok_diag && !((mag + (double)at) <= 8.0 * scale);
+            // |carried magnitude| <= 8 s_i s_j, i.e. (mag + at) inv_i inv_j <= 8 (NaN: invalid window)
+            const bool inexact = valid && ok_diag && !((mag + (double)at) * (ii * ij) <= 8.0);
             unsigned redo = (__ballot_sync(gmask, inexact) >> gbase) & GM;
             if (redo) {   // rare: exact direct sums for the flagged cells of this chunk
                 const unsigned tail = (__ballot_sync(gmask, valid) >> gbase) & GM;
@@ -911,8 +907,8 @@ __global__ void __launch_bounds__(256) k_runs(const Run* __restrict__ runs, cons
                 const double cl = __shfl_sync(gmask, cv, last, G);
                 carry = cl; mag = fabs(cl);
             } else {
-                carry = __shfl_sync(gmask, cv, G - 1, G);
-                mag += (double)__shfl_sync(gmask, at, G - 1, G);
+                carry = __shfl_sync(gmask, cv, nv - 1, G);
+                mag += (double)__shfl_sync(gmask, at, nv - 1, G);
             }
             if (valid && ok_diag) {
                 const double r = fma(-(cv * ii), ij, 1.0);
