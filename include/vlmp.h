@@ -173,6 +173,16 @@ int vlmp_discords_pruned(vlmp_session* s, int32_t lmin, int32_t lmax, int32_t k,
                          double* out_dist, int64_t* out_off, double* counters);
 
 /*
+ * One full row from scratch (profile.py:263-269 row_profile, the formulas of _row_arrays
+ * :235-260): for every window j of this length, dist[j] (owner-first, numpy's operation order;
+ * +inf for trivial matches and constant neighbours), f[j] the bound factor
+ * sqrt(l (1 - max(q, 0)^2)) (optional), qt[j] the dot product of the two raw windows
+ * (optional; direct FP64 sums where the reference uses FFT correlation). Arrays of
+ * n - length + 1 doubles. Needs only vlmp_set_series.
+ */
+int vlmp_row_profile(vlmp_session* s, int64_t owner, int32_t length, double* dist, double* f, double* qt);
+
+/*
  * Motif-set range queries (motifsets.py:158-165, the row_profile path of _range_members):
  * for query q, every offset j with dist(owners[q], j) < radii[q] at length lengths[q],
  * from the owner's full row with the reference formula (profile.py:235-260); trivial

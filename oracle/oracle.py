@@ -166,6 +166,39 @@ def range_row(series, owner, m, r):
     return np.flatnonzero(dist < r)
 
 
+def row_full(series, owner, m):
+    """(dist, f, qt) of one full row: profile.py:263-269 row_profile via _row_arrays
+    (profile.py:235-260) with want_f, direct dot products in place of the FFT."""
+    t = np.asarray(series.values, dtype=np.float64)
+    n = t.shape[0]
+    N = n - m + 1
+    c1, c2 = series._cum, series._cum2
+    s = c1[m:] - c1[:-m]
+    ss = c2[m:] - c2[:-m]
+    mu = s / m
+    var = ss / m - mu * mu
+    np.maximum(var, 0.0, out=var)
+    sd = np.sqrt(var)
+    from numpy.lib.stride_tricks import sliding_window_view
+    qt = sliding_window_view(t, m)[:N] @ t[owner:owner + m]
+    with np.errstate(invalid="ignore", divide="ignore"):
+        q_raw = (qt - m * mu[owner] * mu) / (m * sd[owner] * sd)
+        rad = 2.0 * m * (1.0 - q_raw)
+    np.maximum(rad, 0.0, out=rad)
+    dist = np.sqrt(rad)
+    bad = ~(sd >= series.sigma_floor)
+    e = (m + 1) // 2
+    lo, hi = max(0, owner - e + 1), min(N, owner + e)
+    dist[bad] = np.inf
+    dist[lo:hi] = np.inf
+    qc = np.clip(q_raw, -1.0, 1.0)
+    np.maximum(qc, 0.0, out=qc)
+    f = np.sqrt(m * (1.0 - qc * qc))
+    f[bad] = np.inf
+    f[lo:hi] = np.inf
+    return dist, f, qt
+
+
 def discords_m1(vals, m, k):
     lib = load()
     v = np.ascontiguousarray(vals, dtype=np.float64)

@@ -16,7 +16,7 @@ from .results import (VALMP, DiscordMatrix, DiscordScan, LengthTrace, MatrixProf
                       VariableLengthDiscordMatrix, top_variable_length_motif,
                       update_fixed_length_discords, update_valmp,
                       update_variable_length_discords)
-from .api import (MiningResult, compute_matrix_profile, mine, motifs_per_length,
+from .api import (MiningResult, compute_matrix_profile, mine, motifs_per_length, row_profile,
                   topkm_discord_discovery, validate_range, valmod)
 from .motifsets import MotifSet, compute_var_length_motif_sets, validate_disjoint
 
@@ -27,7 +27,8 @@ __all__ = [
     "MatrixProfile", "PairRanking", "ProfileResult", "RankedPair", "RunTrace",
     "VariableLengthDiscordMatrix", "top_variable_length_motif",
     "update_fixed_length_discords", "update_valmp", "update_variable_length_discords",
-    "compute_matrix_profile", "mine", "MiningResult", "motifs_per_length", "topkm_discord_discovery",
+    "compute_matrix_profile", "mine", "MiningResult", "motifs_per_length", "row_profile",
+    "topkm_discord_discovery",
     "validate_range", "valmod", "MotifSet", "compute_var_length_motif_sets", "validate_disjoint",
     "SeriesMineError", "EmptySeriesError", "NonFiniteError", "LengthExceedsSeriesError",
     "OutOfRangeError", "ZeroVarianceError", "SeriesTooShortError", "AllConstantError",

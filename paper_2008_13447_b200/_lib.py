@@ -47,6 +47,7 @@ SIGNATURES = {
     "vlmp_get_profile_m": (C.c_int, [C.c_void_p, C.c_int32, C.c_void_p, C.c_void_p]),
     "vlmp_discords_m": (C.c_int, [C.c_void_p, C.c_int32, C.c_void_p, C.c_void_p]),
     "vlmp_stats": (C.c_int, [C.c_void_p, C.c_void_p, C.c_int32]),
+    "vlmp_row_profile": (C.c_int, [C.c_void_p, C.c_int64, C.c_int32, C.c_void_p, C.c_void_p, C.c_void_p]),
     "vlmp_event_record": (C.c_int, [C.c_void_p, C.c_int32]),
     "vlmp_event_elapsed": (C.c_int, [C.c_void_p, C.POINTER(C.c_float)]),
     "vlmp_measure_fp64_peak": (C.c_int, [C.c_void_p, _c_double_p]),
@@ -253,6 +254,14 @@ class Session:
         self._check(self.lib.vlmp_discords_pruned(self.h, int(lmin), int(lmax), int(k), int(m), int(p),
                                                   _ptr(d), _ptr(o), _ptr(c)))
         return d, o, c
+
+    def row_profile(self, owner, length, want_f=False):
+        """(dist, f or None, qt) of one full row (vlmp_row_profile)."""
+        N = self.n - int(length) + 1
+        d = np.empty(N); qt = np.empty(N); f = np.empty(N) if want_f else None
+        self._check(self.lib.vlmp_row_profile(self.h, int(owner), int(length), _ptr(d),
+                                              _ptr(f) if want_f else None, _ptr(qt)))
+        return d, f, qt
 
     def stats(self):
         out = np.zeros(24)

@@ -275,6 +275,24 @@ def topkm_discord_discovery(series, lmin: int, lmax: int, k: int, m: int, p: int
     return DiscordScan(merged, per_length)
 
 
+def row_profile(series, i: int, length: int, want_f: bool = False):
+    """One full distance row from scratch (profile.py:263-269): (dist, f_row or None, qt_row)
+    over every window of this length, with `_row_arrays`' formulas (profile.py:235-260) --
+    trivial matches and constant neighbours +inf. The dot products are direct FP64 sums on the
+    GPU (the reference correlates by FFT; they agree within ~1e-11 relative)."""
+    series = as_series(series)
+    if length < 4 or 2 * length > series.n:
+        raise E.SeriesTooShortError(f"need 4 <= length <= n/2 (length={length}, n={series.n})")
+    if not 0 <= i <= series.n - length:
+        raise E.OutOfRangeError(f"window {i} of length {length} outside the series (n={series.n})")
+    sess = _lib.session(_device())
+    with sess.lock:
+        sess.generation += 1
+        sess.set_series(series.values, series._cum, series._cum2, series.sigma_floor)
+        dist, f, qt = sess.row_profile(i, length, want_f=want_f)
+    return dist, f, qt
+
+
 def compute_matrix_profile(series, length: int, p: int, m_track: int = 0,
                            threads: int = 1) -> ProfileResult:
     """Exact matrix profile at one length (partials are not materialised)."""

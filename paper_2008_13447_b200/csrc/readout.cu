@@ -255,6 +255,45 @@ __global__ void k_range_query(RangeArgs a) {
     }
 }
 
+// One full row from scratch (profile.py:263-269 row_profile -> _row_arrays :235-260): dot
+// products qt_j = sum_k t[i+k] t[j+k] (direct FP64; the reference uses FFT correlation, within
+// ~1e-11), window statistics as moving_stats, then the owner-first distance and bound factor in
+// numpy's operation order; trivial cells and constant neighbours are +inf. One thread per column,
+// the owner window staged in shared memory.
+struct RowArgs {
+    const double* tn; const double* cum; const double* cum2;
+    long long n, i; int m; double floor_;
+    double* dist; double* f; double* qt;
+};
+
+__global__ void k_row_profile(RowArgs a) {
+    extern __shared__ double xo[];
+    for (int k = threadIdx.x; k < a.m; k += blockDim.x) xo[k] = a.tn[a.i + k];
+    __syncthreads();
+    const long long N = a.n - a.m + 1;
+    const long long j = blockIdx.x * (long long)blockDim.x + threadIdx.x;
+    if (j >= N) return;
+    double qt = 0.0;
+    for (int k = 0; k < a.m; ++k) qt = fma(xo[k], a.tn[j + k], qt);
+    double mui, sdi, muj, sdj;
+    win_stats(a.cum, a.cum2, a.i, a.m, mui, sdi);
+    win_stats(a.cum, a.cum2, j, a.m, muj, sdj);
+    const long long e = (a.m + 1) / 2;
+    const long long lo = a.i - e + 1 > 0 ? a.i - e + 1 : 0, hi = a.i + e < N ? a.i + e : N;
+    const bool bad = !(sdj >= a.floor_) || (j >= lo && j < hi);
+    const double L = (double)a.m;
+    const double q = __ddiv_rn(__dsub_rn(qt, __dmul_rn(__dmul_rn(L, mui), muj)), __dmul_rn(__dmul_rn(L, sdi), sdj));
+    double rad = __dmul_rn(__dmul_rn(2.0, L), __dsub_rn(1.0, q));
+    if (rad < 0.0) rad = 0.0;                    // np.maximum(rad, 0): NaN stays NaN
+    a.dist[j] = bad ? INFINITY : __dsqrt_rn(rad);
+    if (a.f) {
+        double qc = q < -1.0 ? -1.0 : (q > 1.0 ? 1.0 : q);   // np.clip (NaN stays NaN)
+        if (qc < 0.0) qc = 0.0;
+        a.f[j] = bad ? INFINITY : __dsqrt_rn(__dmul_rn(L, __dsub_rn(1.0, __dmul_rn(qc, qc))));
+    }
+    if (a.qt) a.qt[j] = qt;
+}
+
 // VALMP improvement events with norm <= tau (motifsets.py:105-117 stream)
 struct EvArgs {
     const double* mp; const int* ip; double tau;
@@ -487,6 +526,29 @@ int vlmp_ranking_events(vlmp_session* s, double tau, int64_t cap, int64_t* ev_of
     }
     CU(cudaStreamSynchronize(st));
     *count = (int64_t)hc;
+    return 0;
+}
+
+int vlmp_row_profile(vlmp_session* s, int64_t owner, int32_t length, double* dist, double* f, double* qt) {
+    if (!s || !dist) return fail(VLMP_E_INVALID_PARAMETERS, "null argument");
+    if (s->n <= 0) return fail(VLMP_E_STATE, "no series uploaded");
+    if (length < 4 || 2LL * length > s->n || owner < 0 || owner > s->n - length)
+        return fail(VLMP_E_INVALID_PARAMETERS, "row owner/length outside the series");
+    std::lock_guard<std::mutex> g(s->lock);
+    CU(cudaSetDevice(s->device));
+    cudaStream_t st = s->stream;
+    const long long N = s->n - length + 1;
+    double* d = nullptr;
+    CU(cudaMallocAsync((void**)&d, 3 * N * sizeof(double), st));
+    RowArgs ra{s->d_tn, s->d_cum, s->d_cum2, s->n, (long long)owner, length, s->floor_, d, f ? d + N : nullptr,
+               qt ? d + 2 * N : nullptr};
+    k_row_profile<<<blocks(N, 256), 256, (size_t)length * sizeof(double), st>>>(ra);
+    CU(cudaGetLastError());
+    CU(cudaMemcpyAsync(dist, d, N * sizeof(double), cudaMemcpyDeviceToHost, st));
+    if (f) CU(cudaMemcpyAsync(f, d + N, N * sizeof(double), cudaMemcpyDeviceToHost, st));
+    if (qt) CU(cudaMemcpyAsync(qt, d + 2 * N, N * sizeof(double), cudaMemcpyDeviceToHost, st));
+    CU(cudaFreeAsync(d, st));
+    CU(cudaStreamSynchronize(st));
     return 0;
 }
 

@@ -414,3 +414,38 @@ def test_log_overflow_reruns_exactly(monkeypatch):
     for L, (mp, ip) in zip(range(32, 49), want):
         got = run.profile(L)
         assert np.array_equal(got[1], ip) and np.array_equal(got[0], mp), L
+
+
+def test_row_profile_matches_reference(oracle_mod):
+    """row_profile (vlmp_row_profile, profile.py:263-269) against the reference's own
+    row_profile fixtures (tests/golden/make_rowprofile_golden.py, FFT dot products) and against
+    the oracle's direct-sum row on config 2's series."""
+    g = load_golden("rowprofile")
+    names = sorted({k[:-5] for k in g if k.endswith("_meta")})
+    for name in names:
+        i, L = (int(x) for x in g[name + "_meta"])
+        s = vl.ingest(g[name.split("_")[0] + "_t"])
+        d, f, qt = vl.row_profile(s, i, L, want_f=True)
+        rd, rf, rqt = g[name + "_dist"], g[name + "_f"], g[name + "_qt"]
+        assert np.array_equal(np.isinf(d), np.isinf(rd)), name
+        fin = np.isfinite(rd)
+        assert np.allclose(d[fin], rd[fin], rtol=0, atol=1e-9), name
+        assert np.allclose(f[fin], rf[fin], rtol=0, atol=1e-9), name
+        assert np.allclose(qt, rqt, rtol=1e-9, atol=1e-9 * np.abs(rqt).max()), name
+        d2, f2, qt2 = vl.row_profile(s, i, L)
+        assert f2 is None and np.array_equal(d2, d) and np.array_equal(qt2, qt)
+    s = vl.ingest(gen.series_for(2))
+    for i, L in ((0, 256), (5234, 300), (40000, 384), (s.n - 384, 384)):
+        d, f, qt = vl.row_profile(s, i, L, want_f=True)
+        od, of, oqt = oracle_mod.row_full(s, i, L)
+        assert np.array_equal(np.isinf(d), np.isinf(od)), (i, L)
+        fin = np.isfinite(od)
+        assert np.allclose(d[fin], od[fin], rtol=1e-9, atol=1e-9), (i, L)
+        assert np.allclose(f[fin], of[fin], rtol=1e-9, atol=1e-9), (i, L)
+        j = int(np.argmin(d))     # the row's nearest neighbour equals the exhaustive profile's
+        mp, ip = oracle_mod.profile(s, L, nthreads=1, row_lo=i, row_hi=i + 1)
+        assert j == ip[i] or abs(d[j] - d[ip[i]]) <= 1e-9 * d[j], (i, L, j, ip[i])
+    with pytest.raises(vl.OutOfRangeError):
+        vl.row_profile(s, s.n - 10, 256)
+    with pytest.raises(vl.SeriesTooShortError):
+        vl.row_profile(s, 0, 3)

@@ -202,3 +202,38 @@ def test_batch_discord_merge_equals_sequential(seed):
     assert np.array_equal(seq.dist, bat.dist)
     assert np.array_equal(seq.offset, bat.offset)
     assert np.array_equal(seq.length, bat.length)
+
+
+def test_frontend_swaps_the_reference_entry_points():
+    """paper_2008_13447_b200.frontend installs the drop-in into the reference's package and CLI
+    (no GPU work: only the swap is checked); skipped when the reference is not installed."""
+    import importlib
+    import os
+    import sys
+    ref = os.path.join(os.path.dirname(os.path.dirname(os.path.abspath(__file__))), "baseline", "_ref")
+    if not os.path.isdir(os.path.join(ref, "seriesmine")):
+        pytest.skip("baseline/_ref not installed")
+    from paper_2008_13447_b200 import frontend
+    import paper_2008_13447_b200 as drop_in
+    sm = frontend._import_reference()
+    saved = {k: getattr(sm.cli, k) for k in ("valmod", "topkm_discord_discovery", "compute_matrix_profile",
+                                            "compute_var_length_motif_sets")}
+    saved_pkg = {k: getattr(sm, k) for k in ("valmod", "topkm_discord_discovery", "compute_var_length_motif_sets")}
+    from paper_2008_13447_b200 import exceptions as dx
+    saved_exc = {k: getattr(dx, k) for k in dx._NAMES}
+    try:
+        orig = frontend.swap_into(sm)
+        assert orig["valmod"] is saved["valmod"]
+        assert sm.cli.valmod is drop_in.valmod and sm.valmod is drop_in.valmod
+        assert sm.cli.topkm_discord_discovery is drop_in.topkm_discord_discovery
+        assert sm.cli.compute_matrix_profile is drop_in.compute_matrix_profile
+        assert sm.cli.compute_var_length_motif_sets is drop_in.compute_var_length_motif_sets
+        runner = frontend._gpu_bench_runner(sm, orig)
+        assert callable(runner)
+    finally:
+        for k, v in saved.items():
+            setattr(sm.cli, k, v)
+        for k, v in saved_pkg.items():
+            setattr(sm, k, v)
+        for k, v in saved_exc.items():
+            setattr(dx, k, v)

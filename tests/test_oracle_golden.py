@@ -125,3 +125,22 @@ def test_motif_sets_oracle_rows_match_reference(name, oracle_mod):
         got = [(st.anchor, st.length, st.radius, st.members.tolist())
                for st in expand_sets(pairs, rows, rf)]
         assert got == golden_sets(g, tag), (name, tag)
+
+
+def test_row_full_matches_reference_row_profile(oracle_mod):
+    """oracle.row_full (direct dot products) against the reference's own row_profile
+    (FFT correlation; tests/golden/make_rowprofile_golden.py): same +inf cells, distances and
+    bound factors within 1e-9, dot products within 1e-9 relative."""
+    g = load_golden("rowprofile")
+    names = sorted({k[:-5] for k in g if k.endswith("_meta")})
+    assert names
+    for name in names:
+        i, L = (int(x) for x in g[name + "_meta"])
+        s = ingest(g[name.split("_")[0] + "_t"])
+        d, f, qt = oracle_mod.row_full(s, i, L)
+        rd, rf, rqt = g[name + "_dist"], g[name + "_f"], g[name + "_qt"]
+        assert np.array_equal(np.isinf(d), np.isinf(rd)), name
+        fin = np.isfinite(rd)
+        assert np.allclose(d[fin], rd[fin], rtol=0, atol=1e-9), name
+        assert np.allclose(f[fin], rf[fin], rtol=0, atol=1e-9), name
+        assert np.allclose(qt, rqt, rtol=1e-9, atol=1e-9 * np.abs(rqt).max()), name
