@@ -746,10 +746,8 @@ __global__ void __launch_bounds__(32, VLMP_FILTER32_WARPS_PER_SM) k_tile32(Tile3
             {   // rotation: phys (kk-1) mod 8 receives lane+1's outgoing pair
                 const int q = (kk + DP - 1) % DP;
                 if (lane == 0 && kk == 0) fresh_pair(F[q], G[q], sm.fresh[b][0]);
-#if !VLMP_ABL_NOSHFL       // (dev ablations: timing only, results are wrong)
                 F[q] = __shfl_sync(FULLMASK, F[q], (lane + 1) & 31);
                 G[q] = __shfl_sync(FULLMASK, G[q], (lane + 1) & 31);
-#endif
                 const float4 cq = sm.cq[b][kk * CQS + lane];
                 NA[q] = pk2(fmaxf(-cq.x, __fmul_ru(-pr.w, cq.y)), fmaxf(-cq.z, __fmul_ru(-pr.w, cq.w)));
             }
@@ -759,11 +757,7 @@ __global__ void __launch_bounds__(32, VLMP_FILTER32_WARPS_PER_SM) k_tile32(Tile3
                 const int p = (s + kk) % DP;
                 cov[s] = fma2(bc2(pr.x), G[p], cov[s]);
                 cov[s] = fma2(F[p], bc2(pr.y), cov[s]);
-#if VLMP_ABL_NOTEST
-                const u64 zz = cov[s] | 0x8000000080000000ull;
-#else
                 const u64 zz = fma2(NA[p], bc2(pr.z), cov[s]);
-#endif
                 z[s] = (unsigned)zz; z[s + 8] = (unsigned)(zz >> 32);
             }
             {   // sign bits ANDed by a depth-3 tree of 3-input LOP3s (left to itself the compiler
@@ -773,11 +767,7 @@ __global__ void __launch_bounds__(32, VLMP_FILTER32_WARPS_PER_SM) k_tile32(Tile3
                 const unsigned t4 = and3(z[6], z[14], z[7]);
                 z[0] = and3(and3(t0, t1, t2), t3, and3(t4, z[15], ~0u));
             }
-#if VLMP_ABL_NOBRANCH
-            nslow += z[0] >> 31;
-#else
             pass_prev = (int)z[0] >= 0;
-#endif
             bprev = pr.z;
             if (kk + 1 < GRP && lane == 0) fresh_pair(F[kk % DP], G[kk % DP], sm.fresh[b][kk + 1]);
         }
