@@ -860,6 +860,8 @@ static int pp_replay_length(vlmp_session* s, int m, const Prm* prm, const double
     const int chunks = (int)((N + RC_COLS - 1) / RC_COLS);
     const size_t smem = ((size_t)((m + 1) & ~1) + RC_COLS + m + 8) * sizeof(double);
     const size_t bsmem = ((size_t)((m + 1) & ~1) + PB_W + m + 16) * sizeof(double);
+    if (blocks_path && bsmem + sizeof(PBSmem) > 227 * 1024)
+        return fail(VLMP_E_INVALID_PARAMETERS, "pruned scan: window length too large for a row block's shared memory");
     if (blocks_path) CU(cudaFuncSetAttribute(k_pp_block, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bsmem));
     else CU(cudaFuncSetAttribute(k_pp_rows, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
     *rows_out = 0; *gave_up = false; *stops = 0;
@@ -988,6 +990,9 @@ int pruned_impl(vlmp_session* s, int lmin, int lmax, int k, int mb, int P, doubl
     s->stats[0] = ms; s->stats[7] = (double)full_lengths;
     s->stats_dirty = false;
     s->mbest = 0;                    // d_ipm / d_mpm now hold the last full length only
+    // the 1-best buffers describe one fallback length, not a profile of [lmin, lmax]: read-offs
+    // of the session's profile state must not pick them up
+    s->have_profile = false; s->have_final = false; s->have_finals = false;
     return 0;
 }
 
