@@ -287,7 +287,6 @@ def row_profile(series, i: int, length: int, want_f: bool = False):
         raise E.OutOfRangeError(f"window {i} of length {length} outside the series (n={series.n})")
     sess = _lib.session(_device())
     with sess.lock:
-        sess.generation += 1
         sess.set_series(series.values, series._cum, series._cum2, series.sigma_floor)
         dist, f, qt = sess.row_profile(i, length, want_f=want_f)
     return dist, f, qt

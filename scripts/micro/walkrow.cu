@@ -16,7 +16,7 @@ __device__ __forceinline__ unsigned and3(unsigned x, unsigned y, unsigned z) {
 constexpr int DP = 8, GRP = 8, CQS = 33;
 
 template <int F_TEST, int F_TREE, int F_BR, int F_SH, int F_LD>
-__global__ void __launch_bounds__(32, 16) k_walk(const float4* rows, const float4* cqs, u64* out, int iters) {
+__global__ void __launch_bounds__(32, 12) k_walk(const float4* rows, const float4* cqs, u64* out, int iters) {
     __shared__ float4 srow[GRP];
     __shared__ float4 scq[GRP * CQS];
     __shared__ unsigned short msk[32 * GRP];
@@ -34,18 +34,28 @@ __global__ void __launch_bounds__(32, 16) k_walk(const float4* rows, const float
     float4 prn = srow[0];
     unsigned acc = 0, nslow = 0, tacc = ~0u;
     for (int it = 0; it < iters; ++it) {
+        u64 NAg[GRP];
+        if (F_LD == 5) {   // the 8 entering columns' thresholds of this lane, once per group
+#pragma unroll
+            for (int kk = 0; kk < GRP; ++kk) {
+                const float4 cq = scq[kk * CQS + lane];
+                const float w = srow[kk].w;
+                NAg[kk] = pk2(fmaxf(-cq.x, __fmul_ru(-w, cq.y)), fmaxf(-cq.z, __fmul_ru(-w, cq.w)));
+            }
+        }
 #pragma unroll
         for (int kk = 0; kk < GRP; ++kk) {
             // F_LD: 1 row + column factors from smem, 2 column factors only, 3 row factors only,
             // 4 as 1 with the row factors prefetched one row ahead
             float4 pr;
             if (F_LD == 4) { pr = prn; prn = srow[(kk + 1) % GRP]; }
-            else pr = (F_LD == 1 || F_LD == 3) ? srow[kk] : rr;
+            else pr = (F_LD == 1 || F_LD == 3 || F_LD == 5) ? srow[kk] : rr;
             const int q = (kk + DP - 1) % DP;
             if (F_SH) {
                 F[q] = __shfl_sync(0xffffffffu, F[q], (lane + 1) & 31);
                 G[q] = __shfl_sync(0xffffffffu, G[q], (lane + 1) & 31);
             }
+            if (F_LD == 5) NA[q] = NAg[kk];
             if (F_LD == 1 || F_LD == 2 || F_LD == 4) {
                 const float4 cq = scq[kk * CQS + lane];
                 NA[q] = pk2(fmaxf(-cq.x, __fmul_ru(-pr.w, cq.y)), fmaxf(-cq.z, __fmul_ru(-pr.w, cq.w)));
@@ -128,6 +138,7 @@ int main() {
         run<1, 1, 1, 1, 0>("+tree+branch+shfl", w, rows, cqs, out);
         run<1, 1, 1, 1, 1>("+tree+branch+shfl+lds", w, rows, cqs, out);
         run<1, 1, 0, 1, 1>("+tree+shfl+lds (no br)", w, rows, cqs, out);
+        run<1, 1, 1, 1, 5>("full, NA precomputed/group", w, rows, cqs, out);
         run<1, 1, 1, 1, 2>("full, cq from smem only", w, rows, cqs, out);
         run<1, 1, 1, 1, 3>("full, rows from smem only", w, rows, cqs, out);
         run<1, 1, 1, 1, 4>("full, rows prefetched", w, rows, cqs, out);
