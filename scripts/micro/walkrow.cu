@@ -106,6 +106,87 @@ __global__ void __launch_bounds__(32, 12) k_walk(const float4* rows, const float
     if (h == 0x12345) out[0] = h + msk[lane];
 }
 
+// two lengths per walk: cov_{m+1} = cov_m + w dz_i dz_j (Welford), its own test; per row
+// 16 rec + 8 test + 8 ext + 8 test FFMA2, a 32-value sign tree, one branch, 6 SHFL, 3 LDS
+template <int F_BR>
+__global__ void __launch_bounds__(32, 12) k_walk2(const float4* rows, const float4* cqs, u64* out, int iters) {
+    __shared__ float4 srow[GRP], srow2[GRP];
+    __shared__ float4 scq[GRP * CQS], scq2[GRP * CQS];
+    __shared__ unsigned short msk[32 * GRP];
+    const int lane = threadIdx.x;
+    if (lane < GRP) { srow[lane] = rows[lane]; srow2[lane] = rows[lane]; }
+    for (int k = lane; k < GRP * CQS; k += 32) { scq[k] = cqs[k]; scq2[k] = cqs[k]; }
+    __syncwarp();
+    u64 cov[DP], F[DP], G[DP], Z[DP], NA[DP], NB[DP];
+#pragma unroll
+    for (int s = 0; s < DP; ++s) {
+        cov[s] = pk2(1e-3f * s, 2e-3f * s); F[s] = pk2(1e-4f, 2e-4f); G[s] = pk2(3e-4f, 1e-4f);
+        Z[s] = pk2(2e-4f, 1e-4f); NA[s] = pk2(-1e30f, -1e30f); NB[s] = NA[s];
+    }
+    unsigned acc = 0, nslow = 0;
+    for (int it = 0; it < iters; ++it) {
+#pragma unroll
+        for (int kk = 0; kk < GRP; ++kk) {
+            const float4 pr = srow[kk], pr2 = srow2[kk];
+            const int q = (kk + DP - 1) % DP;
+            F[q] = __shfl_sync(0xffffffffu, F[q], (lane + 1) & 31);
+            G[q] = __shfl_sync(0xffffffffu, G[q], (lane + 1) & 31);
+            Z[q] = __shfl_sync(0xffffffffu, Z[q], (lane + 1) & 31);
+            const float4 cq = scq[kk * CQS + lane], cq2 = scq2[kk * CQS + lane];
+            NA[q] = pk2(fmaxf(-cq.x, __fmul_ru(-pr.w, cq.y)), fmaxf(-cq.z, __fmul_ru(-pr.w, cq.w)));
+            NB[q] = pk2(fmaxf(-cq2.x, __fmul_ru(-pr2.w, cq2.y)), fmaxf(-cq2.z, __fmul_ru(-pr2.w, cq2.w)));
+            unsigned z[32];
+#pragma unroll
+            for (int s = 0; s < DP; ++s) {
+                const int p = (s + kk) % DP;
+                cov[s] = fma2(bc2(pr.x), G[p], cov[s]);
+                cov[s] = fma2(F[p], bc2(pr.y), cov[s]);
+                const u64 zz = fma2(NA[p], bc2(pr.z), cov[s]);
+                const u64 c1 = fma2(bc2(pr2.x), Z[p], cov[s]);
+                const u64 zz2 = fma2(NB[p], bc2(pr2.z), c1);
+                z[s] = (unsigned)zz; z[s + 8] = (unsigned)(zz >> 32);
+                z[s + 16] = (unsigned)zz2; z[s + 24] = (unsigned)(zz2 >> 32);
+            }
+            unsigned t[11];
+#pragma unroll
+            for (int u = 0; u < 10; ++u) t[u] = and3(z[3 * u], z[3 * u + 1], z[3 * u + 2]);
+            t[10] = and3(z[30], z[31], ~0u);
+            const unsigned t1 = and3(t[0], t[1], t[2]), t2 = and3(t[3], t[4], t[5]), t3 = and3(t[6], t[7], t[8]);
+            const unsigned tt = and3(and3(t1, t2, t3), t[9], t[10]);
+            if (F_BR) {
+                if (__builtin_expect((int)tt >= 0, 0)) {
+                    unsigned m = 0;
+#pragma unroll
+                    for (int s = 0; s < DP; ++s) m |= ((unsigned)cov[s] >> 31) << s;
+                    msk[lane * GRP + kk] = (unsigned short)m;
+                    ++nslow;
+                }
+            } else acc += tt >> 31;
+        }
+    }
+    u64 h = acc + nslow;
+#pragma unroll
+    for (int s = 0; s < DP; ++s) h ^= cov[s] ^ F[s] ^ G[s] ^ Z[s];
+    if (h == 0x12345) out[0] = h + msk[lane];
+}
+
+template <int BR>
+void run2(const char* name, int warps_per_sm, float4* rows, float4* cqs, u64* out) {
+    int sms; cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, 0);
+    const int blocks = sms * warps_per_sm, iters = 4000;
+    k_walk2<BR><<<blocks, 32>>>(rows, cqs, out, 10);
+    cudaEvent_t e0, e1; cudaEventCreate(&e0); cudaEventCreate(&e1);
+    float best = 1e30f;
+    for (int rep = 0; rep < 3; ++rep) {
+        cudaEventRecord(e0); k_walk2<BR><<<blocks, 32>>>(rows, cqs, out, iters); cudaEventRecord(e1);
+        cudaEventSynchronize(e1); float ms; cudaEventElapsedTime(&ms, e0, e1); if (ms < best) best = ms;
+    }
+    const double upd = (double)blocks * 32 * 16 * GRP * iters * 2;   // cell-lengths
+    int clk; cudaDeviceGetAttribute(&clk, cudaDevAttrClockRate, 0);
+    printf("%-26s warps/SM=%2d  %.3e cell-lengths/s  %.2f per SM/clk\n", name, warps_per_sm,
+           upd / (best * 1e-3), upd / (best * 1e-3) / sms / (clk * 1e3));
+}
+
 template <int A, int B, int C, int D, int E>
 void run(const char* name, int warps_per_sm, float4* rows, float4* cqs, u64* out) {
     int sms; cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, 0);
@@ -131,6 +212,10 @@ int main() {
     for (int k = 0; k < 8; ++k) hr[k] = make_float4(1e-3f, 2e-3f, 1.0f, 0.5f);
     for (int k = 0; k < 8 * 33; ++k) hc[k] = make_float4(1e30f, 1.0f, 1e30f, 1.0f);
     cudaMemcpy(rows, hr, sizeof(hr), cudaMemcpyHostToDevice); cudaMemcpy(cqs, hc, sizeof(hc), cudaMemcpyHostToDevice);
+    for (int w : {8, 10, 12}) {
+        run2<1>("TWO LENGTHS full", w, rows, cqs, out);
+        run2<0>("TWO LENGTHS no br", w, rows, cqs, out);
+    }
     for (int w : {12, 16}) {
         run<0, 0, 0, 0, 0>("rec (16 FFMA2)", w, rows, cqs, out);
         run<1, 1, 0, 0, 0>("+tree", w, rows, cqs, out);
