@@ -370,7 +370,7 @@ def run_ours(args):
         e2e_s /= reps
         e2e_line = {"value": W / e2e_s, "unit": UNIT,
                     "h2d_bytes_per_step": int(8 * (s.n + 2 * (s.n + 1))),
-                    "d2h_bytes_per_step": int(n0 * (8 * 4 + 1) + nl * (2 * c.k_motif * 24 + kd * 16)),
+                    "d2h_bytes_per_step": int(n0 * (8 * 4 + 1) + nl * (2 * c.k_motif * 24 + c.k_discord * 16)),
                     "ms_per_step": e2e_s * 1e3, "api": "paper_2008_13447_b200.mine (host numpy in, host results out)"}
     clk.__exit__(None, None, None)
 

@@ -343,18 +343,22 @@ class MiningResult:
 def mine(series, lmin: int, lmax: int, k_motif: int = 1, k_discord: int = 1, *,
          ranking=None) -> MiningResult:
     """One GPU pass over [lmin, lmax] returning every read-off the reference's
-    valmod + topkm_discord_discovery (m = 1) + per-length PairRanking(k) produce."""
+    valmod + topkm_discord_discovery (m = 1) + per-length PairRanking(k) produce.
+    k_motif = 0 / k_discord = 0 skips that read-off (its result is empty)."""
     from .results import RunTrace
     series = as_series(series)
     validate_range(series, lmin, lmax)
     _check_profile_length(series, lmin)
-    if not (1 <= k_motif <= 32) or not (1 <= k_discord <= 32):
-        raise E.InvalidParametersError("k_motif and k_discord must be in [1, 32]")
+    if not (0 <= k_motif <= 32) or not (0 <= k_discord <= 32):
+        raise E.InvalidParametersError("k_motif and k_discord must be in [0, 32]")
     with _session_lock():
         run = GpuRun(series, lmin, lmax)
         v = run.valmp()
-        motifs = _topk_from_rows(run, k_motif)
-        dist, off = run.discords(k_discord)
+        motifs = _topk_from_rows(run, k_motif) if k_motif else {L: [] for L in range(lmin, lmax + 1)}
+        if k_discord:
+            dist, off = run.discords(k_discord)
+        else:
+            dist = np.empty((lmax - lmin + 1, 0)); off = np.empty((lmax - lmin + 1, 0), dtype=np.int64)
         if ranking is not None:
             _feed_ranking(run, v, ranking)
     trace = RunTrace()
@@ -366,8 +370,9 @@ def mine(series, lmin: int, lmax: int, k_motif: int = 1, k_discord: int = 1, *,
                          full_recompute=False, motif=top[0] if top else None)
     # per-length matrices are (k, 1) views of one batch array; the cross-length merge is
     # update_variable_length_discords over ascending lengths, vectorised
-    dist3 = np.array(dist, dtype=np.float64).reshape(-1, k_discord, 1)
-    off3 = np.array(off, dtype=np.int64).reshape(-1, k_discord, 1)
+    nl = lmax - lmin + 1
+    dist3 = np.array(dist, dtype=np.float64).reshape(nl, k_discord, 1)
+    off3 = np.array(off, dtype=np.int64).reshape(nl, k_discord, 1)
     offs = off3[:, :, 0].tolist()
     per_length = {lmin + li: DiscordMatrix(dist3[li], off3[li], lmin + li, {o for o in offs[li] if o >= 0})
                   for li in range(lmax - lmin + 1)}

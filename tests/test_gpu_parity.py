@@ -449,3 +449,18 @@ def test_row_profile_matches_reference(oracle_mod):
         vl.row_profile(s, s.n - 10, 256)
     with pytest.raises(vl.SeriesTooShortError):
         vl.row_profile(s, 0, 3)
+
+
+def test_mine_skips_read_offs_with_k_zero():
+    """mine(k_motif=0) / mine(k_discord=0) (BASELINE configs 4 and 5 ask for only one of the
+    two): the other read-offs equal a full mine() call's."""
+    s = vl.ingest(np.cumsum(np.random.default_rng(3).standard_normal(3000)))
+    full = vl.mine(s, 40, 50, k_motif=2, k_discord=2)
+    no_d = vl.mine(s, 40, 50, k_motif=2, k_discord=0)
+    no_m = vl.mine(s, 40, 50, k_motif=0, k_discord=2)
+    assert no_d.motifs == full.motifs and no_m.motifs == {L: [] for L in range(40, 51)}
+    assert np.array_equal(no_d.valmp.indices, full.valmp.indices)
+    assert no_d.discords.merged.offset.shape == (0, 1)
+    assert np.array_equal(no_m.discords.merged.offset, full.discords.merged.offset)
+    for L in range(40, 51):
+        assert np.array_equal(no_m.discords.per_length[L].offset, full.discords.per_length[L].offset)
