@@ -137,6 +137,19 @@ int vlmp_smallest_rows(vlmp_session* s, int32_t k2, int64_t* out_off,
 /* Top-k 1st discords per length (discords.py:68-93 replay): [n_len][k]. */
 int vlmp_discords(vlmp_session* s, int32_t k, double* out_dist, int64_t* out_off);
 /*
+ * Phase 2 and the standard read-offs in one call with a single host wait: vlmp_finalize, then
+ * (k2 > 0) vlmp_smallest_rows(k2), (k > 0) vlmp_discords(k) and (v_dist != NULL)
+ * vlmp_get_valmp, all enqueued behind phase 1 and copied through pinned staging -- the same
+ * outputs as those four calls (the read-off set valmod.py:192-258 + discords.py:206-247 +
+ * the per-length rankings need), without the device idling between them while the host
+ * wakes up. end_event (0 / 1, or -1 for none) records vlmp_event_record's slot on the stream
+ * after the last copy and before the host waits.
+ */
+int vlmp_finalize_collect(vlmp_session* s, int32_t k2, int64_t* rows_off, int64_t* rows_nbr,
+                          double* rows_d, int32_t k, double* disc_dist, int64_t* disc_off,
+                          double* v_dist, double* v_norm, int64_t* v_len, int64_t* v_idx,
+                          uint8_t* v_pop, int32_t end_event);
+/*
  * VALMP improvement events with norm <= tau, in (length, offset) order
  * (the stream valmod feeds to a PairRanking, motifsets.py:105-117).
  * Returns the total count in *count (may exceed cap; then call again).

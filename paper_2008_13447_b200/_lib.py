@@ -40,6 +40,8 @@ SIGNATURES = {
     "vlmp_get_profile": (C.c_int, [C.c_void_p, C.c_int32, C.c_void_p, C.c_void_p]),
     "vlmp_smallest_rows": (C.c_int, [C.c_void_p, C.c_int32, C.c_void_p, C.c_void_p, C.c_void_p]),
     "vlmp_discords": (C.c_int, [C.c_void_p, C.c_int32, C.c_void_p, C.c_void_p]),
+    "vlmp_finalize_collect": (C.c_int, [C.c_void_p, C.c_int32, C.c_void_p, C.c_void_p, C.c_void_p, C.c_int32,
+                                        C.c_void_p, C.c_void_p] + [C.c_void_p] * 5 + [C.c_int32]),
     "vlmp_ranking_events": (C.c_int, [C.c_void_p, C.c_double, C.c_int64] + [C.c_void_p] * 5 + [_c_int64_p]),
     "vlmp_range_query": (C.c_int, [C.c_void_p, C.c_int64, C.c_void_p, C.c_void_p, C.c_void_p, C.c_int64,
                                    C.c_void_p, C.c_void_p]),
@@ -174,6 +176,28 @@ class Session:
 
     def finalize_readoffs(self):
         self._check(self.lib.vlmp_finalize_readoffs(self.h))
+
+    def finalize_collect(self, k2=0, k=0, valmp=False, end_event=-1):
+        """finalize + smallest_rows(k2) + discords(k) + valmp_arrays in one call with one host
+        wait (vlmp_finalize_collect); 0 / False skips a read-off (None in its place)."""
+        nl = self.lmax - self.lmin + 1
+        n0 = self.n - self.lmin + 1
+        off = np.empty((nl, k2), dtype=np.int64); nbr = np.empty((nl, k2), dtype=np.int64)
+        rd = np.empty((nl, k2))
+        dd = np.empty((nl, k)); do = np.empty((nl, k), dtype=np.int64)
+        if valmp:
+            v = (np.empty(n0), np.empty(n0), np.empty(n0, dtype=np.int64), np.empty(n0, dtype=np.int64),
+                 np.empty(n0, dtype=np.uint8))
+            vp = [_ptr(a) for a in v]
+        else:
+            v, vp = None, [None] * 5
+        self._check(self.lib.vlmp_finalize_collect(self.h, int(k2), _ptr(off), _ptr(nbr), _ptr(rd), int(k),
+                                                   _ptr(dd), _ptr(do), *vp, int(end_event)))
+        rows = (off, nbr, rd) if k2 else None
+        disc = (dd, do) if k else None
+        if v is not None:
+            v = v[:4] + (v[4].astype(bool),)
+        return rows, disc, v
 
     # -- read-offs -------------------------------------------------------------
     def valmp_arrays(self):

@@ -79,14 +79,23 @@ class GpuRun:
     entry point here does. Read-offs outside that window raise if another run intervened.
     """
 
-    def __init__(self, series, lmin: int, lmax: int, flags: int = 0, device: int | None = None):
+    def __init__(self, series, lmin: int, lmax: int, flags: int = 0, device: int | None = None,
+                 collect: tuple[int, int, bool] | None = None):
+        """collect = (k2, k, valmp): fetch smallest_rows(k2), discords(k) and the VALMP arrays
+        together with phase 2 in one device round trip (vlmp_finalize_collect); the read-off
+        methods then return those copies."""
         self.series = series
         self.lmin, self.lmax = int(lmin), int(lmax)
         self.sess = _lib.session(_device() if device is None else device)
+        self._rows = self._disc = self._v = None
         with self.sess.lock:
             self.sess.set_series(series.values, series._cum, series._cum2, series.sigma_floor)
             self.sess.profile(lmin, lmax, 0, -1, flags)
-            self.sess.finalize()
+            if collect is None:
+                self.sess.finalize()
+            else:
+                k2, k, want_v = collect
+                self._rows, self._disc, self._v = self.sess.finalize_collect(k2, k, want_v)
             self.stats = self.sess.stats()
             self.generation = self.sess.generation
 
@@ -104,9 +113,12 @@ class GpuRun:
                                 "hold the run (with GpuRun(...) as run:) until its read-offs are done")
 
     def valmp(self) -> VALMP:
-        with self.sess.lock:
-            self._check()
-            d, nm, ln, ix, pop = self.sess.valmp_arrays()
+        if self._v is not None:
+            d, nm, ln, ix, pop = self._v
+        else:
+            with self.sess.lock:
+                self._check()
+                d, nm, ln, ix, pop = self.sess.valmp_arrays()
         v = VALMP(d.shape[0])
         v.distances[:] = d
         v.norm_distances[:] = nm
@@ -116,11 +128,15 @@ class GpuRun:
         return v
 
     def smallest_rows(self, k2: int):
+        if self._rows is not None and self._rows[0].shape[1] == k2:
+            return self._rows
         with self.sess.lock:
             self._check()
             return self.sess.smallest_rows(k2)
 
     def discords(self, k: int):
+        if self._disc is not None and self._disc[0].shape[1] == k:
+            return self._disc
         with self.sess.lock:
             self._check()
             return self.sess.discords(k)
@@ -193,7 +209,8 @@ def valmod(series, lmin: int, lmax: int, p: int, *, ranking=None, trace=None,
         raise E.InvalidParametersError("p must be at least 1")
     _check_profile_length(series, lmin)
     with _session_lock():
-        run = GpuRun(series, lmin, lmax)
+        # phase 2 and the three read-offs in one device round trip
+        run = GpuRun(series, lmin, lmax, collect=(2 * k_motif, k_discord, True))
         v = run.valmp()
         motifs = _per_length_motifs(run) if trace is not None else None
         if ranking is not None:
@@ -352,7 +369,8 @@ def mine(series, lmin: int, lmax: int, k_motif: int = 1, k_discord: int = 1, *,
     if not (0 <= k_motif <= 32) or not (0 <= k_discord <= 32):
         raise E.InvalidParametersError("k_motif and k_discord must be in [0, 32]")
     with _session_lock():
-        run = GpuRun(series, lmin, lmax)
+        # phase 2 and the three read-offs in one device round trip
+        run = GpuRun(series, lmin, lmax, collect=(2 * k_motif, k_discord, True))
         v = run.valmp()
         motifs = _topk_from_rows(run, k_motif) if k_motif else {L: [] for L in range(lmin, lmax + 1)}
         if k_discord:

@@ -543,7 +543,12 @@ __global__ void __launch_bounds__(32, VLMP_FILTER32_WARPS_PER_SM) k_tile32(Tile3
         for (int s = 0; s < DP; ++s) {
             const float ca = (liveA && d0 + DP * lane + s >= a.e) ? __fadd_ru((float)(cA64[s] * s2), eps) : -INFINITY;
             const float cb = (liveB && d0 + PSEP + DP * lane + s >= a.e) ? __fadd_ru((float)(cB64[s] * s2), eps) : -INFINITY;
+#if VLMP_DEV_NOPASS
+            // dev ablation (wrong results, timing only): no cell ever passes, same instruction stream
+            cov[s] = pk2(-1e30f, -1e30f); (void)ca; (void)cb;
+#else
             cov[s] = pk2(ca, cb);
+#endif
         }
     }
 

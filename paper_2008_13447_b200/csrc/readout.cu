@@ -453,6 +453,103 @@ int vlmp_get_profile(vlmp_session* s, int32_t length, double* mp, int64_t* ip) {
     return 0;
 }
 
+// vlmp_finalize_collect: phase 2 and the standard read-offs enqueued behind phase 1 in one go,
+// copied into pinned staging, one host wait. Staging layout (8-byte words, then the VALMP
+// populated bytes): rows off / nbr / d [cr each], discords d / off [cd each], valmp dist /
+// norm / len / idx [n0 each], pop [n0 bytes].
+static int collect_enqueue(vlmp_session* s, int k2, int k, bool want_v, int end_event, long long cr, long long cd,
+                           long long n0) {
+    int rc = finalize_enqueue(s, 0, s->n_len - 1, true);
+    if (rc) return rc;
+    cudaStream_t st = s->stream;
+    long long* i64 = s->d_ro_i64; double* f64 = s->d_ro_f64;
+    unsigned char* h = s->h_col;
+    long long* h8 = reinterpret_cast<long long*>(h);
+    if (k2) {
+        SmallArgs sa{s->d_mp, s->d_ip, i64, i64 + cr, f64, s->n, s->A, s->lmin, k2};
+        k_smallest<<<s->n_len, 256, 0, st>>>(sa);
+        CU(cudaMemcpyAsync(h8, i64, 2 * cr * 8, cudaMemcpyDeviceToHost, st));
+        CU(cudaMemcpyAsync(h8 + 2 * cr, f64, cr * 8, cudaMemcpyDeviceToHost, st));
+    }
+    if (k) {
+        DiscArgs da{s->d_mp, f64 + cr, i64 + 2 * cr, s->n, s->A, s->lmin, s->n_len, k};
+        k_discords<<<s->n_len, 32, 0, st>>>(da);
+        CU(cudaMemcpyAsync(h8 + 3 * cr, f64 + cr, cd * 8, cudaMemcpyDeviceToHost, st));
+        CU(cudaMemcpyAsync(h8 + 3 * cr + cd, i64 + 2 * cr, cd * 8, cudaMemcpyDeviceToHost, st));
+    }
+    if (want_v) {
+        long long* hv = h8 + 3 * cr + 2 * cd;
+        CU(cudaMemcpyAsync(hv, s->d_vdist, n0 * 8, cudaMemcpyDeviceToHost, st));
+        CU(cudaMemcpyAsync(hv + n0, s->d_vnorm, n0 * 8, cudaMemcpyDeviceToHost, st));
+        CU(cudaMemcpyAsync(hv + 2 * n0, s->d_vlen, n0 * 8, cudaMemcpyDeviceToHost, st));
+        CU(cudaMemcpyAsync(hv + 3 * n0, s->d_vidx, n0 * 8, cudaMemcpyDeviceToHost, st));
+        CU(cudaMemcpyAsync(hv + 4 * n0, s->d_vpop, n0, cudaMemcpyDeviceToHost, st));
+    }
+    if (end_event >= 0) CU(cudaEventRecord(s->ev[6 + end_event], st));
+    CU(cudaGetLastError());
+    return 0;
+}
+
+int vlmp_finalize_collect(vlmp_session* s, int32_t k2, int64_t* rows_off, int64_t* rows_nbr, double* rows_d,
+                          int32_t k, double* disc_dist, int64_t* disc_off,
+                          double* v_dist, double* v_norm, int64_t* v_len, int64_t* v_idx, uint8_t* v_pop,
+                          int32_t end_event) {
+    if (!s || !s->have_profile) return fail(VLMP_E_STATE, "no profile run");
+    if (k2 < 0 || k2 > 64) return fail(VLMP_E_INVALID_PARAMETERS, "k2 must be in [0, 64]");
+    if (k < 0 || k > 32) return fail(VLMP_E_INVALID_PARAMETERS, "k must be in [0, 32]");
+    if (end_event < -1 || end_event > 1) return fail(VLMP_E_INVALID_PARAMETERS, "end_event must be -1, 0 or 1");
+    if ((k2 && (!rows_off || !rows_nbr || !rows_d)) || (k && (!disc_dist || !disc_off)))
+        return fail(VLMP_E_INVALID_PARAMETERS, "null output buffer");
+    const bool want_v = v_dist != nullptr;
+    if (want_v && (!v_norm || !v_len || !v_idx || !v_pop)) return fail(VLMP_E_INVALID_PARAMETERS, "null VALMP buffer");
+    std::lock_guard<std::mutex> g(s->lock);
+    CU(cudaSetDevice(s->device));
+    const long long cr = (long long)s->n_len * k2, cd = (long long)s->n_len * k;
+    const long long n0 = s->n - s->lmin + 1;
+    int rc;
+    if ((rc = ensure(s->d_ro_i64, s->ro_i64_cap, (size_t)std::max(1LL, 2 * cr + cd)))) return rc;
+    if ((rc = ensure(s->d_ro_f64, s->ro_f64_cap, (size_t)std::max(1LL, cr + cd)))) return rc;
+    const size_t need = (size_t)(3 * cr + 2 * cd + (want_v ? 4 * n0 : 0)) * 8 + (want_v ? (size_t)n0 : 0) + 8;
+    if (s->h_col_cap < need) {
+        if (s->h_col) cudaFreeHost(s->h_col);
+        s->h_col = nullptr; s->h_col_cap = 0;
+        CU(cudaMallocHost((void**)&s->h_col, need));
+        s->h_col_cap = need;
+    }
+    // as finalize_impl: everything is enqueued behind the unchecked phase 1; a redo of phase 1
+    // (lost run log) enqueues it all again behind the redo
+    for (int attempt = 0; attempt < 2; ++attempt) {
+        if ((rc = collect_enqueue(s, k2, k, want_v, end_event, cr, cd, n0))) return rc;
+        bool redone = false;
+        if ((rc = settle_profile(s, &redone))) return rc;
+        if (!redone) break;
+    }
+    CU(cudaStreamSynchronize(s->stream));
+    s->stats[9] += 1 + (k2 ? 1 : 0) + (k ? 1 : 0);
+    s->have_final = true;
+    s->have_finals = true;
+    s->stats_dirty = true;
+    const long long* h8 = reinterpret_cast<const long long*>(s->h_col);
+    if (k2) {
+        memcpy(rows_off, h8, cr * 8);
+        memcpy(rows_nbr, h8 + cr, cr * 8);
+        memcpy(rows_d, h8 + 2 * cr, cr * 8);
+    }
+    if (k) {
+        memcpy(disc_dist, h8 + 3 * cr, cd * 8);
+        memcpy(disc_off, h8 + 3 * cr + cd, cd * 8);
+    }
+    if (want_v) {
+        const long long* hv = h8 + 3 * cr + 2 * cd;
+        memcpy(v_dist, hv, n0 * 8);
+        memcpy(v_norm, hv + n0, n0 * 8);
+        memcpy(v_len, hv + 2 * n0, n0 * 8);
+        memcpy(v_idx, hv + 3 * n0, n0 * 8);
+        memcpy(v_pop, hv + 4 * n0, n0);
+    }
+    return 0;
+}
+
 int vlmp_smallest_rows(vlmp_session* s, int32_t k2, int64_t* out_off, int64_t* out_nbr, double* out_d) {
     if (!s || !s->have_final) return fail(VLMP_E_STATE, "not finalized");
     if (k2 < 1 || k2 > 64) return fail(VLMP_E_INVALID_PARAMETERS, "k2 must be in [1, 64]");

@@ -88,6 +88,7 @@ void vlmp_destroy(vlmp_session* s) {
     if (s->h_span) cudaFreeHost(s->h_span);
     if (s->g_exec) cudaGraphExecDestroy(s->g_exec);
     if (s->h_chk) cudaFreeHost(s->h_chk);
+    if (s->h_col) cudaFreeHost(s->h_col);
     pruned_free(s);
     if (s->stream) cudaStreamDestroy(s->stream);
     delete s;

@@ -288,6 +288,7 @@ struct vlmp_session {
     bool pending = false, stats_dirty = false;          // phase 1 enqueued, not yet settled
     PendingRun prun;
     unsigned long long* h_chk = nullptr; size_t h_chk_cap = 0;   // pinned: its overflow counters
+    unsigned char* h_col = nullptr; size_t h_col_cap = 0;        // pinned staging of vlmp_finalize_collect
     std::vector<cudaEvent_t> lev;   // 2 per length: tile-kernel start/stop
     unsigned long long* d_span = nullptr; size_t span_cap = 0;   // [n_len][4] k_tile32 / k_runs spans (ns)
     unsigned long long* h_span = nullptr; size_t h_span_cap = 0;

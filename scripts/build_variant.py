@@ -1,6 +1,6 @@
-"""Build a variant of libvlmp.so with extra -D flags into scripts/variants/ (dev aid, CPU).
+"""Build a variant of libvlmp.so with extra -D flags into scripts/vlibs/ (dev aid, CPU; travels with gpurun).
 
-    python scripts/build_variant.py NAME -DVLMP_ROWPAIR=1 [...]   -> scripts/variants/libvlmp_NAME.so
+    python scripts/build_variant.py NAME -DVLMP_ROWPAIR=1 [...]   -> scripts/vlibs/libvlmp_NAME.so
 Prints the ptxas register / spill lines of k_tile32. Select it with VLMP_LIB=<path>.
 """
 import os

@@ -41,7 +41,7 @@ def child(lib):
                 d.update(np.ascontiguousarray(mp).tobytes())
                 d.update(np.ascontiguousarray(ip).tobytes())
             h = d.hexdigest()[:16]
-    keys = ("walk_ms", "runs_ms", "tile_ms", "profile_ms", "run_cells", "slow_rowsteps", "exact_redo", "fallback_lengths")
+    keys = ("walk_ms", "runs_ms", "tile_ms", "profile_ms", "run_cells", "slow_merges", "slow_rowsteps", "max_runs", "exact_redo", "fallback_lengths")
     out = {"lib": os.path.basename(lib), "cfg1_mismatches": bad, "digest": h}
     out.update({k: best.get(k) for k in keys})
     print("RESULT " + json.dumps(out), flush=True)

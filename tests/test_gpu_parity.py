@@ -464,3 +464,48 @@ def test_mine_skips_read_offs_with_k_zero():
     assert np.array_equal(no_m.discords.merged.offset, full.discords.merged.offset)
     for L in range(40, 51):
         assert np.array_equal(no_m.discords.per_length[L].offset, full.discords.per_length[L].offset)
+
+
+@pytest.mark.parametrize("k2,k,want_v", [(6, 3, True), (2, 0, True), (0, 5, False), (4, 1, False)])
+def test_finalize_collect_equals_separate_readoffs(k2, k, want_v):
+    """vlmp_finalize_collect (phase 2 + read-offs, one host wait) returns exactly what
+    vlmp_finalize + smallest_rows + discords + get_valmp return one by one."""
+    s = vl.ingest(gen.series_for(1))
+    sess = _lib.session(0)
+    with sess.lock:
+        sess.set_series(s.values, s._cum, s._cum2, s.sigma_floor)
+        sess.profile(32, 64, 0, -1, 0)
+        sess.finalize()
+        rows1 = sess.smallest_rows(k2) if k2 else None
+        disc1 = sess.discords(k) if k else None
+        v1 = sess.valmp_arrays()
+        sess.profile(32, 64, 0, -1, 0)
+        rows2, disc2, v2 = sess.finalize_collect(k2, k, want_v, end_event=1)
+        v3 = sess.valmp_arrays()            # the session state after collect is finalized as usual
+    if k2:
+        assert all(np.array_equal(a, b) for a, b in zip(rows1, rows2))
+    else:
+        assert rows2 is None
+    if k:
+        assert all(np.array_equal(a, b) for a, b in zip(disc1, disc2))
+    else:
+        assert disc2 is None
+    if want_v:
+        assert all(np.array_equal(a, b) for a, b in zip(v1, v2))
+    else:
+        assert v2 is None
+    assert all(np.array_equal(a, b) for a, b in zip(v1, v3))
+
+
+def test_mine_collect_matches_separate_path():
+    """mine() (collected read-offs) equals the same read-offs fetched one call at a time."""
+    s = vl.ingest(gen.series_for(1))
+    res = vl.mine(s, 32, 64, k_motif=3, k_discord=2)
+    with api.GpuRun(s, 32, 64) as run:
+        v = run.valmp()
+        d, o = run.discords(2)
+        motifs = api._topk_from_rows(run, 3)
+    assert np.array_equal(res.valmp.indices, v.indices) and np.array_equal(res.valmp.distances, v.distances)
+    assert res.motifs == motifs
+    for li, L in enumerate(range(32, 65)):
+        assert np.array_equal(res.discords.per_length[L].offset[:, 0], o[li])
