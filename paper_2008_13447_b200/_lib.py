@@ -77,7 +77,10 @@ def load():
                 f"{LIB_PATH} is missing: build the CUDA library first "
                 "(python -c 'import __graft_entry__ as g; g.build()'); no CPU fallback exists")
         lib = C.CDLL(LIB_PATH)
+        dev_variant = LIB_PATH != os.path.join(HERE, "libvlmp.so")   # scripts/variant_ab.py builds
         for name, (res, args) in SIGNATURES.items():
+            if dev_variant and not hasattr(lib, name):
+                continue          # an older dev build: its missing entry points are never called
             fn = getattr(lib, name)
             fn.restype = res
             fn.argtypes = args

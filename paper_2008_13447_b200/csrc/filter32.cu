@@ -135,7 +135,8 @@ struct Tile32Args {
     const float4* p32; const float2* cq; const unsigned* magblk; long long nb;
     const double* __restrict__ tn; const double* __restrict__ mu; double* seeds;
     const int2* tiles;      // FP64 tile list (band, segment)
-    const int2* tiles32;    // FP32 tiles: {FP64 tile of the lower band, of the upper band or -1}
+    const int4* tiles32;    // FP32 tiles: {FP64 tile of the lower band, of the upper band or -1,
+                            //  band and segment of the lower one}
     Run* runs; unsigned long long* run_count; long long run_cap;
     unsigned long long* counters;   // [2] flagged lane-rows, [3] runs
     const int* forced;
@@ -205,8 +206,9 @@ __global__ void __launch_bounds__(32, VLMP_FILTER32_WARPS_PER_SM) k_tile32(Tile3
     const int lane = threadIdx.x;
     const int wid = blockIdx.x;
     if (wid >= a.n_tiles32) return;
-    const int2 pr2 = a.tiles32[wid];
-    const int2 tA = a.tiles[pr2.x];
+    const int4 t4 = a.tiles32[wid];
+    const int2 pr2 = make_int2(t4.x, t4.y);
+    const int2 tA = make_int2(t4.z, t4.w);
     const long long d0 = a.dlo + (long long)tA.x * BAND;
     const long long i0 = (long long)tA.y * a.S;
     const long long rows_valid = a.N - d0 - i0;
@@ -471,10 +473,12 @@ __global__ void __launch_bounds__(32, VLMP_FILTER32_WARPS_PER_SM) k_tile32(Tile3
         __device__ ~SpanEnd() { if (p && lane == 0) atomicMax(p + 1, gtime()); }
     } span_end{a.span, lane};
     if (wid >= a.n_tiles32) return;
-    const int2 pr2 = a.tiles32[wid];
-    const int2 tA = a.tiles[pr2.x];
-    const long long d0 = a.dlo + (long long)tA.x * BAND;
-    const long long i0 = (long long)tA.y * a.S;
+    // one 16-byte descriptor per tile (the FP64 tile indices of both bands and the lower band's
+    // (band, segment)): the prologue's loads below depend on it alone
+    const int4 t4 = a.tiles32[wid];
+    const int2 pr2 = make_int2(t4.x, t4.y);
+    const long long d0 = a.dlo + (long long)t4.z * BAND;
+    const long long i0 = (long long)t4.w * a.S;
     const long long rows_valid = a.N - d0 - i0;
     const bool liveA = rows_valid > 0 && d0 + BAND - 1 >= a.e;
     const bool liveB = pr2.y >= 0 && rows_valid - PSEP > 0 && d0 + PSEP + BAND - 1 >= a.e;
@@ -488,18 +492,82 @@ __global__ void __launch_bounds__(32, VLMP_FILTER32_WARPS_PER_SM) k_tile32(Tile3
     // error grows by at most 2u|cov| + 3.02u(|df_i dg_j| + |df_j dg_i|), u = 2^-24, with
     // |cov| <= s_i s_j (Cauchy-Schwarz); S + 1 rows (with the seed pre-adjust) plus the seed's
     // conversion, over the maxima of s, |df|, |dg| on the tile's rows and columns.
+    // ---- staging: rows (lanes 0-7), fresh B columns (lanes 8-15), entering column factors.
+    // Group 0's copies are issued first: they are in flight during the prologue's loads.
+    const char* src_rf; unsigned dst_rf;
+    {
+        const int q = lane & 7;
+        if (lane < 8) {
+            src_rf = reinterpret_cast<const char*>(a.p32 + i0 + q);
+            dst_rf = (unsigned)__cvta_generic_to_shared(&sm.row[0][q]);
+        } else {
+            src_rf = PSEP == BAND ? reinterpret_cast<const char*>(a.p32 + i0 + q + d0 + 2 * BAND - 1)
+                                  : reinterpret_cast<const char*>(a.pf4 + i0 + q + d0 + BAND - 1);
+            dst_rf = (unsigned)__cvta_generic_to_shared(&sm.fresh[0][q]);
+        }
+    }
+    // entering pair f = 8L + kk (f = lane + 32k): one 16-byte {aA, bA, aB, bB} -> slot kk * 33 + L
+    const char* src_cq = reinterpret_cast<const char*>(a.cq4 + i0 + d0 + DP - 1 + lane);
+    const unsigned dst_cq = (unsigned)__cvta_generic_to_shared(&sm.cq[0][(lane % 8) * CQS + lane / 8]);
+    constexpr unsigned RFP = sizeof(float4) * GRP, CQP = sizeof(float4) * GRP * CQS;
+    auto stage = [&](int g, int b) {
+        const long long gr = (long long)g * (GRP * sizeof(float4));
+        if (lane < 16) cpa<0, 0, 16>(dst_rf + (unsigned)b * RFP, src_rf + gr);
+        const unsigned dc = dst_cq + (unsigned)b * CQP;
+        const char* sc = src_cq + (long long)g * (GRP * sizeof(float4));
+#define STG(K) cpa_l1<(K) * 4 * 16, (K) * 512>(dc, sc);
+        STG(0) STG(1) STG(2) STG(3) STG(4) STG(5) STG(6) STG(7)
+#undef STG
+        cp_async_commit();
+    };
+    stage(0, 0);
+
+    // ---- prologue loads in three independent batches (block maxima, ring, seeds): the warp
+    // pays about one memory round trip for them, not one per dependent step
+    // block maxima over the tile's rows and columns for the FP32 slack: <= 32 blocks each side
+    // in practice, so one predicated load per lane and quantity
+    unsigned r[3], c[3];
+    const long long rb0 = i0 >> 8, rb1 = (i0 + nrows - 1) >> 8;
+    const long long cb0 = (i0 + d0) >> 8, cb1 = (i0 + nrows - 1 + d0 + PSEP + BAND - 1) >> 8;
+    {
+        const bool rl = rb0 + lane <= rb1, cl = cb0 + lane <= cb1;
+#pragma unroll
+        for (int q = 0; q < 3; ++q) {
+            r[q] = rl ? a.magblk[q * a.nb + rb0 + lane] : 0u;
+            c[q] = cl ? a.magblk[q * a.nb + cb0 + lane] : 0u;
+        }
+    }
+
+    // ---- ring of column pairs; N = -cA
+    u64 F[DP], G[DP], NA[DP];
+    {
+        const float w0 = a.p32[i0].w;
+#pragma unroll
+        for (int s = 0; s < DP; ++s) {
+            const long long ca = s < DP - 1 ? cbA + s : cbA - 1;
+            const float4 pa = a.p32[ca], pb = a.p32[ca + PSEP];
+            F[s] = pk2(pa.x, pb.x); G[s] = pk2(pa.y, pb.y);
+            const float2 qa = a.cq[ca], qb = a.cq[ca + PSEP];
+            NA[s] = pk2(fmaxf(-qa.x, __fmul_ru(-w0, qa.y)), fmaxf(-qb.x, __fmul_ru(-w0, qb.y)));
+        }
+    }
+    const float4 pr0 = a.p32[i0];
+    const float4 plA = a.p32[cbA + DP - 1], plB = a.p32[cbB + DP - 1];
+
     float eps;
 #if VLMP_ROWPAIR
     float eps_rev;   // slack of a covariance recovered one row back (the row pair's first row)
 #endif
     {
-        const long long rb0 = i0 >> 8, rb1 = (i0 + nrows - 1) >> 8;
-        const long long cb0 = (i0 + d0) >> 8, cb1 = (i0 + nrows - 1 + d0 + PSEP + BAND - 1) >> 8;
-        unsigned r[3] = {0, 0, 0}, c[3] = {0, 0, 0};
+        if (rb1 - rb0 >= 32 || cb1 - cb0 >= 32) {   // very long segments (S > 8192)
+#pragma unroll
+            for (int q = 0; q < 3; ++q) {
+                for (long long k = rb0 + 32 + lane; k <= rb1; k += 32) r[q] = max(r[q], a.magblk[q * a.nb + k]);
+                for (long long k = cb0 + 32 + lane; k <= cb1; k += 32) c[q] = max(c[q], a.magblk[q * a.nb + k]);
+            }
+        }
 #pragma unroll
         for (int q = 0; q < 3; ++q) {
-            for (long long k = rb0 + lane; k <= rb1; k += 32) r[q] = max(r[q], a.magblk[q * a.nb + k]);
-            for (long long k = cb0 + lane; k <= cb1; k += 32) c[q] = max(c[q], a.magblk[q * a.nb + k]);
             r[q] = __reduce_max_sync(FULLMASK, r[q]);
             c[q] = __reduce_max_sync(FULLMASK, c[q]);
         }
@@ -551,57 +619,14 @@ __global__ void __launch_bounds__(32, VLMP_FILTER32_WARPS_PER_SM) k_tile32(Tile3
 #endif
         }
     }
-
-    // ---- ring of column pairs; N = -cA
-    u64 F[DP], G[DP], NA[DP];
-    {
-        const float w0 = a.p32[i0].w;
+    // pre-adjust so that the uniform recurrence at row i0 reproduces the seed
 #pragma unroll
-        for (int s = 0; s < DP; ++s) {
-            const long long ca = s < DP - 1 ? cbA + s : cbA - 1;
-            const float4 pa = a.p32[ca], pb = a.p32[ca + PSEP];
-            F[s] = pk2(pa.x, pb.x); G[s] = pk2(pa.y, pb.y);
-            const float2 qa = a.cq[ca], qb = a.cq[ca + PSEP];
-            NA[s] = pk2(fmaxf(-qa.x, __fmul_ru(-w0, qa.y)), fmaxf(-qb.x, __fmul_ru(-w0, qb.y)));
-        }
-        const float4 pr = a.p32[i0];
-        const float4 plA = a.p32[cbA + DP - 1], plB = a.p32[cbB + DP - 1];
-#pragma unroll
-        for (int s = 0; s < DP; ++s) {
-            const u64 f = s < DP - 1 ? F[s] : pk2(plA.x, plB.x);
-            const u64 g = s < DP - 1 ? G[s] : pk2(plA.y, plB.y);
-            cov[s] = fma2(bc2(-pr.y), f, cov[s]);
-            cov[s] = fma2(bc2(-pr.x), g, cov[s]);
-        }
+    for (int s = 0; s < DP; ++s) {
+        const u64 f = s < DP - 1 ? F[s] : pk2(plA.x, plB.x);
+        const u64 g = s < DP - 1 ? G[s] : pk2(plA.y, plB.y);
+        cov[s] = fma2(bc2(-pr0.y), f, cov[s]);
+        cov[s] = fma2(bc2(-pr0.x), g, cov[s]);
     }
-
-    // ---- staging: rows (lanes 0-7), fresh B columns (lanes 8-15), entering column factors
-    const char* src_rf; unsigned dst_rf;
-    {
-        const int q = lane & 7;
-        if (lane < 8) {
-            src_rf = reinterpret_cast<const char*>(a.p32 + i0 + q);
-            dst_rf = (unsigned)__cvta_generic_to_shared(&sm.row[0][q]);
-        } else {
-            src_rf = PSEP == BAND ? reinterpret_cast<const char*>(a.p32 + i0 + q + d0 + 2 * BAND - 1)
-                                  : reinterpret_cast<const char*>(a.pf4 + i0 + q + d0 + BAND - 1);
-            dst_rf = (unsigned)__cvta_generic_to_shared(&sm.fresh[0][q]);
-        }
-    }
-    // entering pair f = 8L + kk (f = lane + 32k): one 16-byte {aA, bA, aB, bB} -> slot kk * 33 + L
-    const char* src_cq = reinterpret_cast<const char*>(a.cq4 + i0 + d0 + DP - 1 + lane);
-    const unsigned dst_cq = (unsigned)__cvta_generic_to_shared(&sm.cq[0][(lane % 8) * CQS + lane / 8]);
-    constexpr unsigned RFP = sizeof(float4) * GRP, CQP = sizeof(float4) * GRP * CQS;
-    auto stage = [&](int g, int b) {
-        const long long gr = (long long)g * (GRP * sizeof(float4));
-        if (lane < 16) cpa<0, 0, 16>(dst_rf + (unsigned)b * RFP, src_rf + gr);
-        const unsigned dc = dst_cq + (unsigned)b * CQP;
-        const char* sc = src_cq + (long long)g * (GRP * sizeof(float4));
-#define STG(K) cpa_l1<(K) * 4 * 16, (K) * 512>(dc, sc);
-        STG(0) STG(1) STG(2) STG(3) STG(4) STG(5) STG(6) STG(7)
-#undef STG
-        cp_async_commit();
-    };
 
     // ---- runs (cells 0-7: band A diagonal d0 + 8L + s; 8-15: band B, + 256)
     unsigned open = 0;
@@ -634,7 +659,6 @@ __global__ void __launch_bounds__(32, VLMP_FILTER32_WARPS_PER_SM) k_tile32(Tile3
         }
     };
 
-    stage(0, 0);
     cp_async_wait_all();
     __syncwarp();
 
@@ -950,10 +974,10 @@ size_t tile32_smem() { return sizeof(SmemT); }
 
 // FP32 tiles from the FP64 tile list: D2 = 16 pairs (band b, band b+1) of one row segment,
 // b - band_lo even; D2 = 8 keeps the FP64 tiles. Order follows the (longest-first) FP64 list.
-void build_tiles32(const std::vector<int2>& tiles, long long band_lo, std::vector<int2>& out) {
+void build_tiles32(const std::vector<int2>& tiles, long long band_lo, std::vector<int4>& out) {
     out.clear();
     if (D2 == 8) {
-        for (size_t k = 0; k < tiles.size(); ++k) out.push_back(make_int2((int)k, -1));
+        for (size_t k = 0; k < tiles.size(); ++k) out.push_back(make_int4((int)k, -1, tiles[k].x, tiles[k].y));
         return;
     }
     std::vector<std::pair<long long, int>> keyed;   // (band, seg) -> index
@@ -969,7 +993,7 @@ void build_tiles32(const std::vector<int2>& tiles, long long band_lo, std::vecto
     const long long sep = VLMP_PACKED ? VLMP_PAIR_SEP : 1;
     for (size_t k = 0; k < tiles.size(); ++k) {
         if (((long long)tiles[k].x - band_lo) % (2 * sep) >= sep) continue;
-        out.push_back(make_int2((int)k, find(key((long long)tiles[k].x + sep, tiles[k].y))));
+        out.push_back(make_int4((int)k, find(key((long long)tiles[k].x + sep, tiles[k].y)), tiles[k].x, tiles[k].y));
     }
 }
 

@@ -1208,7 +1208,7 @@ static int profile_impl(vlmp_session* s, int32_t lmin, int32_t lmax, int64_t ban
         CU(cudaMemcpyAsync(s->d_tiles_s, tiles_s.data(), Ts * sizeof(int2), cudaMemcpyHostToDevice, st));
         CU(cudaMemcpyAsync(s->d_smap, smap.data(), Ts * sizeof(int), cudaMemcpyHostToDevice, st));
     }
-    std::vector<int2> tiles32;
+    std::vector<int4> tiles32;
     if (fp32) {
         if (!tiles_cached) build_tiles32(tiles, band_lo, tiles32);
         if ((rc = ensure(s->d_tiles32, s->tiles32_cap, std::max<size_t>(tiles32.size(), 1)))) return rc;
@@ -1218,7 +1218,7 @@ static int profile_impl(vlmp_session* s, int32_t lmin, int32_t lmax, int64_t ban
         if ((rc = ensure(s->d_pf4, s->pf4_cap, (size_t)A))) return rc;
         if ((rc = ensure(s->d_magblk, s->magblk_cap, (size_t)(3 * (A / 256 + 1))))) return rc;
         if (!tiles32.empty())
-            CU(cudaMemcpyAsync(s->d_tiles32, tiles32.data(), tiles32.size() * sizeof(int2), cudaMemcpyHostToDevice, st));
+            CU(cudaMemcpyAsync(s->d_tiles32, tiles32.data(), tiles32.size() * sizeof(int4), cudaMemcpyHostToDevice, st));
     }
     const long long T32 = (fp32 && tiles_cached) ? s->tc_T32 : (long long)tiles32.size();
     if (!tiles_cached) {
@@ -1662,7 +1662,7 @@ int mbest_impl(vlmp_session* s, int32_t lmin, int32_t lmax, int32_t mb) {
     // the filtered pass: FP32 walk + exact runs into the candidate slots (filter32.cu) unless the
     // FP64 walk + covariance log is asked for (VLMP_FP64_FILTER, A/B checks)
     const bool fp32 = !getenv("VLMP_FP64_FILTER");
-    std::vector<int2> tiles32;
+    std::vector<int4> tiles32;
     Run* runs = reinterpret_cast<Run*>(s->d_log);
     const long long run_cap = (long long)(s->log_cap * sizeof(RowRec) / sizeof(Run));
     if (fp32) {
@@ -1676,7 +1676,7 @@ int mbest_impl(vlmp_session* s, int32_t lmin, int32_t lmax, int32_t mb) {
         if ((rc = ensure(s->d_forced, s->forced_cap, (size_t)n_len))) return rc;
         CU(cudaMemsetAsync(s->d_forced, 0, n_len * sizeof(int), st));
         if (!tiles32.empty())
-            CU(cudaMemcpyAsync(s->d_tiles32, tiles32.data(), tiles32.size() * sizeof(int2), cudaMemcpyHostToDevice, st));
+            CU(cudaMemcpyAsync(s->d_tiles32, tiles32.data(), tiles32.size() * sizeof(int4), cudaMemcpyHostToDevice, st));
         if ((rc = filter32_setup())) return rc;
     }
     const long long T32 = (long long)tiles32.size();

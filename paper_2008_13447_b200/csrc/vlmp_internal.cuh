@@ -251,7 +251,7 @@ struct vlmp_session {
     float4* d_cq4 = nullptr; size_t cq4_cap = 0;         // packed walk: band-pair {a, b, a', b'}
     float4* d_pf4 = nullptr; size_t pf4_cap = 0;         // packed walk: band-pair {df, df', dg, dg'}
     unsigned* d_magblk = nullptr; size_t magblk_cap = 0; // FP32 filter: per-256-offset magnitude bound
-    int2* d_tiles32 = nullptr; size_t tiles32_cap = 0;   // FP32 filter tiles (pairs of FP64 tiles)
+    int4* d_tiles32 = nullptr; size_t tiles32_cap = 0;   // FP32 filter tiles (pairs of FP64 tiles)
     unsigned long long* d_fixcnt = nullptr; size_t fixcnt_cap = 0;   // per-length re-bounded offsets
     double sscale = 1.0; int hiC = 896 << 20;            // filter: 2^-k scale, hi-word bias
     // tiles / seeds (host tile lists cached per (n, lmin, bands, flags): tc_*)
@@ -305,7 +305,7 @@ namespace vlmp_impl {
 int tile32_width();
 size_t tile32_smem();
 int filter32_setup();
-void build_tiles32(const std::vector<int2>& tiles, long long band_lo, std::vector<int2>& out);
+void build_tiles32(const std::vector<int2>& tiles, long long band_lo, std::vector<int4>& out);
 int launch_filter32(vlmp_session* s, cudaStream_t st, const Prm* prm, const double* mu, long long N, int m, int e,
                     long long dl, int S, int update_seeds, long long n_t32, const int* forced,
                     ulonglong2* acc, Run* runs, unsigned long long* run_count, long long run_cap,
