@@ -45,8 +45,17 @@ constexpr int WIN = VLMP_PACKED ? 8 : D2;   // rows a column meets in one lane (
 #ifndef VLMP_ROWPAIR
 #define VLMP_ROWPAIR 0           // packed walk: one pass test and branch per pair of rows
 #endif
+#ifndef VLMP_MASK_SHF
+#define VLMP_MASK_SHF 1          // packed walk: a flagged row's mask from 8 FFMA2 + one funnel shift per cell
+#endif
 #ifndef VLMP_FILTER32_WARPS_PER_SM
 #define VLMP_FILTER32_WARPS_PER_SM 16   // 128 registers: no spills (20 warps at 96 spill the staging plan)
+#endif
+#ifndef VLMP_RUN_MAXLEN
+#define VLMP_RUN_MAXLEN 64       // packed walk: longer runs are logged in pieces of this many cells (k_runs: one warp per piece)
+#endif
+#ifndef VLMP_RUN_GAP
+#define VLMP_RUN_GAP 28          // packed walk: runs of one diagonal at most this many rows apart are logged as one
 #endif
 
 // ---------------------------------------------------------------------------------
@@ -438,6 +447,10 @@ __device__ __forceinline__ u64 fma2(u64 x, u64 y, u64 z) {
     u64 d; asm("fma.rn.f32x2 %0, %1, %2, %3;" : "=l"(d) : "l"(x), "l"(y), "l"(z)); return d;
 }
 __device__ __forceinline__ u64 bc2(float x) { return pk2(x, x); }
+// volatile: the flagged-row mask's FMAs must not be merged with the fast path's (see fma_nocse)
+__device__ __forceinline__ u64 fma2_nocse(u64 x, u64 y, u64 z) {
+    u64 d; asm volatile("fma.rn.f32x2 %0, %1, %2, %3;" : "=l"(d) : "l"(x), "l"(y), "l"(z)); return d;
+}
 
 __device__ __forceinline__ unsigned and3(unsigned x, unsigned y, unsigned z) {
     unsigned d; asm("lop3.b32 %0, %1, %2, %3, 0x80;" : "=r"(d) : "r"(x), "r"(y), "r"(z)); return d;
@@ -452,6 +465,9 @@ struct Smem32p {
     float4 cq[2][GRP * CQS];     // {aA, bA, aB, bB} of the pair entering lane L at row kk: [kk * 33 + L]
     unsigned short rs[32 * 16];  // run starts per lane and cell (bits 0-7 band A, 8-15 band B)
     unsigned short msk[32 * GRP];
+#if VLMP_RUN_GAP > 0
+    unsigned short re[32 * 16];  // last row of a cell's closed, not yet logged run (gap bridging)
+#endif
 };
 
 // lane 0's outgoing pair becomes lane 31's incoming one. Adjacent bands (PSEP = 256): (lane 0's
@@ -636,13 +652,30 @@ __global__ void __launch_bounds__(32, VLMP_FILTER32_WARPS_PER_SM) k_tile32(Tile3
     unsigned short* msk = sm.msk + lane * GRP;
     auto emit = [&](int c, int r_start, int r_end) {
         const int dcell = (int)(d0 + DP * lane) + (c & 7) + (c >> 3) * PSEP;
-        const unsigned long long at = atomicAdd(a.run_count, 1ull);
-        if ((long long)at < a.run_cap) {
-            Run rr;
-            rr.i = (int)(i0 + r_start); rr.j = rr.i + dcell; rr.len = r_end - r_start + 1; rr.pad = 0;
-            a.runs[at] = rr;
+#if VLMP_RUN_MAXLEN > 0
+        // a long run would keep one k_runs warp busy for its whole length (32 cells per scan step)
+        // while the rest of the grid has drained: log it in pieces, each seeded by its own dot product
+        for (; r_end - r_start + 1 > VLMP_RUN_MAXLEN; r_start += VLMP_RUN_MAXLEN) {
+            const unsigned long long at = atomicAdd(a.run_count, 1ull);
+            if ((long long)at < a.run_cap) {
+                Run rp;
+                rp.i = (int)(i0 + r_start); rp.j = rp.i + dcell; rp.len = VLMP_RUN_MAXLEN; rp.pad = 0;
+                a.runs[at] = rp;
+            }
         }
+#endif
+        Run rr;
+        rr.i = (int)(i0 + r_start); rr.j = rr.i + dcell; rr.len = r_end - r_start + 1; rr.pad = 0;
+        const unsigned long long at = atomicAdd(a.run_count, 1ull);
+        if ((long long)at < a.run_cap) a.runs[at] = rr;
     };
+#if VLMP_RUN_GAP > 0
+    // a closed run waits (pend, re) for the next run of its diagonal: at most VLMP_RUN_GAP rows on,
+    // the two are logged as one -- k_runs then pays one direct dot product instead of two, and the
+    // gap's cells ride along in the same 32-cell scan chunk (every cell is tested exactly there)
+    unsigned pend = 0;
+    unsigned short* re = sm.re + lane * 16;
+#endif
     auto fold_rows = [&](unsigned flags, int gbase) {
         while (flags) {
             const int t = __ffs(flags) - 1; flags &= flags - 1;
@@ -652,8 +685,22 @@ __global__ void __launch_bounds__(32, VLMP_FILTER32_WARPS_PER_SM) k_tile32(Tile3
             int endr;
             if (last_r == r - 1) { ended = open & ~mask; started = mask & ~open; endr = r - 1; }
             else { ended = open; started = mask; endr = last_r; }
+#if VLMP_RUN_GAP > 0
+            pend |= ended;
+            while (ended) { const int q = __ffs(ended) - 1; ended &= ended - 1; re[q] = (unsigned short)endr; }
+            while (started) {
+                const int q = __ffs(started) - 1; started &= started - 1;
+                if (pend >> q & 1u) {
+                    pend &= ~(1u << q);
+                    if (r - (int)re[q] - 1 <= VLMP_RUN_GAP) continue;   // bridged: the run goes on from rs[q]
+                    emit(q, rs[q], re[q]);
+                }
+                rs[q] = (unsigned short)r;
+            }
+#else
             while (ended) { const int q = __ffs(ended) - 1; ended &= ended - 1; emit(q, rs[q], endr); }
             while (started) { const int q = __ffs(started) - 1; started &= started - 1; rs[q] = (unsigned short)r; }
+#endif
             open = mask; last_r = r;
             ++nslow;
         }
@@ -759,6 +806,17 @@ __global__ void __launch_bounds__(32, VLMP_FILTER32_WARPS_PER_SM) k_tile32(Tile3
             const float4 pr = sm.row[b][kk];
             if (__builtin_expect(pass_prev, 0)) {
                 const int kp = (kk + GRP - 1) % DP;
+#if VLMP_MASK_SHF
+                u64 zz[DP];
+#pragma unroll
+                for (int s = 0; s < DP; ++s) zz[s] = fma2_nocse(NA[(s + kp) % DP], bc2(bprev), cov[s]);
+                unsigned acc = 0;   // acc = (acc << 1) | sign, cell 15 (band B, s = 7) first
+#pragma unroll
+                for (int s = DP - 1; s >= 0; --s) acc = __funnelshift_l((unsigned)(zz[s] >> 32), acc, 1);
+#pragma unroll
+                for (int s = DP - 1; s >= 0; --s) acc = __funnelshift_l((unsigned)zz[s], acc, 1);
+                const unsigned mask = ~acc;
+#else
                 unsigned mask = 0;
 #pragma unroll
                 for (int s = 0; s < DP; ++s) {
@@ -768,6 +826,7 @@ __global__ void __launch_bounds__(32, VLMP_FILTER32_WARPS_PER_SM) k_tile32(Tile3
                     mask |= (__float_as_uint(za) >> 31 ^ 1u) << s;
                     mask |= (__float_as_uint(zb) >> 31 ^ 1u) << (s + 8);
                 }
+#endif
                 msk[(kk + GRP - 1) % GRP] = (unsigned short)mask;
                 gflags |= 1u << ((kk + GRP - 1) % GRP);
             }
@@ -820,6 +879,9 @@ __global__ void __launch_bounds__(32, VLMP_FILTER32_WARPS_PER_SM) k_tile32(Tile3
 #endif
     if (gflags) fold_rows(gflags, (ngroups - 1) * GRP);
     while (open) { const int q = __ffs(open) - 1; open &= open - 1; emit(q, rs[q], last_r); }
+#if VLMP_RUN_GAP > 0
+    while (pend) { const int q = __ffs(pend) - 1; pend &= pend - 1; emit(q, rs[q], re[q]); }
+#endif
     if (nslow) atomicAdd(a.counters + 2, (unsigned long long)nslow);
 }
 #endif  // VLMP_PACKED
@@ -839,9 +901,17 @@ __global__ void __launch_bounds__(32, VLMP_FILTER32_WARPS_PER_SM) k_tile32(Tile3
 #ifndef VLMP_RUNS_G
 #define VLMP_RUNS_G 32            // lanes per run in k_runs (8 / 16: several runs per warp)
 #endif
+#ifdef VLMP_RUNS_MINB               // k_runs: minimum resident blocks per SM (register cap); default: none
+#define VLMP_RUNS_BOUNDS __launch_bounds__(256, VLMP_RUNS_MINB)
+#else
+#define VLMP_RUNS_BOUNDS __launch_bounds__(256)
+#endif
+#ifndef VLMP_RUNS_GRID
+#define VLMP_RUNS_GRID 8          // k_runs: blocks per SM in the grid
+#endif
 
 template <int G>
-__global__ void __launch_bounds__(256) k_runs(const Run* __restrict__ runs, const unsigned long long* run_count,
+__global__ void VLMP_RUNS_BOUNDS k_runs(const Run* __restrict__ runs, const unsigned long long* run_count,
                                              long long cap, const Prm* __restrict__ prm,
                                              const double* __restrict__ tn, const double* __restrict__ mu,
                                              int m, int e, ulonglong2* acc, unsigned long long* counters,
@@ -957,8 +1027,17 @@ __global__ void __launch_bounds__(256) k_runs(const Run* __restrict__ runs, cons
         merged += __shfl_xor_sync(FULLMASK, merged, off);
         cells += __shfl_xor_sync(FULLMASK, cells, off);
     }
-    if (lane == 0 && (merged | cells)) { atomicAdd(counters + 0, merged); atomicAdd(counters + 4, cells); }
-    if (span && lane == 0) atomicMax(span + 1, gtime());
+    // one pair of global atomics per block, not per warp
+    __shared__ unsigned long long blk_cnt[2];
+    if (threadIdx.x < 2) blk_cnt[threadIdx.x] = 0;
+    __syncthreads();
+    if (lane == 0 && (merged | cells)) { atomicAdd(&blk_cnt[0], merged); atomicAdd(&blk_cnt[1], cells); }
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        if (blk_cnt[0]) atomicAdd(counters + 0, blk_cnt[0]);
+        if (blk_cnt[1]) atomicAdd(counters + 4, blk_cnt[1]);
+        if (span) atomicMax(span + 1, gtime());
+    }
 }
 
 // ---------------------------------------------------------------------------------
@@ -1013,7 +1092,7 @@ int launch_filter32(vlmp_session* s, cudaStream_t st, const Prm* prm, const doub
                       update_seeds, s->sscale, span, s->d_cq4, s->d_pf4};
         // span: [0, 1] k_tile32's and [2, 3] k_runs' first start / last end (bench.py's roofline)
         k_tile32<<<(unsigned)n_t32, 32, sizeof(SmemT), st>>>(ta);
-        k_runs<VLMP_RUNS_G><<<148 * 8, 256, 0, st>>>(runs, run_count, run_cap, prm, s->d_tn, mu, m, e, acc, s->d_counters,
+        k_runs<VLMP_RUNS_G><<<148 * VLMP_RUNS_GRID, 256, 0, st>>>(runs, run_count, run_cap, prm, s->d_tn, mu, m, e, acc, s->d_counters,
                                         slots, slot_cnt, span ? span + 2 : nullptr);
     }
     return 0;

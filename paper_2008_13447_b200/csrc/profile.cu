@@ -1465,6 +1465,15 @@ int fill_event_stats(vlmp_session* s) {
         if (sp[1] > sp[0]) walk_ms += (double)(sp[1] - sp[0]) * 1e-6;
         if (sp[3] > sp[2]) runs_ms += (double)(sp[3] - sp[2]) * 1e-6;
     }
+    if (const char* sp_path = getenv("VLMP_DUMP_SPANS")) {   // dev aid: per-length kernel spans (ns, device clock)
+        if (FILE* f = fopen(sp_path, "w")) {
+            for (int li : pr.walked) {
+                const unsigned long long* sp = s->h_span + 4 * li;
+                fprintf(f, "%d %llu %llu %llu %llu\n", li, sp[0], sp[1], sp[2], sp[3]);
+            }
+            fclose(f);
+        }
+    }
     if (!pr.graph) {
         for (int li : pr.timed) {
             float lm = 0; CU(cudaEventElapsedTime(&lm, s->lev[2 * li], s->lev[2 * li + 1]));

@@ -12,7 +12,7 @@ sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 from paper_2008_13447_b200 import build as b  # noqa: E402
 
 name, defs = sys.argv[1], sys.argv[2:]
-out_dir = os.path.join(b.ROOT, "scripts", "variants")
+out_dir = os.path.join(b.ROOT, "scripts", "vlibs")
 os.makedirs(out_dir, exist_ok=True)
 out = os.path.join(out_dir, f"libvlmp_{name}.so")
 cmd = [b.nvcc(), *b.NVCC_FLAGS, "-Xptxas=-v", *defs, "-o", out, *b.SRCS]
