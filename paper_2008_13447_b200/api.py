@@ -209,8 +209,8 @@ def valmod(series, lmin: int, lmax: int, p: int, *, ranking=None, trace=None,
         raise E.InvalidParametersError("p must be at least 1")
     _check_profile_length(series, lmin)
     with _session_lock():
-        # phase 2 and the three read-offs in one device round trip
-        run = GpuRun(series, lmin, lmax, collect=(2 * k_motif, k_discord, True))
+        # phase 2, the VALMP arrays and (for a trace) each length's first row in one device round trip
+        run = GpuRun(series, lmin, lmax, collect=(1 if trace is not None else 0, 0, True))
         v = run.valmp()
         motifs = _per_length_motifs(run) if trace is not None else None
         if ranking is not None:

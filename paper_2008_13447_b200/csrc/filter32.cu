@@ -42,8 +42,8 @@ constexpr int WIN = VLMP_PACKED ? 8 : D2;   // rows a column meets in one lane (
 #ifndef VLMP_PAIR_SEP
 #define VLMP_PAIR_SEP 2          // packed walk: band B = band A + VLMP_PAIR_SEP bands (1: adjacent)
 #endif
-#ifndef VLMP_ROWPAIR
-#define VLMP_ROWPAIR 0           // packed walk: one pass test and branch per pair of rows
+#ifndef VLMP_PF_RING
+#define VLMP_PF_RING 1           // packed walk: entering columns' {df, dg} from a second sliding ring (0: lane-to-lane shuffles)
 #endif
 #ifndef VLMP_MASK_SHF
 #define VLMP_MASK_SHF 1          // packed walk: a flagged row's mask from 8 FFMA2 + one funnel shift per cell
@@ -460,9 +460,17 @@ constexpr int DP = 8;        // diagonals per lane per band
 constexpr int GRP = 8;       // rows per staging group (ring phase)
 struct Smem32p {
     float4 row[2][GRP];          // {df, dg, b, w}
+    // {aA, bA, aB, bB} of the column pairs in the tile's sliding 256-pair window, 8 pairs per
+    // 9-entry chunk (the pad entry keeps lane L's read of entry 9 (L + g) + kk conflict free).
+    // Lane L meets chunk (L + g) mod 33 in group g; each group only the chunk entering lane 31
+    // is new -- 128 bytes staged per group, not the whole window.
+    float4 cqr[33 * 9];
+#if VLMP_PF_RING
+    float4 pfr[33 * 9];          // the same window of {dfA, dfB, dgA, dgB}: the pair entering a lane's ring
+#else
     float4 fresh[2][GRP];        // lane 31's entering column(s) at each row: PSEP = 256: the
                                  // B-band p32 entry; else the pf4 entry of the A-band column
-    float4 cq[2][GRP * CQS];     // {aA, bA, aB, bB} of the pair entering lane L at row kk: [kk * 33 + L]
+#endif
     unsigned short rs[32 * 16];  // run starts per lane and cell (bits 0-7 band A, 8-15 band B)
     unsigned short msk[32 * GRP];
 #if VLMP_RUN_GAP > 0
@@ -510,33 +518,60 @@ __global__ void __launch_bounds__(32, VLMP_FILTER32_WARPS_PER_SM) k_tile32(Tile3
     // conversion, over the maxima of s, |df|, |dg| on the tile's rows and columns.
     // ---- staging: rows (lanes 0-7), fresh B columns (lanes 8-15), entering column factors.
     // Group 0's copies are issued first: they are in flight during the prologue's loads.
-    const char* src_rf; unsigned dst_rf;
-    {
-        const int q = lane & 7;
-        if (lane < 8) {
-            src_rf = reinterpret_cast<const char*>(a.p32 + i0 + q);
-            dst_rf = (unsigned)__cvta_generic_to_shared(&sm.row[0][q]);
-        } else {
-            src_rf = PSEP == BAND ? reinterpret_cast<const char*>(a.p32 + i0 + q + d0 + 2 * BAND - 1)
-                                  : reinterpret_cast<const char*>(a.pf4 + i0 + q + d0 + BAND - 1);
-            dst_rf = (unsigned)__cvta_generic_to_shared(&sm.fresh[0][q]);
-        }
+    // one 16-byte cp.async per lane and group: lanes 0-7 the group's rows, 8-15 the eight column
+    // pairs' factors that enter lane 31 during the group, 16-23 their {df, dg} (PF_RING; else lane
+    // 31's fresh columns). All sources advance by 128 bytes per group.
+    const int q8 = lane & 7;
+    const char* src_g; unsigned dst_g;
+    if (lane < 8) {
+        src_g = reinterpret_cast<const char*>(a.p32 + i0 + q8);
+        dst_g = (unsigned)__cvta_generic_to_shared(&sm.row[0][q8]);
+    } else if (lane < 16) {
+        src_g = reinterpret_cast<const char*>(a.cq4 + i0 + d0 + DP - 1 + 248 + q8);
+        dst_g = (unsigned)__cvta_generic_to_shared(&sm.cqr[q8]);
+    } else {
+#if VLMP_PF_RING
+        src_g = reinterpret_cast<const char*>(a.pf4 + i0 + d0 + DP - 1 + 248 + q8);
+        dst_g = (unsigned)__cvta_generic_to_shared(&sm.pfr[q8]);
+#else
+        src_g = PSEP == BAND ? reinterpret_cast<const char*>(a.p32 + i0 + q8 + d0 + 2 * BAND - 1)
+                             : reinterpret_cast<const char*>(a.pf4 + i0 + q8 + d0 + BAND - 1);
+        dst_g = (unsigned)__cvta_generic_to_shared(&sm.fresh[0][q8]);
+#endif
     }
-    // entering pair f = 8L + kk (f = lane + 32k): one 16-byte {aA, bA, aB, bB} -> slot kk * 33 + L
-    const char* src_cq = reinterpret_cast<const char*>(a.cq4 + i0 + d0 + DP - 1 + lane);
-    const unsigned dst_cq = (unsigned)__cvta_generic_to_shared(&sm.cq[0][(lane % 8) * CQS + lane / 8]);
-    constexpr unsigned RFP = sizeof(float4) * GRP, CQP = sizeof(float4) * GRP * CQS;
-    auto stage = [&](int g, int b) {
-        const long long gr = (long long)g * (GRP * sizeof(float4));
-        if (lane < 16) cpa<0, 0, 16>(dst_rf + (unsigned)b * RFP, src_rf + gr);
-        const unsigned dc = dst_cq + (unsigned)b * CQP;
-        const char* sc = src_cq + (long long)g * (GRP * sizeof(float4));
-#define STG(K) cpa_l1<(K) * 4 * 16, (K) * 512>(dc, sc);
+    constexpr unsigned RFP = sizeof(float4) * GRP, CHUNK = sizeof(float4) * 9;
+    // running copy plan, the same instructions for every lane: the next group's source (+128 bytes
+    // per group) and destination -- double-buffered rows (and fresh columns) alternate, a ring's
+    // new chunk walks on by one (chunk (31 + g) mod 33 for group g)
+    const bool dbuf = lane < 8 || (!VLMP_PF_RING && lane >= 16);
+    const char* src_n = src_g + 128;
+    const unsigned dst_step = dbuf ? RFP : CHUNK;
+    const unsigned dst_span = dbuf ? 2 * RFP : 33 * CHUNK;
+    const unsigned dst_lim = dst_g + dst_span;
+    unsigned dst_n = dbuf ? dst_g + RFP : dst_g + 32 * CHUNK;
+    auto stage = [&](int, int) {
+        if (lane < 24) cpa<0, 0, 16>(dst_n, src_n);
+        cp_async_commit();
+        src_n += 128;
+        dst_n += dst_step;
+        if (dst_n >= dst_lim) dst_n -= dst_span;
+    };
+    {   // group 0: rows (fresh columns) and the whole window (entry f = lane + 32 k -> chunk f / 8)
+        if (dbuf) cpa<0, 0, 16>(dst_g, src_g);
+        const char* sc = reinterpret_cast<const char*>(a.cq4 + i0 + d0 + DP - 1 + lane);
+        const unsigned dc = (unsigned)__cvta_generic_to_shared(&sm.cqr[9 * (lane / 8) + q8]);
+#define STG(K) cpa_l1<(K) * 36 * 16, (K) * 512>(dc, sc);
         STG(0) STG(1) STG(2) STG(3) STG(4) STG(5) STG(6) STG(7)
 #undef STG
+#if VLMP_PF_RING
+        const char* sf = reinterpret_cast<const char*>(a.pf4 + i0 + d0 + DP - 1 + lane);
+        const unsigned df_ = (unsigned)__cvta_generic_to_shared(&sm.pfr[9 * (lane / 8) + q8]);
+#define STG(K) cpa_l1<(K) * 36 * 16, (K) * 512>(df_, sf);
+        STG(0) STG(1) STG(2) STG(3) STG(4) STG(5) STG(6) STG(7)
+#undef STG
+#endif
         cp_async_commit();
-    };
-    stage(0, 0);
+    }
 
     // ---- prologue loads in three independent batches (block maxima, ring, seeds): the warp
     // pays about one memory round trip for them, not one per dependent step
@@ -571,9 +606,6 @@ __global__ void __launch_bounds__(32, VLMP_FILTER32_WARPS_PER_SM) k_tile32(Tile3
     const float4 plA = a.p32[cbA + DP - 1], plB = a.p32[cbB + DP - 1];
 
     float eps;
-#if VLMP_ROWPAIR
-    float eps_rev;   // slack of a covariance recovered one row back (the row pair's first row)
-#endif
     {
         if (rb1 - rb0 >= 32 || cb1 - cb0 >= 32) {   // very long segments (S > 8192)
 #pragma unroll
@@ -592,11 +624,6 @@ __global__ void __launch_bounds__(32, VLMP_FILTER32_WARPS_PER_SM) k_tile32(Tile3
         const double K = (double)a.S + 1.0;
         const double bound = 0x1p-24 * 1.01 * ((2.0 * K + 1.0) * 1.001 * Sr * Sc + 3.02 * K * (DFr * DGc + DFc * DGr));
         eps = __double2float_ru(bound);
-#if VLMP_ROWPAIR
-        // one row step undone in FP32 (two FFMA forward, two back): at most four roundings of
-        // magnitudes <= |cov32| + |df_i dg_j| + |df_j dg_i| <= Sr Sc + 2 eps + DFr DGc + DFc DGr
-        eps_rev = __double2float_ru(0x1p-24 * 5.0 * (1.01 * Sr * Sc + 2.0 * (double)eps + DFr * DGc + DFc * DGr));
-#endif
     }
 
     // ---- seeds of both bands (FP64, carried to m+1 in place as k_tile does)
@@ -709,98 +736,18 @@ __global__ void __launch_bounds__(32, VLMP_FILTER32_WARPS_PER_SM) k_tile32(Tile3
     cp_async_wait_all();
     __syncwarp();
 
-#if VLMP_ROWPAIR
-    // Row pairs: rows kk and kk + 1 are walked in one block and their 32 sign bits ANDed into
-    // one pass test and one branch (half the ISETP -> BRA latency chains and reconvergences,
-    // and a block twice as long for the scheduler). A flagged pair recomputes row kk + 1's exact
-    // mask from cov and row kk's from cov with row kk + 1's step undone (slack eps_rev; cell 0's
-    // threshold at row kk is the one row kk + 1's rotation replaced, kept in nold).
-    unsigned gflags = 0;
-    for (int g = 0; g < ngroups; ++g) {
-        const int b = g & 1;
-        if (g + 1 < ngroups) stage(g + 1, b ^ 1);
-#pragma unroll
-        for (int kk = 0; kk < GRP; kk += 2) {
-            const float4 p0 = sm.row[b][kk], p1 = sm.row[b][kk + 1];
-            unsigned t0, t1;
-            u64 nold;
-            {   // row kk: phys (kk-1) mod 8 receives lane+1's outgoing pair
-                const int q = (kk + DP - 1) % DP;
-                if (lane == 0 && kk == 0) fresh_pair(F[q], G[q], sm.fresh[b][0]);
-                F[q] = __shfl_sync(FULLMASK, F[q], (lane + 1) & 31);
-                G[q] = __shfl_sync(FULLMASK, G[q], (lane + 1) & 31);
-                const float4 cq = sm.cq[b][kk * CQS + lane];
-                NA[q] = pk2(fmaxf(-cq.x, __fmul_ru(-p0.w, cq.y)), fmaxf(-cq.z, __fmul_ru(-p0.w, cq.w)));
-                unsigned z[16];
-#pragma unroll
-                for (int s = 0; s < DP; ++s) {
-                    const int p = (s + kk) % DP;
-                    cov[s] = fma2(bc2(p0.x), G[p], cov[s]);
-                    cov[s] = fma2(F[p], bc2(p0.y), cov[s]);
-                    const u64 zz = fma2(NA[p], bc2(p0.z), cov[s]);
-                    z[s] = (unsigned)zz; z[s + 8] = (unsigned)(zz >> 32);
-                }
-                const unsigned a0 = and3(z[0], z[8], z[1]), a1 = and3(z[9], z[2], z[10]);
-                const unsigned a2 = and3(z[3], z[11], z[4]), a3 = and3(z[12], z[5], z[13]);
-                const unsigned a4 = and3(z[6], z[14], z[7]);
-                t0 = and3(and3(a0, a1, a2), a3, and3(a4, z[15], ~0u));
-                if (lane == 0) fresh_pair(F[kk % DP], G[kk % DP], sm.fresh[b][kk + 1]);
-            }
-            {   // row kk + 1: phys kk mod 8
-                const int q = kk % DP;
-                F[q] = __shfl_sync(FULLMASK, F[q], (lane + 1) & 31);
-                G[q] = __shfl_sync(FULLMASK, G[q], (lane + 1) & 31);
-                nold = NA[q];
-                const float4 cq = sm.cq[b][(kk + 1) * CQS + lane];
-                NA[q] = pk2(fmaxf(-cq.x, __fmul_ru(-p1.w, cq.y)), fmaxf(-cq.z, __fmul_ru(-p1.w, cq.w)));
-                unsigned z[16];
-#pragma unroll
-                for (int s = 0; s < DP; ++s) {
-                    const int p = (s + kk + 1) % DP;
-                    cov[s] = fma2(bc2(p1.x), G[p], cov[s]);
-                    cov[s] = fma2(F[p], bc2(p1.y), cov[s]);
-                    const u64 zz = fma2(NA[p], bc2(p1.z), cov[s]);
-                    z[s] = (unsigned)zz; z[s + 8] = (unsigned)(zz >> 32);
-                }
-                const unsigned a0 = and3(z[0], z[8], z[1]), a1 = and3(z[9], z[2], z[10]);
-                const unsigned a2 = and3(z[3], z[11], z[4]), a3 = and3(z[12], z[5], z[13]);
-                const unsigned a4 = and3(z[6], z[14], z[7]);
-                t1 = and3(and3(a0, a1, a2), a3, and3(a4, z[15], ~0u));
-            }
-            if (__builtin_expect((int)(t0 & t1) >= 0, 0)) {   // some cell of the pair passed
-                unsigned m0 = 0, m1 = 0;
-#pragma unroll
-                for (int s = 0; s < DP; ++s) {
-                    const int p = (s + kk + 1) % DP;
-                    const u64 n1 = NA[p];
-                    const float za = fma_nocse(lo2(n1), p1.z, lo2(cov[s]));
-                    const float zb = fma_nocse(hi2(n1), p1.z, hi2(cov[s]));
-                    m1 |= (__float_as_uint(za) >> 31 ^ 1u) << s;
-                    m1 |= (__float_as_uint(zb) >> 31 ^ 1u) << (s + 8);
-                    u64 cr = fma2(F[p], bc2(-p1.y), cov[s]);
-                    cr = fma2(bc2(-p1.x), G[p], cr);
-                    const u64 n0 = s == 0 ? nold : NA[(s + kk) % DP];
-                    const float ya = fma_nocse(lo2(n0), p0.z, lo2(cr) + eps_rev);
-                    const float yb = fma_nocse(hi2(n0), p0.z, hi2(cr) + eps_rev);
-                    m0 |= (__float_as_uint(ya) >> 31 ^ 1u) << s;
-                    m0 |= (__float_as_uint(yb) >> 31 ^ 1u) << (s + 8);
-                }
-                if (m0) { msk[kk] = (unsigned short)m0; gflags |= 1u << kk; }
-                if (m1) { msk[kk + 1] = (unsigned short)m1; gflags |= 1u << (kk + 1); }
-            }
-            if (kk + 2 < GRP && lane == 0) fresh_pair(F[(kk + 1) % DP], G[(kk + 1) % DP], sm.fresh[b][kk + 2]);
-        }
-        if (gflags) { fold_rows(gflags, g * GRP); gflags = 0; }
-        cp_async_wait_all();
-        __syncwarp();
-    }
-#else
     bool pass_prev = false;
     float bprev = 0.f;
     unsigned gflags = 0;
+    int chunk = lane;             // (lane + g) mod 33
     for (int g = 0; g < ngroups; ++g) {
         const int b = g & 1;
         if (g + 1 < ngroups) stage(g + 1, b ^ 1);
+        const float4* cqp = sm.cqr + 9 * chunk;
+#if VLMP_PF_RING
+        const float4* pfp = sm.pfr + 9 * chunk;
+#endif
+        chunk = chunk == 32 ? 0 : chunk + 1;
 #pragma unroll
         for (int kk = 0; kk < GRP; ++kk) {
             const float4 pr = sm.row[b][kk];
@@ -833,10 +780,17 @@ __global__ void __launch_bounds__(32, VLMP_FILTER32_WARPS_PER_SM) k_tile32(Tile3
             if (kk == 0 && g > 0 && gflags) { fold_rows(gflags, (g - 1) * GRP); gflags = 0; }
             {   // rotation: phys (kk-1) mod 8 receives lane+1's outgoing pair
                 const int q = (kk + DP - 1) % DP;
+#if VLMP_PF_RING
+                // the entering pair's {df, dg} straight from the ring: one 16-byte read whose
+                // halves are the two register pairs (no lane-to-lane shuffles, no fresh-column case)
+                const float4 pf = pfp[kk];
+                F[q] = pk2(pf.x, pf.y); G[q] = pk2(pf.z, pf.w);
+#else
                 if (lane == 0 && kk == 0) fresh_pair(F[q], G[q], sm.fresh[b][0]);
                 F[q] = __shfl_sync(FULLMASK, F[q], (lane + 1) & 31);
                 G[q] = __shfl_sync(FULLMASK, G[q], (lane + 1) & 31);
-                const float4 cq = sm.cq[b][kk * CQS + lane];
+#endif
+                const float4 cq = cqp[kk];
                 NA[q] = pk2(fmaxf(-cq.x, __fmul_ru(-pr.w, cq.y)), fmaxf(-cq.z, __fmul_ru(-pr.w, cq.w)));
             }
             unsigned z[16];
@@ -857,7 +811,9 @@ __global__ void __launch_bounds__(32, VLMP_FILTER32_WARPS_PER_SM) k_tile32(Tile3
             }
             pass_prev = (int)z[0] >= 0;
             bprev = pr.z;
+#if !VLMP_PF_RING
             if (kk + 1 < GRP && lane == 0) fresh_pair(F[kk % DP], G[kk % DP], sm.fresh[b][kk + 1]);
+#endif
         }
         cp_async_wait_all();
         __syncwarp();
@@ -876,7 +832,6 @@ __global__ void __launch_bounds__(32, VLMP_FILTER32_WARPS_PER_SM) k_tile32(Tile3
         msk[GRP - 1] = (unsigned short)mask;
         gflags |= 1u << (GRP - 1);
     }
-#endif
     if (gflags) fold_rows(gflags, (ngroups - 1) * GRP);
     while (open) { const int q = __ffs(open) - 1; open &= open - 1; emit(q, rs[q], last_r); }
 #if VLMP_RUN_GAP > 0
@@ -1084,7 +1039,7 @@ int launch_filter32(vlmp_session* s, cudaStream_t st, const Prm* prm, const doub
     const long long nb = A / 256 + 1;
     Prep32Args pa{prm, s->d_cum, s->d_cum2, s->d_p32, s->d_cq32, s->d_magblk, nb, N, A, m, s->sscale,
                   const_cast<int*>(forced), (VLMP_PACKED && n_t32) ? s->d_cq4 : nullptr,
-                  (VLMP_PACKED && n_t32 && VLMP_PAIR_SEP > 1) ? s->d_pf4 : nullptr};
+                  (VLMP_PACKED && n_t32 && (VLMP_PAIR_SEP > 1 || VLMP_PF_RING)) ? s->d_pf4 : nullptr};
     k_prep32<<<blocks(A, 256), 256, 0, st>>>(pa);
     if (n_t32) {
         Tile32Args ta{s->d_p32, s->d_cq32, s->d_magblk, nb, s->d_tn, mu, s->d_seeds, s->d_tiles, s->d_tiles32,
