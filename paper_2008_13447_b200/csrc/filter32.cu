@@ -452,6 +452,12 @@ __device__ __forceinline__ u64 fma2_nocse(u64 x, u64 y, u64 z) {
     u64 d; asm volatile("fma.rn.f32x2 %0, %1, %2, %3;" : "=l"(d) : "l"(x), "l"(y), "l"(z)); return d;
 }
 
+// one 16-byte shared-memory read straight into two 64-bit register pairs (as a float4 read plus
+// pk2 the compiler keeps the ring registers apart and copies the four words every row)
+__device__ __forceinline__ void lds_pair(u64& x, u64& y, const float4* p) {
+    asm volatile("ld.shared.v2.b64 {%0, %1}, [%2];" : "=l"(x), "=l"(y) : "r"((unsigned)__cvta_generic_to_shared(p)));
+}
+
 __device__ __forceinline__ unsigned and3(unsigned x, unsigned y, unsigned z) {
     unsigned d; asm("lop3.b32 %0, %1, %2, %3, 0x80;" : "=r"(d) : "r"(x), "r"(y), "r"(z)); return d;
 }
@@ -596,10 +602,19 @@ __global__ void __launch_bounds__(32, VLMP_FILTER32_WARPS_PER_SM) k_tile32(Tile3
 #pragma unroll
         for (int s = 0; s < DP; ++s) {
             const long long ca = s < DP - 1 ? cbA + s : cbA - 1;
+#if VLMP_PF_RING
+            // the same 16-byte {dfA, dfB, dgA, dgB} / {aA, bA, aB, bB} entries the rings hold (the
+            // ring registers then have one shape everywhere: no moves after the loop's reads)
+            const float4 pf0 = a.pf4[ca];
+            F[s] = pk2(pf0.x, pf0.y); G[s] = pk2(pf0.z, pf0.w);
+            const float4 q0 = a.cq4[ca];
+            NA[s] = pk2(fmaxf(-q0.x, __fmul_ru(-w0, q0.y)), fmaxf(-q0.z, __fmul_ru(-w0, q0.w)));
+#else
             const float4 pa = a.p32[ca], pb = a.p32[ca + PSEP];
             F[s] = pk2(pa.x, pb.x); G[s] = pk2(pa.y, pb.y);
             const float2 qa = a.cq[ca], qb = a.cq[ca + PSEP];
             NA[s] = pk2(fmaxf(-qa.x, __fmul_ru(-w0, qa.y)), fmaxf(-qb.x, __fmul_ru(-w0, qb.y)));
+#endif
         }
     }
     const float4 pr0 = a.p32[i0];
@@ -783,8 +798,7 @@ __global__ void __launch_bounds__(32, VLMP_FILTER32_WARPS_PER_SM) k_tile32(Tile3
 #if VLMP_PF_RING
                 // the entering pair's {df, dg} straight from the ring: one 16-byte read whose
                 // halves are the two register pairs (no lane-to-lane shuffles, no fresh-column case)
-                const float4 pf = pfp[kk];
-                F[q] = pk2(pf.x, pf.y); G[q] = pk2(pf.z, pf.w);
+                lds_pair(F[q], G[q], pfp + kk);
 #else
                 if (lane == 0 && kk == 0) fresh_pair(F[q], G[q], sm.fresh[b][0]);
                 F[q] = __shfl_sync(FULLMASK, F[q], (lane + 1) & 31);
