@@ -432,6 +432,11 @@ def run_ours(args):
                                     "MEASURED_PEAKS.json has no FP32 figure",
                      "walk_ms_per_step": walk_s * 1e3,
                      "share_of_step": walk_s * 1e3 / step_ms,
+                     "chains": int(st.get("chains") or 1),
+                     "chains_note": ("the length range runs as two concurrent chains on two streams (small "
+                                     "series: a length's kernels do not fill the GPU back to back); walk time = "
+                                     "union of the k_tile32 spans; k_runs spans overlap the other chain's walk"
+                                     if (st.get("chains") or 1) > 1 else "one chain"),
                      "k_runs": {"ms_per_step": runs_s * 1e3, "share_of_step": runs_s * 1e3 / step_ms,
                                 "cells_per_step": st.get("run_cells"), "bound": "fp64 / L2 latency",
                                 "fp64_frac": (st.get("run_cells") or 0) * 2 / max(runs_s, 1e-12) / peak_dfma},

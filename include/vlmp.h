@@ -218,8 +218,10 @@ int vlmp_range_query(vlmp_session* s, int64_t n_q, const int64_t* owners, const 
  * out[16] 1 if the filtered lengths ran the FP32 walk (filter32.cu), out[17] largest
  * per-length run count of that walk, out[18] cells evaluated exactly in its runs, out[19] the
  * row-segment length S of the tile walks, out[20] k_tile32 ms (sum over its launches, CUDA
- * events on the session stream), out[21] k_runs ms, out[22] k_tile32 launches, out[23] 1 if the
- * per-length sequence ran as a CUDA graph (n_out <= 24).
+ * events on the session stream; with two chains the union of their spans), out[21] k_runs ms,
+ * out[22] k_tile32 launches, out[23] 1 if the per-length sequence ran as a CUDA graph, out[24]
+ * the number of concurrent chains the length range ran as (2 on small series: the two halves
+ * of the range on two streams; VLMP_CHAINS=1 turns it off) (n_out <= 25).
  */
 int vlmp_stats(vlmp_session* s, double* out, int32_t n_out);
 

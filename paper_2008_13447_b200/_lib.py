@@ -291,13 +291,13 @@ class Session:
         return d, f, qt
 
     def stats(self):
-        out = np.zeros(24)
-        self._check(self.lib.vlmp_stats(self.h, _ptr(out), 24))
+        out = np.zeros(25)
+        self._check(self.lib.vlmp_stats(self.h, _ptr(out), 25))
         keys = ["profile_ms", "finalize_ms", "executed_updates", "W", "tile_ms", "tile_launches",
                 "filtered_lengths", "full_lengths", "slow_merges", "kernel_launches", "first_tile_ms",
                 "slow_rowsteps", "bound_fixes", "exact_redo", "fallback_lengths", "max_log_records",
                 "fp32_walk", "max_runs", "run_cells", "seg_rows", "walk_ms", "runs_ms", "walk_launches",
-                "graph"]
+                "graph", "chains"]
         return {k: float(out[i]) for i, k in enumerate(keys)}
 
     def event_record(self, slot):

@@ -1226,7 +1226,6 @@ static int profile_impl(vlmp_session* s, int32_t lmin, int32_t lmax, int64_t ban
         s->tc_key[4] = mode_key;
         s->tc_T = T; s->tc_Ts = Ts; s->tc_T32 = T32;
     }
-    Run* runs = reinterpret_cast<Run*>(s->d_log);
     const long long run_cap_full = (long long)(s->log_cap * sizeof(RowRec) / sizeof(Run));
     const size_t smem = WARPS_PER_CTA * sizeof(WarpSmem);
     CU(cudaFuncSetAttribute(k_tile<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
@@ -1252,6 +1251,50 @@ static int profile_impl(vlmp_session* s, int32_t lmin, int32_t lmax, int64_t ban
     if (fp32 && (rc = filter32_setup())) return rc;
 
     const bool dumping = getenv("VLMP_DUMP_PRM") || getenv("VLMP_DUMP_RUNS");
+    // Two chains. A length of a small series is a short kernel sequence (config 2: ~4,000 tiles
+    // for 2,368 resident warps, then k_runs, the bounds and the factors of the next length, each
+    // waiting for the one before): the walk ramps up and drains every ~0.4 ms and the GPU idles
+    // in between. So the range is cut into two contiguous halves of equal work that run
+    // concurrently on two streams (forked and joined inside the graph): while one chain is
+    // between walks, the other's tiles fill the SMs. The second chain starts like a length
+    // shard (direct-sum seeds, sampled folds for its first bounds) with its own per-length
+    // scratch; accumulators are per length and the counters atomic, so they are shared.
+    int chains = 1, chain_cut = 0;
+    {
+        const char* ce = getenv("VLMP_CHAINS");
+        const int want = ce ? atoi(ce) : 0;   // 0: automatic, 1: off, 2: on wherever it applies
+        const int lo0 = li_lo <= li_hi ? li_lo : 0;
+        const bool ok = fp32 && flags == 0 && band_lo == 0 && band_hi == nb && li_hi - lo0 + 1 >= 16 && !dumping && T32 > 0;
+        if (ok && (want == 2 || (want == 0 && T32 <= 16 * 2368))) {
+            double tot = 0, acc_w = 0;
+            auto work = [&](int li) { const double k = (double)(n - (lmin + li) + 1 - (lmin + li + 1) / 2); return k > 0 ? k * (k + 1) : 0.0; };
+            for (int li = lo0; li <= li_hi; ++li) tot += work(li);
+            int cut = lo0;
+            for (; cut <= li_hi && acc_w + work(cut) <= 0.5 * tot; ++cut) acc_w += work(cut);
+            cut = std::min(std::max(cut + 2, lo0 + 4), li_hi - 3);   // the second chain also pays a first length
+            chains = 2; chain_cut = cut;
+            if ((rc = ensure(s->x_prm, s->x_prm_cap, (size_t)A))) return rc;
+            if ((rc = ensure(s->x_prm2, s->x_prm2_cap, (size_t)A))) return rc;
+            if ((rc = ensure(s->x_mu, s->x_mu_cap, (size_t)A))) return rc;
+            if ((rc = ensure(s->x_mu2, s->x_mu2_cap, (size_t)A))) return rc;
+            if ((rc = ensure(s->x_p32, s->x_p32_cap, (size_t)A))) return rc;
+            if ((rc = ensure(s->x_cq32, s->x_cq32_cap, (size_t)A))) return rc;
+            if ((rc = ensure(s->x_cq4, s->x_cq4_cap, (size_t)A))) return rc;
+            if ((rc = ensure(s->x_pf4, s->x_pf4_cap, (size_t)A))) return rc;
+            if ((rc = ensure(s->x_magblk, s->x_magblk_cap, (size_t)(3 * (A / 256 + 1))))) return rc;
+            if ((rc = ensure(s->x_seeds, s->x_seeds_cap, (size_t)std::max<long long>(T, 1) * BAND))) return rc;
+            if ((rc = ensure(s->x_log, s->x_log_cap, s->log_cap))) return rc;
+            if (!s->stream2) CU(cudaStreamCreateWithFlags(&s->stream2, cudaStreamNonBlocking));
+            if (!s->ev_fork) CU(cudaEventCreateWithFlags(&s->ev_fork, cudaEventDisableTiming));
+            if (!s->ev_join) CU(cudaEventCreateWithFlags(&s->ev_join, cudaEventDisableTiming));
+        }
+    }
+    auto swap_scratch = [&]() {
+        std::swap(s->d_prm, s->x_prm); std::swap(s->d_prm2, s->x_prm2); std::swap(s->d_mu, s->x_mu);
+        std::swap(s->d_mu2, s->x_mu2); std::swap(s->d_p32, s->x_p32); std::swap(s->d_cq32, s->x_cq32);
+        std::swap(s->d_cq4, s->x_cq4); std::swap(s->d_pf4, s->x_pf4); std::swap(s->d_magblk, s->x_magblk);
+        std::swap(s->d_seeds, s->x_seeds); std::swap(s->d_log, s->x_log);
+    };
     // a CUDA graph of the whole sequence (VLMP_GRAPH=0 / dumping: plain stream launches). Inside
     // the graph, kernel times come from device-clock spans, not events (an event node between
     // kernels serialises the graph at every length: +12 ms per config-2 pass, measured)
@@ -1263,14 +1306,11 @@ static int profile_impl(vlmp_session* s, int32_t lmin, int32_t lmax, int64_t ban
     // The whole per-length sequence is pure stream work (no host decisions between lengths), so
     // it is captured once into a CUDA graph and re-launched while the key below is unchanged:
     // ~6 launches per length become one graph launch (no per-launch host cost in the step).
-    auto enqueue = [&]() -> int {
+    // one chain: lengths li_lo..li_hi (the arguments shadow the call's range) on stream st,
+    // with whatever per-length scratch the session's pointers name at the moment
+    auto run_chain = [&](cudaStream_t st, int li_lo, int li_hi) -> int {
         int rc2;
-        k_fill_acc<<<blocks((long long)n_len * A, 256), 256, 0, st>>>(s->d_acc, (long long)n_len * A);
-        CU(cudaMemsetAsync(s->d_counters, 0, 8 * sizeof(unsigned long long), st));
-        CU(cudaMemsetAsync(s->d_fixcnt, 0, n_len * sizeof(unsigned long long), st));
-        CU(cudaMemsetAsync(s->d_logcnt, 0, n_len * sizeof(unsigned long long), st));
-        CU(cudaMemsetAsync(s->d_forced, 0, n_len * sizeof(int), st));
-        k_span_init<<<blocks(n_len, 128), 128, 0, st>>>(s->d_span, n_len);
+        Run* runs = reinterpret_cast<Run*>(s->d_log);
         if (li_lo > 0 && li_lo <= li_hi && T) {
             if (fp32) {
                 // a later length shard on the FP32 walk: the seeds only start the walk (its slack
@@ -1293,7 +1333,7 @@ static int profile_impl(vlmp_session* s, int32_t lmin, int32_t lmax, int64_t ban
                 klaunch += 3;
             }
         }
-        for (int li = (li_lo <= li_hi ? li_lo : 0); li <= li_hi; ++li) {
+        for (int li = li_lo; li <= li_hi; ++li) {
             const int m = lmin + li;
             const long long N = n - m + 1;
             const int e = (m + 1) / 2;
@@ -1378,13 +1418,37 @@ static int profile_impl(vlmp_session* s, int32_t lmin, int32_t lmax, int64_t ban
         }
         return 0;
     };
+    auto enqueue = [&]() -> int {
+        k_fill_acc<<<blocks((long long)n_len * A, 256), 256, 0, st>>>(s->d_acc, (long long)n_len * A);
+        CU(cudaMemsetAsync(s->d_counters, 0, 8 * sizeof(unsigned long long), st));
+        CU(cudaMemsetAsync(s->d_fixcnt, 0, n_len * sizeof(unsigned long long), st));
+        CU(cudaMemsetAsync(s->d_logcnt, 0, n_len * sizeof(unsigned long long), st));
+        CU(cudaMemsetAsync(s->d_forced, 0, n_len * sizeof(int), st));
+        k_span_init<<<blocks(n_len, 128), 128, 0, st>>>(s->d_span, n_len);
+        const int lo0 = li_lo <= li_hi ? li_lo : 0;
+        if (chains == 1) return run_chain(st, lo0, li_hi);
+        // fork: the second chain's stream joins the capture (or, without a graph, just waits)
+        CU(cudaEventRecord(s->ev_fork, st));
+        CU(cudaStreamWaitEvent(s->stream2, s->ev_fork, 0));
+        int rc2 = run_chain(st, lo0, chain_cut - 1);
+        swap_scratch();
+        const int rc3 = rc2 ? 0 : run_chain(s->stream2, chain_cut, li_hi);
+        swap_scratch();
+        CU(cudaEventRecord(s->ev_join, s->stream2));
+        CU(cudaStreamWaitEvent(st, s->ev_join, 0));
+        return rc2 ? rc2 : rc3;
+    };
     CU(cudaEventRecord(s->ev[0], st));
     if (use_graph) {
         // everything the captured launches bake in: shape, mode, buffers, series scalars
         std::vector<double> key = {(double)n, (double)A, (double)lmin, (double)lmax, (double)band_lo, (double)band_hi,
                                    (double)flags, (double)li_lo, (double)li_hi, (double)T, (double)Ts, (double)T32,
                                    (double)S, (double)eff_cap, (double)run_cap, s->sscale, s->floor_,
-                                   (double)s->hiC, (double)bound_start, (double)fp32};
+                                   (double)s->hiC, (double)bound_start, (double)fp32, (double)chains, (double)chain_cut,
+                                   (double)(uintptr_t)s->x_prm, (double)(uintptr_t)s->x_prm2, (double)(uintptr_t)s->x_mu,
+                                   (double)(uintptr_t)s->x_mu2, (double)(uintptr_t)s->x_p32, (double)(uintptr_t)s->x_cq32,
+                                   (double)(uintptr_t)s->x_cq4, (double)(uintptr_t)s->x_pf4, (double)(uintptr_t)s->x_magblk,
+                                   (double)(uintptr_t)s->x_seeds, (double)(uintptr_t)s->x_log};
         for (const void* ptr : {(const void*)s->d_acc, (const void*)s->d_tn, (const void*)s->d_cum, (const void*)s->d_cum2,
                                 (const void*)s->d_prm, (const void*)s->d_prm2, (const void*)s->d_mu, (const void*)s->d_mu2,
                                 (const void*)s->d_tiles, (const void*)s->d_tiles_s, (const void*)s->d_smap,
@@ -1439,7 +1503,7 @@ static int profile_impl(vlmp_session* s, int32_t lmin, int32_t lmax, int64_t ban
     pr.li_lo = li_lo; pr.li_hi = li_hi; pr.fp32 = fp32; pr.sampled = sampled_start;
     pr.cap_used = fp32 ? run_cap : eff_cap; pr.S = S;
     pr.executed = executed; pr.launches = launches; pr.n_filtered = n_filtered; pr.n_full = n_full;
-    pr.klaunch = klaunch; pr.graph = use_graph; pr.timed = timed; pr.walked = walked;
+    pr.klaunch = klaunch; pr.graph = use_graph; pr.timed = timed; pr.walked = walked; pr.chains = chains;
     s->lmin = lmin; s->lmax = lmax; s->n_len = n_len;
     s->have_profile = true; s->have_final = false; s->have_finals = false;
     s->pending = true; s->stats_dirty = true;
@@ -1464,6 +1528,24 @@ int fill_event_stats(vlmp_session* s) {
         const unsigned long long* sp = s->h_span + 4 * li;
         if (sp[1] > sp[0]) walk_ms += (double)(sp[1] - sp[0]) * 1e-6;
         if (sp[3] > sp[2]) runs_ms += (double)(sp[3] - sp[2]) * 1e-6;
+    }
+    if (pr.chains > 1) {
+        // two concurrent chains: their walk kernels share the SMs, so a launch's own span counts
+        // time it spent beside the other chain's launch. The walk's time is the union of the
+        // spans -- the time during which a walk kernel was running at all.
+        std::vector<std::pair<unsigned long long, unsigned long long>> iv;
+        for (int li : pr.walked) {
+            const unsigned long long* sp = s->h_span + 4 * li;
+            if (sp[1] > sp[0]) iv.push_back({sp[0], sp[1]});
+        }
+        std::sort(iv.begin(), iv.end());
+        unsigned long long covered = 0, cur_lo = 0, cur_hi = 0;
+        for (const auto& x : iv) {
+            if (x.first > cur_hi) { covered += cur_hi - cur_lo; cur_lo = x.first; cur_hi = x.second; }
+            else cur_hi = std::max(cur_hi, x.second);
+        }
+        covered += cur_hi - cur_lo;
+        walk_ms = (double)covered * 1e-6;
     }
     if (const char* sp_path = getenv("VLMP_DUMP_SPANS")) {   // dev aid: per-length kernel spans (ns, device clock)
         if (FILE* f = fopen(sp_path, "w")) {
@@ -1524,6 +1606,7 @@ int settle_profile(vlmp_session* s, bool* redone) {
         s->stats[12] = n_fix; s->stats[14] = n_forced; s->stats[15] = max_log;
         s->stats[16] = pr.fp32 ? 1.0 : 0.0; s->stats[17] = pr.fp32 ? max_log : 0.0; s->stats[18] = (double)h[4];
         s->stats[19] = (double)pr.S; s->stats[22] = (double)pr.walked.size(); s->stats[23] = pr.graph ? 1.0 : 0.0;
+        s->stats[24] = (double)pr.chains;
         s->stats_dirty = true;
         if (!overflow) break;
         if (redone) *redone = true;

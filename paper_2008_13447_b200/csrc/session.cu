@@ -82,6 +82,12 @@ void vlmp_destroy(vlmp_session* s) {
                     s->d_log, s->d_logcnt, s->d_p32, s->d_cq32, s->d_cq4, s->d_pf4, s->d_magblk, s->d_tiles32, s->d_ro_i64, s->d_ro_f64, s->d_ro_cnt,
                     s->d_slots, s->d_slotcnt, s->d_ipm, s->d_mpm, s->d_redo, s->d_vdist, s->d_vnorm, s->d_vlen, s->d_vidx, s->d_vpop};
     for (void* p : ptrs) if (p) cudaFree(p);
+    void* xptrs[] = {s->x_prm, s->x_prm2, s->x_mu, s->x_mu2, s->x_p32, s->x_cq32, s->x_cq4, s->x_pf4,
+                     s->x_magblk, s->x_seeds, s->x_log};
+    for (void* p : xptrs) if (p) cudaFree(p);
+    if (s->ev_fork) cudaEventDestroy(s->ev_fork);
+    if (s->ev_join) cudaEventDestroy(s->ev_join);
+    if (s->stream2) cudaStreamDestroy(s->stream2);
     for (auto& ev : s->ev) if (ev) cudaEventDestroy(ev);
     for (auto& ev : s->lev) cudaEventDestroy(ev);
     if (s->d_span) cudaFree(s->d_span);
@@ -147,7 +153,7 @@ int vlmp_stats(vlmp_session* s, double* out, int32_t n_out) {
         if (!rc) rc = fill_event_stats(s);
         if (rc) return rc;
     }
-    for (int q = 0; q < n_out && q < 24; ++q) out[q] = s->stats[q];
+    for (int q = 0; q < n_out && q < 25; ++q) out[q] = s->stats[q];
     return 0;
 }
 

@@ -227,6 +227,7 @@ struct PendingRun {
     long long cap_used = 0; int S = 0;
     double executed = 0, launches = 0, n_filtered = 0, n_full = 0, klaunch = 0;
     std::vector<int> timed, walked;
+    int chains = 1;   // 2: the length range ran as two concurrent chains (kernel spans overlap)
 };
 
 struct vlmp_session {
@@ -284,7 +285,7 @@ struct vlmp_session {
     long long* d_redo = nullptr; size_t redo_cap = 0;
     // run state
     int lmin = 0, lmax = 0, n_len = 0; bool have_profile = false, have_final = false, have_finals = false;
-    double stats[24] = {};
+    double stats[25] = {};
     bool pending = false, stats_dirty = false;          // phase 1 enqueued, not yet settled
     PendingRun prun;
     unsigned long long* h_chk = nullptr; size_t h_chk_cap = 0;   // pinned: its overflow counters
@@ -297,6 +298,14 @@ struct vlmp_session {
     cudaGraphExec_t g_exec = nullptr;
     std::vector<double> g_key;
     std::vector<double> g_cnt; std::vector<int> g_timed, g_walked;   // its host-side counters
+    // second chain: on small series the two halves of the length range are walked concurrently
+    // (profile_impl), each with its own per-length scratch; accumulators and counters are shared
+    Prm* x_prm = nullptr; Prm* x_prm2 = nullptr; double* x_mu = nullptr; double* x_mu2 = nullptr;
+    float4* x_p32 = nullptr; float2* x_cq32 = nullptr; float4* x_cq4 = nullptr; float4* x_pf4 = nullptr;
+    unsigned* x_magblk = nullptr; double* x_seeds = nullptr; RowRec* x_log = nullptr;
+    size_t x_prm_cap = 0, x_prm2_cap = 0, x_mu_cap = 0, x_mu2_cap = 0, x_p32_cap = 0, x_cq32_cap = 0,
+           x_cq4_cap = 0, x_pf4_cap = 0, x_magblk_cap = 0, x_seeds_cap = 0, x_log_cap = 0;
+    cudaStream_t stream2 = nullptr; cudaEvent_t ev_fork = nullptr, ev_join = nullptr;
     vlmp_impl::PrunedState* pp = nullptr;                  // pruned discord scan (pruned.cu)
 };
 
