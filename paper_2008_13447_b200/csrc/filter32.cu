@@ -42,6 +42,9 @@ constexpr int WIN = VLMP_PACKED ? 8 : D2;   // rows a column meets in one lane (
 #ifndef VLMP_PAIR_SEP
 #define VLMP_PAIR_SEP 2          // packed walk: band B = band A + VLMP_PAIR_SEP bands (1: adjacent)
 #endif
+#ifndef VLMP_PRIO
+#define VLMP_PRIO 1              // the short per-length kernels launch at the highest priority (two chains)
+#endif
 #ifndef VLMP_PF_RING
 #define VLMP_PF_RING 1           // packed walk: entering columns' {df, dg} from a second sliding ring (0: lane-to-lane shuffles)
 #endif
@@ -1054,15 +1057,25 @@ int launch_filter32(vlmp_session* s, cudaStream_t st, const Prm* prm, const doub
     Prep32Args pa{prm, s->d_cum, s->d_cum2, s->d_p32, s->d_cq32, s->d_magblk, nb, N, A, m, s->sscale,
                   const_cast<int*>(forced), (VLMP_PACKED && n_t32) ? s->d_cq4 : nullptr,
                   (VLMP_PACKED && n_t32 && (VLMP_PAIR_SEP > 1 || VLMP_PF_RING)) ? s->d_pf4 : nullptr};
+#if VLMP_PRIO
+    launch_hi(k_prep32, dim3((unsigned)blocks(A, 256)), dim3(256), 0, st, pa);
+#else
     k_prep32<<<blocks(A, 256), 256, 0, st>>>(pa);
+#endif
     if (n_t32) {
         Tile32Args ta{s->d_p32, s->d_cq32, s->d_magblk, nb, s->d_tn, mu, s->d_seeds, s->d_tiles, s->d_tiles32,
                       runs, run_count, run_cap, s->d_counters, forced, N, dl, (int)n_t32, S, m, e,
                       update_seeds, s->sscale, span, s->d_cq4, s->d_pf4};
         // span: [0, 1] k_tile32's and [2, 3] k_runs' first start / last end (bench.py's roofline)
         k_tile32<<<(unsigned)n_t32, 32, sizeof(SmemT), st>>>(ta);
+#if VLMP_PRIO
+        launch_hi(k_runs<VLMP_RUNS_G>, dim3(148 * VLMP_RUNS_GRID), dim3(256), 0, st, (const Run*)runs,
+                  (const unsigned long long*)run_count, run_cap, prm, (const double*)s->d_tn, mu, m, e, acc, s->d_counters,
+                  slots, slot_cnt, span ? span + 2 : (unsigned long long*)nullptr);
+#else
         k_runs<VLMP_RUNS_G><<<148 * VLMP_RUNS_GRID, 256, 0, st>>>(runs, run_count, run_cap, prm, s->d_tn, mu, m, e, acc, s->d_counters,
                                         slots, slot_cnt, span ? span + 2 : nullptr);
+#endif
     }
     return 0;
 }

@@ -1343,7 +1343,7 @@ static int profile_impl(vlmp_session* s, int32_t lmin, int32_t lmax, int64_t ban
             const Prm* prm_prev = (li & 1) ? s->d_prm : s->d_prm2;
             const double* mu_prev = (li & 1) ? s->d_mu : s->d_mu2;
             ParamArgs pa{s->d_tn, s->d_cum, s->d_cum2, prm, mu, n, N, A, m, s->floor_};
-            k_params<<<blocks(A, 256), 256, 0, st>>>(pa);
+            launch_hi(k_params, dim3((unsigned)blocks(A, 256)), dim3(256), 0, st, pa);
             ++klaunch;
             const bool full = (li == li_lo) || (flags & VLMP_F_FULL_EVERY_LENGTH);
             if (li == 0 && T) {
@@ -1354,7 +1354,7 @@ static int profile_impl(vlmp_session* s, int32_t lmin, int32_t lmax, int64_t ban
             if (!full) {
                 Bound2Args ba{s->d_tn, prm, prm_prev, mu_prev, mu, s->d_acc + (long long)(li - 1) * A, prm,
                               N, N + 1, m, e, margin, s->d_fixcnt + li, fp32 ? 1 : 0};
-                k_bound2<<<blocks(N, 256), 256, 0, st>>>(ba);
+                launch_hi(k_bound2, dim3((unsigned)blocks(N, 256)), dim3(256), 0, st, ba);
                 if (!fp32)
                     k_qprep<<<blocks(A, 256), 256, 0, st>>>(prm, s->d_colq, s->d_rowq, N, A, s->sscale,
                                                             s->d_forced + li);
