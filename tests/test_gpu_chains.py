@@ -31,8 +31,8 @@ def _with_env(env, fn):
 def test_two_chains_equal_one_chain(graph):
     import paper_2008_13447_b200 as vl
     from paper_2008_13447_b200 import api, gen
-    s = vl.ingest(gen.series_for(1))            # n = 4096, lengths 32..64: 33 lengths
-    lmin, lmax = 32, 64
+    s = vl.ingest(gen.series_for(1))            # n = 4096
+    lmin, lmax = 24, 72                         # 49 lengths
 
     def go():
         run = api.GpuRun(s, lmin, lmax)
@@ -50,17 +50,17 @@ def test_two_chains_equal_one_chain(graph):
 
 
 def test_chains_default_and_short_ranges():
-    """Automatic: two chains from 16 lengths on; shorter ranges and band shards stay one chain."""
+    """Automatic: two chains from 40 lengths on; shorter ranges and band shards stay one chain."""
     import paper_2008_13447_b200 as vl
     from paper_2008_13447_b200 import _lib, api, gen
     s = vl.ingest(gen.series_for(1))
     os.environ.pop("VLMP_CHAINS", None)
-    assert api.GpuRun(s, 32, 64).stats["chains"] == 2
-    assert api.GpuRun(s, 32, 40).stats["chains"] == 1
+    assert api.GpuRun(s, 24, 72).stats["chains"] == 2
+    assert api.GpuRun(s, 32, 64).stats["chains"] == 1
     sess = _lib.session(0)
     with sess.lock:
         sess.set_series(s.values, s._cum, s._cum2, s.sigma_floor)
-        sess.profile(32, 64, 0, 2, 0)            # a band shard
+        sess.profile(24, 72, 0, 2, 0)            # a band shard
         sess.finalize()
         assert sess.stats()["chains"] == 1
 
@@ -76,7 +76,7 @@ def test_two_chains_against_oracle_with_flat_stretches():
     t[700:760] = t[700]
     t[1500:1800] *= 1e-3
     s = vl.ingest(t)
-    lmin, lmax = 20, 44
+    lmin, lmax = 20, 44                         # 25 lengths: forced (VLMP_CHAINS=2 applies from 16 on)
     run = _with_env({"VLMP_CHAINS": "2"}, lambda: api.GpuRun(s, lmin, lmax))
     assert run.stats["chains"] == 2
     ref = oracle.run(s, lmin, lmax, keep_profiles=True)
