@@ -66,6 +66,9 @@ int vlmp_set_series(vlmp_session* s, const double* t, const double* cum,
  * k_log_merge) instead of the default FP32 walk + exact FP64 run evaluation (filter32.cu);
  * both are exact, the flag exists for A/B checks and is the fallback the library takes
  * itself when the FP32 run log overflows or a bound is too weak for it.
+ * With flags 0, all bands, >= 40 lengths and at most 16 waves of tiles per length (small
+ * series) the two halves of the length range run as two concurrent chains on two streams
+ * inside the call's CUDA graph (same results; environment VLMP_CHAINS=1 turns it off).
  */
 #define VLMP_F_FULL_EVERY_LENGTH 1u
 #define VLMP_F_FP64_FILTER 2u
