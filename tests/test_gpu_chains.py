@@ -89,3 +89,26 @@ def test_two_chains_against_oracle_with_flat_stretches():
         assert np.allclose(mp[fin], omp[fin], atol=1e-7), L
         with np.errstate(invalid="ignore"):
             assert np.all(same | ~fin | (np.abs(mp - omp) < 1e-9)), L
+
+
+def test_log_overflow_redo_with_two_chains(monkeypatch):
+    """A run log too small for a length (VLMP_LOG_CAP test hook) in either chain: the run is
+    redone exactly (one chain, FP64 filter path) and equals the normal result."""
+    import paper_2008_13447_b200 as vl
+    from paper_2008_13447_b200 import api
+    s = vl.ingest(np.cumsum(np.random.default_rng(23).standard_normal(3000)))
+    lmin, lmax = 32, 56
+    monkeypatch.setenv("VLMP_CHAINS", "2")
+    ref = api.GpuRun(s, lmin, lmax)
+    assert ref.stats["chains"] == 2 and ref.stats["exact_redo"] == 0
+    want = _all_profiles(ref, lmin, lmax)
+    monkeypatch.setenv("VLMP_LOG_CAP", "16")
+    run = api.GpuRun(s, lmin, lmax)
+    assert run.stats["exact_redo"] >= 1
+    for (mp, ip), (gmp, gip) in zip(want, _all_profiles(run, lmin, lmax)):
+        assert np.array_equal(gip, ip) and np.array_equal(gmp, mp, equal_nan=True)
+    monkeypatch.delenv("VLMP_LOG_CAP")
+    again = api.GpuRun(s, lmin, lmax)              # and the session recovers its two-chain graph
+    assert again.stats["chains"] == 2 and again.stats["exact_redo"] == 0
+    for (mp, ip), (gmp, gip) in zip(want, _all_profiles(again, lmin, lmax)):
+        assert np.array_equal(gip, ip) and np.array_equal(gmp, mp, equal_nan=True)
