@@ -1015,6 +1015,7 @@ __global__ void VLMP_RUNS_BOUNDS k_runs(const Run* __restrict__ runs, const unsi
 // ---------------------------------------------------------------------------------
 // host side
 int tile32_width() { return D2; }
+const void* tile32_func() { return reinterpret_cast<const void*>(&k_tile32); }
 
 #if VLMP_PACKED
 using SmemT = Smem32p;

@@ -1468,7 +1468,33 @@ static int profile_impl(vlmp_session* s, int32_t lmin, int32_t lmax, int64_t ban
             const cudaError_t ec = cudaStreamEndCapture(st, &g);
             if (rc_cap) { if (g) cudaGraphDestroy(g); return rc_cap; }
             if (ec != cudaSuccess) return fail(VLMP_E_CUDA, std::string("graph capture: ") + cudaGetErrorString(ec));
-            const cudaError_t ei = cudaGraphInstantiate(&s->g_exec, g, 0);
+            unsigned long long inst_flags = 0;
+            if (chains > 1 && !getenv("VLMP_NO_NODE_PRIO")) {
+                // With two chains the short kernels between a chain's walks must not queue behind the
+                // other chain's pending walk blocks: every node but the walks gets the highest
+                // priority, and the graph is instantiated to use node priorities (a launch
+                // attribute set during capture does not reach the node; without the instantiate
+                // flag the nodes run at the launch stream's priority).
+                size_t nn = 0;
+                int p_lo = 0, p_hi = 0;
+                cudaDeviceGetStreamPriorityRange(&p_lo, &p_hi);
+                if (cudaGraphGetNodes(g, nullptr, &nn) == cudaSuccess && nn) {
+                    std::vector<cudaGraphNode_t> nodes(nn);
+                    cudaGraphGetNodes(g, nodes.data(), &nn);
+                    for (cudaGraphNode_t nd : nodes) {
+                        cudaGraphNodeType ty;
+                        if (cudaGraphNodeGetType(nd, &ty) != cudaSuccess || ty != cudaGraphNodeTypeKernel) continue;
+                        cudaKernelNodeParams kp;
+                        if (cudaGraphKernelNodeGetParams(nd, &kp) != cudaSuccess) continue;
+                        cudaKernelNodeAttrValue v;
+                        v.priority = kp.func == tile32_func() ? p_lo : p_hi;
+                        cudaGraphKernelNodeSetAttribute(nd, cudaKernelNodeAttributePriority, &v);
+                    }
+                    inst_flags = cudaGraphInstantiateFlagUseNodePriority;
+                }
+                cudaGetLastError();
+            }
+            const cudaError_t ei = cudaGraphInstantiateWithFlags(&s->g_exec, g, inst_flags);
             cudaGraphDestroy(g);
             if (ei != cudaSuccess) { s->g_exec = nullptr; return fail(VLMP_E_CUDA, std::string("graph instantiate: ") + cudaGetErrorString(ei)); }
             s->g_key = key;

@@ -154,10 +154,10 @@ inline cudaError_t rec_event(cudaEvent_t ev, cudaStream_t st) {
 
 // Launch at the device's highest priority. With two chains sharing the GPU the short kernels
 // between a chain's walks (k_runs, parameters, bounds, factors) otherwise queue behind every
-// pending block of the other chain's walk (~200 us each time). Measured: with plain stream
-// launches (VLMP_GRAPH=0) the wait drops to ~4 us and a config-2 pass from 52.2 to 50.7 ms;
-// inside the CUDA graph the attribute has no effect (nor has cudaKernelNodeAttributePriority set
-// on the captured nodes), so the default path keeps the 200 us waits.
+// pending block of the other chain's walk (~200 us each time; ~2 us at high priority). This
+// attribute reaches plain stream launches (VLMP_GRAPH=0); a captured node does not keep it, so
+// profile_impl sets cudaKernelNodeAttributePriority on the graph's nodes and instantiates it
+// with cudaGraphInstantiateFlagUseNodePriority.
 template <typename... KArgs, typename... Args>
 inline cudaError_t launch_hi(void (*kern)(KArgs...), dim3 grid, dim3 block, size_t smem, cudaStream_t st,
                              Args&&... args) {
@@ -330,6 +330,7 @@ struct vlmp_session {
 namespace vlmp_impl {
 // filter32.cu
 int tile32_width();
+const void* tile32_func();   // the FP32 walk kernel (profile.cu: graph node priorities)
 size_t tile32_smem();
 int filter32_setup();
 void build_tiles32(const std::vector<int2>& tiles, long long band_lo, std::vector<int4>& out);
